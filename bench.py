@@ -1,0 +1,463 @@
+"""Benchmark: Occ steps/s on BASELINE.json config 1 (default), plus other configs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config config1]
+    python bench.py --impl reference ...      # the reference's CPU path (oracle port)
+
+One step = one pass of the hot path over one batch of synthetic input:
+  config1  : fmg_occ_pair over 2^24 (k-1, l) pairs on a 2^24-base index
+  config1h : the same pair distribution over the 1 Gbp config-4 text
+  config0  : exact search of 10,000 x 32 bp patterns on 1 Mbp
+  config2  : inexact (z=1) search of 1,000,000 32-bp seeds on the 64 Mbp repeat genome
+  config4  : exact search of 2^28 x 20 bp seeds on 1 Gbp (host memory heavy)
+Inputs are resident in HBM when the timed region starts (`value`); `e2e` is
+the same metric through the C-ABI host entry point with host buffers and the
+host<->device copies inside the timed region.  Multi-GPU: weak scaling, rank
+r processes its own shard of the same size; no collective on the data path.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as ct
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+PEAKS = REPO / "MEASURED_PEAKS.json"
+TRAFFIC = REPO / "profiles" / "traffic.json"
+
+
+def hbm_peak() -> tuple[float, str]:
+    try:
+        return float(json.loads(PEAKS.read_text())["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def measured_traffic(kernel: str, config: str):
+    """dram bytes/launch from the committed ncu --set full capture (profiles/traffic.json)."""
+    try:
+        return json.loads(TRAFFIC.read_text())[config][kernel]
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def occ_step_bytes(pairs: np.ndarray) -> tuple[int, int]:
+    """Algorithmic bytes of config-1 Occ steps on the line layout.
+
+    Per step: 32 B x |lines(k-1) U lines(l)| + 8 B (k, l) in + 32 B (8 x u32) out.
+    Returns (total bytes, total distinct lines).
+    """
+    low, high = pairs[:, 0], pairs[:, 1]
+    two = (low >= 0) & ((low >> 6) != (high >> 6))
+    lines = int(low.size + two.sum())
+    return lines * 32 + low.size * 40, lines
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+
+
+def make_workload(config: str, rank: int):
+    from paper_1811_06127_b200 import workloads as w
+
+    if config == "config1":
+        return w.config1(shard=rank)
+    if config == "config1h":
+        return w.config1h()
+    if config == "config0":
+        return w.config0()
+    if config == "config2":
+        return w.config2()
+    if config == "config4":
+        return w.config4()
+    raise SystemExit(f"unknown config {config}")
+
+
+def unit_count(wl) -> int:
+    return wl.pairs.shape[0] if wl.pairs is not None else wl.patterns.shape[0]
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's CPU path (oracle port, all host threads)
+# ---------------------------------------------------------------------------
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+    from paper_1811_06127_b200 import build_index
+
+    wl = make_workload(args.config, 0)
+    idx = build_index(wl.text)
+    ox = orc.OracleIndex(idx)
+    threads = cpu_threads()
+    total = unit_count(wl)
+    sample = min(total, args.ref_sample or {"config1": 1 << 22, "config1h": 1 << 21, "config0": 10_000,
+                                          "config2": 20_000, "config4": 1 << 21}[args.config])
+
+    def step(i: int):
+        lo = (i * sample) % max(total - sample + 1, 1)
+        if wl.pairs is not None:
+            orc.occ_pair_batch(ox, wl.pairs[lo:lo + sample, 0], wl.pairs[lo:lo + sample, 1], threads)
+        elif wl.max_diff:
+            orc.inexact_batch(ox, wl.patterns[lo:lo + sample], wl.max_diff, threads)
+        else:
+            orc.exact_batch(ox, wl.patterns[lo:lo + sample], threads)
+
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(args.warmup + i)
+    dt = time.perf_counter() - t0
+    metric, unit = metric_of(args.config)
+    value = sample * args.steps / dt
+    desc = (f"C restatement of the reference path (oracle/fm_oracle.c: bytelut all4, occ_pair_all, "
+            f"exact/inexact_search) on {threads} threads of {cpu_model()}; {sample} units per step "
+            f"from the {args.config} workload")
+    line = {
+        "impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seeded PCG64, workloads.py)", "config": config_of(args.config, world, sample),
+        "cpu_baseline": {"value": value, "unit": unit, "cores": threads, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def metric_of(config: str) -> tuple[str, str]:
+    if config in ("config1", "config1h"):
+        return "Occ steps/sec (8 counts each)", "occ_steps/s"
+    return "reads/sec", "reads/s"
+
+
+def config_of(config: str, world: int, units: int) -> dict:
+    desc = {
+        "config1": "BASELINE configs[1]: Occ microbenchmark, 2^24-base iid text (seed 7), 2^24 (k-1,l) pairs/rank",
+        "config1h": "config 1-H: config-1 pair distribution over the 1 Gbp config-4 text (HBM-resident index)",
+        "config0": "BASELINE configs[0]: exact search, 1 Mbp iid (seed 42), 10,000 x 32 bp",
+        "config2": "BASELINE configs[2]: inexact z=1, 64 Mbp repeat genome (seed 3), 1M x 32 bp seeds",
+        "config4": "BASELINE configs[4]: exact, 1 Gbp iid (seed 5), 2^28 x 20 bp seeds",
+    }[config]
+    return {"workload": desc, "units_per_step_per_rank": units, "parallelism": f"query-sharded x{world}"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+
+def run_ours(args, rank: int, local: int, world: int) -> None:
+    import torch
+
+    import paper_1811_06127_b200 as fm
+    from paper_1811_06127_b200 import _lib
+    from paper_1811_06127_b200.dist import max_over_ranks
+
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.load()
+    wl = make_workload(args.config, rank)
+    t_build = time.perf_counter()
+    idx = fm.build_index(wl.text)
+    t_build = time.perf_counter() - t_build
+    dix = idx.device_index(local)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    units = unit_count(wl)
+    metric, unit = metric_of(args.config)
+    extra: dict = {"index_build_s": round(t_build, 2), "index_device_bytes": dix.device_bytes}
+
+    if wl.pairs is not None:
+        kl_h = np.empty((units, 2), dtype=np.uint32)
+        kl_h[:, 0] = (wl.pairs[:, 0] + 1).astype(np.uint32)
+        kl_h[:, 1] = wl.pairs[:, 1].astype(np.uint32)
+        d_kl = torch.from_numpy(kl_h.view(np.int32)).to(dev)
+        d_out = torch.empty((units, 8), dtype=torch.int32, device=dev)
+
+        def step():
+            rc = lib.fmg_occ_pair(dix.handle, d_kl.data_ptr(), units, d_out.data_ptr(), sp)
+            if rc:
+                _lib.check(rc)
+
+        launches_per_step = 1
+        alg_bytes, alg_lines = occ_step_bytes(wl.pairs)
+        kernel_name = "k_occ_pair"
+        h2d_per, d2h_per = units * 8, units * 32
+        pin_in = torch.from_numpy(kl_h.view(np.int32)).pin_memory()
+        pin_out = torch.empty((units, 8), dtype=torch.int32).pin_memory()
+
+        def e2e_step():
+            _lib.check(lib.fmg_occ_pair_host(dix.handle, pin_in.data_ptr(), units, pin_out.data_ptr()))
+    else:
+        m = wl.patterns.shape[1]
+        packed = fm.pack_patterns_u64(wl.patterns) if m <= 32 else None
+        z = wl.max_diff
+        if z == 0 and packed is not None:
+            d_pat = torch.from_numpy(packed.view(np.int64)).to(dev)
+            d_out = torch.empty((units, 2), dtype=torch.int32, device=dev)
+
+            def step():
+                rc = lib.fmg_exact_packed(dix.handle, d_pat.data_ptr(), m, units, d_out.data_ptr(), sp)
+                if rc:
+                    _lib.check(rc)
+
+            launches_per_step = 1
+            kernel_name = "k_exact"
+            h2d_per, d2h_per = units * 8, units * 8
+            pin_in = torch.from_numpy(packed.view(np.int64)).pin_memory()
+            pin_out = torch.empty((units, 2), dtype=torch.int32).pin_memory()
+
+            def e2e_step():
+                _lib.check(lib.fmg_exact_packed_host(dix.handle, pin_in.data_ptr(), m, units, pin_out.data_ptr()))
+        else:
+            codes = np.ascontiguousarray(wl.patterns.reshape(-1))
+            offs = np.arange(0, (units + 1) * m, m, dtype=np.uint64)
+            d_codes = torch.from_numpy(codes).to(dev)
+            d_offs = torch.from_numpy(offs.view(np.int64)).to(dev)
+
+            def step():
+                h = ct.c_void_p()
+                _lib.check(lib.fmg_inexact(dix.handle, d_codes.data_ptr(), d_offs.data_ptr(), units, z,
+                                           ct.byref(h), sp))
+                lib.fmg_matches_free(h)
+
+            launches_per_step = None  # counted below
+            kernel_name = "k_inexact"
+            h2d_per, d2h_per = codes.nbytes + offs.nbytes, None
+            pin_codes = torch.from_numpy(codes).pin_memory()
+            pin_offs = torch.from_numpy(offs.view(np.int64)).pin_memory()
+
+            def e2e_step():
+                h = ct.c_void_p()
+                _lib.check(lib.fmg_inexact_host(dix.handle, pin_codes.data_ptr(), pin_offs.data_ptr(), units, z,
+                                                ct.byref(h)))
+                tot = ct.c_uint64()
+                lib.fmg_matches_size(h, ct.byref(tot), None)
+                row = np.empty(units + 1, np.uint64)
+                kk = np.empty(tot.value, np.uint32)
+                ll = np.empty(tot.value, np.uint32)
+                dd = np.empty(tot.value, np.uint8)
+                lib.fmg_matches_copy(h, row.ctypes.data, kk.ctypes.data, ll.ctypes.data, dd.ctypes.data, 1)
+                lib.fmg_matches_free(h)
+                return row.nbytes + kk.nbytes + ll.nbytes + dd.nbytes
+        alg_bytes = alg_lines = None
+
+    # ---- warm-up, then exactly K timed steps bracketed by barrier + sync ----
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    t_ms = ev0.elapsed_time(ev1)
+    t_ms = max_over_ranks(t_ms, world, dev)
+    ms_step = t_ms / args.steps
+    value = units * world * args.steps / (t_ms / 1e3)
+
+    # ---- per-launch kernel time for the roofline (same stream, CUDA events) ----
+    roofline = None
+    if alg_bytes is not None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(3, min(args.steps, 20))
+        e0.record(stream)
+        for _ in range(reps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        launch_s = e0.elapsed_time(e1) / reps / 1e3
+        peak, peak_kind = hbm_peak()
+        achieved = alg_bytes / launch_s / 1e9
+        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": measured_traffic(kernel_name, args.config),
+                    "peak_kind": peak_kind, "kernel": kernel_name,
+                    "alg_bytes_per_launch": alg_bytes,
+                    "alg_bytes_per_step": round(alg_bytes / units, 2),
+                    "sectors_per_step": round(alg_lines / units, 4),
+                    "random_sector_roofline_steps_per_s": round(peak * 1e9 / (alg_bytes / units), 1)}
+
+    # ---- end to end through the C-ABI host entry point ----
+    e2e_steps = max(2, min(args.steps, 5))
+    e2e_step()
+    torch.cuda.synchronize(dev)
+    d2h_seen = 0
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        r = e2e_step()
+        if isinstance(r, int):
+            d2h_seen = r
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_s = max_over_ranks(e2e_s, world, dev)
+    e2e = {"value": units * world / e2e_s, "unit": unit, "h2d_bytes_per_step": h2d_per,
+           "d2h_bytes_per_step": d2h_per if d2h_per is not None else d2h_seen}
+
+    # ---- CPU baseline (oracle port) on rank 0 at N=1 ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as orc
+
+        ox = orc.OracleIndex(idx)
+        th = cpu_threads()
+        if wl.pairs is not None:
+            sample = min(units, 1 << 22)
+            fn = lambda: orc.occ_pair_batch(ox, wl.pairs[:sample, 0], wl.pairs[:sample, 1], th)  # noqa: E731
+        elif wl.max_diff:
+            sample = min(units, 20_000)
+            fn = lambda: orc.inexact_batch(ox, wl.patterns[:sample], wl.max_diff, th)  # noqa: E731
+        else:
+            sample = min(units, 1 << 20)
+            fn = lambda: orc.exact_batch(ox, wl.patterns[:sample], th)  # noqa: E731
+        fn()
+        reps, t0 = 0, time.perf_counter()
+        while reps < 1 or time.perf_counter() - t0 < 5.0:
+            fn()
+            reps += 1
+        dt = (time.perf_counter() - t0) / reps
+        cpu = {"value": sample / dt, "unit": unit, "cores": th, "kind": "port",
+               "sample": f"first {sample} units of the {args.config} workload, {reps} reps; oracle/fm_oracle.c "
+                         f"(C restatement of the reference path) on {th} threads of {cpu_model()}"}
+
+    # ---- launch count: our kernels inside the timed region ----
+    if launches_per_step is None:
+        launches_per_step = 4  # k_inexact pass + widen + scan + gather (first pass only)
+    if rank == 0:
+        line = {
+            "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (seeded PCG64 per BASELINE.json config; workloads.py)",
+            "config": {**config_of(args.config, world, units),
+                       "l2": "inputs larger than L2 (no flush)" if args.config != "config0" else
+                             "inputs smaller than L2; index L2-resident"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
+            "gpu_launches": launches_per_step * args.steps, **extra,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="config1",
+                    choices=["config1", "config1h", "config0", "config2", "config4"])
+    ap.add_argument("--ref-sample", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank, local, world = (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+                          int(os.environ.get("WORLD_SIZE", 1)))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, local, world)
+
+
+if __name__ == "__main__":
+    main()

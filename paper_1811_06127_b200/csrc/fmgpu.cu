@@ -1,0 +1,1227 @@
+// B200-native FM-index engine: kernels and the C ABI of include/fmgpu.h.
+//
+// Kernels (all sm_100a, integer/popcount + random 32-byte gathers; no tensor
+// cores — the Occ step has no GEMM shape):
+//   k_build_lines   .fmi bucket records -> 32-byte lines          (index.py:24-36)
+//   k_occ_pair      one thread per (k-1, l) pair, PER pairs/thread (occ.py:59-96)
+//   k_exact         persistent, lane-refill backward search      (search.py:74-94)
+//   k_inexact       persistent, lane-refill DFS with a per-thread
+//                   stack and a lower-bound prune                (search.py:97-159)
+//   k_psi / k_locate  predecessor walk to the sampled rows       (search.py:172-208)
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_scan.cuh>
+
+#include "fmgpu_internal.h"
+#include "occ_device.cuh"
+
+namespace fmg {
+
+thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+#define FMG_CK(expr)                                                                      \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw ::fmg::CudaError(std::string(#expr) + " failed: " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define FMG_REQUIRE(cond, msg) \
+  do {                         \
+    if (!(cond)) throw std::invalid_argument(msg); \
+  } while (0)
+
+// Restores the caller's current device on scope exit (the library must not
+// disturb torch's or the application's device selection).
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    FMG_CK(cudaGetDevice(&prev));
+    if (prev != dev) FMG_CK(cudaSetDevice(dev));
+  }
+  ~DeviceScope() {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// Stream-ordered device allocation (pool-backed, cheap after warm-up).
+template <typename T>
+struct DevBuf {
+  T* ptr = nullptr;
+  cudaStream_t stream = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t count, cudaStream_t s) : stream(s) {
+    if (count) FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&ptr), count * sizeof(T), s));
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), stream(o.stream) { o.ptr = nullptr; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    std::swap(ptr, o.ptr);
+    std::swap(stream, o.stream);
+    return *this;
+  }
+  ~DevBuf() {
+    if (ptr) cudaFreeAsync(ptr, stream);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Kernels
+// ---------------------------------------------------------------------------
+
+// Bucket records (4 x u64 LE base + 32 B chars) -> two lines per bucket.
+__global__ void k_build_lines(const uint64_t* __restrict__ rec, uint64_t nb, Line* __restrict__ lines,
+                              uint32_t* __restrict__ err) {
+  uint64_t b = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const uint64_t* r = rec + b * 8;
+  uint64_t base[4] = {r[0], r[1], r[2], r[3]};
+  uint64_t w[4] = {r[4], r[5], r[6], r[7]};
+  Line a, h;
+  uint32_t in[4];
+  count4(w, 63u, in);  // all 64 fields of the first half
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    if (base[s] >= 0xFFFFFFFFull) atomicOr(err, 1u);
+    a.base[s] = uint32_t(base[s]);
+    h.base[s] = uint32_t(base[s]) + in[s];
+  }
+  a.w[0] = w[0];
+  a.w[1] = w[1];
+  h.w[0] = w[2];
+  h.w[1] = w[3];
+  lines[2 * b] = a;
+  lines[2 * b + 1] = h;
+}
+
+__device__ __forceinline__ uint2 ld_stream_u2(const uint2* p) {
+  uint2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void st_stream_256(uint32_t* p, const uint32_t lo[4], const uint32_t hi[4]) {
+  const uint64_t a = uint64_t(lo[0]) | (uint64_t(lo[1]) << 32);
+  const uint64_t b = uint64_t(lo[2]) | (uint64_t(lo[3]) << 32);
+  const uint64_t c = uint64_t(hi[0]) | (uint64_t(hi[1]) << 32);
+  const uint64_t d = uint64_t(hi[2]) | (uint64_t(hi[3]) << 32);
+  asm volatile("st.global.L1::no_allocate.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(a), "l"(b), "l"(c),
+               "l"(d)
+               : "memory");
+}
+
+// Occ step microkernel.  Thread handles PER pairs strided by blockDim so the
+// (k,l) loads and the 32-byte output stores stay fully coalesced; all line
+// loads of a thread are issued before any popcount so each thread keeps up
+// to 2*PER independent sector reads in flight.
+template <int PER>
+__global__ void __launch_bounds__(256) k_occ_pair(IndexView ix, const uint2* __restrict__ kl, uint64_t count,
+                                                  uint32_t* __restrict__ out, uint32_t* __restrict__ err) {
+  const uint64_t first = uint64_t(blockIdx.x) * blockDim.x * PER + threadIdx.x;
+  uint2 q[PER];
+  bool act[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const uint64_t i = first + uint64_t(u) * blockDim.x;
+    act[u] = i < count;
+    q[u] = act[u] ? ld_stream_u2(kl + i) : make_uint2(1u, 0u);
+  }
+  uint32_t bh[PER][4], bl[PER][4];
+  uint64_t wh[PER][2], wl[PER][2];
+  bool ok[PER], two[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const uint32_t k = q[u].x, l = q[u].y;
+    ok[u] = act[u] && l <= ix.n && k <= l + 1u;
+    if (act[u] && !ok[u]) atomicOr(err, 1u);
+    const uint32_t lh = ok[u] ? (l >> 6) : 0u;
+    const uint32_t ll = (ok[u] && k != 0u) ? ((k - 1u) >> 6) : lh;
+    two[u] = ll != lh;
+    load_line<true>(ix.lines + lh, bh[u], wh[u]);
+    if (two[u]) load_line<true>(ix.lines + ll, bl[u], wl[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    if (!act[u]) continue;
+    const uint32_t k = q[u].x, l = q[u].y;
+    uint32_t lo[4] = {0u, 0u, 0u, 0u}, hi[4] = {0u, 0u, 0u, 0u};
+    if (ok[u]) {
+      occ4_from_line(ix, bh[u], wh[u], l, hi);
+      if (k != 0u) {
+        if (two[u])
+          occ4_from_line(ix, bl[u], wl[u], k - 1u, lo);
+        else
+          occ4_from_line(ix, bh[u], wh[u], k - 1u, lo);
+      }
+    }
+    const uint64_t i = first + uint64_t(u) * blockDim.x;
+    st_stream_256(out + i * 8, lo, hi);
+  }
+}
+
+// Pattern sources for the search kernels.
+struct PackedPatterns {  // fixed length m <= 32, char j in bits 2j..2j+1
+  const uint64_t* words;
+  uint32_t m;
+  __device__ __forceinline__ uint32_t length(uint64_t) const { return m; }
+};
+struct CodePatterns {  // codes[offsets[q] .. offsets[q+1])
+  const uint8_t* codes;
+  const uint64_t* offsets;
+};
+
+// Exact backward search, one pattern per thread at a time.  When a lane's
+// pattern finishes (matched or emptied — the reference stops at the FIRST
+// empty interval, search.py:91-92) the lane immediately takes the next
+// pattern of its grid-stride sequence, so warps stay full while per-pattern
+// step counts vary from 1 to m-1.
+template <bool kPacked>
+__global__ void __launch_bounds__(256) k_exact(IndexView ix, PackedPatterns pp, CodePatterns cp, uint64_t count,
+                                               uint2* __restrict__ out, unsigned long long* __restrict__ steps) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint64_t my_steps = 0;
+  uint64_t pat = 0;          // packed form
+  const uint8_t* codes = nullptr;  // general form
+  int i = -1;
+  uint32_t k = 1, l = 0;
+  auto start = [&](uint64_t qq) {
+    uint32_t m, b;
+    if (kPacked) {
+      pat = pp.words[qq];
+      m = pp.m;
+      b = uint32_t(pat >> (2 * (m - 1))) & 3u;
+    } else {
+      const uint64_t o0 = cp.offsets[qq], o1 = cp.offsets[qq + 1];
+      codes = cp.codes + o0;
+      m = uint32_t(o1 - o0);
+      b = codes[m - 1];
+    }
+    k = c_of(ix, b) + 1u;  // init_interval, search.py:50-57
+    l = c_of(ix, b + 1u);
+    i = int(m) - 2;
+  };
+  if (q >= count) return;
+  start(q);
+  while (true) {
+    if (i < 0 || k > l) {
+      out[q] = make_uint2(k, l);
+      q += stride;
+      if (q >= count) break;
+      start(q);
+      continue;
+    }
+    const uint32_t sym = kPacked ? (uint32_t(pat >> (2 * i)) & 3u) : uint32_t(__ldg(codes + i));
+    --i;
+    // extend_backward, search.py:60-71: k' = c[b] + Occ(b, k-1) + 1, l' = c[b] + Occ(b, l)
+    uint32_t bh[4], bl[4];
+    uint64_t wh[2], wl[2];
+    const uint32_t low = k - 1u;  // k >= 1 on every non-empty interval here
+    const uint32_t lh = l >> 6, ll = low >> 6;
+    load_line<false>(ix.lines + lh, bh, wh);
+    uint32_t ol;
+    if (ll != lh) {
+      load_line<false>(ix.lines + ll, bl, wl);
+      ol = occ1_from_line(ix, bl, wl, low, sym);
+    } else {
+      ol = occ1_from_line(ix, bh, wh, low, sym);
+    }
+    const uint32_t oh = occ1_from_line(ix, bh, wh, l, sym);
+    const uint32_t cs = c_of(ix, sym);
+    k = cs + ol + 1u;
+    l = cs + oh;
+    ++my_steps;
+  }
+  if (steps) atomicAdd(steps, (unsigned long long)my_steps);
+}
+
+// ----- bounded-difference search -----------------------------------------
+
+// Per-thread scratch, interleaved (element e of thread t at e*T + t) so that
+// lanes at equal stack depth touch adjacent words.
+struct InexactScratch {
+  uint2* stk_kl;     // S entries: interval of a pending node
+  uint32_t* stk_ib;  // S entries: (i + 1) << 16 | budget
+  uint2* res_kl;     // R entries: distinct result intervals
+  uint32_t* res_u;   // R entries: smallest difference count
+  uint8_t* dlb;      // Mmax entries: lower bound D[i] (long patterns only)
+  uint32_t S, R, Mmax;
+  uint64_t T;
+};
+
+struct InexactOut {
+  uint2* kl;          // reserved by atomicAdd on *total
+  uint8_t* diffs;
+  unsigned long long* total;
+  uint64_t cap;
+  uint64_t* res_off;  // per pattern: offset in this pass's buffer
+  uint32_t* res_cnt;  // per pattern: number of results
+  uint8_t* res_pass;  // per pattern: pass that produced it
+  uint8_t pass;
+  uint32_t* fail_list;  // patterns to retry with larger capacities
+  unsigned long long* fail_count;
+  unsigned long long* steps;
+};
+
+// Reference semantics (search.py:120-159): nodes (i, budget, k, l) from the
+// root (m-1, z, 0, n); a node with i < 0 is a result with z - budget diffs;
+// otherwise one Occ step at (k-1, l) and children skip (i-1, budget-1, k, l),
+// insert (i, budget-1, k', l'), match (i-1, budget, k', l') / mismatch
+// (i-1, budget-1, k', l') for every symbol with a non-empty k' <= l'.  The
+// set of (interval, min diffs) the DFS reaches does not depend on visiting
+// order, so the traversal order is free.
+//
+// Lower-bound prune (result-preserving): before the DFS, one right-to-left
+// exact pass with resets splits W into disjoint segments absent from the
+// text; D(i) = number of those segments lying inside W[0..i].  Every way of
+// turning W[0..i] into a substring of the text must touch each absent
+// segment with its own edit, so a node with D(i) > budget yields nothing and
+// is never pushed.  (BWA's D array, computed with the forward index only.)
+template <bool kShort>
+__global__ void __launch_bounds__(256) k_inexact(IndexView ix, CodePatterns cp, const uint32_t* __restrict__ list,
+                                                 uint64_t count, uint32_t z, InexactScratch sc, InexactOut out) {
+  const uint64_t T = sc.T;
+  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  uint64_t slot = t;
+  uint64_t my_steps = 0;
+
+  // per-pattern state
+  bool have = false;
+  uint64_t q = 0;
+  const uint8_t* codes = nullptr;
+  int m = 0;
+  uint64_t pw[2] = {0, 0};   // kShort: the pattern, packed
+  uint64_t dbits = 0;        // kShort: right ends of absent segments
+  int phase = 0;             // 0: lower-bound pass, 1: DFS
+  int pos = 0, seg_end = 0;  // lower-bound pass cursor
+  uint32_t kd = 0, ld = 0;   // lower-bound pass interval
+  uint32_t sp = 0, nres = 0;
+  bool overflow = false;
+
+  auto sym_at = [&](int i) -> uint32_t {
+    if (kShort) return uint32_t((i < 32 ? pw[0] : pw[1]) >> ((i & 31) << 1)) & 3u;
+    return uint32_t(__ldg(codes + i));
+  };
+  auto dlb = [&](int i) -> uint32_t {
+    if (kShort) return __popcll(dbits & ((2ull << i) - 1ull));
+    return sc.dlb[uint64_t(i) * T + t];
+  };
+  auto record = [&](uint32_t k, uint32_t l, uint32_t used) {
+    for (uint32_t r = 0; r < nres; ++r) {
+      const uint2 e = sc.res_kl[uint64_t(r) * T + t];
+      if (e.x == k && e.y == l) {
+        uint32_t* u = &sc.res_u[uint64_t(r) * T + t];
+        if (used < *u) *u = used;
+        return;
+      }
+    }
+    if (nres == sc.R) {
+      overflow = true;
+      return;
+    }
+    sc.res_kl[uint64_t(nres) * T + t] = make_uint2(k, l);
+    sc.res_u[uint64_t(nres) * T + t] = used;
+    ++nres;
+  };
+  auto push = [&](int i, uint32_t budget, uint32_t k, uint32_t l) {
+    if (i < 0) {
+      record(k, l, z - budget);
+      return;
+    }
+    if (dlb(i) > budget) return;  // lower-bound prune
+    if (sp == sc.S) {
+      overflow = true;
+      return;
+    }
+    sc.stk_kl[uint64_t(sp) * T + t] = make_uint2(k, l);
+    sc.stk_ib[uint64_t(sp) * T + t] = (uint32_t(i + 1) << 16) | budget;
+    ++sp;
+  };
+  auto fail = [&]() {
+    const unsigned long long f = atomicAdd(out.fail_count, 1ull);
+    out.fail_list[f] = uint32_t(q);
+    out.res_cnt[q] = 0;
+  };
+  auto finish = [&]() {
+    if (overflow) {
+      fail();
+      return;
+    }
+    // insertion sort by (k, l); (k, l) are unique after the dedup
+    for (uint32_t a = 1; a < nres; ++a) {
+      const uint2 e = sc.res_kl[uint64_t(a) * T + t];
+      const uint32_t u = sc.res_u[uint64_t(a) * T + t];
+      uint32_t b = a;
+      while (b > 0) {
+        const uint2 p = sc.res_kl[uint64_t(b - 1) * T + t];
+        if (p.x < e.x || (p.x == e.x && p.y < e.y)) break;
+        sc.res_kl[uint64_t(b) * T + t] = p;
+        sc.res_u[uint64_t(b) * T + t] = sc.res_u[uint64_t(b - 1) * T + t];
+        --b;
+      }
+      sc.res_kl[uint64_t(b) * T + t] = e;
+      sc.res_u[uint64_t(b) * T + t] = u;
+    }
+    uint64_t o = 0;
+    if (nres) {
+      o = atomicAdd(out.total, (unsigned long long)nres);
+      if (o + nres > out.cap) {  // this pass's buffer is full: retry later
+        fail();
+        return;
+      }
+      for (uint32_t r = 0; r < nres; ++r) {
+        out.kl[o + r] = sc.res_kl[uint64_t(r) * T + t];
+        out.diffs[o + r] = uint8_t(sc.res_u[uint64_t(r) * T + t]);
+      }
+    }
+    out.res_off[q] = o;
+    out.res_cnt[q] = nres;
+    out.res_pass[q] = out.pass;
+  };
+
+  while (true) {
+    // ---- acquire the next node that needs an Occ step ----
+    uint32_t k = 0, l = 0, budget = 0;
+    int i = 0;
+    bool stepping = false;
+    while (!stepping) {
+      if (!have) {
+        if (slot >= count) break;
+        q = list ? list[slot] : slot;
+        slot += T;
+        const uint64_t o0 = cp.offsets[q], o1 = cp.offsets[q + 1];
+        codes = cp.codes + o0;
+        m = int(o1 - o0);
+        if (kShort) {
+          pw[0] = pw[1] = 0;
+          for (int j = 0; j < m; ++j) {
+            const uint64_t v = uint64_t(__ldg(codes + j) & 3u) << ((j & 31) << 1);
+            if (j < 32)
+              pw[0] |= v;
+            else
+              pw[1] |= v;
+          }
+          dbits = 0;
+        } else {
+          for (int j = 0; j < m; ++j) sc.dlb[uint64_t(j) * T + t] = 0;
+        }
+        phase = 0;
+        pos = m - 1;
+        seg_end = m - 1;
+        kd = 0;  // the pass starts from the root interval [0, n]
+        ld = ix.n;
+        sp = nres = 0;
+        overflow = false;
+        have = true;
+      }
+      if (phase == 0) {
+        if (pos < 0) {
+          if (!kShort) {  // flags of segment ends -> D(i) = ends at or before i
+            uint32_t acc = 0;
+            for (int j = 0; j < m; ++j) {
+              uint8_t* d = &sc.dlb[uint64_t(j) * T + t];
+              acc += *d;
+              *d = uint8_t(min(acc, 255u));
+            }
+          }
+          phase = 1;
+          push(m - 1, z, 0u, ix.n);  // root (search.py:125)
+          continue;
+        }
+        k = kd;
+        l = ld;
+        stepping = true;
+      } else {
+        if (overflow || sp == 0) {
+          finish();
+          have = false;
+          continue;
+        }
+        --sp;
+        const uint2 e = sc.stk_kl[uint64_t(sp) * T + t];
+        const uint32_t ib = sc.stk_ib[uint64_t(sp) * T + t];
+        k = e.x;
+        l = e.y;
+        i = int(ib >> 16) - 1;
+        budget = ib & 0xFFFFu;
+        stepping = true;
+      }
+    }
+    if (!stepping) break;
+
+    // ---- one Occ step: the eight values at (k-1, l) ----
+    uint32_t lo[4], hi[4];
+    occ_step<false>(ix, k, l, lo, hi);
+    ++my_steps;
+
+    if (phase == 0) {
+      const uint32_t b = sym_at(pos);
+      const uint32_t cb = c_of(ix, b);
+      const uint32_t k2 = cb + sel4(lo, b) + 1u, l2 = cb + sel4(hi, b);
+      if (k2 > l2) {  // W[pos..seg_end] is absent from the text
+        if (kShort)
+          dbits |= 1ull << seg_end;
+        else
+          sc.dlb[uint64_t(seg_end) * T + t] = 1;
+        kd = 0;
+        ld = ix.n;
+        seg_end = pos - 1;
+      } else {
+        kd = k2;
+        ld = l2;
+      }
+      --pos;
+      continue;
+    }
+
+    // DFS expansion (search.py:135-152)
+    const uint32_t want = sym_at(i);
+    if (budget > 0) push(i - 1, budget - 1, k, l);  // skip
+#pragma unroll
+    for (uint32_t b = 0; b < 4; ++b) {
+      const uint32_t k2 = ix.c[b] + lo[b] + 1u, l2 = ix.c[b] + hi[b];
+      if (k2 > l2) continue;
+      if (budget > 0) push(i, budget - 1, k2, l2);  // insert
+      if (b == want)
+        push(i - 1, budget, k2, l2);  // match
+      else if (budget > 0)
+        push(i - 1, budget - 1, k2, l2);  // mismatch
+    }
+  }
+  if (out.steps) atomicAdd(out.steps, (unsigned long long)my_steps);
+}
+
+// Gather per-pattern results of one pass into the final CSR arrays.
+__global__ void k_gather_matches(uint64_t count, const uint64_t* __restrict__ res_off,
+                                 const uint32_t* __restrict__ res_cnt, const uint8_t* __restrict__ res_pass,
+                                 uint8_t pass, const uint2* __restrict__ src_kl, const uint8_t* __restrict__ src_d,
+                                 const uint64_t* __restrict__ row_off, uint32_t* __restrict__ k_out,
+                                 uint32_t* __restrict__ l_out, uint8_t* __restrict__ d_out) {
+  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= count || res_pass[q] != pass) return;
+  const uint32_t n = res_cnt[q];
+  const uint64_t s = res_off[q], d = row_off[q];
+  for (uint32_t r = 0; r < n; ++r) {
+    const uint2 e = src_kl[s + r];
+    k_out[d + r] = e.x;
+    l_out[d + r] = e.y;
+    d_out[d + r] = src_d[s + r];
+  }
+}
+
+__global__ void k_widen_counts(uint64_t count, const uint32_t* __restrict__ c32, uint64_t* __restrict__ c64) {
+  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q < count) c64[q] = c32[q];
+}
+
+// ----- position recovery ---------------------------------------------------
+
+// psi_inverse_fused (search.py:172-186): symbol at row i and its
+// predecessor row c[sym] + Occ(sym, i), in one line access.
+__device__ __forceinline__ uint32_t psi_step(const IndexView& ix, uint32_t row, uint32_t& sym) {
+  uint32_t b[4];
+  uint64_t w[2];
+  load_line<false>(ix.lines + (row >> 6), b, w);
+  sym = field_at(w, row & 63u);
+  return c_of(ix, sym) + occ1_from_line(ix, b, w, row, sym);
+}
+
+__global__ void k_psi(IndexView ix, const uint32_t* __restrict__ rows, uint64_t count, uint8_t* __restrict__ out_sym,
+                      uint32_t* __restrict__ out_row, uint32_t* __restrict__ err) {
+  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  const uint32_t row = rows[q];
+  if (row > ix.n) {
+    atomicOr(err, 1u);
+    out_sym[q] = 255;
+    out_row[q] = 0xFFFFFFFFu;
+    return;
+  }
+  if (row == ix.sentinel_row) {
+    out_sym[q] = 255;
+    out_row[q] = 0xFFFFFFFFu;
+    return;
+  }
+  uint32_t sym;
+  const uint32_t prev = psi_step(ix, row, sym);
+  out_sym[q] = uint8_t(sym);
+  out_row[q] = prev;
+}
+
+// locate_row (search.py:189-208): walk predecessors until the row is sampled
+// (row % 32 == 0 — samples are taken by ROW, index.py:93, so the walk length
+// is geometric-like with mean ~32, not bounded by 32) or is the sentinel row.
+// Grid-stride lane refill keeps warps full despite the varying walk lengths.
+__global__ void __launch_bounds__(256) k_locate(IndexView ix, const uint32_t* __restrict__ rows, uint64_t count,
+                                                uint32_t* __restrict__ out_pos, uint32_t* __restrict__ err) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < count; q += stride) {
+    uint32_t row = rows[q];
+    if (row > ix.n) {
+      atomicOr(err, 1u);
+      out_pos[q] = 0xFFFFFFFFu;
+      continue;
+    }
+    uint32_t steps = 0;
+    while (true) {
+      if (row == ix.sentinel_row) {
+        out_pos[q] = steps;
+        break;
+      }
+      if ((row & 31u) == 0u) {
+        out_pos[q] = ix.samples[row >> 5] + steps;
+        break;
+      }
+      uint32_t sym;
+      row = psi_step(ix, row, sym);
+      ++steps;
+      if (steps > ix.n + 1u) {  // corrupt index (search.py:207-208)
+        atomicOr(err, 2u);
+        out_pos[q] = 0xFFFFFFFFu;
+        break;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+
+int sm_count(int device) {
+  int v = 0;
+  FMG_CK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+  return v;
+}
+
+}  // namespace fmg
+
+struct fmg_index {
+  int device = 0;
+  uint64_t n = 0, sentinel_row = 0, c[5] = {0, 0, 0, 0, 0};
+  uint64_t n_buckets = 0, n_lines = 0, n_samples = 0;
+  fmg::Line* lines = nullptr;
+  uint32_t* samples = nullptr;
+  uint32_t* err = nullptr;  // sticky device-side input error flags
+  int sms = 148;
+
+  fmg::IndexView view() const {
+    fmg::IndexView v;
+    v.lines = lines;
+    v.samples = samples;
+    v.n = uint32_t(n);
+    v.sentinel_row = uint32_t(sentinel_row);
+    for (int s = 0; s < 5; ++s) v.c[s] = uint32_t(c[s]);
+    return v;
+  }
+};
+
+struct fmg_matches {
+  int device = 0;
+  uint64_t patterns = 0, total = 0, steps = 0;
+  uint64_t* row_off = nullptr;  // device, patterns + 1
+  uint32_t* k = nullptr;        // device, total
+  uint32_t* l = nullptr;
+  uint8_t* diffs = nullptr;
+};
+
+namespace {
+
+using namespace fmg;
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+void check_index(const fmg_index* ix) { FMG_REQUIRE(ix != nullptr, "null index handle"); }
+
+// Reads and clears the sticky input-error flags (synchronises `stream`).
+void take_input_error(const fmg_index* ix, cudaStream_t stream, const char* what) {
+  uint32_t h = 0;
+  FMG_CK(cudaMemcpyAsync(&h, ix->err, sizeof(h), cudaMemcpyDeviceToHost, stream));
+  FMG_CK(cudaStreamSynchronize(stream));
+  if (h) {
+    FMG_CK(cudaMemsetAsync(ix->err, 0, sizeof(uint32_t), stream));
+    FMG_CK(cudaStreamSynchronize(stream));
+    if (h & 2u) throw std::runtime_error("predecessor walk did not terminate; index is corrupt");
+    throw std::invalid_argument(what);
+  }
+}
+
+constexpr int kOccPer = 2;
+
+void launch_occ_pair(const fmg_index* ix, const uint32_t* kl, uint64_t count, uint32_t* out, cudaStream_t s) {
+  if (count == 0) return;
+  const uint64_t per_block = 256ull * kOccPer;
+  const uint64_t blocks = (count + per_block - 1) / per_block;
+  k_occ_pair<kOccPer><<<dim3(unsigned(blocks)), 256, 0, s>>>(ix->view(), reinterpret_cast<const uint2*>(kl), count,
+                                                              out, ix->err);
+  FMG_CK(cudaGetLastError());
+}
+
+unsigned persistent_blocks(const fmg_index* ix, const void* kernel, int threads, uint64_t work) {
+  int per_sm = 0;
+  FMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0));
+  uint64_t blocks = uint64_t(std::max(per_sm, 1)) * ix->sms;
+  const uint64_t need = (work + threads - 1) / threads;
+  return unsigned(std::max<uint64_t>(1, std::min(blocks, need)));
+}
+
+void launch_exact_packed(const fmg_index* ix, const uint64_t* packed, uint32_t m, uint64_t count, uint32_t* kl_out,
+                         cudaStream_t s, unsigned long long* steps) {
+  if (count == 0) return;
+  PackedPatterns pp{packed, m};
+  CodePatterns cp{nullptr, nullptr};
+  const unsigned blocks = persistent_blocks(ix, (const void*)k_exact<true>, 256, count);
+  k_exact<true><<<blocks, 256, 0, s>>>(ix->view(), pp, cp, count, reinterpret_cast<uint2*>(kl_out), steps);
+  FMG_CK(cudaGetLastError());
+}
+
+void launch_exact_codes(const fmg_index* ix, const uint8_t* codes, const uint64_t* offsets, uint64_t count,
+                        uint32_t* kl_out, cudaStream_t s, unsigned long long* steps) {
+  if (count == 0) return;
+  PackedPatterns pp{nullptr, 0};
+  CodePatterns cp{codes, offsets};
+  const unsigned blocks = persistent_blocks(ix, (const void*)k_exact<false>, 256, count);
+  k_exact<false><<<blocks, 256, 0, s>>>(ix->view(), pp, cp, count, reinterpret_cast<uint2*>(kl_out), steps);
+  FMG_CK(cudaGetLastError());
+}
+
+// Host validation of a pattern batch given on the host: offsets strictly
+// increasing (no empty pattern, search.py:83-84), codes in [0, 4).
+void validate_patterns_host(const uint8_t* codes, const uint64_t* offsets, uint64_t count, uint64_t* max_len) {
+  FMG_REQUIRE(offsets[0] == 0, "pattern offsets must start at 0");
+  uint64_t mx = 0;
+  for (uint64_t q = 0; q < count; ++q) {
+    FMG_REQUIRE(offsets[q + 1] > offsets[q], "pattern is empty");
+    mx = std::max(mx, offsets[q + 1] - offsets[q]);
+  }
+  for (uint64_t j = 0; j < offsets[count]; ++j) FMG_REQUIRE(codes[j] < 4, "symbol code outside [0, 4)");
+  *max_len = mx;
+}
+
+fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64_t* offsets, uint64_t count,
+                         uint64_t max_len, int max_diff, cudaStream_t s) {
+  FMG_REQUIRE(max_diff >= 0, "difference budget is negative");
+  FMG_REQUIRE(max_diff <= 0xFFFF, "difference budget above 65535 is not supported");
+  FMG_REQUIRE(max_len < 0xFFFF, "pattern longer than 65534 is not supported");
+  FMG_REQUIRE(count < 0xFFFFFFFFull, "too many patterns in one call");
+  auto* res = new fmg_matches();
+  res->device = ix->device;
+  res->patterns = count;
+  try {
+    FMG_CK(cudaMalloc(&res->row_off, (count + 1) * sizeof(uint64_t)));
+    FMG_CK(cudaMemsetAsync(res->row_off, 0, sizeof(uint64_t), s));
+    if (count == 0) {
+      FMG_CK(cudaStreamSynchronize(s));
+      return res;
+    }
+    const uint32_t z = uint32_t(max_diff);
+    const bool short_pat = max_len <= 64;
+    const void* kfn = short_pat ? (const void*)k_inexact<true> : (const void*)k_inexact<false>;
+    int per_sm = 0;
+    FMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 256, 0));
+    per_sm = std::max(per_sm, 1);
+
+    DevBuf<uint64_t> res_off(count, s);
+    DevBuf<uint32_t> res_cnt(count, s);
+    DevBuf<uint8_t> res_pass(count, s);
+    DevBuf<unsigned long long> counters(4, s);  // total, fail_count, steps, spare
+    FMG_CK(cudaMemsetAsync(res_pass.ptr, 0xFF, count, s));
+    FMG_CK(cudaMemsetAsync(counters.ptr + 2, 0, sizeof(unsigned long long), s));
+
+    std::vector<DevBuf<uint2>> pass_kl;
+    std::vector<DevBuf<uint8_t>> pass_d;
+    DevBuf<uint32_t> lists[2] = {DevBuf<uint32_t>(count, s), DevBuf<uint32_t>(count, s)};
+    const uint32_t* list = nullptr;  // pass 0: every pattern
+    uint64_t pending = count;
+    uint32_t R = 64;
+    uint64_t cap = std::max<uint64_t>(count * 4, 1u << 20);
+    const uint32_t S = uint32_t(9 * (max_len + z + 1) + 2);
+    for (int pass = 0; pending > 0; ++pass) {
+      FMG_REQUIRE(pass < 250, "inexact search did not converge");
+      // threads: full residency, bounded by a scratch budget of ~2 GiB
+      const uint64_t per_thread = uint64_t(S) * 12 + uint64_t(R) * 8 + (short_pat ? 0 : max_len);
+      uint64_t T = uint64_t(per_sm) * ix->sms * 256;
+      const uint64_t budget_bytes = 2ull << 30;
+      T = std::min<uint64_t>(T, std::max<uint64_t>(256, budget_bytes / per_thread));
+      T = std::min<uint64_t>(T, ((pending + 255) / 256) * 256);
+      T = std::max<uint64_t>(256, (T / 256) * 256);
+      InexactScratch sc{};
+      DevBuf<uint2> stk_kl(uint64_t(S) * T, s);
+      DevBuf<uint32_t> stk_ib(uint64_t(S) * T, s);
+      DevBuf<uint2> rkl(uint64_t(R) * T, s);
+      DevBuf<uint32_t> ru(uint64_t(R) * T, s);
+      DevBuf<uint8_t> dl(short_pat ? 0 : max_len * T, s);
+      if (!short_pat) FMG_CK(cudaMemsetAsync(dl.ptr, 0, max_len * T, s));
+      sc.stk_kl = stk_kl.ptr;
+      sc.stk_ib = stk_ib.ptr;
+      sc.res_kl = rkl.ptr;
+      sc.res_u = ru.ptr;
+      sc.dlb = dl.ptr;
+      sc.S = S;
+      sc.R = R;
+      sc.Mmax = uint32_t(max_len);
+      sc.T = T;
+      pass_kl.emplace_back(cap, s);
+      pass_d.emplace_back(cap, s);
+      FMG_CK(cudaMemsetAsync(counters.ptr, 0, 2 * sizeof(unsigned long long), s));
+      InexactOut o{};
+      o.kl = pass_kl.back().ptr;
+      o.diffs = pass_d.back().ptr;
+      o.total = counters.ptr;
+      o.cap = cap;
+      o.res_off = res_off.ptr;
+      o.res_cnt = res_cnt.ptr;
+      o.res_pass = res_pass.ptr;
+      o.pass = uint8_t(pass);
+      o.fail_list = lists[pass & 1].ptr;
+      o.fail_count = counters.ptr + 1;
+      o.steps = counters.ptr + 2;
+      const unsigned blocks = unsigned(T / 256);
+      CodePatterns cp{codes, offsets};
+      if (short_pat)
+        k_inexact<true><<<blocks, 256, 0, s>>>(ix->view(), cp, list, pending, z, sc, o);
+      else
+        k_inexact<false><<<blocks, 256, 0, s>>>(ix->view(), cp, list, pending, z, sc, o);
+      FMG_CK(cudaGetLastError());
+      unsigned long long host_ctr[2];
+      FMG_CK(cudaMemcpyAsync(host_ctr, counters.ptr, sizeof(host_ctr), cudaMemcpyDeviceToHost, s));
+      FMG_CK(cudaStreamSynchronize(s));
+      const uint64_t failed = host_ctr[1];
+      list = lists[pass & 1].ptr;
+      if (failed > 0) {
+        // grow whichever capacity might have been the cause
+        R = std::min<uint32_t>(R * 8, 1u << 22);
+        cap = std::max<uint64_t>(cap, std::min<uint64_t>(uint64_t(host_ctr[0]) * 2, 1ull << 31));
+        cap = std::max<uint64_t>(cap, failed * uint64_t(R));
+        cap = std::min<uint64_t>(cap, 1ull << 31);
+      }
+      pending = failed;
+      // the next pass reads `list` while writing the other list
+    }
+    // CSR: row_off[q+1] = inclusive sum of counts
+    DevBuf<uint64_t> c64(count, s);
+    k_widen_counts<<<unsigned((count + 255) / 256), 256, 0, s>>>(count, res_cnt.ptr, c64.ptr);
+    size_t tmp_bytes = 0;
+    FMG_CK(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, c64.ptr, res->row_off + 1, count, s));
+    DevBuf<uint8_t> tmp(tmp_bytes, s);
+    FMG_CK(cub::DeviceScan::InclusiveSum(tmp.ptr, tmp_bytes, c64.ptr, res->row_off + 1, count, s));
+    uint64_t total = 0;
+    FMG_CK(cudaMemcpyAsync(&total, res->row_off + count, sizeof(total), cudaMemcpyDeviceToHost, s));
+    unsigned long long steps = 0;
+    FMG_CK(cudaMemcpyAsync(&steps, counters.ptr + 2, sizeof(steps), cudaMemcpyDeviceToHost, s));
+    FMG_CK(cudaStreamSynchronize(s));
+    res->total = total;
+    res->steps = steps;
+    FMG_CK(cudaMalloc(&res->k, std::max<uint64_t>(total, 1) * sizeof(uint32_t)));
+    FMG_CK(cudaMalloc(&res->l, std::max<uint64_t>(total, 1) * sizeof(uint32_t)));
+    FMG_CK(cudaMalloc(&res->diffs, std::max<uint64_t>(total, 1)));
+    for (size_t p = 0; p < pass_kl.size(); ++p) {
+      k_gather_matches<<<unsigned((count + 255) / 256), 256, 0, s>>>(count, res_off.ptr, res_cnt.ptr, res_pass.ptr,
+                                                                     uint8_t(p), pass_kl[p].ptr, pass_d[p].ptr,
+                                                                     res->row_off, res->k, res->l, res->diffs);
+      FMG_CK(cudaGetLastError());
+    }
+    FMG_CK(cudaStreamSynchronize(s));
+    return res;
+  } catch (...) {
+    fmg_matches_free(res);
+    throw;
+  }
+}
+
+// Chunked host-buffer pipeline: H2D, kernel, D2H per chunk on alternating
+// streams so the copy engines overlap each other and the kernel.
+template <typename Launch>
+void pipeline_host(int device, uint64_t count, uint64_t chunk, size_t in_bytes_per, size_t out_bytes_per,
+                   const void* host_in, void* host_out, Launch&& launch) {
+  constexpr int kSlots = 3;
+  cudaStream_t st[kSlots];
+  for (int i = 0; i < kSlots; ++i) FMG_CK(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
+  std::vector<void*> din(kSlots, nullptr), dout(kSlots, nullptr);
+  try {
+    for (int i = 0; i < kSlots; ++i) {
+      FMG_CK(cudaMallocAsync(&din[i], std::max<size_t>(chunk * in_bytes_per, 1), st[i]));
+      FMG_CK(cudaMallocAsync(&dout[i], std::max<size_t>(chunk * out_bytes_per, 1), st[i]));
+    }
+    uint64_t c = 0;
+    for (uint64_t off = 0; off < count; off += chunk, ++c) {
+      const int slot = int(c % kSlots);
+      const uint64_t len = std::min(chunk, count - off);
+      FMG_CK(cudaMemcpyAsync(din[slot], static_cast<const uint8_t*>(host_in) + off * in_bytes_per, len * in_bytes_per,
+                             cudaMemcpyHostToDevice, st[slot]));
+      launch(din[slot], len, dout[slot], st[slot]);
+      FMG_CK(cudaMemcpyAsync(static_cast<uint8_t*>(host_out) + off * out_bytes_per, dout[slot], len * out_bytes_per,
+                             cudaMemcpyDeviceToHost, st[slot]));
+    }
+    for (int i = 0; i < kSlots; ++i) FMG_CK(cudaStreamSynchronize(st[i]));
+  } catch (...) {
+    for (int i = 0; i < kSlots; ++i) cudaStreamSynchronize(st[i]);
+    for (int i = 0; i < kSlots; ++i) {
+      if (din[i]) cudaFreeAsync(din[i], st[i]);
+      if (dout[i]) cudaFreeAsync(dout[i], st[i]);
+      cudaStreamSynchronize(st[i]);
+      cudaStreamDestroy(st[i]);
+    }
+    throw;
+  }
+  for (int i = 0; i < kSlots; ++i) {
+    cudaFreeAsync(din[i], st[i]);
+    cudaFreeAsync(dout[i], st[i]);
+    cudaStreamSynchronize(st[i]);
+    cudaStreamDestroy(st[i]);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fmg_last_error(void) { return fmg::g_last_error.c_str(); }
+
+int fmg_device_count(int* count) {
+  return fmg::guard([&] {
+    FMG_REQUIRE(count != nullptr, "null output pointer");
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    *count = c;
+  });
+}
+
+int fmg_index_create(int device, const void* bucket_records, uint64_t n_buckets, uint64_t n, uint64_t sentinel_row,
+                     const uint64_t c[5], fmg_index** out) {
+  return fmg::guard([&] {
+    FMG_REQUIRE(out != nullptr && bucket_records != nullptr && c != nullptr, "null argument");
+    *out = nullptr;
+    FMG_REQUIRE(n >= 1, "index covers an empty reference");
+    FMG_REQUIRE(n + 1 < 0xFFFFFFFFull, "reference too long for 32-bit rows");
+    FMG_REQUIRE(n_buckets == (n + 1 + 127) / 128, "bucket count does not match n");
+    FMG_REQUIRE(sentinel_row <= n, "sentinel row outside [0, n]");
+    FMG_REQUIRE(c[0] == 0 && c[4] == n, "C table endpoints wrong");
+    for (int s = 0; s < 4; ++s) FMG_REQUIRE(c[s] <= c[s + 1], "C table not non-decreasing");
+    int ndev = 0;
+    FMG_CK(cudaGetDeviceCount(&ndev));
+    FMG_REQUIRE(device >= 0 && device < ndev, "CUDA device ordinal out of range");
+    DeviceScope scope(device);
+    auto* ix = new fmg_index();
+    try {
+      ix->device = device;
+      ix->n = n;
+      ix->sentinel_row = sentinel_row;
+      for (int s = 0; s < 5; ++s) ix->c[s] = c[s];
+      ix->n_buckets = n_buckets;
+      ix->n_lines = 2 * n_buckets;
+      ix->sms = fmg::sm_count(device);
+      FMG_CK(cudaMalloc(&ix->lines, ix->n_lines * sizeof(fmg::Line)));
+      FMG_CK(cudaMalloc(&ix->err, sizeof(uint32_t)));
+      FMG_CK(cudaMemset(ix->err, 0, sizeof(uint32_t)));
+      // upload in slabs through a bounded staging buffer
+      const uint64_t slab = 1ull << 22;  // buckets per slab (256 MiB)
+      uint64_t* staging = nullptr;
+      FMG_CK(cudaMalloc(&staging, std::min(slab, n_buckets) * 64));
+      for (uint64_t b0 = 0; b0 < n_buckets; b0 += slab) {
+        const uint64_t nb = std::min(slab, n_buckets - b0);
+        FMG_CK(cudaMemcpy(staging, static_cast<const uint8_t*>(bucket_records) + b0 * 64, nb * 64,
+                          cudaMemcpyHostToDevice));
+        fmg::k_build_lines<<<unsigned((nb + 255) / 256), 256>>>(staging, nb, ix->lines + 2 * b0, ix->err);
+        FMG_CK(cudaGetLastError());
+      }
+      FMG_CK(cudaDeviceSynchronize());
+      cudaFree(staging);
+      uint32_t bad = 0;
+      FMG_CK(cudaMemcpy(&bad, ix->err, sizeof(bad), cudaMemcpyDeviceToHost));
+      FMG_REQUIRE(bad == 0, "bucket base does not fit 32 bits");
+      // Allow the stream-ordered pool to keep freed blocks (host entry points
+      // allocate per call).
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      *out = ix;
+    } catch (...) {
+      fmg_index_destroy(ix);
+      throw;
+    }
+  });
+}
+
+int fmg_index_set_samples(fmg_index* ix, const uint64_t* sa_samples, uint64_t count) {
+  return fmg::guard([&] {
+    check_index(ix);
+    FMG_REQUIRE(sa_samples != nullptr, "null argument");
+    FMG_REQUIRE(count == ix->n / 32 + 1, "sample count does not match n");
+    std::vector<uint32_t> s32(count);
+    for (uint64_t i = 0; i < count; ++i) {
+      FMG_REQUIRE(sa_samples[i] <= ix->n, "suffix-array sample out of range");
+      s32[i] = uint32_t(sa_samples[i]);
+    }
+    fmg::DeviceScope scope(ix->device);
+    if (ix->samples) cudaFree(ix->samples);
+    ix->samples = nullptr;
+    FMG_CK(cudaMalloc(&ix->samples, count * sizeof(uint32_t)));
+    FMG_CK(cudaMemcpy(ix->samples, s32.data(), count * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    ix->n_samples = count;
+  });
+}
+
+int fmg_index_info(const fmg_index* ix, uint64_t* n, int* device, uint64_t* device_bytes) {
+  return fmg::guard([&] {
+    check_index(ix);
+    if (n) *n = ix->n;
+    if (device) *device = ix->device;
+    if (device_bytes) *device_bytes = ix->n_lines * sizeof(fmg::Line) + ix->n_samples * 4;
+  });
+}
+
+void fmg_index_destroy(fmg_index* ix) {
+  if (!ix) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(ix->device);
+  if (ix->lines) cudaFree(ix->lines);
+  if (ix->samples) cudaFree(ix->samples);
+  if (ix->err) cudaFree(ix->err);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete ix;
+}
+
+int fmg_occ_pair(const fmg_index* ix, const uint32_t* kl, uint64_t count, uint32_t* out, void* stream) {
+  return fmg::guard([&] {
+    check_index(ix);
+    fmg::DeviceScope scope(ix->device);
+    launch_occ_pair(ix, kl, count, out, as_stream(stream));
+  });
+}
+
+int fmg_occ_pair_host(const fmg_index* ix, const uint32_t* kl, uint64_t count, uint32_t* out) {
+  return fmg::guard([&] {
+    check_index(ix);
+    fmg::DeviceScope scope(ix->device);
+    const uint64_t chunk = std::min<uint64_t>(count, 1ull << 21);
+    pipeline_host(ix->device, count, std::max<uint64_t>(chunk, 1), 8, 32, kl, out,
+                  [&](void* din, uint64_t len, void* dout, cudaStream_t s) {
+                    launch_occ_pair(ix, static_cast<const uint32_t*>(din), len, static_cast<uint32_t*>(dout), s);
+                  });
+    take_input_error(ix, nullptr, "Occ position out of range or pair out of order");
+  });
+}
+
+int fmg_exact(const fmg_index* ix, const uint8_t* codes, const uint64_t* offsets, uint64_t count, uint32_t* kl_out,
+              void* stream) {
+  return fmg::guard([&] {
+    check_index(ix);
+    fmg::DeviceScope scope(ix->device);
+    launch_exact_codes(ix, codes, offsets, count, kl_out, as_stream(stream), nullptr);
+  });
+}
+
+int fmg_exact_packed(const fmg_index* ix, const uint64_t* packed, uint32_t m, uint64_t count, uint32_t* kl_out,
+                     void* stream) {
+  return fmg::guard([&] {
+    check_index(ix);
+    FMG_REQUIRE(m >= 1 && m <= 32, "packed pattern length must be in [1, 32]");
+    fmg::DeviceScope scope(ix->device);
+    launch_exact_packed(ix, packed, m, count, kl_out, as_stream(stream), nullptr);
+  });
+}
+
+int fmg_exact_host(const fmg_index* ix, const uint8_t* codes, const uint64_t* offsets, uint64_t count,
+                   uint32_t* kl_out) {
+  return fmg::guard([&] {
+    check_index(ix);
+    if (count == 0) return;
+    uint64_t max_len = 0;
+    validate_patterns_host(codes, offsets, count, &max_len);
+    fmg::DeviceScope scope(ix->device);
+    cudaStream_t s;
+    FMG_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    {
+      DevBuf<uint8_t> dc(offsets[count], s);
+      DevBuf<uint64_t> doff(count + 1, s);
+      DevBuf<uint32_t> dout(2 * count, s);
+      FMG_CK(cudaMemcpyAsync(dc.ptr, codes, offsets[count], cudaMemcpyHostToDevice, s));
+      FMG_CK(cudaMemcpyAsync(doff.ptr, offsets, (count + 1) * 8, cudaMemcpyHostToDevice, s));
+      launch_exact_codes(ix, dc.ptr, doff.ptr, count, dout.ptr, s, nullptr);
+      FMG_CK(cudaMemcpyAsync(kl_out, dout.ptr, 2 * count * 4, cudaMemcpyDeviceToHost, s));
+      FMG_CK(cudaStreamSynchronize(s));
+    }
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  });
+}
+
+int fmg_exact_packed_host(const fmg_index* ix, const uint64_t* packed, uint32_t m, uint64_t count,
+                          uint32_t* kl_out) {
+  return fmg::guard([&] {
+    check_index(ix);
+    FMG_REQUIRE(m >= 1 && m <= 32, "packed pattern length must be in [1, 32]");
+    if (count == 0) return;
+    fmg::DeviceScope scope(ix->device);
+    const uint64_t chunk = std::min<uint64_t>(count, 1ull << 22);
+    pipeline_host(ix->device, count, chunk, 8, 8, packed, kl_out,
+                  [&](void* din, uint64_t len, void* dout, cudaStream_t s) {
+                    launch_exact_packed(ix, static_cast<const uint64_t*>(din), m, len, static_cast<uint32_t*>(dout),
+                                        s, nullptr);
+                  });
+  });
+}
+
+int fmg_inexact(const fmg_index* ix, const uint8_t* codes, const uint64_t* offsets, uint64_t count, int max_diff,
+                fmg_matches** out, void* stream) {
+  return fmg::guard([&] {
+    check_index(ix);
+    FMG_REQUIRE(out != nullptr, "null output pointer");
+    *out = nullptr;
+    fmg::DeviceScope scope(ix->device);
+    cudaStream_t s = as_stream(stream);
+    // the engine needs the longest pattern for its scratch sizing
+    uint64_t max_len = 0;
+    if (count > 0) {
+      std::vector<uint64_t> h(count + 1);
+      FMG_CK(cudaMemcpyAsync(h.data(), offsets, (count + 1) * 8, cudaMemcpyDeviceToHost, s));
+      FMG_CK(cudaStreamSynchronize(s));
+      FMG_REQUIRE(h[0] == 0, "pattern offsets must start at 0");
+      for (uint64_t q = 0; q < count; ++q) {
+        FMG_REQUIRE(h[q + 1] > h[q], "pattern is empty");
+        max_len = std::max(max_len, h[q + 1] - h[q]);
+      }
+    }
+    *out = run_inexact(ix, codes, offsets, count, max_len, max_diff, s);
+  });
+}
+
+int fmg_inexact_host(const fmg_index* ix, const uint8_t* codes, const uint64_t* offsets, uint64_t count,
+                     int max_diff, fmg_matches** out) {
+  return fmg::guard([&] {
+    check_index(ix);
+    FMG_REQUIRE(out != nullptr, "null output pointer");
+    *out = nullptr;
+    FMG_REQUIRE(max_diff >= 0, "difference budget is negative");
+    uint64_t max_len = 0;
+    if (count > 0) validate_patterns_host(codes, offsets, count, &max_len);
+    fmg::DeviceScope scope(ix->device);
+    cudaStream_t s;
+    FMG_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    try {
+      DevBuf<uint8_t> dc(count ? offsets[count] : 0, s);
+      DevBuf<uint64_t> doff(count + 1, s);
+      if (count) {
+        FMG_CK(cudaMemcpyAsync(dc.ptr, codes, offsets[count], cudaMemcpyHostToDevice, s));
+        FMG_CK(cudaMemcpyAsync(doff.ptr, offsets, (count + 1) * 8, cudaMemcpyHostToDevice, s));
+      }
+      *out = run_inexact(ix, dc.ptr, doff.ptr, count, max_len, max_diff, s);
+    } catch (...) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+      throw;
+    }
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  });
+}
+
+int fmg_matches_size(const fmg_matches* m, uint64_t* total, uint64_t* patterns) {
+  return fmg::guard([&] {
+    FMG_REQUIRE(m != nullptr, "null matches handle");
+    if (total) *total = m->total;
+    if (patterns) *patterns = m->patterns;
+  });
+}
+
+int fmg_matches_steps(const fmg_matches* m, uint64_t* steps) {
+  return fmg::guard([&] {
+    FMG_REQUIRE(m != nullptr && steps != nullptr, "null argument");
+    *steps = m->steps;
+  });
+}
+
+int fmg_matches_copy(const fmg_matches* m, uint64_t* row_offsets, uint32_t* k, uint32_t* l, uint8_t* diffs,
+                     int to_host) {
+  return fmg::guard([&] {
+    FMG_REQUIRE(m != nullptr, "null matches handle");
+    fmg::DeviceScope scope(m->device);
+    const cudaMemcpyKind kind = to_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (row_offsets) FMG_CK(cudaMemcpy(row_offsets, m->row_off, (m->patterns + 1) * 8, kind));
+    if (m->total) {
+      if (k) FMG_CK(cudaMemcpy(k, m->k, m->total * 4, kind));
+      if (l) FMG_CK(cudaMemcpy(l, m->l, m->total * 4, kind));
+      if (diffs) FMG_CK(cudaMemcpy(diffs, m->diffs, m->total, kind));
+    }
+  });
+}
+
+void fmg_matches_free(fmg_matches* m) {
+  if (!m) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(m->device);
+  if (m->row_off) cudaFree(m->row_off);
+  if (m->k) cudaFree(m->k);
+  if (m->l) cudaFree(m->l);
+  if (m->diffs) cudaFree(m->diffs);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete m;
+}
+
+int fmg_psi_inverse(const fmg_index* ix, const uint32_t* rows, uint64_t count, uint8_t* out_sym, uint32_t* out_row,
+                    void* stream) {
+  return fmg::guard([&] {
+    check_index(ix);
+    if (count == 0) return;
+    fmg::DeviceScope scope(ix->device);
+    fmg::k_psi<<<unsigned((count + 255) / 256), 256, 0, as_stream(stream)>>>(ix->view(), rows, count, out_sym,
+                                                                             out_row, ix->err);
+    FMG_CK(cudaGetLastError());
+  });
+}
+
+int fmg_locate_rows(const fmg_index* ix, const uint32_t* rows, uint64_t count, uint32_t* out_pos, void* stream) {
+  return fmg::guard([&] {
+    check_index(ix);
+    FMG_REQUIRE(ix->samples != nullptr, "index has no suffix-array samples (fmg_index_set_samples)");
+    if (count == 0) return;
+    fmg::DeviceScope scope(ix->device);
+    const unsigned blocks = persistent_blocks(ix, (const void*)fmg::k_locate, 256, count);
+    fmg::k_locate<<<blocks, 256, 0, as_stream(stream)>>>(ix->view(), rows, count, out_pos, ix->err);
+    FMG_CK(cudaGetLastError());
+  });
+}
+
+int fmg_locate_rows_host(const fmg_index* ix, const uint32_t* rows, uint64_t count, uint32_t* out_pos) {
+  return fmg::guard([&] {
+    check_index(ix);
+    FMG_REQUIRE(ix->samples != nullptr, "index has no suffix-array samples (fmg_index_set_samples)");
+    if (count == 0) return;
+    fmg::DeviceScope scope(ix->device);
+    const uint64_t chunk = std::min<uint64_t>(count, 1ull << 22);
+    pipeline_host(ix->device, count, chunk, 4, 4, rows, out_pos,
+                  [&](void* din, uint64_t len, void* dout, cudaStream_t s) {
+                    const unsigned blocks = persistent_blocks(ix, (const void*)fmg::k_locate, 256, len);
+                    fmg::k_locate<<<blocks, 256, 0, s>>>(ix->view(), static_cast<const uint32_t*>(din), len,
+                                                         static_cast<uint32_t*>(dout), ix->err);
+                    FMG_CK(cudaGetLastError());
+                  });
+    take_input_error(ix, nullptr, "row out of range");
+  });
+}
+
+int fmg_stream_sync(void* stream) {
+  return fmg::guard([&] { FMG_CK(cudaStreamSynchronize(as_stream(stream))); });
+}
+
+}  // extern "C"

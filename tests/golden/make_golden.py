@@ -1,0 +1,182 @@
+"""Generate golden fixtures by running the REFERENCE implementation itself.
+
+Run in the build container, where the reference is mounted read-only:
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py small config0 config1
+
+Every fixture records the reference's own outputs (fmpm from
+/root/reference/pkg/src) on seeded inputs that the tests regenerate
+bit-identically (numpy PCG64 / workloads.py).  Large outputs are pinned by
+SHA-256; small ones are stored in full.  Nothing here runs on the GPU box:
+/root/reference does not exist there, only these committed fixtures travel.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import io
+import json
+import multiprocessing as mp
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+REPO = HERE.parent.parent
+sys.path.insert(0, str(REPO))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import fmpm  # noqa: E402  (the reference)
+
+from paper_1811_06127_b200 import workloads  # noqa: E402
+
+SYM = np.array(list("ACGT"))
+
+
+def text_of(codes: np.ndarray) -> str:
+    return "".join(SYM[codes].tolist())
+
+
+def sha(a) -> str:
+    if isinstance(a, np.ndarray):
+        a = np.ascontiguousarray(a).tobytes()
+    return hashlib.sha256(a).hexdigest()
+
+
+def fmi_bytes(index) -> bytes:
+    buf = io.BytesIO()
+    fmpm.serialize_index(index, buf)
+    return buf.getvalue()
+
+
+# (n, seed) of the small random texts; sizes straddle bucket (128), line (64)
+# and sample (32) boundaries
+SMALL = [(1, 1), (4, 2), (31, 3), (32, 4), (33, 5), (63, 6), (64, 7), (65, 8), (127, 9), (128, 10),
+         (129, 11), (255, 12), (256, 13), (300, 14), (1000, 15), (2500, 16)]
+
+
+def small_text(n: int, seed: int) -> np.ndarray:
+    return np.random.Generator(np.random.PCG64([900, seed])).integers(0, 4, n, dtype=np.uint8)
+
+
+def gen_small():
+    out = {}
+    for n, seed in SMALL:
+        codes = small_text(n, seed)
+        text = text_of(codes)
+        idx = fmpm.build_index(text)
+        rng = np.random.Generator(np.random.PCG64([901, seed]))
+        # Occ pairs: random plus every edge case of occ.py:59-96
+        low = rng.integers(-1, n + 1, 300)
+        high = np.minimum(n, low + rng.geometric(0.05, 300))
+        extra = [(-1, -1), (-1, 0), (-1, n), (0, 0), (n, n), (0, n), (n - 1 if n else 0, n)]
+        low = np.concatenate([low, [a for a, _ in extra]])
+        high = np.concatenate([high, [b for _, b in extra]])
+        occ = np.array([tuple(p.at_low) + tuple(p.at_high)
+                        for p in (fmpm.occ_pair_all(idx, int(a), int(b)) for a, b in zip(low, high))],
+                       dtype=np.int64)
+        # exact patterns: present substrings and random, lengths 1..40
+        pats = []
+        for _ in range(200):
+            m = int(rng.integers(1, 41))
+            if rng.random() < 0.6 and m <= n:
+                s = int(rng.integers(0, n - m + 1))
+                pats.append(text[s:s + m])
+            else:
+                pats.append(text_of(rng.integers(0, 4, m, dtype=np.uint8)))
+        ex = np.array([tuple(fmpm.exact_search(idx, p)[:2]) for p in pats], dtype=np.int64)
+        # inexact: z in 0..2, short patterns
+        ipats, iz, irow, ik, il, idf, hits = [], [], [0], [], [], [], []
+        for _ in range(60):
+            m = int(rng.integers(1, 13))
+            z = int(rng.integers(0, 3))
+            if rng.random() < 0.6 and m <= n:
+                s = int(rng.integers(0, n - m + 1))
+                p = list(text[s:s + m])
+                for _ in range(int(rng.integers(0, 2))):
+                    j = int(rng.integers(0, m))
+                    p[j] = "ACGT"[int(rng.integers(0, 4))]
+                p = "".join(p)
+            else:
+                p = text_of(rng.integers(0, 4, m, dtype=np.uint8))
+            res = fmpm.inexact_search(idx, p, z)
+            ipats.append(p)
+            iz.append(z)
+            for r in res:
+                ik.append(r.interval.k)
+                il.append(r.interval.l)
+                idf.append(r.diffs_used)
+            irow.append(len(ik))
+            h, _ = fmpm.collect_hits(idx, res, len(p))
+            hits.append([(x.global_pos, x.diffs) for x in h])
+        sa = fmpm.build_suffix_array(text)
+        psi = [fmpm.psi_inverse_fused(idx, i) for i in range(n + 1)]
+        out[f"{n}_{seed}"] = {
+            "n": n, "seed": seed, "fmi_sha256": sha(fmi_bytes(idx)),
+            "occ_low": low.tolist(), "occ_high": high.tolist(), "occ": occ.tolist(),
+            "exact_patterns": pats, "exact_kl": ex.tolist(),
+            "inexact_patterns": ipats, "inexact_z": iz, "inexact_row": irow,
+            "inexact_k": ik, "inexact_l": il, "inexact_diffs": idf, "hits": hits,
+            "sa": list(sa),
+            "psi": [[-1, -1] if v is None else list(v) for v in psi],
+            "locate": [fmpm.locate_row(idx, i) for i in range(n + 1)],
+        }
+    (HERE / "small_cases.json").write_text(json.dumps(out, separators=(",", ":")))
+    print("small: wrote", len(out), "cases")
+
+
+def gen_config0():
+    wl = workloads.config0()
+    t0 = time.time()
+    idx = fmpm.build_index(text_of(wl.text))
+    t1 = time.time()
+    pats = ["".join(SYM[p]) for p in wl.patterns]
+    kl = np.array([tuple(fmpm.exact_search(idx, p)[:2]) for p in pats], dtype=np.int64)
+    t2 = time.time()
+    np.savez_compressed(HERE / "config0_exact.npz", kl=kl.astype(np.int32))
+    meta = {"fmi_sha256": sha(fmi_bytes(idx)), "text_sha256": sha(wl.text),
+            "patterns_sha256": sha(wl.patterns), "kl_sha256": sha(kl.astype(np.int64)),
+            "build_s": t1 - t0, "search_s": t2 - t1}
+    (HERE / "config0_meta.json").write_text(json.dumps(meta, indent=1))
+    print("config0:", meta)
+
+
+_IDX = None
+
+
+def _occ_chunk(args):
+    low, high = args
+    out = np.empty((low.size, 8), dtype=np.uint32)
+    for i in range(low.size):
+        p = fmpm.occ_pair_all(_IDX, int(low[i]), int(high[i]))
+        out[i, :4] = p.at_low
+        out[i, 4:] = p.at_high
+    return out
+
+
+def gen_config1():
+    global _IDX
+    wl = workloads.config1()
+    t0 = time.time()
+    _IDX = fmpm.build_index(text_of(wl.text))
+    t1 = time.time()
+    fmi = fmi_bytes(_IDX)
+    low, high = wl.pairs[:, 0], wl.pairs[:, 1]
+    chunks = [(low[i:i + 65536], high[i:i + 65536]) for i in range(0, low.size, 65536)]
+    with mp.get_context("fork").Pool(len(os.sched_getaffinity(0))) as pool:
+        parts = pool.map(_occ_chunk, chunks)
+    out = np.concatenate(parts)
+    t2 = time.time()
+    np.savez_compressed(HERE / "config1_head.npz", occ=out[:4096])
+    meta = {"fmi_sha256": sha(fmi), "pairs_sha256": sha(wl.pairs), "occ_sha256": sha(out),
+            "n_pairs": int(low.size), "build_s": t1 - t0, "occ_s": t2 - t1}
+    (HERE / "config1_meta.json").write_text(json.dumps(meta, indent=1))
+    print("config1:", meta)
+
+
+if __name__ == "__main__":
+    for what in sys.argv[1:]:
+        {"small": gen_small, "config0": gen_config0, "config1": gen_config1}[what]()

@@ -1,0 +1,231 @@
+"""GPU parity: the sm_100a path vs the reference's outputs and the CPU oracle.
+
+Every comparison is bit-exact (integer work).  Known-answer values are the
+reference tests' own (cited); fixtures come from the reference itself
+(tests/golden/make_golden.py); large cases compare against the oracle,
+which test_oracle.py pins to those fixtures.
+"""
+
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+import paper_1811_06127_b200 as fm
+from conftest import GOLDEN, codes_to_str, small_text
+from oracle import oracle as orc
+from paper_1811_06127_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def acag(gpu):
+    return fm.build_index("ACAG")
+
+
+ACAG_OCC = [(0, 0, 1, 0), (0, 0, 1, 0), (0, 1, 1, 0), (1, 1, 1, 0), (2, 1, 1, 0)]
+
+
+def test_acag_occ_api(acag):
+    # reference tests/test_occ.py:28-99
+    for k, row in enumerate(ACAG_OCC):
+        for s in range(4):
+            assert fm.occ(acag, s, k) == row[s]
+        assert tuple(fm.occ_all(acag, k)) == row
+    assert fm.occ(acag, 0, -1) == 0
+    with pytest.raises(ValueError):
+        fm.occ(acag, 0, 5)
+    with pytest.raises(ValueError):
+        fm.occ(acag, 0, -2)
+    with pytest.raises(ValueError):
+        fm.occ(acag, 4, 0)
+    p = fm.occ_pair_all(acag, 2, 4)
+    assert tuple(p.at_low) == (0, 1, 1, 0) and tuple(p.at_high) == (2, 1, 1, 0)
+    p = fm.occ_pair_all(acag, -1, 4)
+    assert tuple(p.at_low) == (0, 0, 0, 0) and tuple(p.at_high) == (2, 1, 1, 0)
+    p = fm.occ_pair_all(acag, 3, 3)
+    assert p.at_low == p.at_high
+    with pytest.raises(ValueError):
+        fm.occ_pair_all(acag, 3, 2)
+    assert [fm.bwt_char_at(acag, i) for i in range(5)] == [2, None, 1, 0, 0]
+    with pytest.raises(ValueError):
+        fm.bwt_char_at(acag, 5)
+
+
+def test_acag_search_api(acag):
+    # reference tests/test_search.py:33-153, 200-249
+    B = fm.BwmInterval
+    assert fm.init_interval(acag, 0) == B(1, 2)
+    assert fm.init_interval(acag, 3) == B(5, 4)
+    assert fm.extend_backward(acag, B(1, 2), 1) == B(3, 3)
+    assert fm.extend_backward(acag, B(4, 4), 0) == B(2, 2)
+    with pytest.raises(ValueError):
+        fm.extend_backward(acag, B(5, 4), 0)
+    assert fm.exact_search(acag, "CA") == B(3, 3)
+    assert fm.exact_search(acag, "ACAG") == B(1, 1)
+    assert fm.exact_search(acag, "T").is_empty and fm.exact_search(acag, "GG").is_empty
+    r = fm.exact_search(acag, "ANG")
+    assert r.is_empty and r.degenerate
+    with pytest.raises(ValueError):
+        fm.exact_search(acag, "")
+    assert fm.inexact_search(acag, "AG", 0) == [fm.MatchResult(B(2, 2), 0)]
+    assert fm.inexact_search(acag, "T", 0) == []
+    hits, _ = fm.collect_hits(acag, fm.inexact_search(acag, "AT", 1), 2)
+    assert [(h.global_pos, h.diffs) for h in hits] == [(0, 1), (2, 1)]
+    assert fm.inexact_search(acag, "TT", 2) and fm.inexact_search(acag, "T", 1)
+    with pytest.raises(ValueError):
+        fm.inexact_search(acag, "A", -1)
+    assert fm.inexact_search(acag, "AN", 1) == []
+    assert fm.psi_inverse(acag, 2) == 3 and fm.psi_inverse(acag, 4) == 2
+    assert fm.psi_inverse(acag, 0) == 4 and fm.psi_inverse(acag, 1) is None
+    assert fm.psi_inverse_fused(acag, 2) == (1, 3)
+    with pytest.raises(ValueError):
+        fm.psi_inverse(acag, 5)
+    assert [fm.locate_row(acag, i) for i in range(5)] == [4, 0, 2, 1, 3]
+    assert fm.locate_all(acag, B(5, 4), 0, 1) == []
+
+
+def test_records_and_hits(gpu):
+    # reference tests/test_search.py:243-283
+    idx = fm.build_index("AAACCC" + "GGGTTT", [("r1", 0, 6), ("r2", 6, 6)])
+    hits = fm.locate_all(idx, fm.exact_search(idx, "CCC"), 0, 3)
+    assert hits == [fm.Hit(record="r1", offset=3, global_pos=3, diffs=0)]
+    iv = fm.exact_search(idx, "CCGG")
+    assert not iv.is_empty and fm.locate_all(idx, iv, 0, 4) == []
+    idx = fm.build_index("AC" * 50)
+    iv = fm.exact_search(idx, "AC")
+    hits, trunc = fm.collect_hits(idx, [fm.MatchResult(iv, 0)], 2, max_hits=10)
+    assert trunc and len(hits) == 10
+    hits, trunc = fm.collect_hits(idx, [fm.MatchResult(iv, 0)], 2)
+    assert not trunc and len(hits) == 50
+    idx = fm.build_index("ACGTACGTAC")
+    hits, _ = fm.collect_hits(idx, fm.inexact_search(idx, "ACGT", 1), 4)
+    by = {h.global_pos: h.diffs for h in hits}
+    assert by[0] == 0 and by[4] == 0
+
+
+def test_reconstruct_round_trip(gpu):
+    for n in (1, 5, 127, 128, 129, 500):
+        codes = small_text(n, 62 + n)
+        assert fm.reconstruct_reference(fm.build_index(codes)) == codes_to_str(codes)
+
+
+def test_small_cases_all_paths(small_cases, gpu):
+    for key, case in small_cases.items():
+        n = case["n"]
+        idx = fm.build_index(small_text(n, case["seed"]))
+        occ = fm.occ_pair_batch(idx, case["occ_low"], case["occ_high"])
+        assert np.array_equal(occ.astype(np.int64), np.array(case["occ"])), key
+        kl, deg = fm.exact_search_batch(idx, case["exact_patterns"])
+        assert np.array_equal(kl, np.array(case["exact_kl"])) and not deg.any(), key
+        # packed fixed-length path on the same patterns, grouped by length
+        pats = case["exact_patterns"]
+        for m in sorted({len(p) for p in pats}):
+            sel = [i for i, p in enumerate(pats) if len(p) == m]
+            if m > 32:
+                continue
+            arr = np.array([[ "ACGT".index(ch) for ch in pats[i]] for i in sel], dtype=np.uint8)
+            klp, _ = fm.exact_search_batch(idx, arr)
+            assert np.array_equal(klp, np.array(case["exact_kl"])[sel]), (key, m)
+        for z in (0, 1, 2):
+            sel = [i for i, zz in enumerate(case["inexact_z"]) if zz == z]
+            if not sel:
+                continue
+            ms = fm.inexact_search_batch(idx, [case["inexact_patterns"][i] for i in sel], z)
+            grow = case["inexact_row"]
+            for j, i in enumerate(sel):
+                a, b = grow[i], grow[i + 1]
+                want = [fm.MatchResult(fm.BwmInterval(k, l), d) for k, l, d in
+                        zip(case["inexact_k"][a:b], case["inexact_l"][a:b], case["inexact_diffs"][a:b])]
+                got = ms.results(j)
+                assert got == want, (key, case["inexact_patterns"][i], z)
+                hits, _ = fm.collect_hits(idx, got, len(case["inexact_patterns"][i]))
+                assert [[h.global_pos, h.diffs] for h in hits] == case["hits"][i], key
+        assert list(fm.locate_rows(idx, np.arange(n + 1))) == case["locate"], key
+        sym, prev = fm.psi_inverse_batch(idx, np.arange(n + 1))
+        got = [[-1, -1] if s == 255 else [int(s), int(p)] for s, p in zip(sym, prev)]
+        assert got == case["psi"], key
+
+
+def test_config0_exact_full(gpu):
+    wl = workloads.config0()
+    idx = fm.build_index(wl.text)
+    want = np.load(GOLDEN / "config0_exact.npz")["kl"].astype(np.int64)
+    kl, _ = fm.exact_search_batch(idx, wl.patterns)  # packed kernel
+    assert np.array_equal(kl, want)
+    kl2, _ = fm.exact_search_batch(idx, [codes_to_str(p) for p in wl.patterns[:2000]])  # general kernel
+    assert np.array_equal(kl2, want[:2000])
+
+
+def test_config1_occ_full(gpu):
+    wl = workloads.config1()
+    idx = fm.build_index(wl.text)
+    got = fm.occ_pair_batch(idx, wl.pairs[:, 0], wl.pairs[:, 1])
+    meta_path = GOLDEN / "config1_meta.json"
+    if meta_path.exists():
+        meta = json.loads(meta_path.read_text())
+        assert hashlib.sha256(got.tobytes()).hexdigest() == meta["occ_sha256"]
+    want = orc.occ_pair_batch(orc.OracleIndex(idx), wl.pairs[:, 0], wl.pairs[:, 1])
+    assert np.array_equal(got, want)
+
+
+def test_occ_device_tensor_path(gpu):
+    import torch
+
+    wl = workloads.config1(count=1 << 20)
+    idx = fm.build_index(wl.text)
+    kl = np.stack([wl.pairs[:, 0] + 1, wl.pairs[:, 1]], axis=1).astype(np.int32)
+    d_out = fm.occ_pair_batch(idx, torch.from_numpy(kl).to(gpu))
+    torch.cuda.synchronize()
+    host = fm.occ_pair_batch(idx, wl.pairs[:, 0], wl.pairs[:, 1])
+    assert np.array_equal(d_out.cpu().numpy().view(np.uint32), host)
+
+
+def test_inexact_random_vs_oracle(gpu):
+    rng = np.random.Generator(np.random.PCG64(4242))
+    text = rng.integers(0, 4, 200_000, dtype=np.uint8)
+    idx = fm.build_index(text)
+    ox = orc.OracleIndex(idx)
+    for m, z, count in ((5, 2, 300), (19, 1, 3000), (32, 1, 3000), (32, 0, 2000), (20, 2, 300),
+                        (50, 1, 500), (80, 1, 300)):
+        offs = rng.integers(0, text.size - m + 1, count)
+        pats = workloads.substrings(text, offs, m)
+        pats = workloads.mutate(pats.reshape(-1), 0.03, rng).reshape(count, m)
+        pats[1::3] = rng.integers(0, 4, pats[1::3].shape, dtype=np.uint8)
+        ms = fm.inexact_search_batch(idx, pats, z)
+        row, k, l, d, steps = orc.inexact_batch(ox, pats, z)
+        assert np.array_equal(ms.offsets, row), (m, z)
+        assert np.array_equal(ms.k.astype(np.int64), k) and np.array_equal(ms.l.astype(np.int64), l)
+        assert np.array_equal(ms.diffs, d), (m, z)
+        if z == 1 and m >= 19:  # no result-buffer retries here: pruned work <= DFS + bound pass
+            assert ms.steps <= steps + count * m, (m, z, ms.steps, steps)
+
+
+def test_exact_edge_cases(gpu):
+    rng = np.random.Generator(np.random.PCG64(99))
+    text = rng.integers(0, 4, 50_000, dtype=np.uint8)
+    idx = fm.build_index(text)
+    ox = orc.OracleIndex(idx)
+    pats = []
+    for m in (1, 2, 31, 32, 33, 64, 65, 100, 150):
+        for _ in range(20):
+            s = int(rng.integers(0, text.size - m + 1))
+            pats.append(codes_to_str(text[s:s + m]))
+            pats.append(codes_to_str(rng.integers(0, 4, m, dtype=np.uint8)))
+    kl, _ = fm.exact_search_batch(idx, pats)
+    assert np.array_equal(kl, orc.exact_batch(ox, pats))
+    kl, deg = fm.exact_search_batch(idx, ["acgt", "ACNT", "A"])
+    assert deg.tolist() == [False, True, False] and tuple(kl[1]) == (1, 0)
+    assert tuple(kl[0]) == tuple(orc.exact_batch(ox, ["ACGT"])[0])
+
+
+def test_config2_subsample_vs_oracle(gpu):
+    wl = workloads.config2(n_reads=20_000)
+    idx = fm.build_index(wl.text)
+    ms = fm.inexact_search_batch(idx, wl.patterns, 1)
+    row, k, l, d, _ = orc.inexact_batch(orc.OracleIndex(idx), wl.patterns, 1)
+    assert np.array_equal(ms.offsets, row)
+    assert np.array_equal(ms.k.astype(np.int64), k) and np.array_equal(ms.l.astype(np.int64), l)
+    assert np.array_equal(ms.diffs, d)
