@@ -13,7 +13,9 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <string>
 #include <vector>
 
@@ -79,29 +81,46 @@ struct DevBuf {
 // Kernels
 // ---------------------------------------------------------------------------
 
-// Bucket records (4 x u64 LE base + 32 B chars) -> two lines per bucket.
-__global__ void k_build_lines(const uint64_t* __restrict__ rec, uint64_t nb, Line* __restrict__ lines,
-                              uint32_t* __restrict__ err) {
-  uint64_t b = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (b >= nb) return;
-  const uint64_t* r = rec + b * 8;
-  uint64_t base[4] = {r[0], r[1], r[2], r[3]};
-  uint64_t w[4] = {r[4], r[5], r[6], r[7]};
-  Line a, h;
-  uint32_t in[4];
-  count4(w, 63u, in);  // all 64 fields of the first half
+// Counts of A, C, G, T among all 32 fields of one packed word.
+__device__ __forceinline__ void add_word_counts(uint64_t w, uint32_t c[4]) {
+  const uint64_t lo = w & kFieldLo, hi = (w >> 1) & kFieldLo;
+  const uint32_t t = __popcll(lo & hi), h = __popcll(hi), l = __popcll(lo);
+  c[3] += t;
+  c[2] += h - t;
+  c[1] += l - t;
+  c[0] += 32u - h - l + t;
+}
+
+// Bucket records (4 x u64 LE base + 32 B chars, 128 chars each) -> lines of
+// 32W chars.  Line j starts at char 32Wj, which is a multiple of 32 and so
+// falls on a word boundary of its bucket; its checkpoint is the bucket base
+// plus the counts of the bucket's words before it.
+template <int W>
+__global__ void k_build_lines(const uint64_t* __restrict__ rec, uint64_t nb, uint8_t* __restrict__ lines,
+                              uint64_t n_lines, uint32_t* __restrict__ err) {
+  const uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n_lines) return;
+  const uint64_t c0 = j * LineTraits<W>::kChars;
+  const uint64_t b0 = c0 >> 7;
+  const uint64_t* r = rec + b0 * 8;
+  uint32_t base[4];
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
-    if (base[s] >= 0xFFFFFFFFull) atomicOr(err, 1u);
-    a.base[s] = uint32_t(base[s]);
-    h.base[s] = uint32_t(base[s]) + in[s];
+    if (r[s] >= 0xFFFFFFFFull) atomicOr(err, 1u);
+    base[s] = uint32_t(r[s]);
   }
-  a.w[0] = w[0];
-  a.w[1] = w[1];
-  h.w[0] = w[2];
-  h.w[1] = w[3];
-  lines[2 * b] = a;
-  lines[2 * b + 1] = h;
+  const uint32_t skip = uint32_t((c0 & 127u) >> 5);
+  for (uint32_t q = 0; q < skip; ++q) add_word_counts(r[4 + q], base);
+  Line<W> out;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) out.base[s] = base[s];
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    const uint64_t c = c0 + 32u * k;
+    const uint64_t b = c >> 7;
+    out.w[k] = (b < nb) ? rec[b * 8 + 4 + ((c & 127u) >> 5)] : 0ull;
+  }
+  reinterpret_cast<Line<W>*>(lines)[j] = out;
 }
 
 __device__ __forceinline__ uint2 ld_stream_u2(const uint2* p) {
@@ -123,10 +142,11 @@ __device__ __forceinline__ void st_stream_256(uint32_t* p, const uint32_t lo[4],
 // Occ step microkernel.  Thread handles PER pairs strided by blockDim so the
 // (k,l) loads and the 32-byte output stores stay fully coalesced; all line
 // loads of a thread are issued before any popcount so each thread keeps up
-// to 2*PER independent sector reads in flight.
-template <int PER>
+// to 2*PER independent line reads in flight.
+template <int PER, int W>
 __global__ void __launch_bounds__(256) k_occ_pair(IndexView ix, const uint2* __restrict__ kl, uint64_t count,
                                                   uint32_t* __restrict__ out, uint32_t* __restrict__ err) {
+  constexpr uint32_t kC = LineTraits<W>::kChars;
   const uint64_t first = uint64_t(blockIdx.x) * blockDim.x * PER + threadIdx.x;
   uint2 q[PER];
   bool act[PER];
@@ -137,18 +157,22 @@ __global__ void __launch_bounds__(256) k_occ_pair(IndexView ix, const uint2* __r
     q[u] = act[u] ? ld_stream_u2(kl + i) : make_uint2(1u, 0u);
   }
   uint32_t bh[PER][4], bl[PER][4];
-  uint64_t wh[PER][2], wl[PER][2];
+  uint64_t wh[PER][W], wl[PER][W];
   bool ok[PER], two[PER];
+  uint32_t rh[PER], rl[PER];
 #pragma unroll
   for (int u = 0; u < PER; ++u) {
     const uint32_t k = q[u].x, l = q[u].y;
     ok[u] = act[u] && l <= ix.n && k <= l + 1u;
     if (act[u] && !ok[u]) atomicOr(err, 1u);
-    const uint32_t lh = ok[u] ? (l >> 6) : 0u;
-    const uint32_t ll = (ok[u] && k != 0u) ? ((k - 1u) >> 6) : lh;
-    two[u] = ll != lh;
-    load_line<true>(ix.lines + lh, bh[u], wh[u]);
-    if (two[u]) load_line<true>(ix.lines + ll, bl[u], wl[u]);
+    const uint32_t hh = ok[u] ? l : 0u;
+    const uint32_t ll = (ok[u] && k != 0u) ? k - 1u : hh;
+    const uint32_t jh = line_of<W>(hh), jl = line_of<W>(ll);
+    rh[u] = hh - jh * kC;
+    rl[u] = ll - jl * kC;
+    two[u] = jl != jh;
+    load_line<W, true>(ix, jh, rh[u], bh[u], wh[u]);
+    if (two[u]) load_line<W, true>(ix, jl, rl[u], bl[u], wl[u]);
   }
 #pragma unroll
   for (int u = 0; u < PER; ++u) {
@@ -156,12 +180,12 @@ __global__ void __launch_bounds__(256) k_occ_pair(IndexView ix, const uint2* __r
     const uint32_t k = q[u].x, l = q[u].y;
     uint32_t lo[4] = {0u, 0u, 0u, 0u}, hi[4] = {0u, 0u, 0u, 0u};
     if (ok[u]) {
-      occ4_from_line(ix, bh[u], wh[u], l, hi);
+      occ4_from_line<W>(ix, bh[u], wh[u], l, rh[u], hi);
       if (k != 0u) {
         if (two[u])
-          occ4_from_line(ix, bl[u], wl[u], k - 1u, lo);
+          occ4_from_line<W>(ix, bl[u], wl[u], k - 1u, rl[u], lo);
         else
-          occ4_from_line(ix, bh[u], wh[u], k - 1u, lo);
+          occ4_from_line<W>(ix, bh[u], wh[u], k - 1u, rl[u], lo);
       }
     }
     const uint64_t i = first + uint64_t(u) * blockDim.x;
@@ -185,7 +209,7 @@ struct CodePatterns {  // codes[offsets[q] .. offsets[q+1])
 // empty interval, search.py:91-92) the lane immediately takes the next
 // pattern of its grid-stride sequence, so warps stay full while per-pattern
 // step counts vary from 1 to m-1.
-template <bool kPacked>
+template <bool kPacked, int W>
 __global__ void __launch_bounds__(256) k_exact(IndexView ix, PackedPatterns pp, CodePatterns cp, uint64_t count,
                                                uint2* __restrict__ out, unsigned long long* __restrict__ steps) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
@@ -224,19 +248,21 @@ __global__ void __launch_bounds__(256) k_exact(IndexView ix, PackedPatterns pp, 
     const uint32_t sym = kPacked ? (uint32_t(pat >> (2 * i)) & 3u) : uint32_t(__ldg(codes + i));
     --i;
     // extend_backward, search.py:60-71: k' = c[b] + Occ(b, k-1) + 1, l' = c[b] + Occ(b, l)
+    constexpr uint32_t kC = LineTraits<W>::kChars;
     uint32_t bh[4], bl[4];
-    uint64_t wh[2], wl[2];
+    uint64_t wh[W], wl[W];
     const uint32_t low = k - 1u;  // k >= 1 on every non-empty interval here
-    const uint32_t lh = l >> 6, ll = low >> 6;
-    load_line<false>(ix.lines + lh, bh, wh);
+    const uint32_t jh = line_of<W>(l), jl = line_of<W>(low);
+    const uint32_t rh = l - jh * kC, rl = low - jl * kC;
+    load_line<W, false>(ix, jh, rh, bh, wh);
     uint32_t ol;
-    if (ll != lh) {
-      load_line<false>(ix.lines + ll, bl, wl);
-      ol = occ1_from_line(ix, bl, wl, low, sym);
+    if (jl != jh) {
+      load_line<W, false>(ix, jl, rl, bl, wl);
+      ol = occ1_from_line<W>(ix, bl, wl, low, rl, sym);
     } else {
-      ol = occ1_from_line(ix, bh, wh, low, sym);
+      ol = occ1_from_line<W>(ix, bh, wh, low, rl, sym);
     }
-    const uint32_t oh = occ1_from_line(ix, bh, wh, l, sym);
+    const uint32_t oh = occ1_from_line<W>(ix, bh, wh, l, rh, sym);
     const uint32_t cs = c_of(ix, sym);
     k = cs + ol + 1u;
     l = cs + oh;
@@ -287,7 +313,7 @@ struct InexactOut {
 // turning W[0..i] into a substring of the text must touch each absent
 // segment with its own edit, so a node with D(i) > budget yields nothing and
 // is never pushed.  (BWA's D array, computed with the forward index only.)
-template <bool kShort>
+template <bool kShort, int W>
 __global__ void __launch_bounds__(256) k_inexact(IndexView ix, CodePatterns cp, const uint32_t* __restrict__ list,
                                                  uint64_t count, uint32_t z, InexactScratch sc, InexactOut out) {
   const uint64_t T = sc.T;
@@ -462,7 +488,7 @@ __global__ void __launch_bounds__(256) k_inexact(IndexView ix, CodePatterns cp, 
 
     // ---- one Occ step: the eight values at (k-1, l) ----
     uint32_t lo[4], hi[4];
-    occ_step<false>(ix, k, l, lo, hi);
+    occ_step<W, false>(ix, k, l, lo, hi);
     ++my_steps;
 
     if (phase == 0) {
@@ -529,14 +555,17 @@ __global__ void k_widen_counts(uint64_t count, const uint32_t* __restrict__ c32,
 
 // psi_inverse_fused (search.py:172-186): symbol at row i and its
 // predecessor row c[sym] + Occ(sym, i), in one line access.
+template <int W>
 __device__ __forceinline__ uint32_t psi_step(const IndexView& ix, uint32_t row, uint32_t& sym) {
   uint32_t b[4];
-  uint64_t w[2];
-  load_line<false>(ix.lines + (row >> 6), b, w);
-  sym = field_at(w, row & 63u);
-  return c_of(ix, sym) + occ1_from_line(ix, b, w, row, sym);
+  uint64_t w[W];
+  const uint32_t j = line_of<W>(row), r = row - j * LineTraits<W>::kChars;
+  load_line<W, false>(ix, j, r, b, w);
+  sym = field_at<W>(w, r);
+  return c_of(ix, sym) + occ1_from_line<W>(ix, b, w, row, r, sym);
 }
 
+template <int W>
 __global__ void k_psi(IndexView ix, const uint32_t* __restrict__ rows, uint64_t count, uint8_t* __restrict__ out_sym,
                       uint32_t* __restrict__ out_row, uint32_t* __restrict__ err) {
   const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -554,7 +583,7 @@ __global__ void k_psi(IndexView ix, const uint32_t* __restrict__ rows, uint64_t 
     return;
   }
   uint32_t sym;
-  const uint32_t prev = psi_step(ix, row, sym);
+  const uint32_t prev = psi_step<W>(ix, row, sym);
   out_sym[q] = uint8_t(sym);
   out_row[q] = prev;
 }
@@ -563,6 +592,7 @@ __global__ void k_psi(IndexView ix, const uint32_t* __restrict__ rows, uint64_t 
 // (row % 32 == 0 — samples are taken by ROW, index.py:93, so the walk length
 // is geometric-like with mean ~32, not bounded by 32) or is the sentinel row.
 // Grid-stride lane refill keeps warps full despite the varying walk lengths.
+template <int W>
 __global__ void __launch_bounds__(256) k_locate(IndexView ix, const uint32_t* __restrict__ rows, uint64_t count,
                                                 uint32_t* __restrict__ out_pos, uint32_t* __restrict__ err) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
@@ -584,7 +614,7 @@ __global__ void __launch_bounds__(256) k_locate(IndexView ix, const uint32_t* __
         break;
       }
       uint32_t sym;
-      row = psi_step(ix, row, sym);
+      row = psi_step<W>(ix, row, sym);
       ++steps;
       if (steps > ix.n + 1u) {  // corrupt index (search.py:207-208)
         atomicOr(err, 2u);
@@ -611,7 +641,8 @@ struct fmg_index {
   int device = 0;
   uint64_t n = 0, sentinel_row = 0, c[5] = {0, 0, 0, 0, 0};
   uint64_t n_buckets = 0, n_lines = 0, n_samples = 0;
-  fmg::Line* lines = nullptr;
+  int words = 2;  // line layout: W words of 32 chars per line (occ_device.cuh)
+  uint8_t* lines = nullptr;
   uint32_t* samples = nullptr;
   uint32_t* err = nullptr;  // sticky device-side input error flags
   int sms = 148;
@@ -642,6 +673,22 @@ using namespace fmg;
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Line layout.  W = 2 (32-byte lines, one sector per Occ) is the default for
+// every index size: measured on B200, a random L2 miss costs one DRAM request
+// (~48 G requests/s chip-wide) whatever its size up to 64 B, and W = 6 / 14
+// lines read by one thread need 2-4 requests and 3-7x the popcount work
+// (tools/size_sweep.py, profiles/).  FMG_LINE_WORDS=2|6|14 overrides (the
+// tests exercise every layout).
+int choose_words(uint64_t n_buckets) {
+  if (const char* env = std::getenv("FMG_LINE_WORDS")) {
+    const int w = std::atoi(env);
+    FMG_REQUIRE(w == 2 || w == 6 || w == 14, "FMG_LINE_WORDS must be 2, 6 or 14");
+    return w;
+  }
+  (void)n_buckets;
+  return 2;
+}
+
 void check_index(const fmg_index* ix) { FMG_REQUIRE(ix != nullptr, "null index handle"); }
 
 // Reads and clears the sticky input-error flags (synchronises `stream`).
@@ -657,15 +704,42 @@ void take_input_error(const fmg_index* ix, cudaStream_t stream, const char* what
   }
 }
 
-constexpr int kOccPer = 2;
+// Runs f(std::integral_constant<int, W>) for the index's line layout.
+template <typename F>
+void with_words(const fmg_index* ix, F&& f) {
+  switch (ix->words) {
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    case 6: f(std::integral_constant<int, 6>{}); break;
+    case 14: f(std::integral_constant<int, 14>{}); break;
+    default: throw std::invalid_argument("unsupported line layout");
+  }
+}
 
-void launch_occ_pair(const fmg_index* ix, const uint32_t* kl, uint64_t count, uint32_t* out, cudaStream_t s) {
-  if (count == 0) return;
-  const uint64_t per_block = 256ull * kOccPer;
+constexpr int kOccPer = 1;
+
+template <int PER>
+void launch_occ_pair_t(const fmg_index* ix, const uint32_t* kl, uint64_t count, uint32_t* out, cudaStream_t s,
+                       int threads) {
+  const uint64_t per_block = uint64_t(threads) * PER;
   const uint64_t blocks = (count + per_block - 1) / per_block;
-  k_occ_pair<kOccPer><<<dim3(unsigned(blocks)), 256, 0, s>>>(ix->view(), reinterpret_cast<const uint2*>(kl), count,
-                                                              out, ix->err);
+  with_words(ix, [&](auto wt) {
+    constexpr int W = decltype(wt)::value;
+    k_occ_pair<PER, W><<<dim3(unsigned(blocks)), threads, 0, s>>>(ix->view(), reinterpret_cast<const uint2*>(kl),
+                                                                    count, out, ix->err);
+  });
   FMG_CK(cudaGetLastError());
+}
+
+void launch_occ_pair(const fmg_index* ix, const uint32_t* kl, uint64_t count, uint32_t* out, cudaStream_t s,
+                     int per = kOccPer, int threads = 128) {
+  if (count == 0) return;
+  FMG_REQUIRE(threads == 128 || threads == 256, "threads must be 128 or 256");
+  switch (per) {
+    case 1: launch_occ_pair_t<1>(ix, kl, count, out, s, threads); break;
+    case 2: launch_occ_pair_t<2>(ix, kl, count, out, s, threads); break;
+    case 4: launch_occ_pair_t<4>(ix, kl, count, out, s, threads); break;
+    default: throw std::invalid_argument("per must be 1, 2 or 4");
+  }
 }
 
 unsigned persistent_blocks(const fmg_index* ix, const void* kernel, int threads, uint64_t work) {
@@ -681,8 +755,11 @@ void launch_exact_packed(const fmg_index* ix, const uint64_t* packed, uint32_t m
   if (count == 0) return;
   PackedPatterns pp{packed, m};
   CodePatterns cp{nullptr, nullptr};
-  const unsigned blocks = persistent_blocks(ix, (const void*)k_exact<true>, 256, count);
-  k_exact<true><<<blocks, 256, 0, s>>>(ix->view(), pp, cp, count, reinterpret_cast<uint2*>(kl_out), steps);
+  with_words(ix, [&](auto wt) {
+    constexpr int W = decltype(wt)::value;
+    const unsigned blocks = persistent_blocks(ix, (const void*)k_exact<true, W>, 256, count);
+    k_exact<true, W><<<blocks, 256, 0, s>>>(ix->view(), pp, cp, count, reinterpret_cast<uint2*>(kl_out), steps);
+  });
   FMG_CK(cudaGetLastError());
 }
 
@@ -691,8 +768,20 @@ void launch_exact_codes(const fmg_index* ix, const uint8_t* codes, const uint64_
   if (count == 0) return;
   PackedPatterns pp{nullptr, 0};
   CodePatterns cp{codes, offsets};
-  const unsigned blocks = persistent_blocks(ix, (const void*)k_exact<false>, 256, count);
-  k_exact<false><<<blocks, 256, 0, s>>>(ix->view(), pp, cp, count, reinterpret_cast<uint2*>(kl_out), steps);
+  with_words(ix, [&](auto wt) {
+    constexpr int W = decltype(wt)::value;
+    const unsigned blocks = persistent_blocks(ix, (const void*)k_exact<false, W>, 256, count);
+    k_exact<false, W><<<blocks, 256, 0, s>>>(ix->view(), pp, cp, count, reinterpret_cast<uint2*>(kl_out), steps);
+  });
+  FMG_CK(cudaGetLastError());
+}
+
+void launch_locate(const fmg_index* ix, const uint32_t* rows, uint64_t count, uint32_t* out_pos, cudaStream_t s) {
+  with_words(ix, [&](auto wt) {
+    constexpr int W = decltype(wt)::value;
+    const unsigned blocks = persistent_blocks(ix, (const void*)fmg::k_locate<W>, 256, count);
+    fmg::k_locate<W><<<blocks, 256, 0, s>>>(ix->view(), rows, count, out_pos, ix->err);
+  });
   FMG_CK(cudaGetLastError());
 }
 
@@ -727,7 +816,11 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     }
     const uint32_t z = uint32_t(max_diff);
     const bool short_pat = max_len <= 64;
-    const void* kfn = short_pat ? (const void*)k_inexact<true> : (const void*)k_inexact<false>;
+    const void* kfn = nullptr;
+    with_words(ix, [&](auto wt) {
+      constexpr int W = decltype(wt)::value;
+      kfn = short_pat ? (const void*)k_inexact<true, W> : (const void*)k_inexact<false, W>;
+    });
     int per_sm = 0;
     FMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 256, 0));
     per_sm = std::max(per_sm, 1);
@@ -789,10 +882,13 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       o.steps = counters.ptr + 2;
       const unsigned blocks = unsigned(T / 256);
       CodePatterns cp{codes, offsets};
-      if (short_pat)
-        k_inexact<true><<<blocks, 256, 0, s>>>(ix->view(), cp, list, pending, z, sc, o);
-      else
-        k_inexact<false><<<blocks, 256, 0, s>>>(ix->view(), cp, list, pending, z, sc, o);
+      with_words(ix, [&](auto wt) {
+        constexpr int W = decltype(wt)::value;
+        if (short_pat)
+          k_inexact<true, W><<<blocks, 256, 0, s>>>(ix->view(), cp, list, pending, z, sc, o);
+        else
+          k_inexact<false, W><<<blocks, 256, 0, s>>>(ix->view(), cp, list, pending, z, sc, o);
+      });
       FMG_CK(cudaGetLastError());
       unsigned long long host_ctr[2];
       FMG_CK(cudaMemcpyAsync(host_ctr, counters.ptr, sizeof(host_ctr), cudaMemcpyDeviceToHost, s));
@@ -924,24 +1020,24 @@ int fmg_index_create(int device, const void* bucket_records, uint64_t n_buckets,
       ix->sentinel_row = sentinel_row;
       for (int s = 0; s < 5; ++s) ix->c[s] = c[s];
       ix->n_buckets = n_buckets;
-      ix->n_lines = 2 * n_buckets;
+      ix->words = choose_words(n_buckets);
       ix->sms = fmg::sm_count(device);
-      FMG_CK(cudaMalloc(&ix->lines, ix->n_lines * sizeof(fmg::Line)));
-      FMG_CK(cudaMalloc(&ix->err, sizeof(uint32_t)));
-      FMG_CK(cudaMemset(ix->err, 0, sizeof(uint32_t)));
-      // upload in slabs through a bounded staging buffer
-      const uint64_t slab = 1ull << 22;  // buckets per slab (256 MiB)
-      uint64_t* staging = nullptr;
-      FMG_CK(cudaMalloc(&staging, std::min(slab, n_buckets) * 64));
-      for (uint64_t b0 = 0; b0 < n_buckets; b0 += slab) {
-        const uint64_t nb = std::min(slab, n_buckets - b0);
-        FMG_CK(cudaMemcpy(staging, static_cast<const uint8_t*>(bucket_records) + b0 * 64, nb * 64,
-                          cudaMemcpyHostToDevice));
-        fmg::k_build_lines<<<unsigned((nb + 255) / 256), 256>>>(staging, nb, ix->lines + 2 * b0, ix->err);
-        FMG_CK(cudaGetLastError());
-      }
-      FMG_CK(cudaDeviceSynchronize());
-      cudaFree(staging);
+      with_words(ix, [&](auto wt) {
+        constexpr int W = decltype(wt)::value;
+        ix->n_lines = (n_buckets * 128 + fmg::LineTraits<W>::kChars - 1) / fmg::LineTraits<W>::kChars;
+        FMG_CK(cudaMalloc(&ix->lines, ix->n_lines * fmg::LineTraits<W>::kBytes));
+        FMG_CK(cudaMalloc(&ix->err, sizeof(uint32_t)));
+        FMG_CK(cudaMemset(ix->err, 0, sizeof(uint32_t)));
+        uint64_t* staging = nullptr;
+        FMG_CK(cudaMalloc(&staging, n_buckets * 64));
+        FMG_CK(cudaMemcpy(staging, bucket_records, n_buckets * 64, cudaMemcpyHostToDevice));
+        fmg::k_build_lines<W><<<unsigned((ix->n_lines + 255) / 256), 256>>>(staging, n_buckets, ix->lines,
+                                                                             ix->n_lines, ix->err);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        cudaFree(staging);
+        FMG_CK(e);
+      });
       uint32_t bad = 0;
       FMG_CK(cudaMemcpy(&bad, ix->err, sizeof(bad), cudaMemcpyDeviceToHost));
       FMG_REQUIRE(bad == 0, "bucket base does not fit 32 bits");
@@ -984,7 +1080,11 @@ int fmg_index_info(const fmg_index* ix, uint64_t* n, int* device, uint64_t* devi
     check_index(ix);
     if (n) *n = ix->n;
     if (device) *device = ix->device;
-    if (device_bytes) *device_bytes = ix->n_lines * sizeof(fmg::Line) + ix->n_samples * 4;
+    if (device_bytes) {
+      uint64_t lb = 0;
+      with_words(ix, [&](auto wt) { lb = fmg::LineTraits<decltype(wt)::value>::kBytes; });
+      *device_bytes = ix->n_lines * lb + ix->n_samples * 4;
+    }
   });
 }
 
@@ -1005,6 +1105,30 @@ int fmg_occ_pair(const fmg_index* ix, const uint32_t* kl, uint64_t count, uint32
     check_index(ix);
     fmg::DeviceScope scope(ix->device);
     launch_occ_pair(ix, kl, count, out, as_stream(stream));
+  });
+}
+
+// Tuning hook (not part of include/fmgpu.h): same as fmg_occ_pair with an
+// explicit pairs-per-thread and block size.
+int fmgx_occ_pair_tuned(const fmg_index* ix, const uint32_t* kl, uint64_t count, uint32_t* out, void* stream,
+                        int per, int threads) {
+  return fmg::guard([&] {
+    check_index(ix);
+    fmg::DeviceScope scope(ix->device);
+    launch_occ_pair(ix, kl, count, out, as_stream(stream), per, threads);
+  });
+}
+
+// Tuning hook: L2 fetch granularity of the current context on `device`
+// (cudaLimitMaxL2FetchGranularity; 32 = fetch exactly the 32-byte sector a
+// line load needs).  Returns the previous value in *prev.
+int fmgx_set_l2_fetch_granularity(int device, int bytes, int* prev) {
+  return fmg::guard([&] {
+    fmg::DeviceScope scope(device);
+    size_t old = 0;
+    FMG_CK(cudaDeviceGetLimit(&old, cudaLimitMaxL2FetchGranularity));
+    if (prev) *prev = int(old);
+    if (bytes >= 0) FMG_CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(bytes)));
   });
 }
 
@@ -1184,8 +1308,10 @@ int fmg_psi_inverse(const fmg_index* ix, const uint32_t* rows, uint64_t count, u
     check_index(ix);
     if (count == 0) return;
     fmg::DeviceScope scope(ix->device);
-    fmg::k_psi<<<unsigned((count + 255) / 256), 256, 0, as_stream(stream)>>>(ix->view(), rows, count, out_sym,
-                                                                             out_row, ix->err);
+    with_words(ix, [&](auto wt) {
+      fmg::k_psi<decltype(wt)::value><<<unsigned((count + 255) / 256), 256, 0, as_stream(stream)>>>(
+          ix->view(), rows, count, out_sym, out_row, ix->err);
+    });
     FMG_CK(cudaGetLastError());
   });
 }
@@ -1196,8 +1322,7 @@ int fmg_locate_rows(const fmg_index* ix, const uint32_t* rows, uint64_t count, u
     FMG_REQUIRE(ix->samples != nullptr, "index has no suffix-array samples (fmg_index_set_samples)");
     if (count == 0) return;
     fmg::DeviceScope scope(ix->device);
-    const unsigned blocks = persistent_blocks(ix, (const void*)fmg::k_locate, 256, count);
-    fmg::k_locate<<<blocks, 256, 0, as_stream(stream)>>>(ix->view(), rows, count, out_pos, ix->err);
+    launch_locate(ix, rows, count, out_pos, as_stream(stream));
     FMG_CK(cudaGetLastError());
   });
 }
@@ -1211,9 +1336,7 @@ int fmg_locate_rows_host(const fmg_index* ix, const uint32_t* rows, uint64_t cou
     const uint64_t chunk = std::min<uint64_t>(count, 1ull << 22);
     pipeline_host(ix->device, count, chunk, 4, 4, rows, out_pos,
                   [&](void* din, uint64_t len, void* dout, cudaStream_t s) {
-                    const unsigned blocks = persistent_blocks(ix, (const void*)fmg::k_locate, 256, len);
-                    fmg::k_locate<<<blocks, 256, 0, s>>>(ix->view(), static_cast<const uint32_t*>(din), len,
-                                                         static_cast<uint32_t*>(dout), ix->err);
+                    launch_locate(ix, static_cast<const uint32_t*>(din), len, static_cast<uint32_t*>(dout), s);
                     FMG_CK(cudaGetLastError());
                   });
     take_input_error(ix, nullptr, "row out of range");

@@ -2,40 +2,58 @@
 //
 // Layout.  The reference keeps one 128-character bucket per
 // 4 x u64 base + 32 packed bytes (index.py:24-36, serialize.py:87-92).  On the
-// GPU each bucket is split into two 32-byte LINES of 64 characters:
+// GPU the transform is re-cut into LINES of W 64-bit words (32 characters
+// each), every line carrying its own checkpoint:
 //
-//     struct Line { u32 base[4]; u64 w[2]; }          // 32 B = one DRAM sector
+//     template <int W> struct Line { u32 base[4]; u64 w[W]; }   // 16 + 8W bytes
+//
+//   W = 2  : 32 B,   64 chars — one 32-byte sector per Occ (L2-resident indexes)
+//   W = 6  : 64 B,  192 chars — two lines per 128-byte DRAM fetch
+//   W = 14 : 128 B, 448 chars — one line per 128-byte DRAM fetch
 //
 // base[s] = occurrences of symbol s strictly before the line in the raw packed
 // transform ('$' packed as A, exactly like the reference's bucket bases,
-// index.py:83-91); w[0], w[1] hold characters 0..31 and 32..63 of the line in
-// the reference's bit order (character j in bits 2j..2j+1, alphabet.py:53-56).
-// Any Occ(b, p) therefore reads exactly one 32-byte sector, fetched with one
-// 256-bit load (LDG.E.ENL2.256).
+// index.py:83-91); w[] holds the line's characters in the reference's bit
+// order (character j in bits 2j..2j+1 of its word, alphabet.py:53-56).  Any
+// Occ(b, p) reads one line, with 256-bit loads (LDG.E.ENL2.256), predicated so
+// only the sectors up to p are fetched.  B200 serves a random miss with a
+// 128-byte DRAM fetch (measured, tools/micro/gather.cu), so for HBM-resident
+// indexes the characters per 128 bytes decide throughput; for L2-resident
+// ones the sectors per Occ do.  The host picks W by index size.
 //
 // In-line rank by masked popcount (the GPU-native form of the paper's nibble
 // pipeline, kernels.py:161-211): with lo = w & 0x55.., hi = (w >> 1) & 0x55..
 // and a mask M of the fields 0..r,
 //     T = popc(lo & hi & M)      G = popc(hi & M) - T
 //     C = popc(lo & M) - T       A = (r + 1) - popc(hi & M) - popc(lo & M) + T
-// The A lane then drops the terminator once p >= sentinel_row (occ.py:39-40,
-// 54-55, 92-95).
+// Two words are interleaved (even/odd bits) so each word pair costs three
+// 64-bit popcounts.  The A lane then drops the terminator once
+// p >= sentinel_row (occ.py:39-40, 54-55, 92-95).
 #pragma once
 
 #include <cstdint>
 
 namespace fmg {
 
-struct __align__(32) Line {
+template <int W>
+struct __align__(16) Line {
   uint32_t base[4];
-  uint64_t w[2];
+  uint64_t w[W];
 };
-static_assert(sizeof(Line) == 32, "line must be one 32-byte sector");
+static_assert(sizeof(Line<2>) == 32, "W=2 line must be one 32-byte sector");
+static_assert(sizeof(Line<6>) == 64, "W=6 line must be 64 bytes");
+static_assert(sizeof(Line<14>) == 128, "W=14 line must be 128 bytes");
+
+template <int W>
+struct LineTraits {
+  static constexpr uint32_t kChars = 32u * W;
+  static constexpr uint32_t kBytes = 16u + 8u * W;
+};
 
 // Everything a kernel needs about the index, passed by value (kernel params
 // live in the constant bank, so C[] is a constant-cache broadcast).
 struct IndexView {
-  const Line* lines;
+  const uint8_t* lines;
   const uint32_t* samples;  // suffix-array rows 0, 32, 64, ... (may be null)
   uint32_t n;
   uint32_t sentinel_row;
@@ -44,44 +62,70 @@ struct IndexView {
 
 constexpr uint64_t kFieldLo = 0x5555555555555555ull;
 
-// One 256-bit read-only load of a line.  kStream selects L1::no_allocate for
-// gathers without reuse (Occ microbenchmark); search kernels keep L1
-// allocation so the hot top-of-BWT lines every query starts from are L1 hits.
 template <bool kStream>
-__device__ __forceinline__ void load_line(const Line* p, uint32_t b[4], uint64_t w[2]) {
-  uint64_t a0, a1, a2, a3;
+__device__ __forceinline__ void ld256(const uint8_t* p, uint64_t& a0, uint64_t& a1, uint64_t& a2, uint64_t& a3) {
   if (kStream) {
     asm("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
         : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3)
         : "l"(p));
   } else {
-    asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
-        : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3)
-        : "l"(p));
+    asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3) : "l"(p));
   }
+}
+
+// Line index and offset of transform position p.
+template <int W>
+__device__ __forceinline__ uint32_t line_of(uint32_t p) {
+  return p / LineTraits<W>::kChars;  // constant divisor: shift for W=2, mul-hi otherwise
+}
+
+// Load line j, fetching only the 32-byte sectors that hold fields 0..r.
+// kStream selects L1::no_allocate for gathers without reuse (Occ
+// microbenchmark); search kernels keep L1 allocation so the hot top-of-BWT
+// lines every query starts from are L1 hits.
+template <int W, bool kStream>
+__device__ __forceinline__ void load_line(const IndexView& ix, uint32_t j, uint32_t rmax, uint32_t b[4],
+                                          uint64_t w[W]) {
+  const uint8_t* p = ix.lines + size_t(j) * LineTraits<W>::kBytes;
+  uint64_t a0, a1, a2, a3;
+  ld256<kStream>(p, a0, a1, a2, a3);
   b[0] = uint32_t(a0);
   b[1] = uint32_t(a0 >> 32);
   b[2] = uint32_t(a1);
   b[3] = uint32_t(a1 >> 32);
   w[0] = a2;
   w[1] = a3;
+#pragma unroll
+  for (int k = 2; k < W; k += 4) {
+    if (rmax >= 32u * k) {
+      ld256<kStream>(p + 16 + 8 * k, w[k], w[k + 1], w[k + 2], w[k + 3]);
+    } else {
+      w[k] = w[k + 1] = w[k + 2] = w[k + 3] = 0;
+    }
+  }
 }
 
-// Masks of the 2-bit fields 0..r (inclusive) of a 64-field line.
-__device__ __forceinline__ void prefix_masks(uint32_t r, uint64_t& m0, uint64_t& m1) {
-  m0 = ~0ull >> (62u - 2u * min(r, 31u));
-  m1 = (r >= 32u) ? (~0ull >> (126u - 2u * r)) : 0ull;
+// Mask of the fields of word k that lie in 0..r.
+__device__ __forceinline__ uint64_t word_mask(uint32_t r, int k) {
+  const int d = int(r) - 32 * k;
+  if (d < 0) return 0ull;
+  if (d >= 31) return ~0ull;
+  return ~0ull >> (62 - 2 * d);
 }
 
 // Counts of A, C, G, T among fields 0..r of the line (raw: '$' counts as A).
-__device__ __forceinline__ void count4(const uint64_t w[2], uint32_t r, uint32_t out[4]) {
-  uint64_t m0, m1;
-  prefix_masks(r, m0, m1);
-  const uint64_t lo0 = w[0] & kFieldLo & m0, hi0 = (w[0] >> 1) & kFieldLo & m0;
-  const uint64_t lo1 = w[1] & kFieldLo & m1, hi1 = (w[1] >> 1) & kFieldLo & m1;
-  const uint32_t t = __popcll(lo0 & hi0) + __popcll(lo1 & hi1);
-  const uint32_t h = __popcll(hi0) + __popcll(hi1);
-  const uint32_t l = __popcll(lo0) + __popcll(lo1);
+template <int W>
+__device__ __forceinline__ void count4(const uint64_t w[W], uint32_t r, uint32_t out[4]) {
+  uint32_t t = 0, h = 0, l = 0;
+#pragma unroll
+  for (int k = 0; k < W; k += 2) {
+    const uint64_t x0 = w[k] & word_mask(r, k), x1 = w[k + 1] & word_mask(r, k + 1);
+    const uint64_t lo = (x0 & kFieldLo) | ((x1 & kFieldLo) << 1);
+    const uint64_t hi = ((x0 >> 1) & kFieldLo) | (x1 & ~kFieldLo);
+    t += __popcll(lo & hi);
+    h += __popcll(hi);
+    l += __popcll(lo);
+  }
   out[3] = t;
   out[2] = h - t;
   out[1] = l - t;
@@ -89,31 +133,29 @@ __device__ __forceinline__ void count4(const uint64_t w[2], uint32_t r, uint32_t
 }
 
 // Count of one symbol among fields 0..r of the line (raw).
-__device__ __forceinline__ uint32_t count1(const uint64_t w[2], uint32_t r, uint32_t sym) {
-  uint64_t m0, m1;
-  prefix_masks(r, m0, m1);
+template <int W>
+__device__ __forceinline__ uint32_t count1(const uint64_t w[W], uint32_t r, uint32_t sym) {
   const uint64_t rep = uint64_t(sym) * kFieldLo;  // sym replicated in every field
-  uint64_t x0 = ~(w[0] ^ rep), x1 = ~(w[1] ^ rep);
-  x0 = x0 & (x0 >> 1) & kFieldLo & m0;
-  x1 = x1 & (x1 >> 1) & kFieldLo & m1;
-  return __popcll(x0) + __popcll(x1);
+  uint32_t c = 0;
+#pragma unroll
+  for (int k = 0; k < W; k += 2) {
+    uint64_t x0 = ~(w[k] ^ rep), x1 = ~(w[k + 1] ^ rep);
+    x0 = x0 & (x0 >> 1) & kFieldLo & word_mask(r, k);       // matches on even bits
+    x1 = x1 & (x1 << 1) & ~kFieldLo & word_mask(r, k + 1);  // matches on odd bits
+    c += __popcll(x0 | x1);
+  }
+  return c;
 }
 
 // Symbol stored at field r of the line.
-__device__ __forceinline__ uint32_t field_at(const uint64_t w[2], uint32_t r) {
-  const uint64_t word = (r < 32u) ? w[0] : w[1];
+template <int W>
+__device__ __forceinline__ uint32_t field_at(const uint64_t w[W], uint32_t r) {
+  // branch-free select (a plain `w[r >> 5]` would spill w[] to local memory)
+  const uint32_t q = r >> 5;
+  uint64_t word = 0;
+#pragma unroll
+  for (int k = 0; k < W; ++k) word |= w[k] & (0ull - uint64_t(q == uint32_t(k)));
   return uint32_t((word >> ((r & 31u) << 1)) & 3ull);
-}
-
-// All four Occ(b, p) for 0 <= p <= n given the line holding p.
-__device__ __forceinline__ void occ4_from_line(const IndexView& ix, const uint32_t b[4],
-                                               const uint64_t w[2], uint32_t p, uint32_t out[4]) {
-  uint32_t in[4];
-  count4(w, p & 63u, in);
-  out[0] = b[0] + in[0] - (p >= ix.sentinel_row ? 1u : 0u);
-  out[1] = b[1] + in[1];
-  out[2] = b[2] + in[2];
-  out[3] = b[3] + in[3];
 }
 
 // a[i] for a runtime i without forcing the array into local memory.
@@ -124,10 +166,23 @@ __device__ __forceinline__ uint32_t c_of(const IndexView& ix, uint32_t s) {
   return s == 0u ? ix.c[0] : s == 1u ? ix.c[1] : s == 2u ? ix.c[2] : s == 3u ? ix.c[3] : ix.c[4];
 }
 
+// All four Occ(b, p) for 0 <= p <= n given the line holding p.
+template <int W>
+__device__ __forceinline__ void occ4_from_line(const IndexView& ix, const uint32_t b[4], const uint64_t w[W],
+                                               uint32_t p, uint32_t r, uint32_t out[4]) {
+  uint32_t in[4];
+  count4<W>(w, r, in);
+  out[0] = b[0] + in[0] - (p >= ix.sentinel_row ? 1u : 0u);
+  out[1] = b[1] + in[1];
+  out[2] = b[2] + in[2];
+  out[3] = b[3] + in[3];
+}
+
 // Occ(sym, p) for 0 <= p <= n given the line holding p.
-__device__ __forceinline__ uint32_t occ1_from_line(const IndexView& ix, const uint32_t b[4],
-                                                   const uint64_t w[2], uint32_t p, uint32_t sym) {
-  uint32_t v = sel4(b, sym) + count1(w, p & 63u, sym);
+template <int W>
+__device__ __forceinline__ uint32_t occ1_from_line(const IndexView& ix, const uint32_t b[4], const uint64_t w[W],
+                                                   uint32_t p, uint32_t r, uint32_t sym) {
+  uint32_t v = sel4(b, sym) + count1<W>(w, r, sym);
   if (sym == 0u && p >= ix.sentinel_row) v -= 1u;
   return v;
 }
@@ -136,9 +191,9 @@ __device__ __forceinline__ uint32_t occ1_from_line(const IndexView& ix, const ui
 // Occ(., l).  k == 0 gives lo = 0 (occ.py:74-77); the root interval (0, n)
 // needs no memory at all (Occ(b, n) = c[b+1] - c[b]).  When both ends share a
 // line it is fetched once (occ.py:86-96 does the same per bucket).
-template <bool kStream>
-__device__ __forceinline__ void occ_step(const IndexView& ix, uint32_t k, uint32_t l,
-                                         uint32_t lo[4], uint32_t hi[4]) {
+template <int W, bool kStream>
+__device__ __forceinline__ void occ_step(const IndexView& ix, uint32_t k, uint32_t l, uint32_t lo[4],
+                                         uint32_t hi[4]) {
   if (k == 0u && l == ix.n) {
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
@@ -147,28 +202,25 @@ __device__ __forceinline__ void occ_step(const IndexView& ix, uint32_t k, uint32
     }
     return;
   }
-  uint32_t bh[4], bl[4];
-  uint64_t wh[2], wl[2];
-  const uint32_t lh = l >> 6;
-  load_line<kStream>(ix.lines + lh, bh, wh);
+  constexpr uint32_t kC = LineTraits<W>::kChars;
+  const uint32_t jh = line_of<W>(l), rh = l - jh * kC;
   const bool has_low = k != 0u;
   const uint32_t low = k - 1u;
-  const uint32_t ll = has_low ? (low >> 6) : lh;
-  if (ll != lh) {
-    load_line<kStream>(ix.lines + ll, bl, wl);
-  } else {
-#pragma unroll
-    for (int s = 0; s < 4; ++s) bl[s] = bh[s];
-    wl[0] = wh[0];
-    wl[1] = wh[1];
-  }
-  occ4_from_line(ix, bh, wh, l, hi);
-  if (has_low) {
-    occ4_from_line(ix, bl, wl, low, lo);
+  const uint32_t jl = has_low ? line_of<W>(low) : jh;
+  const uint32_t rl = has_low ? low - jl * kC : 0u;
+  uint32_t bh[4], bl[4];
+  uint64_t wh[W], wl[W];
+  load_line<W, kStream>(ix, jh, rh, bh, wh);
+  if (jl != jh) {
+    load_line<W, kStream>(ix, jl, rl, bl, wl);
+    occ4_from_line<W>(ix, bl, wl, low, rl, lo);
+  } else if (has_low) {
+    occ4_from_line<W>(ix, bh, wh, low, rl, lo);
   } else {
 #pragma unroll
     for (int s = 0; s < 4; ++s) lo[s] = 0u;
   }
+  occ4_from_line<W>(ix, bh, wh, l, rh, hi);
 }
 
 }  // namespace fmg

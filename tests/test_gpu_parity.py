@@ -229,3 +229,29 @@ def test_config2_subsample_vs_oracle(gpu):
     assert np.array_equal(ms.offsets, row)
     assert np.array_equal(ms.k.astype(np.int64), k) and np.array_equal(ms.l.astype(np.int64), l)
     assert np.array_equal(ms.diffs, d)
+
+
+@pytest.mark.parametrize("words", [6, 14])
+def test_alternate_line_layouts(small_cases, gpu, words, monkeypatch):
+    """The W=6 (64 B) and W=14 (128 B) line layouts give identical results."""
+    monkeypatch.setenv("FMG_LINE_WORDS", str(words))
+    for key in ("1000_15", "2500_16", "129_11", "4_2"):
+        case = small_cases[key]
+        n = case["n"]
+        idx = fm.build_index(small_text(n, case["seed"]))
+        occ = fm.occ_pair_batch(idx, case["occ_low"], case["occ_high"])
+        assert np.array_equal(occ.astype(np.int64), np.array(case["occ"])), key
+        kl, _ = fm.exact_search_batch(idx, case["exact_patterns"])
+        assert np.array_equal(kl, np.array(case["exact_kl"])), key
+        assert list(fm.locate_rows(idx, np.arange(n + 1))) == case["locate"], key
+        sel = [i for i, zz in enumerate(case["inexact_z"]) if zz == 1]
+        ms = fm.inexact_search_batch(idx, [case["inexact_patterns"][i] for i in sel], 1)
+        for j, i in enumerate(sel):
+            a, b = case["inexact_row"][i], case["inexact_row"][i + 1]
+            assert [(r.interval.k, r.interval.l, r.diffs_used) for r in ms.results(j)] == list(
+                zip(case["inexact_k"][a:b], case["inexact_l"][a:b], case["inexact_diffs"][a:b])), key
+    wl = workloads.config1(count=1 << 20)
+    idx = fm.build_index(wl.text)
+    got = fm.occ_pair_batch(idx, wl.pairs[:, 0], wl.pairs[:, 1])
+    want = np.load(GOLDEN / "config1_head.npz")["occ"]
+    assert np.array_equal(got[: want.shape[0]], want)
