@@ -234,6 +234,49 @@ def config_of(config: str, world: int, units: int) -> dict:
 # ---------------------------------------------------------------------------
 
 
+def hbm_resident_extra(dev, lib, reps: int = 10) -> dict:
+    """Config 1-H on the same GPU: the config-1 pair distribution over the 1 Gbp
+    config-4 text, whose 500 MB line array cannot live in the 126 MB L2."""
+    import torch
+
+    import paper_1811_06127_b200 as fm
+    from paper_1811_06127_b200 import _lib, workloads
+
+    wl = workloads.config1h()
+    t0 = time.perf_counter()
+    idx = fm.build_index(wl.text, builder="gpu", device=dev.index)
+    build_s = time.perf_counter() - t0
+    dix = idx.device_index(dev.index)
+    units = wl.pairs.shape[0]
+    kl = np.empty((units, 2), dtype=np.uint32)
+    kl[:, 0] = (wl.pairs[:, 0] + 1).astype(np.uint32)
+    kl[:, 1] = wl.pairs[:, 1].astype(np.uint32)
+    d_kl = torch.from_numpy(kl.view(np.int32)).to(dev)
+    d_out = torch.empty((units, 8), dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(3):
+        _lib.check(lib.fmg_occ_pair(dix.handle, d_kl.data_ptr(), units, d_out.data_ptr(), stream.cuda_stream))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        lib.fmg_occ_pair(dix.handle, d_kl.data_ptr(), units, d_out.data_ptr(), stream.cuda_stream)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    launch_s = e0.elapsed_time(e1) / reps / 1e3
+    alg, lines = occ_step_bytes(wl.pairs)
+    peak, kind = hbm_peak()
+    achieved = alg / launch_s / 1e9
+    idx.release_device()
+    return {"workload": "config 1-H: 2^24 config-1 pairs over the 1 Gbp config-4 text (seed 5), "
+                        "500 MB line array, HBM-resident",
+            "value": units / launch_s, "unit": "occ_steps/s", "index_build_s_gpu": round(build_s, 2),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": measured_traffic("k_occ_pair", "config1h"),
+                         "peak_kind": kind, "alg_bytes_per_step": round(alg / units, 2),
+                         "sectors_per_step": round(lines / units, 4),
+                         "random_sector_roofline_steps_per_s": round(peak * 1e9 / (alg / units), 1)}}
+
+
 def run_ours(args, rank: int, local: int, world: int) -> None:
     import torch
 
@@ -418,6 +461,10 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
                "sample": f"first {sample} units of the {args.config} workload, {reps} reps; oracle/fm_oracle.c "
                          f"(C restatement of the reference path) on {th} threads of {cpu_model()}"}
 
+    # ---- config 1-H beside config 1 (rank 0, N=1): the HBM-resident regime ----
+    if args.config == "config1" and rank == 0 and world == 1 and not args.no_hbm_extra:
+        extra["hbm_resident"] = hbm_resident_extra(dev, lib)
+
     # ---- launch count: our kernels inside the timed region ----
     if launches_per_step is None:
         launches_per_step = 4  # k_inexact pass + widen + scan + gather (first pass only)
@@ -448,6 +495,7 @@ def main():
                     choices=["config1", "config1h", "config0", "config2", "config4"])
     ap.add_argument("--ref-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-hbm-extra", action="store_true", help="skip the config 1-H side measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

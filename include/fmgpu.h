@@ -69,6 +69,11 @@ int fmg_device_count(int* count);
 int fmb_suffix_array(const uint8_t* codes, uint64_t n, uint32_t* sa_out /* n+1 */);
 int fmb_build(const uint8_t* codes, uint64_t n, uint8_t* bucket_records, uint64_t* sa_samples,
               uint64_t* c, uint64_t* sentinel_row, int nthreads);
+/* Same outputs, built on GPU `device` (prefix doubling + radix sort in HBM,
+ * ~36 bytes of device memory per character).  `codes` is a HOST pointer;
+ * sa_out (n+1 entries, host) may be NULL. */
+int fmb_build_gpu(int device, const uint8_t* codes, uint64_t n, uint8_t* bucket_records,
+                  uint64_t* sa_samples, uint64_t* c, uint64_t* sentinel_row, uint32_t* sa_out);
 
 /* ---------------------------------------------------------------------------
  * Device index.

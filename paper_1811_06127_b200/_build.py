@@ -17,7 +17,7 @@ REPO_DIR = PKG_DIR.parent
 CSRC = PKG_DIR / "csrc"
 LIB_PATH = PKG_DIR / "libfmgpu.so"
 
-SOURCES = ["fmgpu.cu", "builder.cpp"]
+SOURCES = ["fmgpu.cu", "build_gpu.cu", "builder.cpp"]
 HEADERS = ["fmgpu_internal.h", "occ_device.cuh"]
 
 NVCC_FLAGS = [

@@ -25,6 +25,7 @@ PROTOTYPES: dict[str, tuple] = {
     "fmg_device_count": (ct.c_int, [ct.POINTER(ct.c_int)]),
     "fmb_suffix_array": (ct.c_int, [_vp, ct.c_uint64, _vp]),
     "fmb_build": (ct.c_int, [_vp, ct.c_uint64, _vp, _vp, _vp, _vp, ct.c_int]),
+    "fmb_build_gpu": (ct.c_int, [ct.c_int, _vp, ct.c_uint64, _vp, _vp, _vp, _vp, _vp]),
     "fmg_index_create": (ct.c_int, [ct.c_int, _vp, ct.c_uint64, ct.c_uint64, ct.c_uint64, _vp,
                                     ct.POINTER(_vp)]),
     "fmg_index_set_samples": (ct.c_int, [_vp, _vp, ct.c_uint64]),

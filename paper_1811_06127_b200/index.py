@@ -156,14 +156,23 @@ def build_c_table(totals: Sequence[int]) -> tuple[int, int, int, int, int]:
     return tuple(c)
 
 
+GPU_BUILD_MIN = 1 << 22  # "auto" builds on the GPU from this many characters up
+
+
 def build_index(
-    reference, records: Sequence[tuple[str, int, int]] | None = None, threads: int | None = None
+    reference, records: Sequence[tuple[str, int, int]] | None = None, threads: int | None = None,
+    builder: str = "auto", device: int | None = None,
 ) -> FmIndex:
     """Build the full index for a reference (index.py:67-101), natively.
 
     `reference` is a DNA string (either case) or an array of codes in [0, 4).
-    The suffix array is built by SA-IS in C++ (libfmgpu.so: fmb_build).
+    builder="host": suffix array by SA-IS in C++ (fmb_build); "gpu": prefix
+    doubling in HBM (fmb_build_gpu); "auto": the GPU for references of at
+    least GPU_BUILD_MIN characters when a CUDA device is visible.  Both give
+    identical indexes (the suffix array of text+'$' is unique).
     """
+    if builder not in ("auto", "host", "gpu"):
+        raise ValueError(f"unknown builder {builder!r}")
     if isinstance(reference, np.ndarray):
         codes = np.ascontiguousarray(reference, dtype=np.uint8)
         if codes.size and codes.max() > 3:
@@ -182,12 +191,26 @@ def build_index(
     c = np.zeros(5, dtype=np.uint64)
     sentinel = np.zeros(1, dtype=np.uint64)
     lib = _lib.load()
-    _lib.check(
-        lib.fmb_build(
-            codes.ctypes.data, n, rec.ctypes.data, samples.ctypes.data, c.ctypes.data,
-            sentinel.ctypes.data, int(threads or os.cpu_count() or 1),
+    if builder == "auto":
+        builder = "gpu" if n >= GPU_BUILD_MIN and _lib.device_count() > 0 else "host"
+    if builder == "gpu":
+        from .device import current_device, require_gpu
+
+        require_gpu()
+        dev = current_device() if device is None else int(device)
+        _lib.check(
+            lib.fmb_build_gpu(
+                dev, codes.ctypes.data, n, rec.ctypes.data, samples.ctypes.data, c.ctypes.data,
+                sentinel.ctypes.data, None,
+            )
         )
-    )
+    else:
+        _lib.check(
+            lib.fmb_build(
+                codes.ctypes.data, n, rec.ctypes.data, samples.ctypes.data, c.ctypes.data,
+                sentinel.ctypes.data, int(threads or os.cpu_count() or 1),
+            )
+        )
     return FmIndex(n, c.tolist(), rec, int(sentinel[0]), samples, spans)
 
 

@@ -25,11 +25,14 @@ _lib.check(lib.fmgx_set_l2_fetch_granularity(0, gran, ct.byref(prev)))
 print("l2 fetch granularity: previous", prev.value, "now", gran)
 if which == "config1":
     idx, n = fm.build_index(workloads.config1().text), 1 << 24
+elif which == "config1h":
+    wl = workloads.config1h()
+    idx, n = fm.build_index(wl.text, builder="gpu"), wl.text.size
 elif which == "synthetic_3G":
     idx, n = synthetic_index(3_000_000_000), 3_000_000_000
 else:
     idx, n = synthetic_index(1_000_000_000), 1_000_000_000
-pairs = workloads.occ_pairs(n, 1 << 24, (7, 1))
+pairs = wl.pairs if which == "config1h" else workloads.occ_pairs(n, 1 << 24, (7, 1))
 kl = np.stack([pairs[:, 0] + 1, pairs[:, 1]], 1).astype(np.uint32)
 d_kl = torch.from_numpy(kl.view(np.int32)).cuda()
 d_out = torch.empty((kl.shape[0], 8), dtype=torch.int32, device="cuda")
