@@ -253,5 +253,8 @@ def test_alternate_line_layouts(small_cases, gpu, words, monkeypatch):
     wl = workloads.config1(count=1 << 20)
     idx = fm.build_index(wl.text)
     got = fm.occ_pair_batch(idx, wl.pairs[:, 0], wl.pairs[:, 1])
-    want = np.load(GOLDEN / "config1_head.npz")["occ"]
-    assert np.array_equal(got[: want.shape[0]], want)
+    want = orc.occ_pair_batch(orc.OracleIndex(idx), wl.pairs[:, 0], wl.pairs[:, 1])
+    assert np.array_equal(got, want)
+    pats = workloads.substrings(wl.text, np.arange(0, 1 << 20, 97)[:5000], 24)
+    kl, _ = fm.exact_search_batch(idx, pats)
+    assert np.array_equal(kl, orc.exact_batch(orc.OracleIndex(idx), pats))
