@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -20,6 +21,7 @@
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
 #include "fmgpu_internal.h"
 #include "occ_device.cuh"
@@ -202,6 +204,7 @@ struct PackedPatterns {  // fixed length m <= 32, char j in bits 2j..2j+1
 struct CodePatterns {  // codes[offsets[q] .. offsets[q+1])
   const uint8_t* codes;
   const uint64_t* offsets;
+  const ulonglong2* packed = nullptr;  // inexact, m <= 64: 2-bit packed copy (k_pack_patterns)
 };
 
 // Exact backward search, one pattern per thread at a time.  When a lane's
@@ -273,14 +276,13 @@ __global__ void __launch_bounds__(256) k_exact(IndexView ix, PackedPatterns pp, 
 
 // ----- bounded-difference search -----------------------------------------
 
-// Per-thread scratch, interleaved (element e of thread t at e*T + t) so that
-// lanes at equal stack depth touch adjacent words.
+// Per-thread global scratch for the inexact engine, warp-blocked (element e
+// of lane L of warp w at (w*N + e)*32 + L) so a warp's region is contiguous.
+// The DFS stack itself lives in shared memory (see k_inexact).
 struct InexactScratch {
-  uint2* stk_kl;     // S entries: interval of a pending node
-  uint32_t* stk_ib;  // S entries: (i + 1) << 16 | budget
-  uint2* res_kl;     // R entries: distinct result intervals
-  uint32_t* res_u;   // R entries: smallest difference count
-  uint8_t* dlb;      // Mmax entries: lower bound D[i] (long patterns only)
+  uint4* table;     // H = 2R slots {k, l, epoch, used}: open-addressing dedup of results
+  uint32_t* slots;  // R entries: occupied table slots, in insertion order
+  uint8_t* dlb;     // Mmax entries: lower bound D[i] (long patterns only)
   uint32_t S, R, Mmax;
   uint64_t T;
 };
@@ -296,7 +298,9 @@ struct InexactOut {
   uint8_t pass;
   uint32_t* fail_list;  // patterns to retry with larger capacities
   unsigned long long* fail_count;
+  unsigned long long* next;  // work-queue cursor
   unsigned long long* steps;
+  unsigned long long* unsorted;  // patterns written with > 4 results (post-sorted)
 };
 
 // Reference semantics (search.py:120-159): nodes (i, budget, k, l) from the
@@ -307,6 +311,13 @@ struct InexactOut {
 // set of (interval, min diffs) the DFS reaches does not depend on visiting
 // order, so the traversal order is free.
 //
+// Visiting order: of a node's children the match child (same budget) is
+// pushed first, then the budget-1 children, and the LAST child emitted is
+// not pushed but continued in registers.  A budget-0 node has only its match
+// child, so budget-0 chains — most of the steps — never touch the stack;
+// the stack stays budget-monotone with at most 8 entries per budget level,
+// i.e. depth <= 8(z + 1), small enough for shared memory.
+//
 // Lower-bound prune (result-preserving): before the DFS, one right-to-left
 // exact pass with resets splits W into disjoint segments absent from the
 // text; D(i) = number of those segments lying inside W[0..i].  Every way of
@@ -314,65 +325,93 @@ struct InexactOut {
 // segment with its own edit, so a node with D(i) > budget yields nothing and
 // is never pushed.  (BWA's D array, computed with the forward index only.)
 template <bool kShort, int W>
-__global__ void __launch_bounds__(256) k_inexact(IndexView ix, CodePatterns cp, const uint32_t* __restrict__ list,
+__global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, const uint32_t* __restrict__ list,
                                                  uint64_t count, uint32_t z, InexactScratch sc, InexactOut out) {
-  const uint64_t T = sc.T;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t S = sc.S, nt = blockDim.x, tid = threadIdx.x;
+  uint2* s_kl = reinterpret_cast<uint2*>(smem);               // [S][nt]
+  uint32_t* s_ib = reinterpret_cast<uint32_t*>(s_kl + S * nt);  // [S][nt]
   const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= T) return;
-  uint64_t slot = t;
+  if (t >= sc.T) return;
   uint64_t my_steps = 0;
+  const uint64_t wbase = t >> 5, lane = t & 31u;
+  auto HI = [&](uint32_t e) -> uint64_t { return (wbase * (2u * sc.R) + e) * 32u + lane; };
+  auto LI = [&](uint32_t e) -> uint64_t { return (wbase * sc.R + e) * 32u + lane; };
+  uint32_t epoch = 0;  // per-thread pattern counter: table slots of older patterns read as empty
+  auto DI = [&](uint32_t e) -> uint64_t { return (wbase * sc.Mmax + e) * 32u + lane; };
 
   // per-pattern state
   bool have = false;
   uint64_t q = 0;
   const uint8_t* codes = nullptr;
   int m = 0;
-  uint64_t pw[2] = {0, 0};   // kShort: the pattern, packed
-  uint64_t dbits = 0;        // kShort: right ends of absent segments
-  int phase = 0;             // 0: lower-bound pass, 1: DFS
-  int pos = 0, seg_end = 0;  // lower-bound pass cursor
-  uint32_t kd = 0, ld = 0;   // lower-bound pass interval
+  uint64_t pw0 = 0, pw1 = 0;  // kShort: the pattern, packed
+  uint64_t dbits = 0;         // kShort: right ends of absent segments
+  int phase = 0;              // 0: lower-bound pass, 1: DFS
+  int pos = 0, seg_end = 0;   // lower-bound pass cursor
+  uint32_t kd = 0, ld = 0;    // lower-bound pass interval
   uint32_t sp = 0, nres = 0;
   bool overflow = false;
+  bool cur_valid = false;  // DFS node held in registers
+  int ci = 0;
+  uint32_t cb = 0, ck = 0, cl = 0;
 
   auto sym_at = [&](int i) -> uint32_t {
-    if (kShort) return uint32_t((i < 32 ? pw[0] : pw[1]) >> ((i & 31) << 1)) & 3u;
+    if (kShort) return uint32_t((i < 32 ? pw0 : pw1) >> ((i & 31) << 1)) & 3u;
     return uint32_t(__ldg(codes + i));
   };
   auto dlb = [&](int i) -> uint32_t {
     if (kShort) return __popcll(dbits & ((2ull << i) - 1ull));
-    return sc.dlb[uint64_t(i) * T + t];
+    return sc.dlb[DI(uint32_t(i))];
   };
+  // best[(k, l)] = min used (search.py:127-134) in a per-thread hash table
   auto record = [&](uint32_t k, uint32_t l, uint32_t used) {
-    for (uint32_t r = 0; r < nres; ++r) {
-      const uint2 e = sc.res_kl[uint64_t(r) * T + t];
+    const uint32_t H = 2u * sc.R;
+    uint32_t h = (k * 0x9E3779B1u ^ l * 0x85EBCA77u) & (H - 1u);
+    for (uint32_t probe = 0; probe < H; ++probe, h = (h + 1u) & (H - 1u)) {
+      uint4 e = sc.table[HI(h)];
+      if (e.z != epoch) {  // empty for this pattern: insert
+        if (nres == sc.R) {
+          overflow = true;
+          return;
+        }
+        sc.table[HI(h)] = make_uint4(k, l, epoch, used);
+        sc.slots[LI(nres)] = h;
+        ++nres;
+        return;
+      }
       if (e.x == k && e.y == l) {
-        uint32_t* u = &sc.res_u[uint64_t(r) * T + t];
-        if (used < *u) *u = used;
+        if (used < e.w) sc.table[HI(h)].w = used;
         return;
       }
     }
-    if (nres == sc.R) {
-      overflow = true;
-      return;
-    }
-    sc.res_kl[uint64_t(nres) * T + t] = make_uint2(k, l);
-    sc.res_u[uint64_t(nres) * T + t] = used;
-    ++nres;
+    overflow = true;
   };
-  auto push = [&](int i, uint32_t budget, uint32_t k, uint32_t l) {
+  // Children are emitted in push order; the last viable one becomes the
+  // register-held continue node, earlier ones go to the stack.
+  bool nx_valid = false;
+  int nxi = 0;
+  uint32_t nxb = 0, nxk = 0, nxl = 0;
+  auto emit = [&](int i, uint32_t budget, uint32_t k, uint32_t l) {
     if (i < 0) {
       record(k, l, z - budget);
       return;
     }
     if (dlb(i) > budget) return;  // lower-bound prune
-    if (sp == sc.S) {
-      overflow = true;
-      return;
+    if (nx_valid) {
+      if (sp == S) {
+        overflow = true;
+      } else {
+        s_kl[sp * nt + tid] = make_uint2(nxk, nxl);
+        s_ib[sp * nt + tid] = (uint32_t(nxi + 1) << 16) | nxb;
+        ++sp;
+      }
     }
-    sc.stk_kl[uint64_t(sp) * T + t] = make_uint2(k, l);
-    sc.stk_ib[uint64_t(sp) * T + t] = (uint32_t(i + 1) << 16) | budget;
-    ++sp;
+    nx_valid = true;
+    nxi = i;
+    nxb = budget;
+    nxk = k;
+    nxl = l;
   };
   auto fail = [&]() {
     const unsigned long long f = atomicAdd(out.fail_count, 1ull);
@@ -384,21 +423,6 @@ __global__ void __launch_bounds__(256) k_inexact(IndexView ix, CodePatterns cp, 
       fail();
       return;
     }
-    // insertion sort by (k, l); (k, l) are unique after the dedup
-    for (uint32_t a = 1; a < nres; ++a) {
-      const uint2 e = sc.res_kl[uint64_t(a) * T + t];
-      const uint32_t u = sc.res_u[uint64_t(a) * T + t];
-      uint32_t b = a;
-      while (b > 0) {
-        const uint2 p = sc.res_kl[uint64_t(b - 1) * T + t];
-        if (p.x < e.x || (p.x == e.x && p.y < e.y)) break;
-        sc.res_kl[uint64_t(b) * T + t] = p;
-        sc.res_u[uint64_t(b) * T + t] = sc.res_u[uint64_t(b - 1) * T + t];
-        --b;
-      }
-      sc.res_kl[uint64_t(b) * T + t] = e;
-      sc.res_u[uint64_t(b) * T + t] = u;
-    }
     uint64_t o = 0;
     if (nres) {
       o = atomicAdd(out.total, (unsigned long long)nres);
@@ -406,9 +430,53 @@ __global__ void __launch_bounds__(256) k_inexact(IndexView ix, CodePatterns cp, 
         fail();
         return;
       }
-      for (uint32_t r = 0; r < nres; ++r) {
-        out.kl[o + r] = sc.res_kl[uint64_t(r) * T + t];
-        out.diffs[o + r] = uint8_t(sc.res_u[uint64_t(r) * T + t]);
+      if (nres <= 4) {  // sort by (k, l) in registers; (k, l) are unique
+        uint4 r0 = sc.table[HI(sc.slots[LI(0)])], r1 = r0, r2 = r0, r3 = r0;
+        if (nres > 1) r1 = sc.table[HI(sc.slots[LI(1)])];
+        if (nres > 2) r2 = sc.table[HI(sc.slots[LI(2)])];
+        if (nres > 3) r3 = sc.table[HI(sc.slots[LI(3)])];
+        auto lt = [](const uint4& a, const uint4& b) { return a.x < b.x || (a.x == b.x && a.y < b.y); };
+        auto cswap = [&](uint4& a, uint4& b) {
+          if (lt(b, a)) {
+            const uint4 t2 = a;
+            a = b;
+            b = t2;
+          }
+        };
+        if (nres == 2) cswap(r0, r1);
+        if (nres == 3) {
+          cswap(r0, r1);
+          cswap(r1, r2);
+          cswap(r0, r1);
+        }
+        if (nres == 4) {
+          cswap(r0, r1);
+          cswap(r2, r3);
+          cswap(r0, r2);
+          cswap(r1, r3);
+          cswap(r1, r2);
+        }
+        out.kl[o] = make_uint2(r0.x, r0.y);
+        out.diffs[o] = uint8_t(r0.w);
+        if (nres > 1) {
+          out.kl[o + 1] = make_uint2(r1.x, r1.y);
+          out.diffs[o + 1] = uint8_t(r1.w);
+        }
+        if (nres > 2) {
+          out.kl[o + 2] = make_uint2(r2.x, r2.y);
+          out.diffs[o + 2] = uint8_t(r2.w);
+        }
+        if (nres > 3) {
+          out.kl[o + 3] = make_uint2(r3.x, r3.y);
+          out.diffs[o + 3] = uint8_t(r3.w);
+        }
+      } else {  // unsorted; the host runs a segmented sort afterwards
+        for (uint32_t r = 0; r < nres; ++r) {
+          const uint4 e = sc.table[HI(sc.slots[LI(r)])];
+          out.kl[o + r] = make_uint2(e.x, e.y);
+          out.diffs[o + r] = uint8_t(e.w);
+        }
+        atomicAdd(out.unsorted, 1ull);
       }
     }
     out.res_off[q] = o;
@@ -418,29 +486,25 @@ __global__ void __launch_bounds__(256) k_inexact(IndexView ix, CodePatterns cp, 
 
   while (true) {
     // ---- acquire the next node that needs an Occ step ----
-    uint32_t k = 0, l = 0, budget = 0;
-    int i = 0;
+    uint32_t k = 0, l = 0;
     bool stepping = false;
     while (!stepping) {
       if (!have) {
+        // persistent work queue: one atomic per pattern balances the
+        // per-pattern DFS sizes across lanes and SMs
+        const unsigned long long slot = atomicAdd(out.next, 1ull);
         if (slot >= count) break;
         q = list ? list[slot] : slot;
-        slot += T;
         const uint64_t o0 = cp.offsets[q], o1 = cp.offsets[q + 1];
         codes = cp.codes + o0;
         m = int(o1 - o0);
         if (kShort) {
-          pw[0] = pw[1] = 0;
-          for (int j = 0; j < m; ++j) {
-            const uint64_t v = uint64_t(__ldg(codes + j) & 3u) << ((j & 31) << 1);
-            if (j < 32)
-              pw[0] |= v;
-            else
-              pw[1] |= v;
-          }
+          const ulonglong2 pk = cp.packed[q];
+          pw0 = pk.x;
+          pw1 = pk.y;
           dbits = 0;
         } else {
-          for (int j = 0; j < m; ++j) sc.dlb[uint64_t(j) * T + t] = 0;
+          for (int j = 0; j < m; ++j) sc.dlb[DI(uint32_t(j))] = 0;
         }
         phase = 0;
         pos = m - 1;
@@ -448,7 +512,9 @@ __global__ void __launch_bounds__(256) k_inexact(IndexView ix, CodePatterns cp, 
         kd = 0;  // the pass starts from the root interval [0, n]
         ld = ix.n;
         sp = nres = 0;
+        ++epoch;
         overflow = false;
+        cur_valid = false;
         have = true;
       }
       if (phase == 0) {
@@ -456,31 +522,46 @@ __global__ void __launch_bounds__(256) k_inexact(IndexView ix, CodePatterns cp, 
           if (!kShort) {  // flags of segment ends -> D(i) = ends at or before i
             uint32_t acc = 0;
             for (int j = 0; j < m; ++j) {
-              uint8_t* d = &sc.dlb[uint64_t(j) * T + t];
+              uint8_t* d = &sc.dlb[DI(uint32_t(j))];
               acc += *d;
               *d = uint8_t(min(acc, 255u));
             }
           }
           phase = 1;
-          push(m - 1, z, 0u, ix.n);  // root (search.py:125)
+          // root (search.py:125), held in registers
+          cur_valid = dlb(m - 1) <= z;
+          ci = m - 1;
+          cb = z;
+          ck = 0u;
+          cl = ix.n;
           continue;
         }
         k = kd;
         l = ld;
         stepping = true;
       } else {
-        if (overflow || sp == 0) {
+        if (overflow) {
           finish();
           have = false;
           continue;
         }
-        --sp;
-        const uint2 e = sc.stk_kl[uint64_t(sp) * T + t];
-        const uint32_t ib = sc.stk_ib[uint64_t(sp) * T + t];
-        k = e.x;
-        l = e.y;
-        i = int(ib >> 16) - 1;
-        budget = ib & 0xFFFFu;
+        if (!cur_valid) {
+          if (sp == 0) {
+            finish();
+            have = false;
+            continue;
+          }
+          --sp;
+          const uint2 e = s_kl[sp * nt + tid];
+          const uint32_t ib = s_ib[sp * nt + tid];
+          ci = int(ib >> 16) - 1;
+          cb = ib & 0xFFFFu;
+          ck = e.x;
+          cl = e.y;
+          cur_valid = true;
+        }
+        k = ck;
+        l = cl;
         stepping = true;
       }
     }
@@ -493,13 +574,13 @@ __global__ void __launch_bounds__(256) k_inexact(IndexView ix, CodePatterns cp, 
 
     if (phase == 0) {
       const uint32_t b = sym_at(pos);
-      const uint32_t cb = c_of(ix, b);
-      const uint32_t k2 = cb + sel4(lo, b) + 1u, l2 = cb + sel4(hi, b);
+      const uint32_t cbase = c_of(ix, b);
+      const uint32_t k2 = cbase + sel4(lo, b) + 1u, l2 = cbase + sel4(hi, b);
       if (k2 > l2) {  // W[pos..seg_end] is absent from the text
         if (kShort)
           dbits |= 1ull << seg_end;
         else
-          sc.dlb[uint64_t(seg_end) * T + t] = 1;
+          sc.dlb[DI(uint32_t(seg_end))] = 1;
         kd = 0;
         ld = ix.n;
         seg_end = pos - 1;
@@ -511,19 +592,32 @@ __global__ void __launch_bounds__(256) k_inexact(IndexView ix, CodePatterns cp, 
       continue;
     }
 
-    // DFS expansion (search.py:135-152)
+    // ---- DFS expansion of the register node (search.py:135-152) ----
+    const int i = ci;
+    const uint32_t budget = cb;
     const uint32_t want = sym_at(i);
-    if (budget > 0) push(i - 1, budget - 1, k, l);  // skip
-#pragma unroll
-    for (uint32_t b = 0; b < 4; ++b) {
-      const uint32_t k2 = ix.c[b] + lo[b] + 1u, l2 = ix.c[b] + hi[b];
-      if (k2 > l2) continue;
-      if (budget > 0) push(i, budget - 1, k2, l2);  // insert
-      if (b == want)
-        push(i - 1, budget, k2, l2);  // match
-      else if (budget > 0)
-        push(i - 1, budget - 1, k2, l2);  // mismatch
+    nx_valid = false;
+    // match child first (pushed deepest), then the budget-1 children
+    {
+      const uint32_t cw = c_of(ix, want);
+      const uint32_t k2 = cw + sel4(lo, want) + 1u, l2 = cw + sel4(hi, want);
+      if (k2 <= l2) emit(i - 1, budget, k2, l2);  // match
     }
+    if (budget > 0) {
+      emit(i - 1, budget - 1, k, l);  // skip
+#pragma unroll
+      for (uint32_t b = 0; b < 4; ++b) {
+        const uint32_t k2 = ix.c[b] + lo[b] + 1u, l2 = ix.c[b] + hi[b];
+        if (k2 > l2) continue;
+        emit(i, budget - 1, k2, l2);  // insert
+        if (b != want) emit(i - 1, budget - 1, k2, l2);  // mismatch
+      }
+    }
+    cur_valid = nx_valid;
+    ci = nxi;
+    cb = nxb;
+    ck = nxk;
+    cl = nxl;
   }
   if (out.steps) atomicAdd(out.steps, (unsigned long long)my_steps);
 }
@@ -543,6 +637,59 @@ __global__ void k_gather_matches(uint64_t count, const uint64_t* __restrict__ re
     k_out[d + r] = e.x;
     l_out[d + r] = e.y;
     d_out[d + r] = src_d[s + r];
+  }
+}
+
+// 2-bit packing of patterns of length <= 64 for k_inexact (one coalesced-ish
+// pass so the search kernel starts a pattern with a single 16-byte load).
+__global__ void k_pack_patterns(const uint8_t* __restrict__ codes, const uint64_t* __restrict__ offsets,
+                                uint64_t count, ulonglong2* __restrict__ packed) {
+  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  const uint64_t a = offsets[q], b = offsets[q + 1];
+  uint64_t w0 = 0, w1 = 0;
+  for (uint64_t j = a; j < b && j < a + 64; ++j) {
+    const uint32_t f = uint32_t(j - a);
+    const uint64_t v = uint64_t(codes[j] & 3u) << ((f & 31u) << 1);
+    if (f < 32u)
+      w0 |= v;
+    else
+      w1 |= v;
+  }
+  packed[q] = make_ulonglong2(w0, w1);
+}
+
+// Pattern batch validation on the device: offsets[0] == 0, every pattern
+// non-empty (search.py:83-84), codes in [0, 4); also the longest pattern.
+__global__ void k_check_patterns(const uint8_t* __restrict__ codes, const uint64_t* __restrict__ offsets,
+                                 uint64_t count, unsigned long long* __restrict__ max_len,
+                                 uint32_t* __restrict__ err) {
+  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  const uint64_t a = offsets[q], b = offsets[q + 1];
+  if (q == 0 && a != 0) atomicOr(err, 4u);
+  if (b <= a) {
+    atomicOr(err, 1u);
+    return;
+  }
+  atomicMax(max_len, (unsigned long long)(b - a));
+  for (uint64_t j = a; j < b; ++j)
+    if (codes[j] > 3) atomicOr(err, 2u);
+}
+
+__global__ void k_pack_keys(uint64_t n, const uint32_t* __restrict__ k, const uint32_t* __restrict__ l,
+                            uint64_t* __restrict__ keys) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) keys[i] = (uint64_t(k[i]) << 32) | l[i];
+}
+
+__global__ void k_unpack_keys(uint64_t n, const uint64_t* __restrict__ keys, const uint8_t* __restrict__ d_in,
+                              uint32_t* __restrict__ k, uint32_t* __restrict__ l, uint8_t* __restrict__ d_out) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) {
+    k[i] = uint32_t(keys[i] >> 32);
+    l[i] = uint32_t(keys[i]);
+    d_out[i] = d_in[i];
   }
 }
 
@@ -808,7 +955,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
   res->device = ix->device;
   res->patterns = count;
   try {
-    FMG_CK(cudaMalloc(&res->row_off, (count + 1) * sizeof(uint64_t)));
+    FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->row_off), (count + 1) * sizeof(uint64_t), s));
     FMG_CK(cudaMemsetAsync(res->row_off, 0, sizeof(uint64_t), s));
     if (count == 0) {
       FMG_CK(cudaStreamSynchronize(s));
@@ -821,45 +968,56 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       constexpr int W = decltype(wt)::value;
       kfn = short_pat ? (const void*)k_inexact<true, W> : (const void*)k_inexact<false, W>;
     });
-    int per_sm = 0;
-    FMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 256, 0));
-    per_sm = std::max(per_sm, 1);
+    int smem_optin = 0;
+    FMG_CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ix->device));
 
     DevBuf<uint64_t> res_off(count, s);
     DevBuf<uint32_t> res_cnt(count, s);
     DevBuf<uint8_t> res_pass(count, s);
-    DevBuf<unsigned long long> counters(4, s);  // total, fail_count, steps, spare
+    DevBuf<unsigned long long> counters(5, s);  // total, fail_count, steps, queue cursor, unsorted
     FMG_CK(cudaMemsetAsync(res_pass.ptr, 0xFF, count, s));
     FMG_CK(cudaMemsetAsync(counters.ptr + 2, 0, sizeof(unsigned long long), s));
+    FMG_CK(cudaMemsetAsync(counters.ptr + 4, 0, sizeof(unsigned long long), s));
 
+    DevBuf<ulonglong2> packed(short_pat ? count : 0, s);
+    if (short_pat) {
+      k_pack_patterns<<<unsigned((count + 255) / 256), 256, 0, s>>>(codes, offsets, count, packed.ptr);
+      FMG_CK(cudaGetLastError());
+    }
     std::vector<DevBuf<uint2>> pass_kl;
     std::vector<DevBuf<uint8_t>> pass_d;
     DevBuf<uint32_t> lists[2] = {DevBuf<uint32_t>(count, s), DevBuf<uint32_t>(count, s)};
     const uint32_t* list = nullptr;  // pass 0: every pattern
     uint64_t pending = count;
-    uint32_t R = 64;
+    uint32_t R = 128;  // results per pattern before a retry (hash table of 2R slots)
     uint64_t cap = std::max<uint64_t>(count * 4, 1u << 20);
-    const uint32_t S = uint32_t(9 * (max_len + z + 1) + 2);
+    // Stack: depth <= 8(z+1) with the budget-ordered pushes of k_inexact;
+    // 9(m+z+1)+2 bounds any visiting order.  Grown on overflow.
+    const uint32_t S_max = uint32_t(9 * (max_len + z + 1) + 2);
+    uint32_t S = std::min<uint32_t>(S_max, 8 * (z + 1) + 1);
     for (int pass = 0; pending > 0; ++pass) {
       FMG_REQUIRE(pass < 250, "inexact search did not converge");
+      int nt = 128;
+      while (nt > 32 && size_t(S) * 12 * nt > size_t(96) << 10) nt /= 2;
+      const size_t smem = size_t(S) * 12 * nt;
+      FMG_REQUIRE(smem <= size_t(smem_optin), "inexact search stack does not fit in shared memory");
+      FMG_CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      int per_sm = 0;
+      FMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, nt, smem));
+      per_sm = std::max(per_sm, 1);
       // threads: full residency, bounded by a scratch budget of ~2 GiB
-      const uint64_t per_thread = uint64_t(S) * 12 + uint64_t(R) * 8 + (short_pat ? 0 : max_len);
-      uint64_t T = uint64_t(per_sm) * ix->sms * 256;
-      const uint64_t budget_bytes = 2ull << 30;
-      T = std::min<uint64_t>(T, std::max<uint64_t>(256, budget_bytes / per_thread));
-      T = std::min<uint64_t>(T, ((pending + 255) / 256) * 256);
-      T = std::max<uint64_t>(256, (T / 256) * 256);
+      const uint64_t per_thread = uint64_t(R) * (2 * 16 + 4) + (short_pat ? 0 : max_len);
+      uint64_t T = uint64_t(per_sm) * ix->sms * nt;
+      T = std::min<uint64_t>(T, std::max<uint64_t>(nt, (2ull << 30) / per_thread));
+      T = std::min<uint64_t>(T, ((pending + nt - 1) / nt) * nt);
+      T = std::max<uint64_t>(nt, (T / nt) * nt);
       InexactScratch sc{};
-      DevBuf<uint2> stk_kl(uint64_t(S) * T, s);
-      DevBuf<uint32_t> stk_ib(uint64_t(S) * T, s);
-      DevBuf<uint2> rkl(uint64_t(R) * T, s);
-      DevBuf<uint32_t> ru(uint64_t(R) * T, s);
+      DevBuf<uint4> table(uint64_t(2 * R) * T, s);
+      DevBuf<uint32_t> slots(uint64_t(R) * T, s);
       DevBuf<uint8_t> dl(short_pat ? 0 : max_len * T, s);
-      if (!short_pat) FMG_CK(cudaMemsetAsync(dl.ptr, 0, max_len * T, s));
-      sc.stk_kl = stk_kl.ptr;
-      sc.stk_ib = stk_ib.ptr;
-      sc.res_kl = rkl.ptr;
-      sc.res_u = ru.ptr;
+      FMG_CK(cudaMemsetAsync(table.ptr, 0, uint64_t(2 * R) * T * sizeof(uint4), s));  // epoch 0 = empty
+      sc.table = table.ptr;
+      sc.slots = slots.ptr;
       sc.dlb = dl.ptr;
       sc.S = S;
       sc.R = R;
@@ -868,6 +1026,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       pass_kl.emplace_back(cap, s);
       pass_d.emplace_back(cap, s);
       FMG_CK(cudaMemsetAsync(counters.ptr, 0, 2 * sizeof(unsigned long long), s));
+      FMG_CK(cudaMemsetAsync(counters.ptr + 3, 0, sizeof(unsigned long long), s));
       InexactOut o{};
       o.kl = pass_kl.back().ptr;
       o.diffs = pass_d.back().ptr;
@@ -880,24 +1039,45 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       o.fail_list = lists[pass & 1].ptr;
       o.fail_count = counters.ptr + 1;
       o.steps = counters.ptr + 2;
-      const unsigned blocks = unsigned(T / 256);
-      CodePatterns cp{codes, offsets};
+      o.next = counters.ptr + 3;
+      o.unsorted = counters.ptr + 4;
+      const unsigned blocks = unsigned(T / nt);
+      CodePatterns cp{codes, offsets, packed.ptr};
+      static const bool trace = std::getenv("FMG_TRACE") != nullptr;
+      cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+      if (trace) {
+        cudaEventCreate(&ev0);
+        cudaEventCreate(&ev1);
+        cudaEventRecord(ev0, s);
+      }
       with_words(ix, [&](auto wt) {
         constexpr int W = decltype(wt)::value;
         if (short_pat)
-          k_inexact<true, W><<<blocks, 256, 0, s>>>(ix->view(), cp, list, pending, z, sc, o);
+          k_inexact<true, W><<<blocks, nt, smem, s>>>(ix->view(), cp, list, pending, z, sc, o);
         else
-          k_inexact<false, W><<<blocks, 256, 0, s>>>(ix->view(), cp, list, pending, z, sc, o);
+          k_inexact<false, W><<<blocks, nt, smem, s>>>(ix->view(), cp, list, pending, z, sc, o);
       });
       FMG_CK(cudaGetLastError());
       unsigned long long host_ctr[2];
       FMG_CK(cudaMemcpyAsync(host_ctr, counters.ptr, sizeof(host_ctr), cudaMemcpyDeviceToHost, s));
       FMG_CK(cudaStreamSynchronize(s));
       const uint64_t failed = host_ctr[1];
+      if (trace) {
+        cudaEventRecord(ev1, s);
+        cudaEventSynchronize(ev1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev0, ev1);
+        fprintf(stderr, "[fmg] inexact pass %d: %llu patterns, T=%llu nt=%d S=%u R=%u smem=%zu per_sm=%d: %.3f ms, "
+                "%llu failed\n", pass, (unsigned long long)pending, (unsigned long long)T, nt, S, R, smem, per_sm,
+                ms, (unsigned long long)failed);
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+      }
       list = lists[pass & 1].ptr;
       if (failed > 0) {
         // grow whichever capacity might have been the cause
         R = std::min<uint32_t>(R * 8, 1u << 22);
+        S = std::min<uint32_t>(S_max, S * 2);
         cap = std::max<uint64_t>(cap, std::min<uint64_t>(uint64_t(host_ctr[0]) * 2, 1ull << 31));
         cap = std::max<uint64_t>(cap, failed * uint64_t(R));
         cap = std::min<uint64_t>(cap, 1ull << 31);
@@ -914,18 +1094,35 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     FMG_CK(cub::DeviceScan::InclusiveSum(tmp.ptr, tmp_bytes, c64.ptr, res->row_off + 1, count, s));
     uint64_t total = 0;
     FMG_CK(cudaMemcpyAsync(&total, res->row_off + count, sizeof(total), cudaMemcpyDeviceToHost, s));
-    unsigned long long steps = 0;
+    unsigned long long steps = 0, unsorted = 0;
     FMG_CK(cudaMemcpyAsync(&steps, counters.ptr + 2, sizeof(steps), cudaMemcpyDeviceToHost, s));
+    FMG_CK(cudaMemcpyAsync(&unsorted, counters.ptr + 4, sizeof(unsorted), cudaMemcpyDeviceToHost, s));
     FMG_CK(cudaStreamSynchronize(s));
     res->total = total;
     res->steps = steps;
-    FMG_CK(cudaMalloc(&res->k, std::max<uint64_t>(total, 1) * sizeof(uint32_t)));
-    FMG_CK(cudaMalloc(&res->l, std::max<uint64_t>(total, 1) * sizeof(uint32_t)));
-    FMG_CK(cudaMalloc(&res->diffs, std::max<uint64_t>(total, 1)));
+    FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->k), std::max<uint64_t>(total, 1) * sizeof(uint32_t), s));
+    FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->l), std::max<uint64_t>(total, 1) * sizeof(uint32_t), s));
+    FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->diffs), std::max<uint64_t>(total, 1), s));
     for (size_t p = 0; p < pass_kl.size(); ++p) {
       k_gather_matches<<<unsigned((count + 255) / 256), 256, 0, s>>>(count, res_off.ptr, res_cnt.ptr, res_pass.ptr,
                                                                      uint8_t(p), pass_kl[p].ptr, pass_d[p].ptr,
                                                                      res->row_off, res->k, res->l, res->diffs);
+      FMG_CK(cudaGetLastError());
+    }
+    if (unsorted > 0 && total > 0) {
+      // patterns with > 4 results were written unsorted: segmented sort by (k, l)
+      FMG_REQUIRE(total < (1ull << 31), "too many inexact results for one call");
+      DevBuf<uint64_t> keys(total, s), keys2(total, s);
+      DevBuf<uint8_t> d2(total, s);
+      k_pack_keys<<<unsigned((total + 255) / 256), 256, 0, s>>>(total, res->k, res->l, keys.ptr);
+      size_t sb = 0;
+      FMG_CK(cub::DeviceSegmentedSort::SortPairs(nullptr, sb, keys.ptr, keys2.ptr, res->diffs, d2.ptr, int(total),
+                                                 int(count), res->row_off, res->row_off + 1, s));
+      DevBuf<uint8_t> stmp(sb, s);
+      FMG_CK(cub::DeviceSegmentedSort::SortPairs(stmp.ptr, sb, keys.ptr, keys2.ptr, res->diffs, d2.ptr, int(total),
+                                                 int(count), res->row_off, res->row_off + 1, s));
+      k_unpack_keys<<<unsigned((total + 255) / 256), 256, 0, s>>>(total, keys2.ptr, d2.ptr, res->k, res->l,
+                                                                   res->diffs);
       FMG_CK(cudaGetLastError());
     }
     FMG_CK(cudaStreamSynchronize(s));
@@ -1213,17 +1410,24 @@ int fmg_inexact(const fmg_index* ix, const uint8_t* codes, const uint64_t* offse
     *out = nullptr;
     fmg::DeviceScope scope(ix->device);
     cudaStream_t s = as_stream(stream);
-    // the engine needs the longest pattern for its scratch sizing
+    // validate on the device and find the longest pattern (scratch sizing)
     uint64_t max_len = 0;
     if (count > 0) {
-      std::vector<uint64_t> h(count + 1);
-      FMG_CK(cudaMemcpyAsync(h.data(), offsets, (count + 1) * 8, cudaMemcpyDeviceToHost, s));
+      DevBuf<unsigned long long> ml(1, s);
+      DevBuf<uint32_t> err(1, s);
+      FMG_CK(cudaMemsetAsync(ml.ptr, 0, 8, s));
+      FMG_CK(cudaMemsetAsync(err.ptr, 0, 4, s));
+      k_check_patterns<<<unsigned((count + 255) / 256), 256, 0, s>>>(codes, offsets, count, ml.ptr, err.ptr);
+      FMG_CK(cudaGetLastError());
+      unsigned long long h_ml = 0;
+      uint32_t h_err = 0;
+      FMG_CK(cudaMemcpyAsync(&h_ml, ml.ptr, 8, cudaMemcpyDeviceToHost, s));
+      FMG_CK(cudaMemcpyAsync(&h_err, err.ptr, 4, cudaMemcpyDeviceToHost, s));
       FMG_CK(cudaStreamSynchronize(s));
-      FMG_REQUIRE(h[0] == 0, "pattern offsets must start at 0");
-      for (uint64_t q = 0; q < count; ++q) {
-        FMG_REQUIRE(h[q + 1] > h[q], "pattern is empty");
-        max_len = std::max(max_len, h[q + 1] - h[q]);
-      }
+      FMG_REQUIRE(!(h_err & 4u), "pattern offsets must start at 0");
+      FMG_REQUIRE(!(h_err & 1u), "pattern is empty");
+      FMG_REQUIRE(!(h_err & 2u), "symbol code outside [0, 4)");
+      max_len = h_ml;
     }
     *out = run_inexact(ix, codes, offsets, count, max_len, max_diff, s);
   });
@@ -1294,10 +1498,11 @@ void fmg_matches_free(fmg_matches* m) {
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(m->device);
-  if (m->row_off) cudaFree(m->row_off);
-  if (m->k) cudaFree(m->k);
-  if (m->l) cudaFree(m->l);
-  if (m->diffs) cudaFree(m->diffs);
+  // pool allocations (run_inexact synchronised its stream before returning)
+  if (m->row_off) cudaFreeAsync(m->row_off, 0);
+  if (m->k) cudaFreeAsync(m->k, 0);
+  if (m->l) cudaFreeAsync(m->l, 0);
+  if (m->diffs) cudaFreeAsync(m->diffs, 0);
   if (prev >= 0) cudaSetDevice(prev);
   delete m;
 }
