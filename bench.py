@@ -154,11 +154,27 @@ def make_workload(config: str, rank: int):
         return w.config2()
     if config == "config4":
         return w.config4()
+    if config == "config3":
+        return w.config3(n_reads=int(os.environ.get("FMG_C3_READS", 10_000_000)),
+                         n=int(os.environ.get("FMG_C3_BASES", 3_100_000_000)))
     raise SystemExit(f"unknown config {config}")
 
 
 def unit_count(wl) -> int:
-    return wl.pairs.shape[0] if wl.pairs is not None else wl.patterns.shape[0]
+    if wl.name == "config3":
+        return wl.meta["reads"]
+    if wl.pairs is not None:
+        return wl.pairs.shape[0]
+    return wl.packed.shape[0] if wl.packed is not None else wl.patterns.shape[0]
+
+
+def pattern_sample(wl, lo: int, hi: int) -> np.ndarray:
+    """(hi-lo, m) uint8 codes of a slice of a pattern workload."""
+    if wl.packed is not None:
+        from paper_1811_06127_b200.workloads import unpack_patterns
+
+        return unpack_patterns(wl.packed[lo:hi], wl.meta["m"])
+    return wl.patterns[lo:hi]
 
 
 # ---------------------------------------------------------------------------
@@ -178,16 +194,21 @@ def run_reference(args, rank: int, world: int) -> None:
     threads = cpu_threads()
     total = unit_count(wl)
     sample = min(total, args.ref_sample or {"config1": 1 << 22, "config1h": 1 << 21, "config0": 10_000,
-                                          "config2": 20_000, "config4": 1 << 21}[args.config])
+                                          "config2": 20_000, "config4": 1 << 21, "config3": 2_000}[args.config])
 
     def step(i: int):
         lo = (i * sample) % max(total - sample + 1, 1)
-        if wl.pairs is not None:
+        if wl.name == "config3":  # reads -> their 14 seeds: exact + z=1
+            per = wl.meta["seeds_per_read"]
+            seeds = pattern_sample(wl, lo * per, (lo + sample) * per)
+            orc.exact_batch(ox, seeds, threads)
+            orc.inexact_batch(ox, seeds, 1, threads)
+        elif wl.pairs is not None:
             orc.occ_pair_batch(ox, wl.pairs[lo:lo + sample, 0], wl.pairs[lo:lo + sample, 1], threads)
         elif wl.max_diff:
-            orc.inexact_batch(ox, wl.patterns[lo:lo + sample], wl.max_diff, threads)
+            orc.inexact_batch(ox, pattern_sample(wl, lo, lo + sample), wl.max_diff, threads)
         else:
-            orc.exact_batch(ox, wl.patterns[lo:lo + sample], threads)
+            orc.exact_batch(ox, pattern_sample(wl, lo, lo + sample), threads)
 
     for i in range(args.warmup):
         step(i)
@@ -215,7 +236,7 @@ def run_reference(args, rank: int, world: int) -> None:
 def metric_of(config: str) -> tuple[str, str]:
     if config in ("config1", "config1h"):
         return "Occ steps/sec (8 counts each)", "occ_steps/s"
-    return "reads/sec", "reads/s"
+    return "reads/sec", "reads/s"  # config 3: reads whose 14 seeds got exact + z=1 search
 
 
 def config_of(config: str, world: int, units: int) -> dict:
@@ -225,6 +246,8 @@ def config_of(config: str, world: int, units: int) -> dict:
         "config0": "BASELINE configs[0]: exact search, 1 Mbp iid (seed 42), 10,000 x 32 bp",
         "config2": "BASELINE configs[2]: inexact z=1, 64 Mbp repeat genome (seed 3), 1M x 32 bp seeds",
         "config4": "BASELINE configs[4]: exact, 1 Gbp iid (seed 5), 2^28 x 20 bp seeds",
+        "config3": "BASELINE configs[3]: 3.1 Gbp family genome (seed 11), 10M x 150 bp reads, 14 x 19 bp seeds "
+                   "per read, exact + z=1 on every seed",
     }[config]
     return {"workload": desc, "units_per_step_per_rank": units, "parallelism": f"query-sharded x{world}"}
 
@@ -302,7 +325,52 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
     metric, unit = metric_of(args.config)
     extra: dict = {"index_build_s": round(t_build, 2), "index_device_bytes": dix.device_bytes}
 
-    if wl.pairs is not None:
+    if wl.name == "config3":
+        m = wl.meta["m"]
+        n_seeds = wl.packed.size
+        d_pat = torch.from_numpy(wl.packed.view(np.int64)).to(dev)
+        d_out = torch.empty((n_seeds, 2), dtype=torch.int32, device=dev)
+        chunk = 1 << 24
+        steps_seen = [0]
+
+        def step():
+            _lib.check(lib.fmg_exact_packed(dix.handle, d_pat.data_ptr(), m, n_seeds, d_out.data_ptr(), sp))
+            for c0 in range(0, n_seeds, chunk):
+                h = ct.c_void_p()
+                _lib.check(lib.fmg_inexact_packed(dix.handle, d_pat.data_ptr() + 8 * c0, m,
+                                                  min(chunk, n_seeds - c0), 1, ct.byref(h), sp))
+                st_ = ct.c_uint64()
+                lib.fmg_matches_steps(h, ct.byref(st_))
+                steps_seen[0] += st_.value
+                lib.fmg_matches_free(h)
+
+        launches_per_step = 1 + ((n_seeds + chunk - 1) // chunk) * 6
+        kernel_name = "k_inexact"
+        h2d_per, d2h_per = n_seeds * 8 * 2, None
+        pin_in = torch.from_numpy(wl.packed.view(np.int64)).pin_memory()
+        pin_kl = torch.empty((n_seeds, 2), dtype=torch.int32).pin_memory()
+
+        def e2e_step():
+            _lib.check(lib.fmg_exact_packed_host(dix.handle, pin_in.data_ptr(), m, n_seeds, pin_kl.data_ptr()))
+            out_bytes = pin_kl.numel() * 4
+            for c0 in range(0, n_seeds, chunk):
+                h = ct.c_void_p()
+                cnt = min(chunk, n_seeds - c0)
+                _lib.check(lib.fmg_inexact_packed_host(dix.handle, pin_in.data_ptr() + 8 * c0, m, cnt, 1, ct.byref(h)))
+                tot = ct.c_uint64()
+                lib.fmg_matches_size(h, ct.byref(tot), None)
+                row = np.empty(cnt + 1, np.uint64)
+                kk = np.empty(tot.value, np.uint32)
+                ll = np.empty(tot.value, np.uint32)
+                dd = np.empty(tot.value, np.uint8)
+                lib.fmg_matches_copy(h, row.ctypes.data, kk.ctypes.data, ll.ctypes.data, dd.ctypes.data, 1)
+                lib.fmg_matches_free(h)
+                out_bytes += row.nbytes + kk.nbytes + ll.nbytes + dd.nbytes
+            return out_bytes
+
+        alg_bytes = alg_lines = None
+        extra["seeds_per_step"] = n_seeds
+    elif wl.pairs is not None:
         kl_h = np.empty((units, 2), dtype=np.uint32)
         kl_h[:, 0] = (wl.pairs[:, 0] + 1).astype(np.uint32)
         kl_h[:, 1] = wl.pairs[:, 1].astype(np.uint32)
@@ -324,8 +392,8 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
         def e2e_step():
             _lib.check(lib.fmg_occ_pair_host(dix.handle, pin_in.data_ptr(), units, pin_out.data_ptr()))
     else:
-        m = wl.patterns.shape[1]
-        packed = fm.pack_patterns_u64(wl.patterns) if m <= 32 else None
+        m = wl.meta["m"] if wl.packed is not None else wl.patterns.shape[1]
+        packed = wl.packed if wl.packed is not None else (fm.pack_patterns_u64(wl.patterns) if m <= 32 else None)
         z = wl.max_diff
         if z == 0 and packed is not None:
             d_pat = torch.from_numpy(packed.view(np.int64)).to(dev)
@@ -442,15 +510,25 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
 
         ox = orc.OracleIndex(idx)
         th = cpu_threads()
-        if wl.pairs is not None:
+        if wl.name == "config3":
+            sample = min(units, 2_000)
+            per = wl.meta["seeds_per_read"]
+            sp3 = pattern_sample(wl, 0, sample * per)
+
+            def fn():
+                orc.exact_batch(ox, sp3, th)
+                orc.inexact_batch(ox, sp3, 1, th)
+        elif wl.pairs is not None:
             sample = min(units, 1 << 22)
             fn = lambda: orc.occ_pair_batch(ox, wl.pairs[:sample, 0], wl.pairs[:sample, 1], th)  # noqa: E731
         elif wl.max_diff:
             sample = min(units, 20_000)
-            fn = lambda: orc.inexact_batch(ox, wl.patterns[:sample], wl.max_diff, th)  # noqa: E731
+            sp_ = pattern_sample(wl, 0, sample)
+            fn = lambda: orc.inexact_batch(ox, sp_, wl.max_diff, th)  # noqa: E731
         else:
             sample = min(units, 1 << 20)
-            fn = lambda: orc.exact_batch(ox, wl.patterns[:sample], th)  # noqa: E731
+            sp_ = pattern_sample(wl, 0, sample)
+            fn = lambda: orc.exact_batch(ox, sp_, th)  # noqa: E731
         fn()
         reps, t0 = 0, time.perf_counter()
         while reps < 1 or time.perf_counter() - t0 < 5.0:
@@ -492,7 +570,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="config1",
-                    choices=["config1", "config1h", "config0", "config2", "config4"])
+                    choices=["config1", "config1h", "config0", "config2", "config3", "config4"])
     ap.add_argument("--ref-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-hbm-extra", action="store_true", help="skip the config 1-H side measurement")

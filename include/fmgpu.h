@@ -127,6 +127,11 @@ int fmg_inexact(const fmg_index* index, const uint8_t* codes, const uint64_t* of
                 uint64_t count, int max_diff, fmg_matches** out, void* stream);
 int fmg_inexact_host(const fmg_index* index, const uint8_t* codes, const uint64_t* offsets,
                      uint64_t count, int max_diff, fmg_matches** out);
+/* Fixed-length patterns (1 <= m <= 32) packed as in fmg_exact_packed. */
+int fmg_inexact_packed(const fmg_index* index, const uint64_t* packed, uint32_t m, uint64_t count,
+                       int max_diff, fmg_matches** out, void* stream);
+int fmg_inexact_packed_host(const fmg_index* index, const uint64_t* packed, uint32_t m,
+                            uint64_t count, int max_diff, fmg_matches** out);
 /* Total number of (k, l, diffs) results and the number of patterns. */
 int fmg_matches_size(const fmg_matches* m, uint64_t* total, uint64_t* patterns);
 /* Occ steps the search executed (work counter, for reporting). */

@@ -205,6 +205,8 @@ struct CodePatterns {  // codes[offsets[q] .. offsets[q+1])
   const uint8_t* codes;
   const uint64_t* offsets;
   const ulonglong2* packed = nullptr;  // inexact, m <= 64: 2-bit packed copy (k_pack_patterns)
+  const uint64_t* packed1 = nullptr;   // inexact, fixed m <= 32 given packed by the caller
+  uint32_t fixed_m = 0;
 };
 
 // Exact backward search, one pattern per thread at a time.  When a lane's
@@ -495,15 +497,21 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
         const unsigned long long slot = atomicAdd(out.next, 1ull);
         if (slot >= count) break;
         q = list ? list[slot] : slot;
-        const uint64_t o0 = cp.offsets[q], o1 = cp.offsets[q + 1];
-        codes = cp.codes + o0;
-        m = int(o1 - o0);
-        if (kShort) {
+        if (kShort && cp.packed1) {  // caller-packed fixed-length patterns
+          m = int(cp.fixed_m);
+          pw0 = cp.packed1[q];
+          pw1 = 0;
+          dbits = 0;
+        } else if (kShort) {
+          m = int(cp.offsets[q + 1] - cp.offsets[q]);
           const ulonglong2 pk = cp.packed[q];
           pw0 = pk.x;
           pw1 = pk.y;
           dbits = 0;
         } else {
+          const uint64_t o0 = cp.offsets[q], o1 = cp.offsets[q + 1];
+          codes = cp.codes + o0;
+          m = int(o1 - o0);
           for (int j = 0; j < m; ++j) sc.dlb[DI(uint32_t(j))] = 0;
         }
         phase = 0;
@@ -946,7 +954,7 @@ void validate_patterns_host(const uint8_t* codes, const uint64_t* offsets, uint6
 }
 
 fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64_t* offsets, uint64_t count,
-                         uint64_t max_len, int max_diff, cudaStream_t s) {
+                         uint64_t max_len, int max_diff, cudaStream_t s, const uint64_t* packed1 = nullptr) {
   FMG_REQUIRE(max_diff >= 0, "difference budget is negative");
   FMG_REQUIRE(max_diff <= 0xFFFF, "difference budget above 65535 is not supported");
   FMG_REQUIRE(max_len < 0xFFFF, "pattern longer than 65534 is not supported");
@@ -979,8 +987,8 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     FMG_CK(cudaMemsetAsync(counters.ptr + 2, 0, sizeof(unsigned long long), s));
     FMG_CK(cudaMemsetAsync(counters.ptr + 4, 0, sizeof(unsigned long long), s));
 
-    DevBuf<ulonglong2> packed(short_pat ? count : 0, s);
-    if (short_pat) {
+    DevBuf<ulonglong2> packed((short_pat && !packed1) ? count : 0, s);
+    if (short_pat && !packed1) {
       k_pack_patterns<<<unsigned((count + 255) / 256), 256, 0, s>>>(codes, offsets, count, packed.ptr);
       FMG_CK(cudaGetLastError());
     }
@@ -1042,7 +1050,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       o.next = counters.ptr + 3;
       o.unsorted = counters.ptr + 4;
       const unsigned blocks = unsigned(T / nt);
-      CodePatterns cp{codes, offsets, packed.ptr};
+      CodePatterns cp{codes, offsets, packed.ptr, packed1, uint32_t(max_len)};
       static const bool trace = std::getenv("FMG_TRACE") != nullptr;
       cudaEvent_t ev0 = nullptr, ev1 = nullptr;
       if (trace) {
@@ -1453,6 +1461,43 @@ int fmg_inexact_host(const fmg_index* ix, const uint8_t* codes, const uint64_t* 
         FMG_CK(cudaMemcpyAsync(doff.ptr, offsets, (count + 1) * 8, cudaMemcpyHostToDevice, s));
       }
       *out = run_inexact(ix, dc.ptr, doff.ptr, count, max_len, max_diff, s);
+    } catch (...) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+      throw;
+    }
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  });
+}
+
+int fmg_inexact_packed(const fmg_index* ix, const uint64_t* packed, uint32_t m, uint64_t count, int max_diff,
+                       fmg_matches** out, void* stream) {
+  return fmg::guard([&] {
+    check_index(ix);
+    FMG_REQUIRE(out != nullptr, "null output pointer");
+    *out = nullptr;
+    FMG_REQUIRE(m >= 1 && m <= 32, "packed pattern length must be in [1, 32]");
+    fmg::DeviceScope scope(ix->device);
+    *out = run_inexact(ix, nullptr, nullptr, count, m, max_diff, as_stream(stream), packed);
+  });
+}
+
+int fmg_inexact_packed_host(const fmg_index* ix, const uint64_t* packed, uint32_t m, uint64_t count, int max_diff,
+                            fmg_matches** out) {
+  return fmg::guard([&] {
+    check_index(ix);
+    FMG_REQUIRE(out != nullptr, "null output pointer");
+    *out = nullptr;
+    FMG_REQUIRE(m >= 1 && m <= 32, "packed pattern length must be in [1, 32]");
+    FMG_REQUIRE(max_diff >= 0, "difference budget is negative");
+    fmg::DeviceScope scope(ix->device);
+    cudaStream_t s;
+    FMG_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    try {
+      DevBuf<uint64_t> dp(count, s);
+      if (count) FMG_CK(cudaMemcpyAsync(dp.ptr, packed, count * 8, cudaMemcpyHostToDevice, s));
+      *out = run_inexact(ix, nullptr, nullptr, count, m, max_diff, s, dp.ptr);
     } catch (...) {
       cudaStreamSynchronize(s);
       cudaStreamDestroy(s);
