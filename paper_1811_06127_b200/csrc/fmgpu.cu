@@ -302,7 +302,7 @@ struct InexactOut {
   unsigned long long* fail_count;
   unsigned long long* next;  // work-queue cursor
   unsigned long long* steps;
-  unsigned long long* unsorted;  // patterns written with > 4 results (post-sorted)
+  unsigned long long* unsorted;  // patterns written with > S results (post-sorted)
 };
 
 // Reference semantics (search.py:120-159): nodes (i, budget, k, l) from the
@@ -432,45 +432,25 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
         fail();
         return;
       }
-      if (nres <= 4) {  // sort by (k, l) in registers; (k, l) are unique
-        uint4 r0 = sc.table[HI(sc.slots[LI(0)])], r1 = r0, r2 = r0, r3 = r0;
-        if (nres > 1) r1 = sc.table[HI(sc.slots[LI(1)])];
-        if (nres > 2) r2 = sc.table[HI(sc.slots[LI(2)])];
-        if (nres > 3) r3 = sc.table[HI(sc.slots[LI(3)])];
-        auto lt = [](const uint4& a, const uint4& b) { return a.x < b.x || (a.x == b.x && a.y < b.y); };
-        auto cswap = [&](uint4& a, uint4& b) {
-          if (lt(b, a)) {
-            const uint4 t2 = a;
-            a = b;
-            b = t2;
+      if (nres <= S) {
+        // The DFS stack is empty now: reuse this thread's shared-memory stack
+        // slots to insertion-sort the results by (k, l) (unique after dedup).
+        for (uint32_t r = 0; r < nres; ++r) {
+          const uint4 e = sc.table[HI(sc.slots[LI(r)])];
+          uint32_t b = r;
+          while (b > 0) {
+            const uint2 p = s_kl[(b - 1) * nt + tid];
+            if (p.x < e.x || (p.x == e.x && p.y < e.y)) break;
+            s_kl[b * nt + tid] = p;
+            s_ib[b * nt + tid] = s_ib[(b - 1) * nt + tid];
+            --b;
           }
-        };
-        if (nres == 2) cswap(r0, r1);
-        if (nres == 3) {
-          cswap(r0, r1);
-          cswap(r1, r2);
-          cswap(r0, r1);
+          s_kl[b * nt + tid] = make_uint2(e.x, e.y);
+          s_ib[b * nt + tid] = e.w;
         }
-        if (nres == 4) {
-          cswap(r0, r1);
-          cswap(r2, r3);
-          cswap(r0, r2);
-          cswap(r1, r3);
-          cswap(r1, r2);
-        }
-        out.kl[o] = make_uint2(r0.x, r0.y);
-        out.diffs[o] = uint8_t(r0.w);
-        if (nres > 1) {
-          out.kl[o + 1] = make_uint2(r1.x, r1.y);
-          out.diffs[o + 1] = uint8_t(r1.w);
-        }
-        if (nres > 2) {
-          out.kl[o + 2] = make_uint2(r2.x, r2.y);
-          out.diffs[o + 2] = uint8_t(r2.w);
-        }
-        if (nres > 3) {
-          out.kl[o + 3] = make_uint2(r3.x, r3.y);
-          out.diffs[o + 3] = uint8_t(r3.w);
+        for (uint32_t r = 0; r < nres; ++r) {
+          out.kl[o + r] = s_kl[r * nt + tid];
+          out.diffs[o + r] = uint8_t(s_ib[r * nt + tid]);
         }
       } else {  // unsorted; the host runs a segmented sort afterwards
         for (uint32_t r = 0; r < nres; ++r) {
@@ -997,8 +977,14 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     DevBuf<uint32_t> lists[2] = {DevBuf<uint32_t>(count, s), DevBuf<uint32_t>(count, s)};
     const uint32_t* list = nullptr;  // pass 0: every pattern
     uint64_t pending = count;
-    uint32_t R = 128;  // results per pattern before a retry (hash table of 2R slots)
-    uint64_t cap = std::max<uint64_t>(count * 4, 1u << 20);
+    // R: results per pattern before a retry (per-thread hash table of 2R
+    // slots).  cap: results per pass (9 bytes each) before patterns finishing
+    // later are retried — sized from free memory so a pass rarely fills it.
+    uint32_t R = 256;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = size_t(8) << 30;
+    uint64_t cap = std::max<uint64_t>(count * 16, 1u << 20);
+    cap = std::min<uint64_t>(cap, std::max<uint64_t>(1u << 20, free_b / 4 / 9));
     // Stack: depth <= 8(z+1) with the budget-ordered pushes of k_inexact;
     // 9(m+z+1)+2 bounds any visiting order.  Grown on overflow.
     const uint32_t S_max = uint32_t(9 * (max_len + z + 1) + 2);
@@ -1016,7 +1002,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       // threads: full residency, bounded by a scratch budget of ~2 GiB
       const uint64_t per_thread = uint64_t(R) * (2 * 16 + 4) + (short_pat ? 0 : max_len);
       uint64_t T = uint64_t(per_sm) * ix->sms * nt;
-      T = std::min<uint64_t>(T, std::max<uint64_t>(nt, (2ull << 30) / per_thread));
+      T = std::min<uint64_t>(T, std::max<uint64_t>(nt, std::max<uint64_t>(2ull << 30, free_b / 8) / per_thread));
       T = std::min<uint64_t>(T, ((pending + nt - 1) / nt) * nt);
       T = std::max<uint64_t>(nt, (T / nt) * nt);
       InexactScratch sc{};
@@ -1075,9 +1061,11 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
         cudaEventSynchronize(ev1);
         float ms = 0;
         cudaEventElapsedTime(&ms, ev0, ev1);
+        unsigned long long st = 0;
+        cudaMemcpy(&st, counters.ptr + 2, 8, cudaMemcpyDeviceToHost);
         fprintf(stderr, "[fmg] inexact pass %d: %llu patterns, T=%llu nt=%d S=%u R=%u smem=%zu per_sm=%d: %.3f ms, "
-                "%llu failed\n", pass, (unsigned long long)pending, (unsigned long long)T, nt, S, R, smem, per_sm,
-                ms, (unsigned long long)failed);
+                "%llu failed, %llu steps so far\n", pass, (unsigned long long)pending, (unsigned long long)T, nt, S,
+                R, smem, per_sm, ms, (unsigned long long)failed, st);
         cudaEventDestroy(ev0);
         cudaEventDestroy(ev1);
       }
@@ -1092,6 +1080,13 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       }
       pending = failed;
       // the next pass reads `list` while writing the other list
+    }
+    static const bool trace_post = std::getenv("FMG_TRACE") != nullptr;
+    cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+    if (trace_post) {
+      cudaEventCreate(&pe0);
+      cudaEventCreate(&pe1);
+      cudaEventRecord(pe0, s);
     }
     // CSR: row_off[q+1] = inclusive sum of counts
     DevBuf<uint64_t> c64(count, s);
@@ -1134,6 +1129,16 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       FMG_CK(cudaGetLastError());
     }
     FMG_CK(cudaStreamSynchronize(s));
+    if (trace_post) {
+      cudaEventRecord(pe1, s);
+      cudaEventSynchronize(pe1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, pe0, pe1);
+      fprintf(stderr, "[fmg] inexact post (CSR, gather, %s): %.3f ms, %llu results\n",
+              unsorted ? "segmented sort" : "no sort", ms, (unsigned long long)total);
+      cudaEventDestroy(pe0);
+      cudaEventDestroy(pe1);
+    }
     return res;
   } catch (...) {
     fmg_matches_free(res);
