@@ -195,6 +195,95 @@ __global__ void __launch_bounds__(256) k_occ_pair(IndexView ix, const uint2* __r
   }
 }
 
+// Lane-cooperative Occ step for wide lines (W = 6: 2 lanes, W = 14: 4 lanes).
+// The LANES lanes of a group each load one 32-byte sector of the same line in
+// ONE instruction, so the line costs a single memory request (on B200 a
+// random 64-byte request costs the same as a 32-byte one, 128 bytes 1.2x;
+// tools/micro/gather3.cu), and count the fields of their own words; partial
+// (T, hi, lo) popcounts are summed with xor-shuffles.  Fewer, denser lines
+// mean fewer DRAM requests per step for HBM-resident indexes.
+template <int W>
+__device__ __forceinline__ void partial_counts(const uint64_t v[4], int sector, uint32_t r, uint32_t& t, uint32_t& h,
+                                               uint32_t& l) {
+  // sector 0 holds words 0, 1 (after the 16-byte checkpoint); sector j >= 1
+  // holds words 4j-2 .. 4j+1
+  const int k0 = sector == 0 ? 0 : 4 * sector - 2;
+  const int nw = sector == 0 ? 2 : 4;
+  t = h = l = 0;
+#pragma unroll
+  for (int q = 0; q < 4; q += 2) {
+    if (q >= nw) break;
+    const uint64_t wa = (sector == 0 ? v[2 + q] : v[q]), wb = (sector == 0 ? v[3 + q] : v[q + 1]);
+    const uint64_t x0 = wa & word_mask(r, k0 + q), x1 = wb & word_mask(r, k0 + q + 1);
+    const uint64_t lo = (x0 & kFieldLo) | ((x1 & kFieldLo) << 1);
+    const uint64_t hi = ((x0 >> 1) & kFieldLo) | (x1 & ~kFieldLo);
+    t += __popcll(lo & hi);
+    h += __popcll(hi);
+    l += __popcll(lo);
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) k_occ_pair_coop(IndexView ix, const uint2* __restrict__ kl, uint64_t count,
+                                                       uint32_t* __restrict__ out, uint32_t* __restrict__ err) {
+  constexpr int LANES = int(LineTraits<W>::kBytes / 32);
+  constexpr uint32_t kC = LineTraits<W>::kChars;
+  const int sector = threadIdx.x % LANES;
+  // the lanes of a group always agree on the pair index, so shuffles use the
+  // group's own mask (groups of one warp may leave the loop at different times)
+  const uint32_t gmask = ((1u << LANES) - 1u) << ((threadIdx.x & 31u) & ~uint32_t(LANES - 1));
+  {
+    const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) / LANES;  // one group per pair
+    if (i >= count) return;  // the whole group leaves together
+    const uint2 q = ld_stream_u2(kl + i);
+    const uint32_t k = q.x, l = q.y;
+    const bool ok = l <= ix.n && k <= l + 1u;
+    if (!ok && sector == 0) atomicOr(err, 1u);
+    const uint32_t hh = ok ? l : 0u;
+    const uint32_t ll = (ok && k != 0u) ? k - 1u : hh;
+    const uint32_t jh = line_of<W>(hh), jl = line_of<W>(ll);
+    const uint32_t rh = hh - jh * kC, rl = ll - jl * kC;
+    uint64_t vh[4], vl[4];
+    ld256<true>(ix.lines + size_t(jh) * LineTraits<W>::kBytes + 32 * sector, vh[0], vh[1], vh[2], vh[3]);
+    const bool two = jl != jh;
+    if (two) ld256<true>(ix.lines + size_t(jl) * LineTraits<W>::kBytes + 32 * sector, vl[0], vl[1], vl[2], vl[3]);
+    uint32_t th, hh_, lh, tl, hl, ll_;
+    partial_counts<W>(vh, sector, rh, th, hh_, lh);
+    if (two)
+      partial_counts<W>(vl, sector, rl, tl, hl, ll_);
+    else
+      partial_counts<W>(vh, sector, rl, tl, hl, ll_);
+#pragma unroll
+    for (int d = 1; d < LANES; d <<= 1) {
+      th += __shfl_xor_sync(gmask, th, d);
+      hh_ += __shfl_xor_sync(gmask, hh_, d);
+      lh += __shfl_xor_sync(gmask, lh, d);
+      tl += __shfl_xor_sync(gmask, tl, d);
+      hl += __shfl_xor_sync(gmask, hl, d);
+      ll_ += __shfl_xor_sync(gmask, ll_, d);
+    }
+    if (sector == 0) {
+      uint32_t lo[4] = {0u, 0u, 0u, 0u}, hi[4] = {0u, 0u, 0u, 0u};
+      if (ok) {
+        const uint32_t bh[4] = {uint32_t(vh[0]), uint32_t(vh[0] >> 32), uint32_t(vh[1]), uint32_t(vh[1] >> 32)};
+        hi[3] = bh[3] + th;
+        hi[2] = bh[2] + hh_ - th;
+        hi[1] = bh[1] + lh - th;
+        hi[0] = bh[0] + rh + 1u - hh_ - lh + th - (l >= ix.sentinel_row ? 1u : 0u);
+        if (k != 0u) {
+          const uint64_t b01 = two ? vl[0] : vh[0], b23 = two ? vl[1] : vh[1];
+          const uint32_t bl[4] = {uint32_t(b01), uint32_t(b01 >> 32), uint32_t(b23), uint32_t(b23 >> 32)};
+          lo[3] = bl[3] + tl;
+          lo[2] = bl[2] + hl - tl;
+          lo[1] = bl[1] + ll_ - tl;
+          lo[0] = bl[0] + rl + 1u - hl - ll_ + tl - (k - 1u >= ix.sentinel_row ? 1u : 0u);
+        }
+      }
+      st_stream_256(out + i * 8, lo, hi);
+    }
+  }
+}
+
 // Pattern sources for the search kernels.
 struct PackedPatterns {  // fixed length m <= 32, char j in bits 2j..2j+1
   const uint64_t* words;
@@ -859,8 +948,15 @@ void launch_occ_pair_t(const fmg_index* ix, const uint32_t* kl, uint64_t count, 
   const uint64_t blocks = (count + per_block - 1) / per_block;
   with_words(ix, [&](auto wt) {
     constexpr int W = decltype(wt)::value;
-    k_occ_pair<PER, W><<<dim3(unsigned(blocks)), threads, 0, s>>>(ix->view(), reinterpret_cast<const uint2*>(kl),
-                                                                    count, out, ix->err);
+    if (W == 2) {
+      k_occ_pair<PER, W><<<dim3(unsigned(blocks)), threads, 0, s>>>(ix->view(), reinterpret_cast<const uint2*>(kl),
+                                                                      count, out, ix->err);
+    } else {  // wide lines: lane-cooperative, persistent grid-stride
+      constexpr int LANES = int(LineTraits<W>::kBytes / 32);
+      const uint64_t nb = (count * LANES + 255) / 256;
+      k_occ_pair_coop<W><<<dim3(unsigned(std::max<uint64_t>(nb, 1))), 256, 0, s>>>(
+          ix->view(), reinterpret_cast<const uint2*>(kl), count, out, ix->err);
+    }
   });
   FMG_CK(cudaGetLastError());
 }

@@ -288,3 +288,38 @@ def test_config3_small_scale_vs_oracle(gpu):
     orow, ok, ol, od, _ = orc.inexact_batch(ox, seeds, 1)
     assert np.array_equal(row, orow) and np.array_equal(k.astype(np.int64), ok)
     assert np.array_equal(l.astype(np.int64), ol) and np.array_equal(d, od)
+
+
+def test_config1h_sample_vs_oracle(gpu):
+    """Config 1-H (1 Gbp, HBM-resident index): 2^20 pairs of the bench workload."""
+    wl = workloads.config1h(count=1 << 20)
+    idx = fm.build_index(wl.text, builder="gpu")
+    got = fm.occ_pair_batch(idx, wl.pairs[:, 0], wl.pairs[:, 1])
+    want = orc.occ_pair_batch(orc.OracleIndex(idx), wl.pairs[:, 0], wl.pairs[:, 1])
+    assert np.array_equal(got, want)
+    idx.release_device()
+
+
+@pytest.mark.slow
+def test_config2_full_vs_oracle(gpu):
+    """All 1,000,000 config-2 seeds, z = 1, every result bit-exact."""
+    wl = workloads.config2()
+    idx = fm.build_index(wl.text)
+    ms = fm.inexact_search_batch(idx, wl.patterns, 1)
+    row, k, l, d, _ = orc.inexact_batch(orc.OracleIndex(idx), wl.patterns, 1)
+    assert np.array_equal(ms.offsets, row)
+    assert np.array_equal(ms.k.astype(np.int64), k) and np.array_equal(ms.l.astype(np.int64), l)
+    assert np.array_equal(ms.diffs, d)
+
+
+def test_config4_first_chunk_vs_oracle(gpu):
+    """The first 2^22 seeds of config 4 (identical to the full set's first chunk)."""
+    wl = workloads.config4(count=1 << 22)
+    idx = fm.build_index(wl.text, builder="gpu")
+    seeds = workloads.unpack_patterns(wl.packed, 20)
+    kl, _ = fm.exact_search_batch(idx, seeds)
+    ox = orc.OracleIndex(idx)
+    assert np.array_equal(kl[: 1 << 20], orc.exact_batch(ox, seeds[: 1 << 20]))
+    hit = kl[:, 0] <= kl[:, 1]
+    assert abs(hit.mean() - 0.8) < 0.01  # 80% exact substrings, random 20-mers ~never occur
+    idx.release_device()
