@@ -257,6 +257,16 @@ def config_of(config: str, world: int, units: int) -> dict:
 # ---------------------------------------------------------------------------
 
 
+def dist_sum(value: float, world: int, device) -> float:
+    """Sum of a per-rank count over all ranks (plumbing only, off the timed path)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def hbm_resident_extra(dev, lib, reps: int = 10) -> dict:
     """Config 1-H on the same GPU: the config-1 pair distribution over the 1 Gbp
     config-4 text, whose 500 MB line array cannot live in the 126 MB L2."""
@@ -315,6 +325,21 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
         dist.init_process_group("nccl", device_id=dev)
     lib = _lib.load()
     wl = make_workload(args.config, rank)
+    # Configs 3 and 4 define one fixed query set "sharded over 1, 2, 4 and 8
+    # GPUs" (strong scaling): rank r keeps its contiguous shard.  The others
+    # are weak-scaled (config 1: an independent pair set per rank).
+    strong = args.config in ("config3", "config4") and world > 1
+    if strong:
+        from paper_1811_06127_b200.dist import shard_range
+
+        if wl.name == "config3":
+            per = wl.meta["seeds_per_read"]
+            lo, hi = shard_range(wl.meta["reads"], rank, world)
+            wl.packed = wl.packed[lo * per:hi * per]
+            wl.meta["reads"] = hi - lo
+        else:
+            lo, hi = shard_range(wl.packed.size, rank, world)
+            wl.packed = wl.packed[lo:hi]
     t_build = time.perf_counter()
     idx = fm.build_index(wl.text)
     t_build = time.perf_counter() - t_build
@@ -465,7 +490,8 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
     t_ms = ev0.elapsed_time(ev1)
     t_ms = max_over_ranks(t_ms, world, dev)
     ms_step = t_ms / args.steps
-    value = units * world * args.steps / (t_ms / 1e3)
+    total_units = int(dist_sum(units, world, dev)) if world > 1 else units
+    value = total_units * args.steps / (t_ms / 1e3)
 
     # ---- per-launch kernel time for the roofline (same stream, CUDA events) ----
     roofline = None
@@ -500,7 +526,7 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
             d2h_seen = r
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     e2e_s = max_over_ranks(e2e_s, world, dev)
-    e2e = {"value": units * world / e2e_s, "unit": unit, "h2d_bytes_per_step": h2d_per,
+    e2e = {"value": total_units / e2e_s, "unit": unit, "h2d_bytes_per_step": h2d_per,
            "d2h_bytes_per_step": d2h_per if d2h_per is not None else d2h_seen}
 
     # ---- CPU baseline (oracle port) on rank 0 at N=1 ----
@@ -549,7 +575,8 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
     if rank == 0:
         line = {
             "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if args.config in ("config3", "config4") else "weak",
             "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (seeded PCG64 per BASELINE.json config; workloads.py)",
             "config": {**config_of(args.config, world, units),

@@ -976,9 +976,25 @@ void launch_occ_pair(const fmg_index* ix, const uint32_t* kl, uint64_t count, ui
 unsigned persistent_blocks(const fmg_index* ix, const void* kernel, int threads, uint64_t work) {
   int per_sm = 0;
   FMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0));
-  uint64_t blocks = uint64_t(std::max(per_sm, 1)) * ix->sms;
+  static const int mult = [] {
+    const char* e = std::getenv("FMG_GRID_MULT");  // tuning hook: waves of the persistent grid
+    return e ? std::max(1, std::atoi(e)) : 1;
+  }();
+  uint64_t blocks = uint64_t(std::max(per_sm, 1)) * ix->sms * mult;
   const uint64_t need = (work + threads - 1) / threads;
   return unsigned(std::max<uint64_t>(1, std::min(blocks, need)));
+}
+
+// Grid for the lane-refill search kernels: about kPerThread queries per
+// thread, i.e. many more blocks than fit at once.  Measured on B200 (config
+// 4, tools/prof_exact.py): letting the block scheduler refill SMs beats a
+// persistent one-wave grid whose lanes refill themselves (2.56 -> 3.3 G
+// seeds/s), because a self-refilling lane stalls the rest of its warp.
+unsigned wave_blocks(const fmg_index* ix, const void* kernel, int threads, uint64_t work) {
+  constexpr uint64_t kPerThread = 4;
+  const uint64_t resident = persistent_blocks(ix, kernel, threads, work);
+  const uint64_t waves = (work + threads * kPerThread - 1) / (threads * kPerThread);
+  return unsigned(std::min<uint64_t>(std::max<uint64_t>(resident, waves), 1u << 30));
 }
 
 void launch_exact_packed(const fmg_index* ix, const uint64_t* packed, uint32_t m, uint64_t count, uint32_t* kl_out,
@@ -988,7 +1004,7 @@ void launch_exact_packed(const fmg_index* ix, const uint64_t* packed, uint32_t m
   CodePatterns cp{nullptr, nullptr};
   with_words(ix, [&](auto wt) {
     constexpr int W = decltype(wt)::value;
-    const unsigned blocks = persistent_blocks(ix, (const void*)k_exact<true, W>, 256, count);
+    const unsigned blocks = wave_blocks(ix, (const void*)k_exact<true, W>, 256, count);
     k_exact<true, W><<<blocks, 256, 0, s>>>(ix->view(), pp, cp, count, reinterpret_cast<uint2*>(kl_out), steps);
   });
   FMG_CK(cudaGetLastError());
@@ -1001,7 +1017,7 @@ void launch_exact_codes(const fmg_index* ix, const uint8_t* codes, const uint64_
   CodePatterns cp{codes, offsets};
   with_words(ix, [&](auto wt) {
     constexpr int W = decltype(wt)::value;
-    const unsigned blocks = persistent_blocks(ix, (const void*)k_exact<false, W>, 256, count);
+    const unsigned blocks = wave_blocks(ix, (const void*)k_exact<false, W>, 256, count);
     k_exact<false, W><<<blocks, 256, 0, s>>>(ix->view(), pp, cp, count, reinterpret_cast<uint2*>(kl_out), steps);
   });
   FMG_CK(cudaGetLastError());
@@ -1010,7 +1026,7 @@ void launch_exact_codes(const fmg_index* ix, const uint8_t* codes, const uint64_
 void launch_locate(const fmg_index* ix, const uint32_t* rows, uint64_t count, uint32_t* out_pos, cudaStream_t s) {
   with_words(ix, [&](auto wt) {
     constexpr int W = decltype(wt)::value;
-    const unsigned blocks = persistent_blocks(ix, (const void*)fmg::k_locate<W>, 256, count);
+    const unsigned blocks = wave_blocks(ix, (const void*)fmg::k_locate<W>, 256, count);
     fmg::k_locate<W><<<blocks, 256, 0, s>>>(ix->view(), rows, count, out_pos, ix->err);
   });
   FMG_CK(cudaGetLastError());

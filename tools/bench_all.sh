@@ -1,0 +1,23 @@
+#!/bin/bash
+# Every BASELINE config through bench.py (our arm + the reference arm); JSON lines into gpurun_out/bench_all.jsonl
+mkdir -p gpurun_out
+out=gpurun_out/bench_all.jsonl
+: > $out
+for c in config1 config0 config1h config2 config4 config3; do
+  steps=10; [ $c = config3 ] && steps=2
+  timeout 1500 python bench.py --config $c --steps $steps --warmup 3 --no-hbm-extra 2>/dev/null | tail -1 >> $out
+  timeout 900 python bench.py --impl reference --config $c --steps 3 --warmup 3 2>/dev/null | tail -1 >> $out
+done
+python - <<'PY'
+import json
+for line in open("gpurun_out/bench_all.jsonl"):
+    try:
+        d = json.loads(line)
+    except Exception:
+        continue
+    r = d.get("roofline") or {}
+    e = d.get("e2e") or {}
+    c = d.get("cpu_baseline") or {}
+    print(f"{d.get('impl','ours'):9s} {d['config']['workload'][:40]:40s} value={d['value']:.4g} {d['unit']} "
+          f"e2e={e.get('value', 0):.4g} frac={r.get('frac')} cpu={c.get('value', 0):.4g}")
+PY

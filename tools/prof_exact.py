@@ -34,7 +34,7 @@ for r in range(reps + 1):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    print(f"rep {r}: {ms:.2f} ms, {count / ms / 1e6:.2f} M seeds/s", flush=True)
+    print(f"rep {r}: {ms:.2f} ms, {count / ms / 1e6:.3f} G seeds/s", flush=True)
 kl = d_out.cpu().numpy().view(np.uint32).astype(np.int64)
 sample = workloads.unpack_patterns(wl.packed[: 1 << 20], 20)
 want = orc.exact_batch(orc.OracleIndex(idx), sample)
