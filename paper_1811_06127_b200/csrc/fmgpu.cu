@@ -296,6 +296,7 @@ struct CodePatterns {  // codes[offsets[q] .. offsets[q+1])
   const ulonglong2* packed = nullptr;  // inexact, m <= 64: 2-bit packed copy (k_pack_patterns)
   const uint64_t* packed1 = nullptr;   // inexact, fixed m <= 32 given packed by the caller
   uint32_t fixed_m = 0;
+  const uint64_t* dbits = nullptr;     // inexact, m <= 64: lower-bound segment ends (k_dbound)
 };
 
 // Exact backward search, one pattern per thread at a time.  When a lane's
@@ -367,6 +368,73 @@ __global__ void __launch_bounds__(256) k_exact(IndexView ix, PackedPatterns pp, 
 
 // ----- bounded-difference search -----------------------------------------
 
+// Lower-bound pass of the inexact search as its own kernel (patterns of
+// length <= 64): one thread per pattern extends right to left with resets;
+// every time W[pos..seg_end] is absent from the text, bit seg_end is set and
+// the search restarts from the root at pos-1.  D(i) = popcount of the bits
+// <= i (see k_inexact).  Running it apart keeps the DFS kernel's lanes in
+// one phase.
+template <int W>
+__global__ void __launch_bounds__(256) k_dbound(IndexView ix, CodePatterns cp, uint64_t count,
+                                                uint64_t* __restrict__ dbits_out, unsigned long long* steps) {
+  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  uint64_t pw0, pw1;
+  int m;
+  if (cp.packed1) {
+    pw0 = cp.packed1[q];
+    pw1 = 0;
+    m = int(cp.fixed_m);
+  } else {
+    const ulonglong2 pk = cp.packed[q];
+    pw0 = pk.x;
+    pw1 = pk.y;
+    m = int(cp.offsets[q + 1] - cp.offsets[q]);
+  }
+  constexpr uint32_t kC = LineTraits<W>::kChars;
+  uint64_t bits = 0;
+  uint32_t k = 0, l = ix.n;
+  int seg_end = m - 1;
+  uint32_t my_steps = 0;
+  for (int pos = m - 1; pos >= 0; --pos) {
+    const uint32_t b = uint32_t((pos < 32 ? pw0 : pw1) >> ((pos & 31) << 1)) & 3u;
+    const uint32_t cb = c_of(ix, b);
+    uint32_t k2, l2;
+    if (k == 0u && l == ix.n) {  // root: init_interval, no memory
+      k2 = cb + 1u;
+      l2 = c_of(ix, b + 1u);
+    } else {
+      const uint32_t low = k - 1u;
+      const uint32_t jh = line_of<W>(l), jl = line_of<W>(low);
+      const uint32_t rh = l - jh * kC, rl = low - jl * kC;
+      uint32_t bh[4], bl[4];
+      uint64_t wh[W], wl[W];
+      load_line<W, false>(ix, jh, rh, bh, wh);
+      uint32_t ol;
+      if (jl != jh) {
+        load_line<W, false>(ix, jl, rl, bl, wl);
+        ol = occ1_from_line<W>(ix, bl, wl, low, rl, b);
+      } else {
+        ol = occ1_from_line<W>(ix, bh, wh, low, rl, b);
+      }
+      k2 = cb + ol + 1u;
+      l2 = cb + occ1_from_line<W>(ix, bh, wh, l, rh, b);
+      ++my_steps;
+    }
+    if (k2 > l2) {  // W[pos..seg_end] is absent from the text
+      bits |= 1ull << seg_end;
+      k = 0;
+      l = ix.n;
+      seg_end = pos - 1;
+    } else {
+      k = k2;
+      l = l2;
+    }
+  }
+  dbits_out[q] = bits;
+  if (steps) atomicAdd(steps, (unsigned long long)my_steps);
+}
+
 // Per-thread global scratch for the inexact engine, warp-blocked (element e
 // of lane L of warp w at (w*N + e)*32 + L) so a warp's region is contiguous.
 // The DFS stack itself lives in shared memory (see k_inexact).
@@ -402,12 +470,12 @@ struct InexactOut {
 // set of (interval, min diffs) the DFS reaches does not depend on visiting
 // order, so the traversal order is free.
 //
-// Visiting order: of a node's children the match child (same budget) is
-// pushed first, then the budget-1 children, and the LAST child emitted is
-// not pushed but continued in registers.  A budget-0 node has only its match
-// child, so budget-0 chains — most of the steps — never touch the stack;
-// the stack stays budget-monotone with at most 8 entries per budget level,
-// i.e. depth <= 8(z + 1), small enough for shared memory.
+// Visiting order: a budget-0 node has only its match child, which is
+// continued in registers, so budget-0 chains — most of the steps — never
+// touch the stack.  A node with budget >= 1 pushes its match child (same
+// budget) first and then its budget-1 children, and the next iteration pops
+// the last one; the stack stays budget-monotone with at most 9 entries per
+// budget level, i.e. depth <= 9(z + 1), small enough for shared memory.
 //
 // Lower-bound prune (result-preserving): before the DFS, one right-to-left
 // exact pass with resets splits W into disjoint segments absent from the
@@ -478,32 +546,6 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
     }
     overflow = true;
   };
-  // Children are emitted in push order; the last viable one becomes the
-  // register-held continue node, earlier ones go to the stack.
-  bool nx_valid = false;
-  int nxi = 0;
-  uint32_t nxb = 0, nxk = 0, nxl = 0;
-  auto emit = [&](int i, uint32_t budget, uint32_t k, uint32_t l) {
-    if (i < 0) {
-      record(k, l, z - budget);
-      return;
-    }
-    if (dlb(i) > budget) return;  // lower-bound prune
-    if (nx_valid) {
-      if (sp == S) {
-        overflow = true;
-      } else {
-        s_kl[sp * nt + tid] = make_uint2(nxk, nxl);
-        s_ib[sp * nt + tid] = (uint32_t(nxi + 1) << 16) | nxb;
-        ++sp;
-      }
-    }
-    nx_valid = true;
-    nxi = i;
-    nxb = budget;
-    nxk = k;
-    nxl = l;
-  };
   auto fail = [&]() {
     const unsigned long long f = atomicAdd(out.fail_count, 1ull);
     out.fail_list[f] = uint32_t(q);
@@ -570,13 +612,13 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
           m = int(cp.fixed_m);
           pw0 = cp.packed1[q];
           pw1 = 0;
-          dbits = 0;
+          dbits = cp.dbits[q];
         } else if (kShort) {
           m = int(cp.offsets[q + 1] - cp.offsets[q]);
           const ulonglong2 pk = cp.packed[q];
           pw0 = pk.x;
           pw1 = pk.y;
-          dbits = 0;
+          dbits = cp.dbits[q];
         } else {
           const uint64_t o0 = cp.offsets[q], o1 = cp.offsets[q + 1];
           codes = cp.codes + o0;
@@ -588,6 +630,7 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
         seg_end = m - 1;
         kd = 0;  // the pass starts from the root interval [0, n]
         ld = ix.n;
+        if (kShort) pos = -1;  // lower bound precomputed by k_dbound
         sp = nres = 0;
         ++epoch;
         overflow = false;
@@ -673,28 +716,66 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
     const int i = ci;
     const uint32_t budget = cb;
     const uint32_t want = sym_at(i);
-    nx_valid = false;
-    // match child first (pushed deepest), then the budget-1 children
-    {
-      const uint32_t cw = c_of(ix, want);
-      const uint32_t k2 = cw + sel4(lo, want) + 1u, l2 = cw + sel4(hi, want);
-      if (k2 <= l2) emit(i - 1, budget, k2, l2);  // match
-    }
-    if (budget > 0) {
-      emit(i - 1, budget - 1, k, l);  // skip
-#pragma unroll
-      for (uint32_t b = 0; b < 4; ++b) {
-        const uint32_t k2 = ix.c[b] + lo[b] + 1u, l2 = ix.c[b] + hi[b];
-        if (k2 > l2) continue;
-        emit(i, budget - 1, k2, l2);  // insert
-        if (b != want) emit(i - 1, budget - 1, k2, l2);  // mismatch
+    const uint32_t cw = c_of(ix, want);
+    const uint32_t kw = cw + sel4(lo, want) + 1u, lw = cw + sel4(hi, want);
+    if (budget == 0) {
+      // budget-0 node: only the match child, continued in registers
+      if (kw > lw) {
+        cur_valid = false;
+      } else if (i == 0) {
+        record(kw, lw, z);
+        cur_valid = false;
+      } else {
+        ci = i - 1;
+        ck = kw;
+        cl = lw;
+        cur_valid = dlb(i - 1) == 0;
       }
+      continue;
     }
-    cur_valid = nx_valid;
-    ci = nxi;
-    cb = nxb;
-    ck = nxk;
-    cl = nxl;
+    // budget >= 1: push every viable child with predicated stores (match
+    // child first, so it is popped last), then pop the top as the continue
+    // node.  Straight-line code: a lane expanding such a node costs its warp
+    // little more than a budget-0 step.
+    const uint32_t bm1 = budget - 1u;
+    const bool at0 = i == 0;
+    const uint32_t d_prev = at0 ? 0u : dlb(i - 1), d_cur = dlb(i);
+    const bool ok_match = !at0 && d_prev <= budget;  // (i-1, budget)
+    const bool ok_prev = !at0 && d_prev <= bm1;      // skip / mismatch: (i-1, budget-1)
+    const bool ok_cur = d_cur <= bm1;                // insert: (i, budget-1)
+    uint32_t k2[4], l2[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      k2[b] = ix.c[b] + lo[b] + 1u;
+      l2[b] = ix.c[b] + hi[b];
+    }
+    if (at0) {  // children with i - 1 < 0 are results (rare)
+      if (kw <= lw) record(kw, lw, z - budget);
+      record(k, l, z - bm1);  // skip
+#pragma unroll
+      for (uint32_t b = 0; b < 4; ++b)
+        if (b != want && k2[b] <= l2[b]) record(k2[b], l2[b], z - bm1);  // mismatch
+    }
+    auto push_if = [&](bool cond, int pi, uint32_t pb, uint32_t pk, uint32_t pl) {
+      if (cond) {
+        if (sp == S) {
+          overflow = true;
+        } else {
+          s_kl[sp * nt + tid] = make_uint2(pk, pl);
+          s_ib[sp * nt + tid] = (uint32_t(pi + 1) << 16) | pb;
+          ++sp;
+        }
+      }
+    };
+    push_if(ok_match && kw <= lw, i - 1, budget, kw, lw);  // match
+    push_if(ok_prev, i - 1, bm1, k, l);                      // skip
+#pragma unroll
+    for (uint32_t b = 0; b < 4; ++b) {
+      const bool ne = k2[b] <= l2[b];
+      push_if(ok_cur && ne, i, bm1, k2[b], l2[b]);                 // insert
+      push_if(ok_prev && ne && b != want, i - 1, bm1, k2[b], l2[b]);  // mismatch
+    }
+    cur_valid = false;  // the next iteration pops the top (the last child pushed)
   }
   if (out.steps) atomicAdd(out.steps, (unsigned long long)my_steps);
 }
@@ -1084,6 +1165,18 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       k_pack_patterns<<<unsigned((count + 255) / 256), 256, 0, s>>>(codes, offsets, count, packed.ptr);
       FMG_CK(cudaGetLastError());
     }
+    DevBuf<uint64_t> dbits(short_pat ? count : 0, s);
+    if (short_pat) {
+      CodePatterns cpd{codes, offsets, packed.ptr, packed1, uint32_t(max_len)};
+      with_words(ix, [&](auto wt) {
+        constexpr int W = decltype(wt)::value;
+        const unsigned nb = wave_blocks(ix, (const void*)k_dbound<W>, 256, count);
+        (void)nb;
+        k_dbound<W><<<unsigned((count + 255) / 256), 256, 0, s>>>(ix->view(), cpd, count, dbits.ptr,
+                                                                    counters.ptr + 2);
+      });
+      FMG_CK(cudaGetLastError());
+    }
     std::vector<DevBuf<uint2>> pass_kl;
     std::vector<DevBuf<uint8_t>> pass_d;
     DevBuf<uint32_t> lists[2] = {DevBuf<uint32_t>(count, s), DevBuf<uint32_t>(count, s)};
@@ -1100,7 +1193,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     // Stack: depth <= 8(z+1) with the budget-ordered pushes of k_inexact;
     // 9(m+z+1)+2 bounds any visiting order.  Grown on overflow.
     const uint32_t S_max = uint32_t(9 * (max_len + z + 1) + 2);
-    uint32_t S = std::min<uint32_t>(S_max, 8 * (z + 1) + 1);
+    uint32_t S = std::min<uint32_t>(S_max, 9 * (z + 1) + 2);
     for (int pass = 0; pending > 0; ++pass) {
       FMG_REQUIRE(pass < 250, "inexact search did not converge");
       int nt = 128;
@@ -1148,7 +1241,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       o.next = counters.ptr + 3;
       o.unsorted = counters.ptr + 4;
       const unsigned blocks = unsigned(T / nt);
-      CodePatterns cp{codes, offsets, packed.ptr, packed1, uint32_t(max_len)};
+      CodePatterns cp{codes, offsets, packed.ptr, packed1, uint32_t(max_len), dbits.ptr};
       static const bool trace = std::getenv("FMG_TRACE") != nullptr;
       cudaEvent_t ev0 = nullptr, ev1 = nullptr;
       if (trace) {
