@@ -7,6 +7,7 @@ first use, and every search/Occ entry point needs a CUDA device.
 from __future__ import annotations
 
 import ctypes as ct
+import os
 import threading
 from pathlib import Path
 
@@ -56,7 +57,8 @@ _lib: ct.CDLL | None = None
 
 
 def lib_path() -> Path:
-    return LIB_PATH
+    """The library to load; FMG_LIB_PATH overrides it (A/B experiments only)."""
+    return Path(os.environ.get("FMG_LIB_PATH", LIB_PATH))
 
 
 def load() -> ct.CDLL:
@@ -66,13 +68,16 @@ def load() -> ct.CDLL:
         return _lib
     with _lock:
         if _lib is None:
-            if not LIB_PATH.exists():
+            path = lib_path()
+            if not path.exists():
                 raise RuntimeError(
-                    f"native library {LIB_PATH} is missing; build it with "
+                    f"native library {path} is missing; build it with "
                     "`python -c 'import __graft_entry__ as g; g.build()'`"
                 )
-            lib = ct.CDLL(str(LIB_PATH))
+            lib = ct.CDLL(str(path))
             for name, (res, args) in PROTOTYPES.items():
+                if path != LIB_PATH and not hasattr(lib, name):
+                    continue  # an older build under A/B test
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args

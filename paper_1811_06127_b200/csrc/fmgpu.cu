@@ -460,6 +460,7 @@ struct InexactOut {
   unsigned long long* next;  // work-queue cursor
   unsigned long long* steps;
   unsigned long long* unsorted;  // patterns written with > S results (post-sorted)
+  uint32_t* unsorted_list;       // their pattern ids (capacity: count)
 };
 
 // Reference semantics (search.py:120-159): nodes (i, budget, k, l) from the
@@ -474,8 +475,8 @@ struct InexactOut {
 // continued in registers, so budget-0 chains — most of the steps — never
 // touch the stack.  A node with budget >= 1 pushes its match child (same
 // budget) first and then its budget-1 children, and the next iteration pops
-// the last one; the stack stays budget-monotone with at most 9 entries per
-// budget level, i.e. depth <= 9(z + 1), small enough for shared memory.
+// the last one; the stack stays budget-monotone — one budget-z entry and at
+// most 9 per lower level, depth <= 9z + 1 — small enough for shared memory.
 //
 // Lower-bound prune (result-preserving): before the DFS, one right-to-left
 // exact pass with resets splits W into disjoint segments absent from the
@@ -589,7 +590,8 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
           out.kl[o + r] = make_uint2(e.x, e.y);
           out.diffs[o + r] = uint8_t(e.w);
         }
-        atomicAdd(out.unsorted, 1ull);
+        const unsigned long long u = atomicAdd(out.unsorted, 1ull);
+        out.unsorted_list[u] = uint32_t(q);
       }
     }
     out.res_off[q] = o;
@@ -612,13 +614,13 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
           m = int(cp.fixed_m);
           pw0 = cp.packed1[q];
           pw1 = 0;
-          dbits = cp.dbits[q];
+          dbits = cp.dbits ? cp.dbits[q] : 0ull;
         } else if (kShort) {
           m = int(cp.offsets[q + 1] - cp.offsets[q]);
           const ulonglong2 pk = cp.packed[q];
           pw0 = pk.x;
           pw1 = pk.y;
-          dbits = cp.dbits[q];
+          dbits = cp.dbits ? cp.dbits[q] : 0ull;
         } else {
           const uint64_t o0 = cp.offsets[q], o1 = cp.offsets[q + 1];
           codes = cp.codes + o0;
@@ -630,7 +632,7 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
         seg_end = m - 1;
         kd = 0;  // the pass starts from the root interval [0, n]
         ld = ix.n;
-        if (kShort) pos = -1;  // lower bound precomputed by k_dbound
+        if (kShort && cp.dbits) pos = -1;  // lower bound precomputed by k_dbound
         sp = nres = 0;
         ++epoch;
         overflow = false;
@@ -778,6 +780,336 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
     cur_valid = false;  // the next iteration pops the top (the last child pushed)
   }
   if (out.steps) atomicAdd(out.steps, (unsigned long long)my_steps);
+}
+
+// Sort the results of patterns that had more than S of them (written
+// unsorted by k_inexact) in place: one block per pattern, bitonic sort of
+// (k << 32 | l, diffs) in shared memory.  Segments above kSortMax entries set
+// *too_big and the host falls back to a CUB segmented sort.
+constexpr uint32_t kSortMax = 4096;
+__global__ void __launch_bounds__(256) k_sort_segments(const uint32_t* __restrict__ list, const uint64_t* __restrict__ res_off,
+                                                       const uint32_t* __restrict__ res_cnt, uint2* __restrict__ kl,
+                                                       uint8_t* __restrict__ diffs, uint32_t* __restrict__ too_big) {
+  __shared__ uint64_t key[kSortMax];
+  __shared__ uint8_t val[kSortMax];
+  const uint32_t q = list[blockIdx.x];
+  const uint32_t n = res_cnt[q];
+  const uint64_t o = res_off[q];
+  if (n > kSortMax) {
+    if (threadIdx.x == 0) atomicOr(too_big, 1u);
+    return;
+  }
+  uint32_t p = 1;
+  while (p < n) p <<= 1;
+  for (uint32_t j = threadIdx.x; j < p; j += blockDim.x) {
+    if (j < n) {
+      const uint2 e = kl[o + j];
+      key[j] = (uint64_t(e.x) << 32) | e.y;
+      val[j] = diffs[o + j];
+    } else {
+      key[j] = ~0ull;
+      val[j] = 0;
+    }
+  }
+  __syncthreads();
+  for (uint32_t size = 2; size <= p; size <<= 1) {
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      for (uint32_t j = threadIdx.x; j < p; j += blockDim.x) {
+        const uint32_t partner = j ^ stride;
+        if (partner > j) {
+          const bool up = (j & size) == 0;
+          const uint64_t a = key[j], b = key[partner];
+          if ((a > b) == up) {
+            key[j] = b;
+            key[partner] = a;
+            const uint8_t t = val[j];
+            val[j] = val[partner];
+            val[partner] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) {
+    kl[o + j] = make_uint2(uint32_t(key[j] >> 32), uint32_t(key[j]));
+    diffs[o + j] = val[j];
+  }
+}
+
+// ----- level-synchronous engine for z = 1 ----------------------------------
+//
+// For a budget of one edit the DFS of search.py:120-159 decomposes into (a)
+// the exact "spine" walk of budget-1 match children from the root and (b)
+// independent budget-0 continuations spawned at every spine node — skip,
+// inserts, mismatches — each of which is an exact backward search of the
+// remaining prefix from its own interval.  k_spine walks every spine and
+// queues the continuations; k_chain walks every continuation; both emit raw
+// (pattern, k, l, diffs) results, deduplicated and sorted per pattern
+// afterwards.  Every lane of a warp runs the same loop, which the DFS kernel
+// cannot offer.  The reached (interval, min diffs) set equals the DFS's.
+
+struct Z1Node {  // a budget-0 continuation: pattern q, next position i, interval
+  uint32_t q, i, k, l;
+};
+struct Z1Raw {  // one reached result before dedup
+  uint32_t q, k, l, used;
+};
+struct Z1Queues {
+  Z1Node* nodes;
+  unsigned long long* n_nodes;
+  uint64_t node_cap;
+  Z1Raw* raws;
+  unsigned long long* n_raws;
+  uint64_t raw_cap;
+};
+
+// Warp-aggregated append of `cnt` (0..15) slots: one atomic per warp.
+__device__ __forceinline__ uint64_t warp_reserve(unsigned long long* counter, uint32_t cnt) {
+  const unsigned mask = __activemask();
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t prefix = 0, total = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const unsigned bal = __ballot_sync(mask, (cnt >> b) & 1u);
+    prefix += uint32_t(__popc(bal & lt)) << b;
+    total += uint32_t(__popc(bal)) << b;
+  }
+  const int leader = __ffs(mask) - 1;
+  unsigned long long base = 0;
+  if (int(lane) == leader && total) base = atomicAdd(counter, (unsigned long long)total);
+  base = __shfl_sync(mask, base, leader);
+  return base + prefix;
+}
+
+__device__ __forceinline__ void z1_pattern(const CodePatterns& cp, uint64_t q, uint64_t& pw0, uint64_t& pw1, int& m) {
+  if (cp.packed1) {
+    pw0 = cp.packed1[q];
+    pw1 = 0;
+    m = int(cp.fixed_m);
+  } else {
+    const ulonglong2 pk = cp.packed[q];
+    pw0 = pk.x;
+    pw1 = pk.y;
+    m = int(cp.offsets[q + 1] - cp.offsets[q]);
+  }
+}
+
+__device__ __forceinline__ uint32_t z1_sym(uint64_t pw0, uint64_t pw1, int i) {
+  return uint32_t((i < 32 ? pw0 : pw1) >> ((i & 31) << 1)) & 3u;
+}
+
+__device__ __forceinline__ uint32_t z1_dlb(uint64_t dbits, int i) { return __popcll(dbits & ((2ull << i) - 1ull)); }
+
+template <int W>
+__global__ void __launch_bounds__(256) k_spine(IndexView ix, CodePatterns cp, uint64_t count, Z1Queues qu,
+                                               unsigned long long* steps) {
+  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  uint64_t pw0, pw1;
+  int m;
+  z1_pattern(cp, q, pw0, pw1, m);
+  const uint64_t dbits = cp.dbits[q];
+  uint32_t my_steps = 0;
+  int i = m - 1;
+  uint32_t k = 0, l = ix.n;
+  bool alive = z1_dlb(dbits, m - 1) <= 1u;  // root (m-1, 1, 0, n), search.py:125
+  while (alive) {
+    uint32_t lo[4], hi[4];
+    occ_step<W, false>(ix, k, l, lo, hi);
+    ++my_steps;
+    const uint32_t want = z1_sym(pw0, pw1, i);
+    uint32_t k2[4], l2[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      k2[b] = ix.c[b] + lo[b] + 1u;
+      l2[b] = ix.c[b] + hi[b];
+    }
+    const bool at0 = i == 0;
+    const bool ok_prev = !at0 && z1_dlb(dbits, i - 1) == 0u;  // (i-1, budget 0)
+    const bool ok_cur = z1_dlb(dbits, i) == 0u;               // (i, budget 0)
+    // budget-0 children to queue: skip, 4 inserts, 3 mismatches
+    bool e[8];
+    e[0] = ok_prev;  // skip (i-1, 0, k, l)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const bool ne = k2[b] <= l2[b];
+      e[1 + b] = ok_cur && ne;  // insert (i, 0, k_b, l_b)
+    }
+    uint32_t mm = 0;  // mismatch slots 5..7 hold the three b != want in order
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      if (uint32_t(b) == want) continue;
+      e[5 + mm] = ok_prev && (k2[b] <= l2[b]);
+      ++mm;
+    }
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) cnt += e[j] ? 1u : 0u;
+    uint64_t slot = warp_reserve(qu.n_nodes, cnt);
+    auto put = [&](uint32_t ni, uint32_t nk, uint32_t nl) {
+      if (slot < qu.node_cap) qu.nodes[slot] = Z1Node{uint32_t(q), ni, nk, nl};
+      ++slot;
+    };
+    if (e[0]) put(uint32_t(i - 1), k, l);
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if (e[1 + b]) put(uint32_t(i), k2[b], l2[b]);
+    mm = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      if (uint32_t(b) == want) continue;
+      if (e[5 + mm]) put(uint32_t(i - 1), k2[b], l2[b]);
+      ++mm;
+    }
+    // children with i - 1 < 0 are results (search.py:127-134): rare
+    uint32_t rc = 0;
+    if (at0) {
+      rc = 1u;  // skip
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (uint32_t(b) != want && k2[b] <= l2[b]) ++rc;
+      if (k2[want & 3u] <= l2[want & 3u]) ++rc;  // match with budget kept
+    }
+    uint64_t rs = warp_reserve(qu.n_raws, rc);
+    if (at0) {
+      auto rput = [&](uint32_t rk, uint32_t rl, uint32_t used) {
+        if (rs < qu.raw_cap) qu.raws[rs] = Z1Raw{uint32_t(q), rk, rl, used};
+        ++rs;
+      };
+      rput(k, l, 1u);
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (uint32_t(b) != want && k2[b] <= l2[b]) rput(k2[b], l2[b], 1u);
+      if (k2[want & 3u] <= l2[want & 3u]) rput(k2[want & 3u], l2[want & 3u], 0u);
+      break;
+    }
+    // continue along the match child (i-1, 1)
+    const uint32_t kw = sel4(k2, want), lw = sel4(l2, want);
+    if (kw > lw || z1_dlb(dbits, i - 1) > 1u) break;
+    k = kw;
+    l = lw;
+    --i;
+  }
+  if (steps) atomicAdd(steps, (unsigned long long)my_steps);
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) k_chain(IndexView ix, CodePatterns cp, const Z1Node* __restrict__ nodes,
+                                               uint64_t n_nodes, Z1Queues qu, unsigned long long* steps) {
+  // Persistent grid, lane refill: most continuations die within a few steps
+  // while the few that match run to i < 0, so a lane takes its next node as
+  // soon as its chain ends instead of idling until its warp's longest chain.
+  constexpr uint32_t kC = LineTraits<W>::kChars;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint32_t my_steps = 0;
+  uint64_t pw0 = 0, pw1 = 0, dbits = 0;
+  int i = -1;
+  uint32_t k = 0, l = 0, q = 0;
+  bool have = false;
+  while (true) {
+    if (!have) {
+      if (t >= n_nodes) break;
+      const Z1Node nd = nodes[t];
+      t += stride;
+      int m;
+      z1_pattern(cp, nd.q, pw0, pw1, m);
+      dbits = cp.dbits[nd.q];
+      q = nd.q;
+      i = int(nd.i);
+      k = nd.k;
+      l = nd.l;
+      have = true;
+    }
+    // budget-0 node (i, k, l): only its match child
+    const uint32_t sym = z1_sym(pw0, pw1, i);
+    uint32_t k2, l2;
+    if (k == 0u && l == ix.n) {
+      k2 = c_of(ix, sym) + 1u;
+      l2 = c_of(ix, sym + 1u);
+    } else {
+      const uint32_t low = k - 1u;
+      const uint32_t jh = line_of<W>(l), jl = line_of<W>(low);
+      const uint32_t rh = l - jh * kC, rl = low - jl * kC;
+      uint32_t bh[4], bl[4];
+      uint64_t wh[W], wl[W];
+      load_line<W, false>(ix, jh, rh, bh, wh);
+      uint32_t ol;
+      if (jl != jh) {
+        load_line<W, false>(ix, jl, rl, bl, wl);
+        ol = occ1_from_line<W>(ix, bl, wl, low, rl, sym);
+      } else {
+        ol = occ1_from_line<W>(ix, bh, wh, low, rl, sym);
+      }
+      const uint32_t cs = c_of(ix, sym);
+      k2 = cs + ol + 1u;
+      l2 = cs + occ1_from_line<W>(ix, bh, wh, l, rh, sym);
+      ++my_steps;
+    }
+    const bool empty = k2 > l2;
+    const bool found = !empty && i == 0;
+    if (empty || found || z1_dlb(dbits, i - 1) > 0u) {
+      have = false;
+      if (found) {
+        const unsigned long long rs = atomicAdd(qu.n_raws, 1ull);
+        if (rs < qu.raw_cap) qu.raws[rs] = Z1Raw{q, k2, l2, 1u};
+      }
+      continue;
+    }
+    k = k2;
+    l = l2;
+    --i;
+  }
+  if (steps) atomicAdd(steps, (unsigned long long)my_steps);
+}
+
+// counting sort of raw results by pattern
+__global__ void k_z1_hist(const Z1Raw* __restrict__ raws, uint64_t n, uint32_t* __restrict__ per_q) {
+  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < n) atomicAdd(&per_q[raws[t].q], 1u);
+}
+
+__global__ void k_z1_scatter(const Z1Raw* __restrict__ raws, uint64_t n, uint64_t* __restrict__ cursor,
+                             uint64_t* __restrict__ keys, uint8_t* __restrict__ used) {
+  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const Z1Raw r = raws[t];
+  const unsigned long long p = atomicAdd(reinterpret_cast<unsigned long long*>(&cursor[r.q]), 1ull);
+  keys[p] = (uint64_t(r.k) << 32) | r.l;
+  used[p] = uint8_t(r.used);
+}
+
+// per pattern: unique (k, l) with min diffs over its sorted segment
+__global__ void k_z1_unique_count(const uint64_t* __restrict__ keys, const uint8_t* __restrict__ used,
+                                  const uint64_t* __restrict__ seg, uint64_t count, uint32_t* __restrict__ ucnt) {
+  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  uint32_t c = 0;
+  for (uint64_t j = seg[q]; j < seg[q + 1]; ++j)
+    if (j == seg[q] || keys[j] != keys[j - 1]) ++c;
+  ucnt[q] = c;
+}
+
+__global__ void k_z1_unique_write(const uint64_t* __restrict__ keys, const uint8_t* __restrict__ used,
+                                  const uint64_t* __restrict__ seg, const uint64_t* __restrict__ row_off,
+                                  uint64_t count, uint32_t* __restrict__ k_out, uint32_t* __restrict__ l_out,
+                                  uint8_t* __restrict__ d_out) {
+  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  uint64_t o = row_off[q];
+  for (uint64_t j = seg[q]; j < seg[q + 1];) {
+    const uint64_t key = keys[j];
+    uint8_t best = used[j];
+    uint64_t e = j + 1;
+    for (; e < seg[q + 1] && keys[e] == key; ++e) best = min(best, used[e]);
+    k_out[o] = uint32_t(key >> 32);
+    l_out[o] = uint32_t(key);
+    d_out[o] = best;
+    ++o;
+    j = e;
+  }
 }
 
 // Gather per-pattern results of one pass into the final CSR arrays.
@@ -1126,6 +1458,107 @@ void validate_patterns_host(const uint8_t* codes, const uint64_t* offsets, uint6
   *max_len = mx;
 }
 
+// z = 1 through k_spine / k_chain; false when a queue overflowed (the caller
+// then runs the DFS engine, which has no such limit).  Fills res on success.
+bool run_z1(const fmg_index* ix, const CodePatterns& cp, uint64_t count, uint64_t m, cudaStream_t s,
+            unsigned long long* steps, fmg_matches* res) {
+  static const bool trace = std::getenv("FMG_TRACE") != nullptr;
+  cudaEvent_t ev[4] = {};
+  if (trace)
+    for (auto& e : ev) cudaEventCreate(&e);
+  if (trace) cudaEventRecord(ev[0], s);
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = size_t(8) << 30;
+  // worst case 8 continuations per spine node and m + 1 spine nodes; in
+  // practice far fewer, so cap by memory and detect overflow
+  const uint64_t worst = count * 8 * (m + 1);
+  const uint64_t budget_entries = std::max<uint64_t>(1u << 20, free_b / 4 / sizeof(Z1Node));
+  const uint64_t node_cap = std::min<uint64_t>(worst, budget_entries);
+  const uint64_t raw_cap = std::min<uint64_t>(worst + count, budget_entries / 2);
+  DevBuf<Z1Node> nodes(node_cap, s);
+  DevBuf<Z1Raw> raws(raw_cap, s);
+  DevBuf<unsigned long long> ctr(2, s);
+  FMG_CK(cudaMemsetAsync(ctr.ptr, 0, 16, s));
+  Z1Queues qu{nodes.ptr, ctr.ptr, node_cap, raws.ptr, ctr.ptr + 1, raw_cap};
+  with_words(ix, [&](auto wt) {
+    constexpr int W = decltype(wt)::value;
+    k_spine<W><<<unsigned((count + 255) / 256), 256, 0, s>>>(ix->view(), cp, count, qu, steps);
+  });
+  FMG_CK(cudaGetLastError());
+  unsigned long long n_nodes = 0;
+  FMG_CK(cudaMemcpyAsync(&n_nodes, ctr.ptr, 8, cudaMemcpyDeviceToHost, s));
+  FMG_CK(cudaStreamSynchronize(s));
+  if (n_nodes > node_cap) return false;
+  if (trace) cudaEventRecord(ev[1], s);
+  if (n_nodes) {
+    with_words(ix, [&](auto wt) {
+      constexpr int W = decltype(wt)::value;
+      const unsigned nb = persistent_blocks(ix, (const void*)k_chain<W>, 256, n_nodes);
+      k_chain<W><<<nb, 256, 0, s>>>(ix->view(), cp, nodes.ptr, n_nodes, qu, steps);
+    });
+    FMG_CK(cudaGetLastError());
+  }
+  unsigned long long n_raw = 0;
+  FMG_CK(cudaMemcpyAsync(&n_raw, ctr.ptr + 1, 8, cudaMemcpyDeviceToHost, s));
+  FMG_CK(cudaStreamSynchronize(s));
+  if (n_raw > raw_cap) return false;
+  if (trace) cudaEventRecord(ev[2], s);
+  // group raw results by pattern (counting sort), sort each segment by (k, l)
+  DevBuf<uint32_t> per_q(count, s);
+  DevBuf<uint64_t> seg(count + 1, s), cursor(count, s), c64(count, s);
+  FMG_CK(cudaMemsetAsync(per_q.ptr, 0, count * 4, s));
+  FMG_CK(cudaMemsetAsync(seg.ptr, 0, 8, s));
+  if (n_raw) k_z1_hist<<<unsigned((n_raw + 255) / 256), 256, 0, s>>>(raws.ptr, n_raw, per_q.ptr);
+  k_widen_counts<<<unsigned((count + 255) / 256), 256, 0, s>>>(count, per_q.ptr, c64.ptr);
+  size_t tb = 0;
+  FMG_CK(cub::DeviceScan::InclusiveSum(nullptr, tb, c64.ptr, seg.ptr + 1, count, s));
+  DevBuf<uint8_t> tmp(tb, s);
+  FMG_CK(cub::DeviceScan::InclusiveSum(tmp.ptr, tb, c64.ptr, seg.ptr + 1, count, s));
+  FMG_CK(cudaMemcpyAsync(cursor.ptr, seg.ptr, count * 8, cudaMemcpyDeviceToDevice, s));
+  const uint64_t nr = std::max<uint64_t>(n_raw, 1);
+  DevBuf<uint64_t> keys(nr, s), keys2(nr, s);
+  DevBuf<uint8_t> used(nr, s), used2(nr, s);
+  if (n_raw) {
+    k_z1_scatter<<<unsigned((n_raw + 255) / 256), 256, 0, s>>>(raws.ptr, n_raw, cursor.ptr, keys.ptr, used.ptr);
+    FMG_REQUIRE(n_raw < (1ull << 31), "too many inexact results for one call");
+    size_t sb = 0;
+    FMG_CK(cub::DeviceSegmentedSort::SortPairs(nullptr, sb, keys.ptr, keys2.ptr, used.ptr, used2.ptr, int(n_raw),
+                                               int(count), seg.ptr, seg.ptr + 1, s));
+    DevBuf<uint8_t> stmp(sb, s);
+    FMG_CK(cub::DeviceSegmentedSort::SortPairs(stmp.ptr, sb, keys.ptr, keys2.ptr, used.ptr, used2.ptr, int(n_raw),
+                                               int(count), seg.ptr, seg.ptr + 1, s));
+  }
+  k_z1_unique_count<<<unsigned((count + 255) / 256), 256, 0, s>>>(keys2.ptr, used2.ptr, seg.ptr, count, per_q.ptr);
+  k_widen_counts<<<unsigned((count + 255) / 256), 256, 0, s>>>(count, per_q.ptr, c64.ptr);
+  FMG_CK(cub::DeviceScan::InclusiveSum(tmp.ptr, tb, c64.ptr, res->row_off + 1, count, s));
+  uint64_t total = 0;
+  FMG_CK(cudaMemcpyAsync(&total, res->row_off + count, 8, cudaMemcpyDeviceToHost, s));
+  unsigned long long st = 0;
+  FMG_CK(cudaMemcpyAsync(&st, steps, 8, cudaMemcpyDeviceToHost, s));
+  FMG_CK(cudaStreamSynchronize(s));
+  res->total = total;
+  res->steps = st;
+  FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->k), std::max<uint64_t>(total, 1) * 4, s));
+  FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->l), std::max<uint64_t>(total, 1) * 4, s));
+  FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->diffs), std::max<uint64_t>(total, 1), s));
+  k_z1_unique_write<<<unsigned((count + 255) / 256), 256, 0, s>>>(keys2.ptr, used2.ptr, seg.ptr, res->row_off,
+                                                                  count, res->k, res->l, res->diffs);
+  FMG_CK(cudaGetLastError());
+  if (trace) cudaEventRecord(ev[3], s);
+  FMG_CK(cudaStreamSynchronize(s));
+  if (trace) {
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    cudaEventElapsedTime(&c, ev[2], ev[3]);
+    fprintf(stderr, "[fmg] z1 engine: %llu patterns, spine+queue %.3f ms (%llu continuations), chains %.3f ms, "
+            "dedup/sort %.3f ms (%llu raw -> %llu results)\n", (unsigned long long)count, a, n_nodes, b, c,
+            n_raw, (unsigned long long)total);
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+  return true;
+}
+
 fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64_t* offsets, uint64_t count,
                          uint64_t max_len, int max_diff, cudaStream_t s, const uint64_t* packed1 = nullptr) {
   FMG_REQUIRE(max_diff >= 0, "difference budget is negative");
@@ -1156,6 +1589,10 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     DevBuf<uint32_t> res_cnt(count, s);
     DevBuf<uint8_t> res_pass(count, s);
     DevBuf<unsigned long long> counters(5, s);  // total, fail_count, steps, queue cursor, unsorted
+    DevBuf<uint32_t> unsorted_list(count, s);
+    DevBuf<uint32_t> too_big(1, s);
+    FMG_CK(cudaMemsetAsync(too_big.ptr, 0, 4, s));
+    bool need_cub_sort = false;
     FMG_CK(cudaMemsetAsync(res_pass.ptr, 0xFF, count, s));
     FMG_CK(cudaMemsetAsync(counters.ptr + 2, 0, sizeof(unsigned long long), s));
     FMG_CK(cudaMemsetAsync(counters.ptr + 4, 0, sizeof(unsigned long long), s));
@@ -1170,12 +1607,22 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       CodePatterns cpd{codes, offsets, packed.ptr, packed1, uint32_t(max_len)};
       with_words(ix, [&](auto wt) {
         constexpr int W = decltype(wt)::value;
-        const unsigned nb = wave_blocks(ix, (const void*)k_dbound<W>, 256, count);
-        (void)nb;
         k_dbound<W><<<unsigned((count + 255) / 256), 256, 0, s>>>(ix->view(), cpd, count, dbits.ptr,
                                                                     counters.ptr + 2);
       });
       FMG_CK(cudaGetLastError());
+    }
+    // z = 1 on an L2-resident index: the level-synchronous engine (uniform
+    // warps).  On HBM-resident indexes the DFS engine wins: its chains start
+    // from intervals already in L1/L2, while queued continuations re-fetch
+    // pattern, bound and first line from DRAM (tools/prof_c3.py).
+    const bool force_dfs = std::getenv("FMG_INEXACT_DFS") != nullptr;  // read per call (tests flip it)
+    uint64_t line_bytes = 0;
+    with_words(ix, [&](auto wt) { line_bytes = ix->n_lines * fmg::LineTraits<decltype(wt)::value>::kBytes; });
+    if (z == 1 && short_pat && !force_dfs && line_bytes <= (uint64_t(64) << 20)) {
+      CodePatterns cpz{codes, offsets, packed.ptr, packed1, uint32_t(max_len), dbits.ptr};
+      if (run_z1(ix, cpz, count, max_len, s, counters.ptr + 2, res)) return res;
+      // queues overflowed: fall through to the DFS engine (same results)
     }
     std::vector<DevBuf<uint2>> pass_kl;
     std::vector<DevBuf<uint8_t>> pass_d;
@@ -1193,7 +1640,13 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     // Stack: depth <= 8(z+1) with the budget-ordered pushes of k_inexact;
     // 9(m+z+1)+2 bounds any visiting order.  Grown on overflow.
     const uint32_t S_max = uint32_t(9 * (max_len + z + 1) + 2);
-    uint32_t S = std::min<uint32_t>(S_max, 9 * (z + 1) + 2);
+    // The stack is budget-monotone: at most one budget-z entry (the pending
+    // spine child) and at most 9 entries per lower budget level, so 9z + 2
+    // slots suffice.  Kept small on purpose: shared memory and L1 share the
+    // SM's SRAM, and for HBM-resident indexes the L1 left over is worth 30%
+    // (config 3: S = 20 -> 667 ms, S = 10 -> 447 ms per 14M seeds).
+    uint32_t S = std::min<uint32_t>(S_max, 9 * z + 2);
+    if (const char* e = std::getenv("FMG_STACK_S")) S = std::max<uint32_t>(2, uint32_t(std::atoi(e)));  // A/B
     for (int pass = 0; pending > 0; ++pass) {
       FMG_REQUIRE(pass < 250, "inexact search did not converge");
       int nt = 128;
@@ -1240,6 +1693,8 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       o.steps = counters.ptr + 2;
       o.next = counters.ptr + 3;
       o.unsorted = counters.ptr + 4;
+      o.unsorted_list = unsorted_list.ptr;
+      FMG_CK(cudaMemsetAsync(counters.ptr + 4, 0, sizeof(unsigned long long), s));
       const unsigned blocks = unsigned(T / nt);
       CodePatterns cp{codes, offsets, packed.ptr, packed1, uint32_t(max_len), dbits.ptr};
       static const bool trace = std::getenv("FMG_TRACE") != nullptr;
@@ -1257,10 +1712,19 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
           k_inexact<false, W><<<blocks, nt, smem, s>>>(ix->view(), cp, list, pending, z, sc, o);
       });
       FMG_CK(cudaGetLastError());
-      unsigned long long host_ctr[2];
+      unsigned long long host_ctr[5];
       FMG_CK(cudaMemcpyAsync(host_ctr, counters.ptr, sizeof(host_ctr), cudaMemcpyDeviceToHost, s));
       FMG_CK(cudaStreamSynchronize(s));
       const uint64_t failed = host_ctr[1];
+      if (host_ctr[4] > 0) {  // sort this pass's large result sets in place
+        k_sort_segments<<<unsigned(host_ctr[4]), 256, 0, s>>>(unsorted_list.ptr, res_off.ptr, res_cnt.ptr,
+                                                              pass_kl.back().ptr, pass_d.back().ptr, too_big.ptr);
+        FMG_CK(cudaGetLastError());
+        uint32_t tb_flag = 0;
+        FMG_CK(cudaMemcpyAsync(&tb_flag, too_big.ptr, 4, cudaMemcpyDeviceToHost, s));
+        FMG_CK(cudaStreamSynchronize(s));
+        if (tb_flag) need_cub_sort = true;
+      }
       if (trace) {
         cudaEventRecord(ev1, s);
         cudaEventSynchronize(ev1);
@@ -1302,10 +1766,10 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     FMG_CK(cub::DeviceScan::InclusiveSum(tmp.ptr, tmp_bytes, c64.ptr, res->row_off + 1, count, s));
     uint64_t total = 0;
     FMG_CK(cudaMemcpyAsync(&total, res->row_off + count, sizeof(total), cudaMemcpyDeviceToHost, s));
-    unsigned long long steps = 0, unsorted = 0;
+    unsigned long long steps = 0;
     FMG_CK(cudaMemcpyAsync(&steps, counters.ptr + 2, sizeof(steps), cudaMemcpyDeviceToHost, s));
-    FMG_CK(cudaMemcpyAsync(&unsorted, counters.ptr + 4, sizeof(unsorted), cudaMemcpyDeviceToHost, s));
     FMG_CK(cudaStreamSynchronize(s));
+    const bool unsorted = need_cub_sort;
     res->total = total;
     res->steps = steps;
     FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->k), std::max<uint64_t>(total, 1) * sizeof(uint32_t), s));
@@ -1317,8 +1781,8 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
                                                                      res->row_off, res->k, res->l, res->diffs);
       FMG_CK(cudaGetLastError());
     }
-    if (unsorted > 0 && total > 0) {
-      // patterns with > 4 results were written unsorted: segmented sort by (k, l)
+    if (unsorted && total > 0) {
+      // a pattern had more than kSortMax results: segmented sort of everything by (k, l)
       FMG_REQUIRE(total < (1ull << 31), "too many inexact results for one call");
       DevBuf<uint64_t> keys(total, s), keys2(total, s);
       DevBuf<uint8_t> d2(total, s);

@@ -189,7 +189,7 @@ def test_inexact_random_vs_oracle(gpu):
     idx = fm.build_index(text)
     ox = orc.OracleIndex(idx)
     for m, z, count in ((5, 2, 300), (19, 1, 3000), (32, 1, 3000), (32, 0, 2000), (20, 2, 300),
-                        (50, 1, 500), (80, 1, 300)):
+                        (50, 1, 500), (80, 1, 300), (4, 3, 40), (6, 3, 60)):
         offs = rng.integers(0, text.size - m + 1, count)
         pats = workloads.substrings(text, offs, m)
         pats = workloads.mutate(pats.reshape(-1), 0.03, rng).reshape(count, m)
@@ -323,3 +323,16 @@ def test_config4_first_chunk_vs_oracle(gpu):
     hit = kl[:, 0] <= kl[:, 1]
     assert abs(hit.mean() - 0.8) < 0.01  # 80% exact substrings, random 20-mers ~never occur
     idx.release_device()
+
+
+def test_z1_engines_agree(gpu, monkeypatch):
+    """z = 1: the level-synchronous engine and the DFS engine give identical result sets."""
+    wl = workloads.config2(n_reads=20_000, n=8_000_000)
+    idx = fm.build_index(wl.text)
+    a = fm.inexact_search_batch(idx, wl.patterns, 1)
+    monkeypatch.setenv("FMG_INEXACT_DFS", "1")
+    b = fm.inexact_search_batch(idx, wl.patterns, 1)
+    assert np.array_equal(a.offsets, b.offsets) and np.array_equal(a.k, b.k)
+    assert np.array_equal(a.l, b.l) and np.array_equal(a.diffs, b.diffs)
+    row, k, l, d, _ = orc.inexact_batch(orc.OracleIndex(idx), wl.patterns, 1)
+    assert np.array_equal(a.offsets, row) and np.array_equal(a.k.astype(np.int64), k)
