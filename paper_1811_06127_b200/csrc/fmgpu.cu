@@ -125,9 +125,19 @@ __global__ void k_build_lines(const uint64_t* __restrict__ rec, uint64_t nb, uin
   reinterpret_cast<Line<W>*>(lines)[j] = out;
 }
 
+// L2 eviction policies: streamed query/result bytes are marked evict-first
+// so they do not push index lines out of L2.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 __device__ __forceinline__ uint2 ld_stream_u2(const uint2* p) {
   uint2 v;
-  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+      : "=r"(v.x), "=r"(v.y)
+      : "l"(p), "l"(policy_evict_first()));
   return v;
 }
 
@@ -136,8 +146,8 @@ __device__ __forceinline__ void st_stream_256(uint32_t* p, const uint32_t lo[4],
   const uint64_t b = uint64_t(lo[2]) | (uint64_t(lo[3]) << 32);
   const uint64_t c = uint64_t(hi[0]) | (uint64_t(hi[1]) << 32);
   const uint64_t d = uint64_t(hi[2]) | (uint64_t(hi[3]) << 32);
-  asm volatile("st.global.L1::no_allocate.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(a), "l"(b), "l"(c),
-               "l"(d)
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "l"(a),
+               "l"(b), "l"(c), "l"(d), "l"(policy_evict_first())
                : "memory");
 }
 
@@ -1445,18 +1455,27 @@ void launch_locate(const fmg_index* ix, const uint32_t* rows, uint64_t count, ui
   FMG_CK(cudaGetLastError());
 }
 
-// Host validation of a pattern batch given on the host: offsets strictly
-// increasing (no empty pattern, search.py:83-84), codes in [0, 4).
-void validate_patterns_host(const uint8_t* codes, const uint64_t* offsets, uint64_t count, uint64_t* max_len) {
-  FMG_REQUIRE(offsets[0] == 0, "pattern offsets must start at 0");
-  uint64_t mx = 0;
-  for (uint64_t q = 0; q < count; ++q) {
-    FMG_REQUIRE(offsets[q + 1] > offsets[q], "pattern is empty");
-    mx = std::max(mx, offsets[q + 1] - offsets[q]);
-  }
-  for (uint64_t j = 0; j < offsets[count]; ++j) FMG_REQUIRE(codes[j] < 4, "symbol code outside [0, 4)");
-  *max_len = mx;
+// Validates a device pattern batch (k_check_patterns) and returns the
+// longest pattern; throws invalid_argument like the reference's ValueErrors.
+uint64_t validate_patterns_device(const uint8_t* codes, const uint64_t* offsets, uint64_t count, cudaStream_t s) {
+  if (count == 0) return 0;
+  DevBuf<unsigned long long> ml(1, s);
+  DevBuf<uint32_t> err(1, s);
+  FMG_CK(cudaMemsetAsync(ml.ptr, 0, 8, s));
+  FMG_CK(cudaMemsetAsync(err.ptr, 0, 4, s));
+  k_check_patterns<<<unsigned((count + 255) / 256), 256, 0, s>>>(codes, offsets, count, ml.ptr, err.ptr);
+  FMG_CK(cudaGetLastError());
+  unsigned long long h_ml = 0;
+  uint32_t h_err = 0;
+  FMG_CK(cudaMemcpyAsync(&h_ml, ml.ptr, 8, cudaMemcpyDeviceToHost, s));
+  FMG_CK(cudaMemcpyAsync(&h_err, err.ptr, 4, cudaMemcpyDeviceToHost, s));
+  FMG_CK(cudaStreamSynchronize(s));
+  FMG_REQUIRE(!(h_err & 4u), "pattern offsets must start at 0");
+  FMG_REQUIRE(!(h_err & 1u), "pattern is empty");
+  FMG_REQUIRE(!(h_err & 2u), "symbol code outside [0, 4)");
+  return h_ml;
 }
+
 
 // z = 1 through k_spine / k_chain; false when a queue overflowed (the caller
 // then runs the DFS engine, which has no such limit).  Fills res on success.
@@ -2048,20 +2067,24 @@ int fmg_exact_host(const fmg_index* ix, const uint8_t* codes, const uint64_t* of
   return fmg::guard([&] {
     check_index(ix);
     if (count == 0) return;
-    uint64_t max_len = 0;
-    validate_patterns_host(codes, offsets, count, &max_len);
+    FMG_REQUIRE(offsets[0] == 0 && offsets[count] >= count, "pattern offsets must start at 0; patterns non-empty");
     fmg::DeviceScope scope(ix->device);
     cudaStream_t s;
     FMG_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    {
+    try {
       DevBuf<uint8_t> dc(offsets[count], s);
       DevBuf<uint64_t> doff(count + 1, s);
       DevBuf<uint32_t> dout(2 * count, s);
       FMG_CK(cudaMemcpyAsync(dc.ptr, codes, offsets[count], cudaMemcpyHostToDevice, s));
       FMG_CK(cudaMemcpyAsync(doff.ptr, offsets, (count + 1) * 8, cudaMemcpyHostToDevice, s));
+      validate_patterns_device(dc.ptr, doff.ptr, count, s);
       launch_exact_codes(ix, dc.ptr, doff.ptr, count, dout.ptr, s, nullptr);
       FMG_CK(cudaMemcpyAsync(kl_out, dout.ptr, 2 * count * 4, cudaMemcpyDeviceToHost, s));
       FMG_CK(cudaStreamSynchronize(s));
+    } catch (...) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+      throw;
     }
     cudaStreamSynchronize(s);
     cudaStreamDestroy(s);
@@ -2092,25 +2115,7 @@ int fmg_inexact(const fmg_index* ix, const uint8_t* codes, const uint64_t* offse
     *out = nullptr;
     fmg::DeviceScope scope(ix->device);
     cudaStream_t s = as_stream(stream);
-    // validate on the device and find the longest pattern (scratch sizing)
-    uint64_t max_len = 0;
-    if (count > 0) {
-      DevBuf<unsigned long long> ml(1, s);
-      DevBuf<uint32_t> err(1, s);
-      FMG_CK(cudaMemsetAsync(ml.ptr, 0, 8, s));
-      FMG_CK(cudaMemsetAsync(err.ptr, 0, 4, s));
-      k_check_patterns<<<unsigned((count + 255) / 256), 256, 0, s>>>(codes, offsets, count, ml.ptr, err.ptr);
-      FMG_CK(cudaGetLastError());
-      unsigned long long h_ml = 0;
-      uint32_t h_err = 0;
-      FMG_CK(cudaMemcpyAsync(&h_ml, ml.ptr, 8, cudaMemcpyDeviceToHost, s));
-      FMG_CK(cudaMemcpyAsync(&h_err, err.ptr, 4, cudaMemcpyDeviceToHost, s));
-      FMG_CK(cudaStreamSynchronize(s));
-      FMG_REQUIRE(!(h_err & 4u), "pattern offsets must start at 0");
-      FMG_REQUIRE(!(h_err & 1u), "pattern is empty");
-      FMG_REQUIRE(!(h_err & 2u), "symbol code outside [0, 4)");
-      max_len = h_ml;
-    }
+    const uint64_t max_len = validate_patterns_device(codes, offsets, count, s);
     *out = run_inexact(ix, codes, offsets, count, max_len, max_diff, s);
   });
 }
@@ -2122,8 +2127,8 @@ int fmg_inexact_host(const fmg_index* ix, const uint8_t* codes, const uint64_t* 
     FMG_REQUIRE(out != nullptr, "null output pointer");
     *out = nullptr;
     FMG_REQUIRE(max_diff >= 0, "difference budget is negative");
-    uint64_t max_len = 0;
-    if (count > 0) validate_patterns_host(codes, offsets, count, &max_len);
+    if (count > 0)
+      FMG_REQUIRE(offsets[0] == 0 && offsets[count] >= count, "pattern offsets must start at 0; patterns non-empty");
     fmg::DeviceScope scope(ix->device);
     cudaStream_t s;
     FMG_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -2134,6 +2139,7 @@ int fmg_inexact_host(const fmg_index* ix, const uint8_t* codes, const uint64_t* 
         FMG_CK(cudaMemcpyAsync(dc.ptr, codes, offsets[count], cudaMemcpyHostToDevice, s));
         FMG_CK(cudaMemcpyAsync(doff.ptr, offsets, (count + 1) * 8, cudaMemcpyHostToDevice, s));
       }
+      const uint64_t max_len = validate_patterns_device(dc.ptr, doff.ptr, count, s);
       *out = run_inexact(ix, dc.ptr, doff.ptr, count, max_len, max_diff, s);
     } catch (...) {
       cudaStreamSynchronize(s);
