@@ -364,3 +364,63 @@ def reconstruct_reference(index: FmIndex, kernel: Kernel | str | None = None) ->
     text[pos[live] - 1] = sym[live]
     lut = np.frombuffer(SYMBOLS.encode(), dtype=np.uint8)
     return lut[text].tobytes().decode("ascii")
+
+
+def collect_hits_batch(index: FmIndex, pid: np.ndarray, k: np.ndarray, l: np.ndarray, diffs: np.ndarray,
+                       pattern_len: np.ndarray, max_hits: int | None = None):
+    """collect_hits (search.py:245-267) for many patterns with ONE locate launch.
+
+    Intervals are given flat: pattern id, k, l, diffs per matched interval
+    (empty intervals allowed and ignored); pattern_len[p] is the length of
+    pattern p.  Returns (hit_pid, positions, diffs, record index, offset)
+    sorted by (pattern, position), the fewest diffs per position, and the
+    per-pattern `truncated` flags of max_hits.
+    """
+    pid = np.asarray(pid, dtype=np.int64)
+    k = np.asarray(k, dtype=np.int64)
+    l = np.asarray(l, dtype=np.int64)
+    diffs = np.asarray(diffs, dtype=np.int64)
+    n_pat = int(np.asarray(pattern_len).size)
+    live = l >= k
+    pid, k, l, diffs = pid[live], k[live], l[live], diffs[live]
+    width = l - k + 1
+    total = int(width.sum())
+    if total == 0:
+        z = np.zeros(0, dtype=np.int64)
+        return z, z, z, z, z, np.zeros(n_pat, dtype=bool)
+    owner = np.repeat(np.arange(width.size), width)
+    starts = np.zeros(width.size, dtype=np.int64)
+    np.cumsum(width[:-1], out=starts[1:])
+    rows = k[owner] + (np.arange(total, dtype=np.int64) - starts[owner])
+    pos = locate_rows(index, rows)
+    hp, hd = pid[owner], diffs[owner]
+    # locate_all filters (search.py:226-238), per interval's own diffs
+    rec_start = np.array([r.start for r in index.records], dtype=np.int64)
+    rec_len = np.array([r.length for r in index.records], dtype=np.int64)
+    keep = pos < index.n
+    pos, hp, hd = pos[keep], hp[keep], hd[keep]
+    which = np.searchsorted(rec_start, pos, side="right") - 1
+    offset = pos - rec_start[which]
+    plen = np.asarray(pattern_len, dtype=np.int64)[hp]
+    ok = offset + np.maximum(plen - hd, 0) <= rec_len[which]
+    pos, hp, hd, which, offset = pos[ok], hp[ok], hd[ok], which[ok], offset[ok]
+    # fewest diffs per (pattern, position), sorted by (pattern, position)
+    order = np.lexsort((hd, pos, hp))
+    pos, hp, hd, which, offset = pos[order], hp[order], hd[order], which[order], offset[order]
+    first = np.ones(pos.size, dtype=bool)
+    first[1:] = (pos[1:] != pos[:-1]) | (hp[1:] != hp[:-1])
+    pos, hp, hd, which, offset = pos[first], hp[first], hd[first], which[first], offset[first]
+    truncated = np.zeros(n_pat, dtype=bool)
+    if max_hits is not None:
+        group_start = np.zeros(hp.size, dtype=np.int64)
+        new = np.ones(hp.size, dtype=bool)
+        new[1:] = hp[1:] != hp[:-1]
+        idx_new = np.flatnonzero(new)
+        group_start[idx_new] = idx_new
+        group_start = np.maximum.accumulate(group_start)
+        rank = np.arange(hp.size) - group_start
+        over = rank >= max_hits
+        truncated[np.unique(hp[over])] = True
+        keep = ~over
+        pos, hp, hd, which, offset = pos[keep], hp[keep], hd[keep], which[keep], offset[keep]
+    return hp, pos, hd, which, offset, truncated

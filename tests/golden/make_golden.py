@@ -177,6 +177,59 @@ def gen_config1():
     print("config1:", meta)
 
 
+def gen_cli():
+    """The reference CLI on a 3-record FASTA: match TSV/stderr at z = 0, 1, 2, --max-hits, bench checksum."""
+    import contextlib
+
+    from fmpm.cli import main as ref_main
+
+    out = HERE / "cli"
+    out.mkdir(exist_ok=True)
+    rng = np.random.Generator(np.random.PCG64(777))
+    recs = [("chr1", 1500), ("chr2", 900), ("chrM", 400)]
+    texts = {name: text_of(rng.integers(0, 4, n, dtype=np.uint8)) for name, n in recs}
+    with open(out / "ref.fa", "w") as fh:
+        for name, _ in recs:
+            seq = texts[name]
+            fh.write(f">{name} synthetic\n")
+            for i in range(0, len(seq), 70):
+                fh.write(seq[i:i + 70] + "\n")
+    whole = "".join(texts[n] for n, _ in recs)
+    pats = []
+    for _ in range(60):
+        m = int(rng.integers(4, 25))
+        s = int(rng.integers(0, len(whole) - m))
+        p = whole[s:s + m]
+        r = rng.random()
+        if r < 0.3:
+            j = int(rng.integers(0, m))
+            p = p[:j] + "ACGT"[(("ACGT".index(p[j])) + 1) % 4] + p[j + 1:]
+        elif r < 0.4:
+            p = p.lower()
+        pats.append(p)
+    pats += ["ACNGT", "AC", "TTTTTTTTTTTTTTTTTTTT", whole[1495:1505]]  # degenerate, frequent, absent, junction
+    (out / "patterns.txt").write_text("\n".join(pats) + "\n")
+    fmi = out / "ref.fmi"
+
+    def run(args, name):
+        so, se = io.StringIO(), io.StringIO()
+        with contextlib.redirect_stdout(so), contextlib.redirect_stderr(se):
+            code = ref_main(args)
+        (out / f"{name}.out").write_text(so.getvalue())
+        (out / f"{name}.err").write_text(se.getvalue())
+        return code
+
+    assert run(["index", str(out / "ref.fa"), "-o", str(fmi)], "index") == 0
+    (out / "ref.fmi.sha256").write_text(sha(fmi.read_bytes()))
+    fmi_bytes = fmi.read_bytes()
+    for z in (0, 1, 2):
+        assert run(["match", str(fmi), "-f", str(out / "patterns.txt"), "-z", str(z)], f"match_z{z}") == 0
+    assert run(["match", str(fmi), "-f", str(out / "patterns.txt"), "-z", "1", "--max-hits", "2"], "match_max2") == 0
+    assert run(["bench", str(fmi), "--iters", "30", "--seed", "3", "--kernels", "bytelut"], "bench") == 0
+    fmi.unlink()  # the tests rebuild it with our own index command
+    print("cli: fixtures written", len(fmi_bytes), "byte index")
+
+
 if __name__ == "__main__":
     for what in sys.argv[1:]:
-        {"small": gen_small, "config0": gen_config0, "config1": gen_config1}[what]()
+        {"small": gen_small, "config0": gen_config0, "config1": gen_config1, "cli": gen_cli}[what]()
