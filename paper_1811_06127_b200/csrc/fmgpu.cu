@@ -205,6 +205,23 @@ __global__ void __launch_bounds__(256) k_occ_pair(IndexView ix, const uint2* __r
   }
 }
 
+// Random-fetch microbenchmark (the ceiling of the HBM-resident Occ step):
+// one random 32-byte read per thread from `bytes` of memory, addresses from a
+// hash (tools/micro/gather*.cu measured 48 G/s on B200 for 4 GiB).
+__global__ void k_random_fetch(const uint8_t* __restrict__ buf, uint64_t n_slots, uint64_t count, uint64_t seed,
+                               unsigned long long* sink) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  uint64_t x = (i + 1) * 0x9E3779B97F4A7C15ull ^ seed;
+  x ^= x >> 31;
+  x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 29;
+  const uint64_t slot = x % n_slots;
+  uint64_t a0, a1, a2, a3;
+  ld256<true>(buf + slot * 32, a0, a1, a2, a3);
+  if ((a0 ^ a1 ^ a2 ^ a3) == 0x123456789ull) atomicAdd(sink, 1ull);
+}
+
 // Lane-cooperative Occ step for wide lines (W = 6: 2 lanes, W = 14: 4 lanes).
 // The LANES lanes of a group each load one 32-byte sector of the same line in
 // ONE instruction, so the line costs a single memory request (on B200 a
@@ -2027,6 +2044,40 @@ int fmgx_set_l2_fetch_granularity(int device, int bytes, int* prev) {
     FMG_CK(cudaDeviceGetLimit(&old, cudaLimitMaxL2FetchGranularity));
     if (prev) *prev = int(old);
     if (bytes >= 0) FMG_CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(bytes)));
+  });
+}
+
+// Measured random 32-byte fetches per second on `device` over `bytes` of
+// memory (>> L2), best of 3 launches of `count` reads.  Used by bench.py as
+// the request roofline of HBM-resident Occ steps.
+int fmgx_random_fetch_rate(int device, uint64_t bytes, uint64_t count, double* rate) {
+  return fmg::guard([&] {
+    FMG_REQUIRE(rate != nullptr && bytes >= 32 && count > 0, "bad argument");
+    fmg::DeviceScope scope(device);
+    uint8_t* buf = nullptr;
+    unsigned long long* sink = nullptr;
+    FMG_CK(cudaMalloc(&buf, bytes));
+    FMG_CK(cudaMalloc(&sink, 8));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    cudaError_t err = cudaMemset(buf, 1, bytes);
+    for (int r = 0; r < 4 && err == cudaSuccess; ++r) {
+      cudaEventRecord(e0);
+      fmg::k_random_fetch<<<unsigned((count + 255) / 256), 256>>>(buf, bytes / 32, count, uint64_t(r) * 7919, sink);
+      cudaEventRecord(e1);
+      err = cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (r > 0) best = std::min(best, ms);  // first launch is warm-up
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(buf);
+    cudaFree(sink);
+    FMG_CK(err);
+    *rate = double(count) / (double(best) * 1e-3);
   });
 }
 
