@@ -205,6 +205,34 @@ __global__ void __launch_bounds__(256) k_occ_pair(IndexView ix, const uint2* __r
   }
 }
 
+// Two lanes per Occ step (W = 2): lane 0 handles position k-1, lane 1
+// position l, each loading ITS line in the same instruction.  When the two
+// lines share a 128-byte chunk (64% of config-1 steps) the coalescer merges
+// them into one L2 request, so requests per step drop from 1.75 (lines) to
+// 1.36 (chunks); each lane counts one position and stores its 16 bytes.
+__global__ void __launch_bounds__(256) k_occ_pair_2l(IndexView ix, const uint2* __restrict__ kl, uint64_t count,
+                                                     uint32_t* __restrict__ out, uint32_t* __restrict__ err) {
+  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t i = t >> 1;
+  const uint32_t role = uint32_t(t & 1u);  // 0: low (k-1), 1: high (l)
+  if (i >= count) return;
+  const uint2 q = ld_stream_u2(kl + i);
+  const uint32_t k = q.x, l = q.y;
+  const bool ok = l <= ix.n && k <= l + 1u;
+  if (!ok && role == 0u) atomicOr(err, 1u);
+  const bool none = !ok || (role == 0u && k == 0u);  // Occ(., -1) = 0
+  const uint32_t p = role ? l : k - 1u;
+  const uint32_t pp = none ? (ok ? l : 0u) : p;  // a lane with nothing to count reads its partner's line
+  uint32_t b[4], r4[4] = {0u, 0u, 0u, 0u};
+  uint64_t w[2];
+  load_line<2, true>(ix, pp >> 6, pp & 63u, b, w);
+  if (!none) occ4_from_line<2>(ix, b, w, p, p & 63u, r4);
+  uint4* dst = reinterpret_cast<uint4*>(out + i * 8 + role * 4);
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(dst), "r"(r4[0]),
+               "r"(r4[1]), "r"(r4[2]), "r"(r4[3]), "l"(policy_evict_first())
+               : "memory");
+}
+
 // Random-fetch microbenchmark (the ceiling of the HBM-resident Occ step):
 // one random 32-byte read per thread from `bytes` of memory, addresses from a
 // hash (tools/micro/gather*.cu measured 48 G/s on B200 for 4 GiB).
@@ -1388,7 +1416,14 @@ void launch_occ_pair_t(const fmg_index* ix, const uint32_t* kl, uint64_t count, 
   const uint64_t blocks = (count + per_block - 1) / per_block;
   with_words(ix, [&](auto wt) {
     constexpr int W = decltype(wt)::value;
-    if (W == 2) {
+    // two lanes per step only for HBM-resident line arrays (> 64 MB): +4% on
+    // config 1-H, -8% on the L2-resident config 1 (profiles/r01_occ.md)
+    const char* e2l = std::getenv("FMG_OCC_2LANE");  // A/B hook
+    const bool two_lane = e2l ? std::atoi(e2l) != 0 : ix->n_lines * 32ull > (64ull << 20);
+    if (W == 2 && two_lane) {
+      k_occ_pair_2l<<<dim3(unsigned((2 * count + 255) / 256)), 256, 0, s>>>(
+          ix->view(), reinterpret_cast<const uint2*>(kl), count, out, ix->err);
+    } else if (W == 2) {
       k_occ_pair<PER, W><<<dim3(unsigned(blocks)), threads, 0, s>>>(ix->view(), reinterpret_cast<const uint2*>(kl),
                                                                       count, out, ix->err);
     } else {  // wide lines: lane-cooperative, persistent grid-stride
