@@ -1,13 +1,11 @@
-// B200-native FM-index engine: kernels and the C ABI of include/fmgpu.h.
-//
-// Kernels (all sm_100a, integer/popcount + random 32-byte gathers; no tensor
-// cores — the Occ step has no GEMM shape):
-//   k_build_lines   .fmi bucket records -> 32-byte lines          (index.py:24-36)
-//   k_occ_pair      one thread per (k-1, l) pair, PER pairs/thread (occ.py:59-96)
-//   k_exact         persistent, lane-refill backward search      (search.py:74-94)
-//   k_inexact       persistent, lane-refill DFS with a per-thread
-//                   stack and a lower-bound prune                (search.py:97-159)
-//   k_psi / k_locate  predecessor walk to the sampled rows       (search.py:172-208)
+// B200-native FM-index engine: host side of libfmgpu.so and the C ABI of
+// include/fmgpu.h.  Kernels (sm_100a, integer/popcount + random 32-byte
+// gathers; no tensor cores — the Occ step has no GEMM shape):
+//   kernels_occ.cuh      k_build_lines, k_occ_pair (+ 2-lane, wide-line coop),
+//                        k_random_fetch                        (occ.py:59-96)
+//   kernels_search.cuh   k_exact, k_psi, k_locate              (search.py:74-94, 172-208)
+//   kernels_inexact.cuh  k_dbound, k_inexact (DFS), k_spine / k_chain (z = 1),
+//                        sort / dedup / gather                 (search.py:97-159)
 
 #include <cuda_runtime.h>
 
@@ -79,1243 +77,13 @@ struct DevBuf {
   }
 };
 
-// ---------------------------------------------------------------------------
-// Kernels
-// ---------------------------------------------------------------------------
+}  // namespace fmg
 
-// Counts of A, C, G, T among all 32 fields of one packed word.
-__device__ __forceinline__ void add_word_counts(uint64_t w, uint32_t c[4]) {
-  const uint64_t lo = w & kFieldLo, hi = (w >> 1) & kFieldLo;
-  const uint32_t t = __popcll(lo & hi), h = __popcll(hi), l = __popcll(lo);
-  c[3] += t;
-  c[2] += h - t;
-  c[1] += l - t;
-  c[0] += 32u - h - l + t;
-}
+#include "kernels_occ.cuh"
+#include "kernels_search.cuh"
+#include "kernels_inexact.cuh"
 
-// Bucket records (4 x u64 LE base + 32 B chars, 128 chars each) -> lines of
-// 32W chars.  Line j starts at char 32Wj, which is a multiple of 32 and so
-// falls on a word boundary of its bucket; its checkpoint is the bucket base
-// plus the counts of the bucket's words before it.
-template <int W>
-__global__ void k_build_lines(const uint64_t* __restrict__ rec, uint64_t nb, uint8_t* __restrict__ lines,
-                              uint64_t n_lines, uint32_t* __restrict__ err) {
-  const uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= n_lines) return;
-  const uint64_t c0 = j * LineTraits<W>::kChars;
-  const uint64_t b0 = c0 >> 7;
-  const uint64_t* r = rec + b0 * 8;
-  uint32_t base[4];
-#pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    if (r[s] >= 0xFFFFFFFFull) atomicOr(err, 1u);
-    base[s] = uint32_t(r[s]);
-  }
-  const uint32_t skip = uint32_t((c0 & 127u) >> 5);
-  for (uint32_t q = 0; q < skip; ++q) add_word_counts(r[4 + q], base);
-  Line<W> out;
-#pragma unroll
-  for (int s = 0; s < 4; ++s) out.base[s] = base[s];
-#pragma unroll
-  for (int k = 0; k < W; ++k) {
-    const uint64_t c = c0 + 32u * k;
-    const uint64_t b = c >> 7;
-    out.w[k] = (b < nb) ? rec[b * 8 + 4 + ((c & 127u) >> 5)] : 0ull;
-  }
-  reinterpret_cast<Line<W>*>(lines)[j] = out;
-}
-
-// L2 eviction policies: streamed query/result bytes are marked evict-first
-// so they do not push index lines out of L2.
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t pol;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-
-__device__ __forceinline__ uint2 ld_stream_u2(const uint2* p) {
-  uint2 v;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
-      : "=r"(v.x), "=r"(v.y)
-      : "l"(p), "l"(policy_evict_first()));
-  return v;
-}
-
-__device__ __forceinline__ void st_stream_256(uint32_t* p, const uint32_t lo[4], const uint32_t hi[4]) {
-  const uint64_t a = uint64_t(lo[0]) | (uint64_t(lo[1]) << 32);
-  const uint64_t b = uint64_t(lo[2]) | (uint64_t(lo[3]) << 32);
-  const uint64_t c = uint64_t(hi[0]) | (uint64_t(hi[1]) << 32);
-  const uint64_t d = uint64_t(hi[2]) | (uint64_t(hi[3]) << 32);
-  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "l"(a),
-               "l"(b), "l"(c), "l"(d), "l"(policy_evict_first())
-               : "memory");
-}
-
-// Occ step microkernel.  Thread handles PER pairs strided by blockDim so the
-// (k,l) loads and the 32-byte output stores stay fully coalesced; all line
-// loads of a thread are issued before any popcount so each thread keeps up
-// to 2*PER independent line reads in flight.
-template <int PER, int W>
-__global__ void __launch_bounds__(256) k_occ_pair(IndexView ix, const uint2* __restrict__ kl, uint64_t count,
-                                                  uint32_t* __restrict__ out, uint32_t* __restrict__ err) {
-  constexpr uint32_t kC = LineTraits<W>::kChars;
-  const uint64_t first = uint64_t(blockIdx.x) * blockDim.x * PER + threadIdx.x;
-  uint2 q[PER];
-  bool act[PER];
-#pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    const uint64_t i = first + uint64_t(u) * blockDim.x;
-    act[u] = i < count;
-    q[u] = act[u] ? ld_stream_u2(kl + i) : make_uint2(1u, 0u);
-  }
-  uint32_t bh[PER][4], bl[PER][4];
-  uint64_t wh[PER][W], wl[PER][W];
-  bool ok[PER], two[PER];
-  uint32_t rh[PER], rl[PER];
-#pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    const uint32_t k = q[u].x, l = q[u].y;
-    ok[u] = act[u] && l <= ix.n && k <= l + 1u;
-    if (act[u] && !ok[u]) atomicOr(err, 1u);
-    const uint32_t hh = ok[u] ? l : 0u;
-    const uint32_t ll = (ok[u] && k != 0u) ? k - 1u : hh;
-    const uint32_t jh = line_of<W>(hh), jl = line_of<W>(ll);
-    rh[u] = hh - jh * kC;
-    rl[u] = ll - jl * kC;
-    two[u] = jl != jh;
-    load_line<W, true>(ix, jh, rh[u], bh[u], wh[u]);
-    if (two[u]) load_line<W, true>(ix, jl, rl[u], bl[u], wl[u]);
-  }
-#pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    if (!act[u]) continue;
-    const uint32_t k = q[u].x, l = q[u].y;
-    uint32_t lo[4] = {0u, 0u, 0u, 0u}, hi[4] = {0u, 0u, 0u, 0u};
-    if (ok[u]) {
-      occ4_from_line<W>(ix, bh[u], wh[u], l, rh[u], hi);
-      if (k != 0u) {
-        if (two[u])
-          occ4_from_line<W>(ix, bl[u], wl[u], k - 1u, rl[u], lo);
-        else
-          occ4_from_line<W>(ix, bh[u], wh[u], k - 1u, rl[u], lo);
-      }
-    }
-    const uint64_t i = first + uint64_t(u) * blockDim.x;
-    st_stream_256(out + i * 8, lo, hi);
-  }
-}
-
-// Two lanes per Occ step (W = 2): lane 0 handles position k-1, lane 1
-// position l, each loading ITS line in the same instruction.  When the two
-// lines share a 128-byte chunk (64% of config-1 steps) the coalescer merges
-// them into one L2 request, so requests per step drop from 1.75 (lines) to
-// 1.36 (chunks); each lane counts one position and stores its 16 bytes.
-__global__ void __launch_bounds__(256) k_occ_pair_2l(IndexView ix, const uint2* __restrict__ kl, uint64_t count,
-                                                     uint32_t* __restrict__ out, uint32_t* __restrict__ err) {
-  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint64_t i = t >> 1;
-  const uint32_t role = uint32_t(t & 1u);  // 0: low (k-1), 1: high (l)
-  if (i >= count) return;
-  const uint2 q = ld_stream_u2(kl + i);
-  const uint32_t k = q.x, l = q.y;
-  const bool ok = l <= ix.n && k <= l + 1u;
-  if (!ok && role == 0u) atomicOr(err, 1u);
-  const bool none = !ok || (role == 0u && k == 0u);  // Occ(., -1) = 0
-  const uint32_t p = role ? l : k - 1u;
-  const uint32_t pp = none ? (ok ? l : 0u) : p;  // a lane with nothing to count reads its partner's line
-  uint32_t b[4], r4[4] = {0u, 0u, 0u, 0u};
-  uint64_t w[2];
-  load_line<2, true>(ix, pp >> 6, pp & 63u, b, w);
-  if (!none) occ4_from_line<2>(ix, b, w, p, p & 63u, r4);
-  uint4* dst = reinterpret_cast<uint4*>(out + i * 8 + role * 4);
-  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(dst), "r"(r4[0]),
-               "r"(r4[1]), "r"(r4[2]), "r"(r4[3]), "l"(policy_evict_first())
-               : "memory");
-}
-
-// Random-fetch microbenchmark (the ceiling of the HBM-resident Occ step):
-// one random 32-byte read per thread from `bytes` of memory, addresses from a
-// hash (tools/micro/gather*.cu measured 48 G/s on B200 for 4 GiB).
-__global__ void k_random_fetch(const uint8_t* __restrict__ buf, uint64_t n_slots, uint64_t count, uint64_t seed,
-                               unsigned long long* sink) {
-  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= count) return;
-  uint64_t x = (i + 1) * 0x9E3779B97F4A7C15ull ^ seed;
-  x ^= x >> 31;
-  x *= 0xBF58476D1CE4E5B9ull;
-  x ^= x >> 29;
-  const uint64_t slot = x % n_slots;
-  uint64_t a0, a1, a2, a3;
-  ld256<true>(buf + slot * 32, a0, a1, a2, a3);
-  if ((a0 ^ a1 ^ a2 ^ a3) == 0x123456789ull) atomicAdd(sink, 1ull);
-}
-
-// Lane-cooperative Occ step for wide lines (W = 6: 2 lanes, W = 14: 4 lanes).
-// The LANES lanes of a group each load one 32-byte sector of the same line in
-// ONE instruction, so the line costs a single memory request (on B200 a
-// random 64-byte request costs the same as a 32-byte one, 128 bytes 1.2x;
-// tools/micro/gather3.cu), and count the fields of their own words; partial
-// (T, hi, lo) popcounts are summed with xor-shuffles.  Fewer, denser lines
-// mean fewer DRAM requests per step for HBM-resident indexes.
-template <int W>
-__device__ __forceinline__ void partial_counts(const uint64_t v[4], int sector, uint32_t r, uint32_t& t, uint32_t& h,
-                                               uint32_t& l) {
-  // sector 0 holds words 0, 1 (after the 16-byte checkpoint); sector j >= 1
-  // holds words 4j-2 .. 4j+1
-  const int k0 = sector == 0 ? 0 : 4 * sector - 2;
-  const int nw = sector == 0 ? 2 : 4;
-  t = h = l = 0;
-#pragma unroll
-  for (int q = 0; q < 4; q += 2) {
-    if (q >= nw) break;
-    const uint64_t wa = (sector == 0 ? v[2 + q] : v[q]), wb = (sector == 0 ? v[3 + q] : v[q + 1]);
-    const uint64_t x0 = wa & word_mask(r, k0 + q), x1 = wb & word_mask(r, k0 + q + 1);
-    const uint64_t lo = (x0 & kFieldLo) | ((x1 & kFieldLo) << 1);
-    const uint64_t hi = ((x0 >> 1) & kFieldLo) | (x1 & ~kFieldLo);
-    t += __popcll(lo & hi);
-    h += __popcll(hi);
-    l += __popcll(lo);
-  }
-}
-
-template <int W>
-__global__ void __launch_bounds__(256) k_occ_pair_coop(IndexView ix, const uint2* __restrict__ kl, uint64_t count,
-                                                       uint32_t* __restrict__ out, uint32_t* __restrict__ err) {
-  constexpr int LANES = int(LineTraits<W>::kBytes / 32);
-  constexpr uint32_t kC = LineTraits<W>::kChars;
-  const int sector = threadIdx.x % LANES;
-  // the lanes of a group always agree on the pair index, so shuffles use the
-  // group's own mask (groups of one warp may leave the loop at different times)
-  const uint32_t gmask = ((1u << LANES) - 1u) << ((threadIdx.x & 31u) & ~uint32_t(LANES - 1));
-  {
-    const uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) / LANES;  // one group per pair
-    if (i >= count) return;  // the whole group leaves together
-    const uint2 q = ld_stream_u2(kl + i);
-    const uint32_t k = q.x, l = q.y;
-    const bool ok = l <= ix.n && k <= l + 1u;
-    if (!ok && sector == 0) atomicOr(err, 1u);
-    const uint32_t hh = ok ? l : 0u;
-    const uint32_t ll = (ok && k != 0u) ? k - 1u : hh;
-    const uint32_t jh = line_of<W>(hh), jl = line_of<W>(ll);
-    const uint32_t rh = hh - jh * kC, rl = ll - jl * kC;
-    uint64_t vh[4], vl[4];
-    ld256<true>(ix.lines + size_t(jh) * LineTraits<W>::kBytes + 32 * sector, vh[0], vh[1], vh[2], vh[3]);
-    const bool two = jl != jh;
-    if (two) ld256<true>(ix.lines + size_t(jl) * LineTraits<W>::kBytes + 32 * sector, vl[0], vl[1], vl[2], vl[3]);
-    uint32_t th, hh_, lh, tl, hl, ll_;
-    partial_counts<W>(vh, sector, rh, th, hh_, lh);
-    if (two)
-      partial_counts<W>(vl, sector, rl, tl, hl, ll_);
-    else
-      partial_counts<W>(vh, sector, rl, tl, hl, ll_);
-#pragma unroll
-    for (int d = 1; d < LANES; d <<= 1) {
-      th += __shfl_xor_sync(gmask, th, d);
-      hh_ += __shfl_xor_sync(gmask, hh_, d);
-      lh += __shfl_xor_sync(gmask, lh, d);
-      tl += __shfl_xor_sync(gmask, tl, d);
-      hl += __shfl_xor_sync(gmask, hl, d);
-      ll_ += __shfl_xor_sync(gmask, ll_, d);
-    }
-    if (sector == 0) {
-      uint32_t lo[4] = {0u, 0u, 0u, 0u}, hi[4] = {0u, 0u, 0u, 0u};
-      if (ok) {
-        const uint32_t bh[4] = {uint32_t(vh[0]), uint32_t(vh[0] >> 32), uint32_t(vh[1]), uint32_t(vh[1] >> 32)};
-        hi[3] = bh[3] + th;
-        hi[2] = bh[2] + hh_ - th;
-        hi[1] = bh[1] + lh - th;
-        hi[0] = bh[0] + rh + 1u - hh_ - lh + th - (l >= ix.sentinel_row ? 1u : 0u);
-        if (k != 0u) {
-          const uint64_t b01 = two ? vl[0] : vh[0], b23 = two ? vl[1] : vh[1];
-          const uint32_t bl[4] = {uint32_t(b01), uint32_t(b01 >> 32), uint32_t(b23), uint32_t(b23 >> 32)};
-          lo[3] = bl[3] + tl;
-          lo[2] = bl[2] + hl - tl;
-          lo[1] = bl[1] + ll_ - tl;
-          lo[0] = bl[0] + rl + 1u - hl - ll_ + tl - (k - 1u >= ix.sentinel_row ? 1u : 0u);
-        }
-      }
-      st_stream_256(out + i * 8, lo, hi);
-    }
-  }
-}
-
-// Pattern sources for the search kernels.
-struct PackedPatterns {  // fixed length m <= 32, char j in bits 2j..2j+1
-  const uint64_t* words;
-  uint32_t m;
-  __device__ __forceinline__ uint32_t length(uint64_t) const { return m; }
-};
-struct CodePatterns {  // codes[offsets[q] .. offsets[q+1])
-  const uint8_t* codes;
-  const uint64_t* offsets;
-  const ulonglong2* packed = nullptr;  // inexact, m <= 64: 2-bit packed copy (k_pack_patterns)
-  const uint64_t* packed1 = nullptr;   // inexact, fixed m <= 32 given packed by the caller
-  uint32_t fixed_m = 0;
-  const uint64_t* dbits = nullptr;     // inexact, m <= 64: lower-bound segment ends (k_dbound)
-};
-
-// Exact backward search, one pattern per thread at a time.  When a lane's
-// pattern finishes (matched or emptied — the reference stops at the FIRST
-// empty interval, search.py:91-92) the lane immediately takes the next
-// pattern of its grid-stride sequence, so warps stay full while per-pattern
-// step counts vary from 1 to m-1.
-template <bool kPacked, int W>
-__global__ void __launch_bounds__(256) k_exact(IndexView ix, PackedPatterns pp, CodePatterns cp, uint64_t count,
-                                               uint2* __restrict__ out, unsigned long long* __restrict__ steps) {
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  uint64_t my_steps = 0;
-  uint64_t pat = 0;          // packed form
-  const uint8_t* codes = nullptr;  // general form
-  int i = -1;
-  uint32_t k = 1, l = 0;
-  auto start = [&](uint64_t qq) {
-    uint32_t m, b;
-    if (kPacked) {
-      pat = pp.words[qq];
-      m = pp.m;
-      b = uint32_t(pat >> (2 * (m - 1))) & 3u;
-    } else {
-      const uint64_t o0 = cp.offsets[qq], o1 = cp.offsets[qq + 1];
-      codes = cp.codes + o0;
-      m = uint32_t(o1 - o0);
-      b = codes[m - 1];
-    }
-    k = c_of(ix, b) + 1u;  // init_interval, search.py:50-57
-    l = c_of(ix, b + 1u);
-    i = int(m) - 2;
-  };
-  if (q >= count) return;
-  start(q);
-  while (true) {
-    if (i < 0 || k > l) {
-      out[q] = make_uint2(k, l);
-      q += stride;
-      if (q >= count) break;
-      start(q);
-      continue;
-    }
-    const uint32_t sym = kPacked ? (uint32_t(pat >> (2 * i)) & 3u) : uint32_t(__ldg(codes + i));
-    --i;
-    // extend_backward, search.py:60-71: k' = c[b] + Occ(b, k-1) + 1, l' = c[b] + Occ(b, l)
-    constexpr uint32_t kC = LineTraits<W>::kChars;
-    uint32_t bh[4], bl[4];
-    uint64_t wh[W], wl[W];
-    const uint32_t low = k - 1u;  // k >= 1 on every non-empty interval here
-    const uint32_t jh = line_of<W>(l), jl = line_of<W>(low);
-    const uint32_t rh = l - jh * kC, rl = low - jl * kC;
-    load_line<W, false>(ix, jh, rh, bh, wh);
-    uint32_t ol;
-    if (jl != jh) {
-      load_line<W, false>(ix, jl, rl, bl, wl);
-      ol = occ1_from_line<W>(ix, bl, wl, low, rl, sym);
-    } else {
-      ol = occ1_from_line<W>(ix, bh, wh, low, rl, sym);
-    }
-    const uint32_t oh = occ1_from_line<W>(ix, bh, wh, l, rh, sym);
-    const uint32_t cs = c_of(ix, sym);
-    k = cs + ol + 1u;
-    l = cs + oh;
-    ++my_steps;
-  }
-  if (steps) atomicAdd(steps, (unsigned long long)my_steps);
-}
-
-// ----- bounded-difference search -----------------------------------------
-
-// Lower-bound pass of the inexact search as its own kernel (patterns of
-// length <= 64): one thread per pattern extends right to left with resets;
-// every time W[pos..seg_end] is absent from the text, bit seg_end is set and
-// the search restarts from the root at pos-1.  D(i) = popcount of the bits
-// <= i (see k_inexact).  Running it apart keeps the DFS kernel's lanes in
-// one phase.
-template <int W>
-__global__ void __launch_bounds__(256) k_dbound(IndexView ix, CodePatterns cp, uint64_t count,
-                                                uint64_t* __restrict__ dbits_out, unsigned long long* steps) {
-  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (q >= count) return;
-  uint64_t pw0, pw1;
-  int m;
-  if (cp.packed1) {
-    pw0 = cp.packed1[q];
-    pw1 = 0;
-    m = int(cp.fixed_m);
-  } else {
-    const ulonglong2 pk = cp.packed[q];
-    pw0 = pk.x;
-    pw1 = pk.y;
-    m = int(cp.offsets[q + 1] - cp.offsets[q]);
-  }
-  constexpr uint32_t kC = LineTraits<W>::kChars;
-  uint64_t bits = 0;
-  uint32_t k = 0, l = ix.n;
-  int seg_end = m - 1;
-  uint32_t my_steps = 0;
-  for (int pos = m - 1; pos >= 0; --pos) {
-    const uint32_t b = uint32_t((pos < 32 ? pw0 : pw1) >> ((pos & 31) << 1)) & 3u;
-    const uint32_t cb = c_of(ix, b);
-    uint32_t k2, l2;
-    if (k == 0u && l == ix.n) {  // root: init_interval, no memory
-      k2 = cb + 1u;
-      l2 = c_of(ix, b + 1u);
-    } else {
-      const uint32_t low = k - 1u;
-      const uint32_t jh = line_of<W>(l), jl = line_of<W>(low);
-      const uint32_t rh = l - jh * kC, rl = low - jl * kC;
-      uint32_t bh[4], bl[4];
-      uint64_t wh[W], wl[W];
-      load_line<W, false>(ix, jh, rh, bh, wh);
-      uint32_t ol;
-      if (jl != jh) {
-        load_line<W, false>(ix, jl, rl, bl, wl);
-        ol = occ1_from_line<W>(ix, bl, wl, low, rl, b);
-      } else {
-        ol = occ1_from_line<W>(ix, bh, wh, low, rl, b);
-      }
-      k2 = cb + ol + 1u;
-      l2 = cb + occ1_from_line<W>(ix, bh, wh, l, rh, b);
-      ++my_steps;
-    }
-    if (k2 > l2) {  // W[pos..seg_end] is absent from the text
-      bits |= 1ull << seg_end;
-      k = 0;
-      l = ix.n;
-      seg_end = pos - 1;
-    } else {
-      k = k2;
-      l = l2;
-    }
-  }
-  dbits_out[q] = bits;
-  if (steps) atomicAdd(steps, (unsigned long long)my_steps);
-}
-
-// Per-thread global scratch for the inexact engine, warp-blocked (element e
-// of lane L of warp w at (w*N + e)*32 + L) so a warp's region is contiguous.
-// The DFS stack itself lives in shared memory (see k_inexact).
-struct InexactScratch {
-  uint4* table;     // H = 2R slots {k, l, epoch, used}: open-addressing dedup of results
-  uint32_t* slots;  // R entries: occupied table slots, in insertion order
-  uint8_t* dlb;     // Mmax entries: lower bound D[i] (long patterns only)
-  uint32_t S, R, Mmax;
-  uint64_t T;
-};
-
-struct InexactOut {
-  uint2* kl;          // reserved by atomicAdd on *total
-  uint8_t* diffs;
-  unsigned long long* total;
-  uint64_t cap;
-  uint64_t* res_off;  // per pattern: offset in this pass's buffer
-  uint32_t* res_cnt;  // per pattern: number of results
-  uint8_t* res_pass;  // per pattern: pass that produced it
-  uint8_t pass;
-  uint32_t* fail_list;  // patterns to retry with larger capacities
-  unsigned long long* fail_count;
-  unsigned long long* next;  // work-queue cursor
-  unsigned long long* steps;
-  unsigned long long* unsorted;  // patterns written with > S results (post-sorted)
-  uint32_t* unsorted_list;       // their pattern ids (capacity: count)
-};
-
-// Reference semantics (search.py:120-159): nodes (i, budget, k, l) from the
-// root (m-1, z, 0, n); a node with i < 0 is a result with z - budget diffs;
-// otherwise one Occ step at (k-1, l) and children skip (i-1, budget-1, k, l),
-// insert (i, budget-1, k', l'), match (i-1, budget, k', l') / mismatch
-// (i-1, budget-1, k', l') for every symbol with a non-empty k' <= l'.  The
-// set of (interval, min diffs) the DFS reaches does not depend on visiting
-// order, so the traversal order is free.
-//
-// Visiting order: a budget-0 node has only its match child, which is
-// continued in registers, so budget-0 chains — most of the steps — never
-// touch the stack.  A node with budget >= 1 pushes its match child (same
-// budget) first and then its budget-1 children, and the next iteration pops
-// the last one; the stack stays budget-monotone — one budget-z entry and at
-// most 9 per lower level, depth <= 9z + 1 — small enough for shared memory.
-//
-// Lower-bound prune (result-preserving): before the DFS, one right-to-left
-// exact pass with resets splits W into disjoint segments absent from the
-// text; D(i) = number of those segments lying inside W[0..i].  Every way of
-// turning W[0..i] into a substring of the text must touch each absent
-// segment with its own edit, so a node with D(i) > budget yields nothing and
-// is never pushed.  (BWA's D array, computed with the forward index only.)
-template <bool kShort, int W>
-__global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, const uint32_t* __restrict__ list,
-                                                 uint64_t count, uint32_t z, InexactScratch sc, InexactOut out) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const uint32_t S = sc.S, nt = blockDim.x, tid = threadIdx.x;
-  uint2* s_kl = reinterpret_cast<uint2*>(smem);               // [S][nt]
-  uint32_t* s_ib = reinterpret_cast<uint32_t*>(s_kl + S * nt);  // [S][nt]
-  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= sc.T) return;
-  uint64_t my_steps = 0;
-  const uint64_t wbase = t >> 5, lane = t & 31u;
-  auto HI = [&](uint32_t e) -> uint64_t { return (wbase * (2u * sc.R) + e) * 32u + lane; };
-  auto LI = [&](uint32_t e) -> uint64_t { return (wbase * sc.R + e) * 32u + lane; };
-  uint32_t epoch = 0;  // per-thread pattern counter: table slots of older patterns read as empty
-  auto DI = [&](uint32_t e) -> uint64_t { return (wbase * sc.Mmax + e) * 32u + lane; };
-
-  // per-pattern state
-  bool have = false;
-  uint64_t q = 0;
-  const uint8_t* codes = nullptr;
-  int m = 0;
-  uint64_t pw0 = 0, pw1 = 0;  // kShort: the pattern, packed
-  uint64_t dbits = 0;         // kShort: right ends of absent segments
-  int phase = 0;              // 0: lower-bound pass, 1: DFS
-  int pos = 0, seg_end = 0;   // lower-bound pass cursor
-  uint32_t kd = 0, ld = 0;    // lower-bound pass interval
-  uint32_t sp = 0, nres = 0;
-  bool overflow = false;
-  bool cur_valid = false;  // DFS node held in registers
-  int ci = 0;
-  uint32_t cb = 0, ck = 0, cl = 0;
-
-  auto sym_at = [&](int i) -> uint32_t {
-    if (kShort) return uint32_t((i < 32 ? pw0 : pw1) >> ((i & 31) << 1)) & 3u;
-    return uint32_t(__ldg(codes + i));
-  };
-  auto dlb = [&](int i) -> uint32_t {
-    if (kShort) return __popcll(dbits & ((2ull << i) - 1ull));
-    return sc.dlb[DI(uint32_t(i))];
-  };
-  // best[(k, l)] = min used (search.py:127-134) in a per-thread hash table
-  auto record = [&](uint32_t k, uint32_t l, uint32_t used) {
-    const uint32_t H = 2u * sc.R;
-    uint32_t h = (k * 0x9E3779B1u ^ l * 0x85EBCA77u) & (H - 1u);
-    for (uint32_t probe = 0; probe < H; ++probe, h = (h + 1u) & (H - 1u)) {
-      uint4 e = sc.table[HI(h)];
-      if (e.z != epoch) {  // empty for this pattern: insert
-        if (nres == sc.R) {
-          overflow = true;
-          return;
-        }
-        sc.table[HI(h)] = make_uint4(k, l, epoch, used);
-        sc.slots[LI(nres)] = h;
-        ++nres;
-        return;
-      }
-      if (e.x == k && e.y == l) {
-        if (used < e.w) sc.table[HI(h)].w = used;
-        return;
-      }
-    }
-    overflow = true;
-  };
-  auto fail = [&]() {
-    const unsigned long long f = atomicAdd(out.fail_count, 1ull);
-    out.fail_list[f] = uint32_t(q);
-    out.res_cnt[q] = 0;
-  };
-  auto finish = [&]() {
-    if (overflow) {
-      fail();
-      return;
-    }
-    uint64_t o = 0;
-    if (nres) {
-      o = atomicAdd(out.total, (unsigned long long)nres);
-      if (o + nres > out.cap) {  // this pass's buffer is full: retry later
-        fail();
-        return;
-      }
-      if (nres <= S) {
-        // The DFS stack is empty now: reuse this thread's shared-memory stack
-        // slots to insertion-sort the results by (k, l) (unique after dedup).
-        for (uint32_t r = 0; r < nres; ++r) {
-          const uint4 e = sc.table[HI(sc.slots[LI(r)])];
-          uint32_t b = r;
-          while (b > 0) {
-            const uint2 p = s_kl[(b - 1) * nt + tid];
-            if (p.x < e.x || (p.x == e.x && p.y < e.y)) break;
-            s_kl[b * nt + tid] = p;
-            s_ib[b * nt + tid] = s_ib[(b - 1) * nt + tid];
-            --b;
-          }
-          s_kl[b * nt + tid] = make_uint2(e.x, e.y);
-          s_ib[b * nt + tid] = e.w;
-        }
-        for (uint32_t r = 0; r < nres; ++r) {
-          out.kl[o + r] = s_kl[r * nt + tid];
-          out.diffs[o + r] = uint8_t(s_ib[r * nt + tid]);
-        }
-      } else {  // unsorted; the host runs a segmented sort afterwards
-        for (uint32_t r = 0; r < nres; ++r) {
-          const uint4 e = sc.table[HI(sc.slots[LI(r)])];
-          out.kl[o + r] = make_uint2(e.x, e.y);
-          out.diffs[o + r] = uint8_t(e.w);
-        }
-        const unsigned long long u = atomicAdd(out.unsorted, 1ull);
-        out.unsorted_list[u] = uint32_t(q);
-      }
-    }
-    out.res_off[q] = o;
-    out.res_cnt[q] = nres;
-    out.res_pass[q] = out.pass;
-  };
-
-  while (true) {
-    // ---- acquire the next node that needs an Occ step ----
-    uint32_t k = 0, l = 0;
-    bool stepping = false;
-    while (!stepping) {
-      if (!have) {
-        // persistent work queue: one atomic per pattern balances the
-        // per-pattern DFS sizes across lanes and SMs
-        const unsigned long long slot = atomicAdd(out.next, 1ull);
-        if (slot >= count) break;
-        q = list ? list[slot] : slot;
-        if (kShort && cp.packed1) {  // caller-packed fixed-length patterns
-          m = int(cp.fixed_m);
-          pw0 = cp.packed1[q];
-          pw1 = 0;
-          dbits = cp.dbits ? cp.dbits[q] : 0ull;
-        } else if (kShort) {
-          m = int(cp.offsets[q + 1] - cp.offsets[q]);
-          const ulonglong2 pk = cp.packed[q];
-          pw0 = pk.x;
-          pw1 = pk.y;
-          dbits = cp.dbits ? cp.dbits[q] : 0ull;
-        } else {
-          const uint64_t o0 = cp.offsets[q], o1 = cp.offsets[q + 1];
-          codes = cp.codes + o0;
-          m = int(o1 - o0);
-          for (int j = 0; j < m; ++j) sc.dlb[DI(uint32_t(j))] = 0;
-        }
-        phase = 0;
-        pos = m - 1;
-        seg_end = m - 1;
-        kd = 0;  // the pass starts from the root interval [0, n]
-        ld = ix.n;
-        if (kShort && cp.dbits) pos = -1;  // lower bound precomputed by k_dbound
-        sp = nres = 0;
-        ++epoch;
-        overflow = false;
-        cur_valid = false;
-        have = true;
-      }
-      if (phase == 0) {
-        if (pos < 0) {
-          if (!kShort) {  // flags of segment ends -> D(i) = ends at or before i
-            uint32_t acc = 0;
-            for (int j = 0; j < m; ++j) {
-              uint8_t* d = &sc.dlb[DI(uint32_t(j))];
-              acc += *d;
-              *d = uint8_t(min(acc, 255u));
-            }
-          }
-          phase = 1;
-          // root (search.py:125), held in registers
-          cur_valid = dlb(m - 1) <= z;
-          ci = m - 1;
-          cb = z;
-          ck = 0u;
-          cl = ix.n;
-          continue;
-        }
-        k = kd;
-        l = ld;
-        stepping = true;
-      } else {
-        if (overflow) {
-          finish();
-          have = false;
-          continue;
-        }
-        if (!cur_valid) {
-          if (sp == 0) {
-            finish();
-            have = false;
-            continue;
-          }
-          --sp;
-          const uint2 e = s_kl[sp * nt + tid];
-          const uint32_t ib = s_ib[sp * nt + tid];
-          ci = int(ib >> 16) - 1;
-          cb = ib & 0xFFFFu;
-          ck = e.x;
-          cl = e.y;
-          cur_valid = true;
-        }
-        k = ck;
-        l = cl;
-        stepping = true;
-      }
-    }
-    if (!stepping) break;
-
-    // ---- one Occ step: the eight values at (k-1, l) ----
-    uint32_t lo[4], hi[4];
-    occ_step<W, false>(ix, k, l, lo, hi);
-    ++my_steps;
-
-    if (phase == 0) {
-      const uint32_t b = sym_at(pos);
-      const uint32_t cbase = c_of(ix, b);
-      const uint32_t k2 = cbase + sel4(lo, b) + 1u, l2 = cbase + sel4(hi, b);
-      if (k2 > l2) {  // W[pos..seg_end] is absent from the text
-        if (kShort)
-          dbits |= 1ull << seg_end;
-        else
-          sc.dlb[DI(uint32_t(seg_end))] = 1;
-        kd = 0;
-        ld = ix.n;
-        seg_end = pos - 1;
-      } else {
-        kd = k2;
-        ld = l2;
-      }
-      --pos;
-      continue;
-    }
-
-    // ---- DFS expansion of the register node (search.py:135-152) ----
-    const int i = ci;
-    const uint32_t budget = cb;
-    const uint32_t want = sym_at(i);
-    const uint32_t cw = c_of(ix, want);
-    const uint32_t kw = cw + sel4(lo, want) + 1u, lw = cw + sel4(hi, want);
-    if (budget == 0) {
-      // budget-0 node: only the match child, continued in registers
-      if (kw > lw) {
-        cur_valid = false;
-      } else if (i == 0) {
-        record(kw, lw, z);
-        cur_valid = false;
-      } else {
-        ci = i - 1;
-        ck = kw;
-        cl = lw;
-        cur_valid = dlb(i - 1) == 0;
-      }
-      continue;
-    }
-    // budget >= 1: push every viable child with predicated stores (match
-    // child first, so it is popped last), then pop the top as the continue
-    // node.  Straight-line code: a lane expanding such a node costs its warp
-    // little more than a budget-0 step.
-    const uint32_t bm1 = budget - 1u;
-    const bool at0 = i == 0;
-    const uint32_t d_prev = at0 ? 0u : dlb(i - 1), d_cur = dlb(i);
-    const bool ok_match = !at0 && d_prev <= budget;  // (i-1, budget)
-    const bool ok_prev = !at0 && d_prev <= bm1;      // skip / mismatch: (i-1, budget-1)
-    const bool ok_cur = d_cur <= bm1;                // insert: (i, budget-1)
-    uint32_t k2[4], l2[4];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      k2[b] = ix.c[b] + lo[b] + 1u;
-      l2[b] = ix.c[b] + hi[b];
-    }
-    if (at0) {  // children with i - 1 < 0 are results (rare)
-      if (kw <= lw) record(kw, lw, z - budget);
-      record(k, l, z - bm1);  // skip
-#pragma unroll
-      for (uint32_t b = 0; b < 4; ++b)
-        if (b != want && k2[b] <= l2[b]) record(k2[b], l2[b], z - bm1);  // mismatch
-    }
-    auto push_if = [&](bool cond, int pi, uint32_t pb, uint32_t pk, uint32_t pl) {
-      if (cond) {
-        if (sp == S) {
-          overflow = true;
-        } else {
-          s_kl[sp * nt + tid] = make_uint2(pk, pl);
-          s_ib[sp * nt + tid] = (uint32_t(pi + 1) << 16) | pb;
-          ++sp;
-        }
-      }
-    };
-    push_if(ok_match && kw <= lw, i - 1, budget, kw, lw);  // match
-    push_if(ok_prev, i - 1, bm1, k, l);                      // skip
-#pragma unroll
-    for (uint32_t b = 0; b < 4; ++b) {
-      const bool ne = k2[b] <= l2[b];
-      push_if(ok_cur && ne, i, bm1, k2[b], l2[b]);                 // insert
-      push_if(ok_prev && ne && b != want, i - 1, bm1, k2[b], l2[b]);  // mismatch
-    }
-    cur_valid = false;  // the next iteration pops the top (the last child pushed)
-  }
-  if (out.steps) atomicAdd(out.steps, (unsigned long long)my_steps);
-}
-
-// Sort the results of patterns that had more than S of them (written
-// unsorted by k_inexact) in place: one block per pattern, bitonic sort of
-// (k << 32 | l, diffs) in shared memory.  Segments above kSortMax entries set
-// *too_big and the host falls back to a CUB segmented sort.
-constexpr uint32_t kSortMax = 4096;
-__global__ void __launch_bounds__(256) k_sort_segments(const uint32_t* __restrict__ list, const uint64_t* __restrict__ res_off,
-                                                       const uint32_t* __restrict__ res_cnt, uint2* __restrict__ kl,
-                                                       uint8_t* __restrict__ diffs, uint32_t* __restrict__ too_big) {
-  __shared__ uint64_t key[kSortMax];
-  __shared__ uint8_t val[kSortMax];
-  const uint32_t q = list[blockIdx.x];
-  const uint32_t n = res_cnt[q];
-  const uint64_t o = res_off[q];
-  if (n > kSortMax) {
-    if (threadIdx.x == 0) atomicOr(too_big, 1u);
-    return;
-  }
-  uint32_t p = 1;
-  while (p < n) p <<= 1;
-  for (uint32_t j = threadIdx.x; j < p; j += blockDim.x) {
-    if (j < n) {
-      const uint2 e = kl[o + j];
-      key[j] = (uint64_t(e.x) << 32) | e.y;
-      val[j] = diffs[o + j];
-    } else {
-      key[j] = ~0ull;
-      val[j] = 0;
-    }
-  }
-  __syncthreads();
-  for (uint32_t size = 2; size <= p; size <<= 1) {
-    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-      for (uint32_t j = threadIdx.x; j < p; j += blockDim.x) {
-        const uint32_t partner = j ^ stride;
-        if (partner > j) {
-          const bool up = (j & size) == 0;
-          const uint64_t a = key[j], b = key[partner];
-          if ((a > b) == up) {
-            key[j] = b;
-            key[partner] = a;
-            const uint8_t t = val[j];
-            val[j] = val[partner];
-            val[partner] = t;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) {
-    kl[o + j] = make_uint2(uint32_t(key[j] >> 32), uint32_t(key[j]));
-    diffs[o + j] = val[j];
-  }
-}
-
-// ----- level-synchronous engine for z = 1 ----------------------------------
-//
-// For a budget of one edit the DFS of search.py:120-159 decomposes into (a)
-// the exact "spine" walk of budget-1 match children from the root and (b)
-// independent budget-0 continuations spawned at every spine node — skip,
-// inserts, mismatches — each of which is an exact backward search of the
-// remaining prefix from its own interval.  k_spine walks every spine and
-// queues the continuations; k_chain walks every continuation; both emit raw
-// (pattern, k, l, diffs) results, deduplicated and sorted per pattern
-// afterwards.  Every lane of a warp runs the same loop, which the DFS kernel
-// cannot offer.  The reached (interval, min diffs) set equals the DFS's.
-
-struct Z1Node {  // a budget-0 continuation: pattern q, next position i, interval
-  uint32_t q, i, k, l;
-};
-struct Z1Raw {  // one reached result before dedup
-  uint32_t q, k, l, used;
-};
-struct Z1Queues {
-  Z1Node* nodes;
-  unsigned long long* n_nodes;
-  uint64_t node_cap;
-  Z1Raw* raws;
-  unsigned long long* n_raws;
-  uint64_t raw_cap;
-};
-
-// Warp-aggregated append of `cnt` (0..15) slots: one atomic per warp.
-__device__ __forceinline__ uint64_t warp_reserve(unsigned long long* counter, uint32_t cnt) {
-  const unsigned mask = __activemask();
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t lt = (1u << lane) - 1u;
-  uint32_t prefix = 0, total = 0;
-#pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    const unsigned bal = __ballot_sync(mask, (cnt >> b) & 1u);
-    prefix += uint32_t(__popc(bal & lt)) << b;
-    total += uint32_t(__popc(bal)) << b;
-  }
-  const int leader = __ffs(mask) - 1;
-  unsigned long long base = 0;
-  if (int(lane) == leader && total) base = atomicAdd(counter, (unsigned long long)total);
-  base = __shfl_sync(mask, base, leader);
-  return base + prefix;
-}
-
-__device__ __forceinline__ void z1_pattern(const CodePatterns& cp, uint64_t q, uint64_t& pw0, uint64_t& pw1, int& m) {
-  if (cp.packed1) {
-    pw0 = cp.packed1[q];
-    pw1 = 0;
-    m = int(cp.fixed_m);
-  } else {
-    const ulonglong2 pk = cp.packed[q];
-    pw0 = pk.x;
-    pw1 = pk.y;
-    m = int(cp.offsets[q + 1] - cp.offsets[q]);
-  }
-}
-
-__device__ __forceinline__ uint32_t z1_sym(uint64_t pw0, uint64_t pw1, int i) {
-  return uint32_t((i < 32 ? pw0 : pw1) >> ((i & 31) << 1)) & 3u;
-}
-
-__device__ __forceinline__ uint32_t z1_dlb(uint64_t dbits, int i) { return __popcll(dbits & ((2ull << i) - 1ull)); }
-
-template <int W>
-__global__ void __launch_bounds__(256) k_spine(IndexView ix, CodePatterns cp, uint64_t count, Z1Queues qu,
-                                               unsigned long long* steps) {
-  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (q >= count) return;
-  uint64_t pw0, pw1;
-  int m;
-  z1_pattern(cp, q, pw0, pw1, m);
-  const uint64_t dbits = cp.dbits[q];
-  uint32_t my_steps = 0;
-  int i = m - 1;
-  uint32_t k = 0, l = ix.n;
-  bool alive = z1_dlb(dbits, m - 1) <= 1u;  // root (m-1, 1, 0, n), search.py:125
-  while (alive) {
-    uint32_t lo[4], hi[4];
-    occ_step<W, false>(ix, k, l, lo, hi);
-    ++my_steps;
-    const uint32_t want = z1_sym(pw0, pw1, i);
-    uint32_t k2[4], l2[4];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      k2[b] = ix.c[b] + lo[b] + 1u;
-      l2[b] = ix.c[b] + hi[b];
-    }
-    const bool at0 = i == 0;
-    const bool ok_prev = !at0 && z1_dlb(dbits, i - 1) == 0u;  // (i-1, budget 0)
-    const bool ok_cur = z1_dlb(dbits, i) == 0u;               // (i, budget 0)
-    // budget-0 children to queue: skip, 4 inserts, 3 mismatches
-    bool e[8];
-    e[0] = ok_prev;  // skip (i-1, 0, k, l)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const bool ne = k2[b] <= l2[b];
-      e[1 + b] = ok_cur && ne;  // insert (i, 0, k_b, l_b)
-    }
-    uint32_t mm = 0;  // mismatch slots 5..7 hold the three b != want in order
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      if (uint32_t(b) == want) continue;
-      e[5 + mm] = ok_prev && (k2[b] <= l2[b]);
-      ++mm;
-    }
-    uint32_t cnt = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) cnt += e[j] ? 1u : 0u;
-    uint64_t slot = warp_reserve(qu.n_nodes, cnt);
-    auto put = [&](uint32_t ni, uint32_t nk, uint32_t nl) {
-      if (slot < qu.node_cap) qu.nodes[slot] = Z1Node{uint32_t(q), ni, nk, nl};
-      ++slot;
-    };
-    if (e[0]) put(uint32_t(i - 1), k, l);
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-      if (e[1 + b]) put(uint32_t(i), k2[b], l2[b]);
-    mm = 0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      if (uint32_t(b) == want) continue;
-      if (e[5 + mm]) put(uint32_t(i - 1), k2[b], l2[b]);
-      ++mm;
-    }
-    // children with i - 1 < 0 are results (search.py:127-134): rare
-    uint32_t rc = 0;
-    if (at0) {
-      rc = 1u;  // skip
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-        if (uint32_t(b) != want && k2[b] <= l2[b]) ++rc;
-      if (k2[want & 3u] <= l2[want & 3u]) ++rc;  // match with budget kept
-    }
-    uint64_t rs = warp_reserve(qu.n_raws, rc);
-    if (at0) {
-      auto rput = [&](uint32_t rk, uint32_t rl, uint32_t used) {
-        if (rs < qu.raw_cap) qu.raws[rs] = Z1Raw{uint32_t(q), rk, rl, used};
-        ++rs;
-      };
-      rput(k, l, 1u);
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-        if (uint32_t(b) != want && k2[b] <= l2[b]) rput(k2[b], l2[b], 1u);
-      if (k2[want & 3u] <= l2[want & 3u]) rput(k2[want & 3u], l2[want & 3u], 0u);
-      break;
-    }
-    // continue along the match child (i-1, 1)
-    const uint32_t kw = sel4(k2, want), lw = sel4(l2, want);
-    if (kw > lw || z1_dlb(dbits, i - 1) > 1u) break;
-    k = kw;
-    l = lw;
-    --i;
-  }
-  if (steps) atomicAdd(steps, (unsigned long long)my_steps);
-}
-
-template <int W>
-__global__ void __launch_bounds__(256) k_chain(IndexView ix, CodePatterns cp, const Z1Node* __restrict__ nodes,
-                                               uint64_t n_nodes, Z1Queues qu, unsigned long long* steps) {
-  // Persistent grid, lane refill: most continuations die within a few steps
-  // while the few that match run to i < 0, so a lane takes its next node as
-  // soon as its chain ends instead of idling until its warp's longest chain.
-  constexpr uint32_t kC = LineTraits<W>::kChars;
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  uint32_t my_steps = 0;
-  uint64_t pw0 = 0, pw1 = 0, dbits = 0;
-  int i = -1;
-  uint32_t k = 0, l = 0, q = 0;
-  bool have = false;
-  while (true) {
-    if (!have) {
-      if (t >= n_nodes) break;
-      const Z1Node nd = nodes[t];
-      t += stride;
-      int m;
-      z1_pattern(cp, nd.q, pw0, pw1, m);
-      dbits = cp.dbits[nd.q];
-      q = nd.q;
-      i = int(nd.i);
-      k = nd.k;
-      l = nd.l;
-      have = true;
-    }
-    // budget-0 node (i, k, l): only its match child
-    const uint32_t sym = z1_sym(pw0, pw1, i);
-    uint32_t k2, l2;
-    if (k == 0u && l == ix.n) {
-      k2 = c_of(ix, sym) + 1u;
-      l2 = c_of(ix, sym + 1u);
-    } else {
-      const uint32_t low = k - 1u;
-      const uint32_t jh = line_of<W>(l), jl = line_of<W>(low);
-      const uint32_t rh = l - jh * kC, rl = low - jl * kC;
-      uint32_t bh[4], bl[4];
-      uint64_t wh[W], wl[W];
-      load_line<W, false>(ix, jh, rh, bh, wh);
-      uint32_t ol;
-      if (jl != jh) {
-        load_line<W, false>(ix, jl, rl, bl, wl);
-        ol = occ1_from_line<W>(ix, bl, wl, low, rl, sym);
-      } else {
-        ol = occ1_from_line<W>(ix, bh, wh, low, rl, sym);
-      }
-      const uint32_t cs = c_of(ix, sym);
-      k2 = cs + ol + 1u;
-      l2 = cs + occ1_from_line<W>(ix, bh, wh, l, rh, sym);
-      ++my_steps;
-    }
-    const bool empty = k2 > l2;
-    const bool found = !empty && i == 0;
-    if (empty || found || z1_dlb(dbits, i - 1) > 0u) {
-      have = false;
-      if (found) {
-        const unsigned long long rs = atomicAdd(qu.n_raws, 1ull);
-        if (rs < qu.raw_cap) qu.raws[rs] = Z1Raw{q, k2, l2, 1u};
-      }
-      continue;
-    }
-    k = k2;
-    l = l2;
-    --i;
-  }
-  if (steps) atomicAdd(steps, (unsigned long long)my_steps);
-}
-
-// counting sort of raw results by pattern
-__global__ void k_z1_hist(const Z1Raw* __restrict__ raws, uint64_t n, uint32_t* __restrict__ per_q) {
-  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t < n) atomicAdd(&per_q[raws[t].q], 1u);
-}
-
-__global__ void k_z1_scatter(const Z1Raw* __restrict__ raws, uint64_t n, uint64_t* __restrict__ cursor,
-                             uint64_t* __restrict__ keys, uint8_t* __restrict__ used) {
-  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  const Z1Raw r = raws[t];
-  const unsigned long long p = atomicAdd(reinterpret_cast<unsigned long long*>(&cursor[r.q]), 1ull);
-  keys[p] = (uint64_t(r.k) << 32) | r.l;
-  used[p] = uint8_t(r.used);
-}
-
-// per pattern: unique (k, l) with min diffs over its sorted segment
-__global__ void k_z1_unique_count(const uint64_t* __restrict__ keys, const uint8_t* __restrict__ used,
-                                  const uint64_t* __restrict__ seg, uint64_t count, uint32_t* __restrict__ ucnt) {
-  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (q >= count) return;
-  uint32_t c = 0;
-  for (uint64_t j = seg[q]; j < seg[q + 1]; ++j)
-    if (j == seg[q] || keys[j] != keys[j - 1]) ++c;
-  ucnt[q] = c;
-}
-
-__global__ void k_z1_unique_write(const uint64_t* __restrict__ keys, const uint8_t* __restrict__ used,
-                                  const uint64_t* __restrict__ seg, const uint64_t* __restrict__ row_off,
-                                  uint64_t count, uint32_t* __restrict__ k_out, uint32_t* __restrict__ l_out,
-                                  uint8_t* __restrict__ d_out) {
-  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (q >= count) return;
-  uint64_t o = row_off[q];
-  for (uint64_t j = seg[q]; j < seg[q + 1];) {
-    const uint64_t key = keys[j];
-    uint8_t best = used[j];
-    uint64_t e = j + 1;
-    for (; e < seg[q + 1] && keys[e] == key; ++e) best = min(best, used[e]);
-    k_out[o] = uint32_t(key >> 32);
-    l_out[o] = uint32_t(key);
-    d_out[o] = best;
-    ++o;
-    j = e;
-  }
-}
-
-// Gather per-pattern results of one pass into the final CSR arrays.
-__global__ void k_gather_matches(uint64_t count, const uint64_t* __restrict__ res_off,
-                                 const uint32_t* __restrict__ res_cnt, const uint8_t* __restrict__ res_pass,
-                                 uint8_t pass, const uint2* __restrict__ src_kl, const uint8_t* __restrict__ src_d,
-                                 const uint64_t* __restrict__ row_off, uint32_t* __restrict__ k_out,
-                                 uint32_t* __restrict__ l_out, uint8_t* __restrict__ d_out) {
-  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (q >= count || res_pass[q] != pass) return;
-  const uint32_t n = res_cnt[q];
-  const uint64_t s = res_off[q], d = row_off[q];
-  for (uint32_t r = 0; r < n; ++r) {
-    const uint2 e = src_kl[s + r];
-    k_out[d + r] = e.x;
-    l_out[d + r] = e.y;
-    d_out[d + r] = src_d[s + r];
-  }
-}
-
-// 2-bit packing of patterns of length <= 64 for k_inexact (one coalesced-ish
-// pass so the search kernel starts a pattern with a single 16-byte load).
-__global__ void k_pack_patterns(const uint8_t* __restrict__ codes, const uint64_t* __restrict__ offsets,
-                                uint64_t count, ulonglong2* __restrict__ packed) {
-  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (q >= count) return;
-  const uint64_t a = offsets[q], b = offsets[q + 1];
-  uint64_t w0 = 0, w1 = 0;
-  for (uint64_t j = a; j < b && j < a + 64; ++j) {
-    const uint32_t f = uint32_t(j - a);
-    const uint64_t v = uint64_t(codes[j] & 3u) << ((f & 31u) << 1);
-    if (f < 32u)
-      w0 |= v;
-    else
-      w1 |= v;
-  }
-  packed[q] = make_ulonglong2(w0, w1);
-}
-
-// Pattern batch validation on the device: offsets[0] == 0, every pattern
-// non-empty (search.py:83-84), codes in [0, 4); also the longest pattern.
-__global__ void k_check_patterns(const uint8_t* __restrict__ codes, const uint64_t* __restrict__ offsets,
-                                 uint64_t count, unsigned long long* __restrict__ max_len,
-                                 uint32_t* __restrict__ err) {
-  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (q >= count) return;
-  const uint64_t a = offsets[q], b = offsets[q + 1];
-  if (q == 0 && a != 0) atomicOr(err, 4u);
-  if (b <= a) {
-    atomicOr(err, 1u);
-    return;
-  }
-  atomicMax(max_len, (unsigned long long)(b - a));
-  for (uint64_t j = a; j < b; ++j)
-    if (codes[j] > 3) atomicOr(err, 2u);
-}
-
-__global__ void k_pack_keys(uint64_t n, const uint32_t* __restrict__ k, const uint32_t* __restrict__ l,
-                            uint64_t* __restrict__ keys) {
-  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) keys[i] = (uint64_t(k[i]) << 32) | l[i];
-}
-
-__global__ void k_unpack_keys(uint64_t n, const uint64_t* __restrict__ keys, const uint8_t* __restrict__ d_in,
-                              uint32_t* __restrict__ k, uint32_t* __restrict__ l, uint8_t* __restrict__ d_out) {
-  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) {
-    k[i] = uint32_t(keys[i] >> 32);
-    l[i] = uint32_t(keys[i]);
-    d_out[i] = d_in[i];
-  }
-}
-
-__global__ void k_widen_counts(uint64_t count, const uint32_t* __restrict__ c32, uint64_t* __restrict__ c64) {
-  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (q < count) c64[q] = c32[q];
-}
-
-// ----- position recovery ---------------------------------------------------
-
-// psi_inverse_fused (search.py:172-186): symbol at row i and its
-// predecessor row c[sym] + Occ(sym, i), in one line access.
-template <int W>
-__device__ __forceinline__ uint32_t psi_step(const IndexView& ix, uint32_t row, uint32_t& sym) {
-  uint32_t b[4];
-  uint64_t w[W];
-  const uint32_t j = line_of<W>(row), r = row - j * LineTraits<W>::kChars;
-  load_line<W, false>(ix, j, r, b, w);
-  sym = field_at<W>(w, r);
-  return c_of(ix, sym) + occ1_from_line<W>(ix, b, w, row, r, sym);
-}
-
-template <int W>
-__global__ void k_psi(IndexView ix, const uint32_t* __restrict__ rows, uint64_t count, uint8_t* __restrict__ out_sym,
-                      uint32_t* __restrict__ out_row, uint32_t* __restrict__ err) {
-  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (q >= count) return;
-  const uint32_t row = rows[q];
-  if (row > ix.n) {
-    atomicOr(err, 1u);
-    out_sym[q] = 255;
-    out_row[q] = 0xFFFFFFFFu;
-    return;
-  }
-  if (row == ix.sentinel_row) {
-    out_sym[q] = 255;
-    out_row[q] = 0xFFFFFFFFu;
-    return;
-  }
-  uint32_t sym;
-  const uint32_t prev = psi_step<W>(ix, row, sym);
-  out_sym[q] = uint8_t(sym);
-  out_row[q] = prev;
-}
-
-// locate_row (search.py:189-208): walk predecessors until the row is sampled
-// (row % 32 == 0 — samples are taken by ROW, index.py:93, so the walk length
-// is geometric-like with mean ~32, not bounded by 32) or is the sentinel row.
-// Grid-stride lane refill keeps warps full despite the varying walk lengths.
-template <int W>
-__global__ void __launch_bounds__(256) k_locate(IndexView ix, const uint32_t* __restrict__ rows, uint64_t count,
-                                                uint32_t* __restrict__ out_pos, uint32_t* __restrict__ err) {
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < count; q += stride) {
-    uint32_t row = rows[q];
-    if (row > ix.n) {
-      atomicOr(err, 1u);
-      out_pos[q] = 0xFFFFFFFFu;
-      continue;
-    }
-    uint32_t steps = 0;
-    while (true) {
-      if (row == ix.sentinel_row) {
-        out_pos[q] = steps;
-        break;
-      }
-      if ((row & 31u) == 0u) {
-        out_pos[q] = ix.samples[row >> 5] + steps;
-        break;
-      }
-      uint32_t sym;
-      row = psi_step<W>(ix, row, sym);
-      ++steps;
-      if (steps > ix.n + 1u) {  // corrupt index (search.py:207-208)
-        atomicOr(err, 2u);
-        out_pos[q] = 0xFFFFFFFFu;
-        break;
-      }
-    }
-  }
-}
+namespace fmg {
 
 // ---------------------------------------------------------------------------
 // Host side

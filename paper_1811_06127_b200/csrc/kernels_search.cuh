@@ -1,0 +1,168 @@
+// Exact backward search and position recovery kernels (search.py:74-94, 172-208).
+// Part of libfmgpu.so (sm_100a); included once by fmgpu.cu.
+#pragma once
+
+#include <cstdint>
+
+#include "occ_device.cuh"
+
+namespace fmg {
+
+// Pattern sources for the search kernels.
+struct PackedPatterns {  // fixed length m <= 32, char j in bits 2j..2j+1
+  const uint64_t* words;
+  uint32_t m;
+  __device__ __forceinline__ uint32_t length(uint64_t) const { return m; }
+};
+struct CodePatterns {  // codes[offsets[q] .. offsets[q+1])
+  const uint8_t* codes;
+  const uint64_t* offsets;
+  const ulonglong2* packed = nullptr;  // inexact, m <= 64: 2-bit packed copy (k_pack_patterns)
+  const uint64_t* packed1 = nullptr;   // inexact, fixed m <= 32 given packed by the caller
+  uint32_t fixed_m = 0;
+  const uint64_t* dbits = nullptr;     // inexact, m <= 64: lower-bound segment ends (k_dbound)
+};
+
+// Exact backward search, one pattern per thread at a time.  When a lane's
+// pattern finishes (matched or emptied — the reference stops at the FIRST
+// empty interval, search.py:91-92) the lane immediately takes the next
+// pattern of its grid-stride sequence, so warps stay full while per-pattern
+// step counts vary from 1 to m-1.
+template <bool kPacked, int W>
+__global__ void __launch_bounds__(256) k_exact(IndexView ix, PackedPatterns pp, CodePatterns cp, uint64_t count,
+                                               uint2* __restrict__ out, unsigned long long* __restrict__ steps) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint64_t my_steps = 0;
+  uint64_t pat = 0;          // packed form
+  const uint8_t* codes = nullptr;  // general form
+  int i = -1;
+  uint32_t k = 1, l = 0;
+  auto start = [&](uint64_t qq) {
+    uint32_t m, b;
+    if (kPacked) {
+      pat = pp.words[qq];
+      m = pp.m;
+      b = uint32_t(pat >> (2 * (m - 1))) & 3u;
+    } else {
+      const uint64_t o0 = cp.offsets[qq], o1 = cp.offsets[qq + 1];
+      codes = cp.codes + o0;
+      m = uint32_t(o1 - o0);
+      b = codes[m - 1];
+    }
+    k = c_of(ix, b) + 1u;  // init_interval, search.py:50-57
+    l = c_of(ix, b + 1u);
+    i = int(m) - 2;
+  };
+  if (q >= count) return;
+  start(q);
+  while (true) {
+    if (i < 0 || k > l) {
+      out[q] = make_uint2(k, l);
+      q += stride;
+      if (q >= count) break;
+      start(q);
+      continue;
+    }
+    const uint32_t sym = kPacked ? (uint32_t(pat >> (2 * i)) & 3u) : uint32_t(__ldg(codes + i));
+    --i;
+    // extend_backward, search.py:60-71: k' = c[b] + Occ(b, k-1) + 1, l' = c[b] + Occ(b, l)
+    constexpr uint32_t kC = LineTraits<W>::kChars;
+    uint32_t bh[4], bl[4];
+    uint64_t wh[W], wl[W];
+    const uint32_t low = k - 1u;  // k >= 1 on every non-empty interval here
+    const uint32_t jh = line_of<W>(l), jl = line_of<W>(low);
+    const uint32_t rh = l - jh * kC, rl = low - jl * kC;
+    load_line<W, false>(ix, jh, rh, bh, wh);
+    uint32_t ol;
+    if (jl != jh) {
+      load_line<W, false>(ix, jl, rl, bl, wl);
+      ol = occ1_from_line<W>(ix, bl, wl, low, rl, sym);
+    } else {
+      ol = occ1_from_line<W>(ix, bh, wh, low, rl, sym);
+    }
+    const uint32_t oh = occ1_from_line<W>(ix, bh, wh, l, rh, sym);
+    const uint32_t cs = c_of(ix, sym);
+    k = cs + ol + 1u;
+    l = cs + oh;
+    ++my_steps;
+  }
+  if (steps) atomicAdd(steps, (unsigned long long)my_steps);
+}
+
+
+// ----- position recovery ---------------------------------------------------
+
+// psi_inverse_fused (search.py:172-186): symbol at row i and its
+// predecessor row c[sym] + Occ(sym, i), in one line access.
+template <int W>
+__device__ __forceinline__ uint32_t psi_step(const IndexView& ix, uint32_t row, uint32_t& sym) {
+  uint32_t b[4];
+  uint64_t w[W];
+  const uint32_t j = line_of<W>(row), r = row - j * LineTraits<W>::kChars;
+  load_line<W, false>(ix, j, r, b, w);
+  sym = field_at<W>(w, r);
+  return c_of(ix, sym) + occ1_from_line<W>(ix, b, w, row, r, sym);
+}
+
+template <int W>
+__global__ void k_psi(IndexView ix, const uint32_t* __restrict__ rows, uint64_t count, uint8_t* __restrict__ out_sym,
+                      uint32_t* __restrict__ out_row, uint32_t* __restrict__ err) {
+  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  const uint32_t row = rows[q];
+  if (row > ix.n) {
+    atomicOr(err, 1u);
+    out_sym[q] = 255;
+    out_row[q] = 0xFFFFFFFFu;
+    return;
+  }
+  if (row == ix.sentinel_row) {
+    out_sym[q] = 255;
+    out_row[q] = 0xFFFFFFFFu;
+    return;
+  }
+  uint32_t sym;
+  const uint32_t prev = psi_step<W>(ix, row, sym);
+  out_sym[q] = uint8_t(sym);
+  out_row[q] = prev;
+}
+
+// locate_row (search.py:189-208): walk predecessors until the row is sampled
+// (row % 32 == 0 — samples are taken by ROW, index.py:93, so the walk length
+// is geometric-like with mean ~32, not bounded by 32) or is the sentinel row.
+// Grid-stride lane refill keeps warps full despite the varying walk lengths.
+template <int W>
+__global__ void __launch_bounds__(256) k_locate(IndexView ix, const uint32_t* __restrict__ rows, uint64_t count,
+                                                uint32_t* __restrict__ out_pos, uint32_t* __restrict__ err) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < count; q += stride) {
+    uint32_t row = rows[q];
+    if (row > ix.n) {
+      atomicOr(err, 1u);
+      out_pos[q] = 0xFFFFFFFFu;
+      continue;
+    }
+    uint32_t steps = 0;
+    while (true) {
+      if (row == ix.sentinel_row) {
+        out_pos[q] = steps;
+        break;
+      }
+      if ((row & 31u) == 0u) {
+        out_pos[q] = ix.samples[row >> 5] + steps;
+        break;
+      }
+      uint32_t sym;
+      row = psi_step<W>(ix, row, sym);
+      ++steps;
+      if (steps > ix.n + 1u) {  // corrupt index (search.py:207-208)
+        atomicOr(err, 2u);
+        out_pos[q] = 0xFFFFFFFFu;
+        break;
+      }
+    }
+  }
+}
+
+}  // namespace fmg
