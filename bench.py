@@ -375,7 +375,10 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
     idx = fm.build_index(wl.text)
     t_build = time.perf_counter() - t_build
     dix = idx.device_index(local)
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated non-blocking stream: the legacy default stream would
+    # serialise against the library's stream-ordered allocations
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
     units = unit_count(wl)
     metric, unit = metric_of(args.config)
