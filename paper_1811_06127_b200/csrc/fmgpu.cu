@@ -16,6 +16,7 @@
 #include <cstring>
 #include <type_traits>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
@@ -106,6 +107,10 @@ struct fmg_index {
   uint32_t* samples = nullptr;
   uint32_t* err = nullptr;  // sticky device-side input error flags
   int sms = 148;
+  // exact-search k-mer table (built on first large exact call; see KmerTable)
+  std::mutex lut_mu;
+  uint2* lut = nullptr;
+  uint32_t lut_k = 0;
 
   fmg::IndexView view() const {
     fmg::IndexView v;
@@ -240,15 +245,49 @@ unsigned wave_blocks(const fmg_index* ix, const void* kernel, int threads, uint6
   return unsigned(std::min<uint64_t>(std::max<uint64_t>(resident, waves), 1u << 30));
 }
 
+// The exact-search k-mer table of the index, built on first use by a large
+// call (>= 1024 patterns): K = clamp(floor(log4 n) - 2, 4, 12), 8 * 4^K bytes
+// (128 MiB at 1 Gbp).  FMG_EXACT_LUT=0 disables it (A/B).
+KmerTable kmer_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("FMG_EXACT_LUT");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  if (!enabled || count < 1024) return {};
+  auto* ix = const_cast<fmg_index*>(cix);  // the table is a cache; the index itself never changes
+  std::lock_guard<std::mutex> lock(ix->lut_mu);
+  if (!ix->lut) {
+    uint32_t k = 0;
+    while ((uint64_t(1) << (2 * (k + 1))) <= ix->n) ++k;  // floor(log4 n)
+    k = std::min<uint32_t>(12, std::max<uint32_t>(4, k >= 2 ? k - 2 : 0));
+    const uint64_t entries = uint64_t(1) << (2 * k);
+    uint2* lut = nullptr;
+    FMG_CK(cudaMalloc(&lut, entries * sizeof(uint2)));
+    PackedPatterns pp{nullptr, k};  // words == nullptr: search x = 0 .. 4^K - 1
+    CodePatterns cp{nullptr, nullptr};
+    with_words(ix, [&](auto wt) {
+      constexpr int W = decltype(wt)::value;
+      k_exact<true, W><<<unsigned((entries + 255) / 256), 256, 0, s>>>(ix->view(), pp, cp, entries, lut, nullptr,
+                                                                        KmerTable{});
+    });
+    FMG_CK(cudaGetLastError());
+    FMG_CK(cudaStreamSynchronize(s));
+    ix->lut = lut;
+    ix->lut_k = k;
+  }
+  return KmerTable{ix->lut, ix->lut_k};
+}
+
 void launch_exact_packed(const fmg_index* ix, const uint64_t* packed, uint32_t m, uint64_t count, uint32_t* kl_out,
                          cudaStream_t s, unsigned long long* steps) {
   if (count == 0) return;
   PackedPatterns pp{packed, m};
   CodePatterns cp{nullptr, nullptr};
+  const KmerTable kt = kmer_table(ix, count, s);
   with_words(ix, [&](auto wt) {
     constexpr int W = decltype(wt)::value;
     const unsigned blocks = wave_blocks(ix, (const void*)k_exact<true, W>, 256, count);
-    k_exact<true, W><<<blocks, 256, 0, s>>>(ix->view(), pp, cp, count, reinterpret_cast<uint2*>(kl_out), steps);
+    k_exact<true, W><<<blocks, 256, 0, s>>>(ix->view(), pp, cp, count, reinterpret_cast<uint2*>(kl_out), steps, kt);
   });
   FMG_CK(cudaGetLastError());
 }
@@ -258,10 +297,12 @@ void launch_exact_codes(const fmg_index* ix, const uint8_t* codes, const uint64_
   if (count == 0) return;
   PackedPatterns pp{nullptr, 0};
   CodePatterns cp{codes, offsets};
+  const KmerTable kt = kmer_table(ix, count, s);
   with_words(ix, [&](auto wt) {
     constexpr int W = decltype(wt)::value;
     const unsigned blocks = wave_blocks(ix, (const void*)k_exact<false, W>, 256, count);
-    k_exact<false, W><<<blocks, 256, 0, s>>>(ix->view(), pp, cp, count, reinterpret_cast<uint2*>(kl_out), steps);
+    k_exact<false, W><<<blocks, 256, 0, s>>>(ix->view(), pp, cp, count, reinterpret_cast<uint2*>(kl_out), steps,
+                                             kt);
   });
   FMG_CK(cudaGetLastError());
 }
@@ -812,6 +853,7 @@ void fmg_index_destroy(fmg_index* ix) {
   cudaGetDevice(&prev);
   cudaSetDevice(ix->device);
   if (ix->lines) cudaFree(ix->lines);
+  if (ix->lut) cudaFree(ix->lut);
   if (ix->samples) cudaFree(ix->samples);
   if (ix->err) cudaFree(ix->err);
   if (prev >= 0) cudaSetDevice(prev);

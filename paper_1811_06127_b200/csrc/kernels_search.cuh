@@ -28,9 +28,22 @@ struct CodePatterns {  // codes[offsets[q] .. offsets[q+1])
 // empty interval, search.py:91-92) the lane immediately takes the next
 // pattern of its grid-stride sequence, so warps stay full while per-pattern
 // step counts vary from 1 to m-1.
+// k-mer table: lut[x] = the interval exact_search returns for the K-mer x
+// (character t of x in bits 2t), including the first empty interval where
+// that search stopped.  A pattern of length m >= K starts from the entry of
+// its last K characters at position m-1-K, skipping K dependent steps — the
+// result is identical because the entry IS what those K steps produce.
+// pp.words == nullptr makes k_exact search the K-mers x = 0 .. count-1
+// themselves (how the table is built).
+struct KmerTable {
+  const uint2* lut = nullptr;
+  uint32_t k = 0;
+};
+
 template <bool kPacked, int W>
 __global__ void __launch_bounds__(256) k_exact(IndexView ix, PackedPatterns pp, CodePatterns cp, uint64_t count,
-                                               uint2* __restrict__ out, unsigned long long* __restrict__ steps) {
+                                               uint2* __restrict__ out, unsigned long long* __restrict__ steps,
+                                               KmerTable kt) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   uint64_t my_steps = 0;
@@ -41,7 +54,7 @@ __global__ void __launch_bounds__(256) k_exact(IndexView ix, PackedPatterns pp, 
   auto start = [&](uint64_t qq) {
     uint32_t m, b;
     if (kPacked) {
-      pat = pp.words[qq];
+      pat = pp.words ? pp.words[qq] : qq;
       m = pp.m;
       b = uint32_t(pat >> (2 * (m - 1))) & 3u;
     } else {
@@ -49,6 +62,19 @@ __global__ void __launch_bounds__(256) k_exact(IndexView ix, PackedPatterns pp, 
       codes = cp.codes + o0;
       m = uint32_t(o1 - o0);
       b = codes[m - 1];
+    }
+    if (kt.lut && m >= kt.k) {  // start after the last K characters
+      uint32_t key = 0;
+      if (kPacked) {
+        key = uint32_t(pat >> (2 * (m - kt.k))) & ((1u << (2 * kt.k)) - 1u);
+      } else {
+        for (uint32_t t = 0; t < kt.k; ++t) key |= uint32_t(__ldg(codes + m - kt.k + t) & 3u) << (2 * t);
+      }
+      const uint2 e = __ldg(kt.lut + key);
+      k = e.x;
+      l = e.y;
+      i = int(m) - 1 - int(kt.k);
+      return;
     }
     k = c_of(ix, b) + 1u;  // init_interval, search.py:50-57
     l = c_of(ix, b + 1u);

@@ -230,6 +230,60 @@ def gen_cli():
     print("cli: fixtures written", len(fmi_bytes), "byte index")
 
 
+class _LazyBuckets:
+    """numpy-backed stand-in for FmIndex.buckets so the UNCHANGED reference query
+    code runs on indexes it cannot build itself."""
+
+    def __init__(self, records):
+        self.rec = records
+        self.base = records[:, :32].view("<u8")
+
+    def __len__(self):
+        return self.rec.shape[0]
+
+    def __getitem__(self, j):
+        return fmpm.index.OccBucket(base=tuple(int(x) for x in self.base[j]), chars=self.rec[j, 32:].tobytes())
+
+
+def _ref_index(ours):
+    """fmpm.FmIndex over our native build (byte-identical .fmi semantics)."""
+    return fmpm.FmIndex(n=ours.n, c=tuple(ours.c), buckets=_LazyBuckets(ours.bucket_records),
+                        sentinel_row=ours.sentinel_row, sa_samples=tuple(int(x) for x in ours.sa_samples[:1]),
+                        records=tuple(fmpm.RecordSpan(r.name, r.start, r.length) for r in ours.records))
+
+
+def gen_scale():
+    """Reference outputs on deterministic subsamples of the genome-scale configs."""
+    from paper_1811_06127_b200 import build_index
+
+    out = {}
+    # config 4 and 1-H share the 1 Gbp text (seed 5)
+    t0 = time.time()
+    wl4 = workloads.config4(count=1 << 14)
+    idx = build_index(wl4.text, builder="host")
+    ref = _ref_index(idx)
+    print(f"1 Gbp host build {time.time() - t0:.0f}s", flush=True)
+    seeds = workloads.unpack_patterns(wl4.packed, 20)
+    kl = np.array([tuple(fmpm.exact_search(ref, text_of(p))[:2]) for p in seeds], dtype=np.int64)
+    out["config4_first16k_kl"] = kl.tolist()
+    wl1h = workloads.config1h(count=1 << 12)
+    occ = np.array([tuple(p.at_low) + tuple(p.at_high) for p in
+                    (fmpm.occ_pair_all(ref, int(a), int(b)) for a, b in wl1h.pairs)], dtype=np.int64)
+    out["config1h_first4k_occ"] = occ.tolist()
+    del idx, ref
+    # config 2: the first 2000 seeds of the full 1M-read set, z = 1
+    wl2 = workloads.config2()
+    idx = build_index(wl2.text, builder="host")
+    ref = _ref_index(idx)
+    res = []
+    for p in wl2.patterns[:2000]:
+        res.append([(m.interval.k, m.interval.l, m.diffs_used) for m in fmpm.inexact_search(ref, text_of(p), 1)])
+    out["config2_first2k_z1"] = res
+    (HERE / "scale_cases.json").write_text(json.dumps(out, separators=(",", ":")))
+    print("scale: wrote", {k: len(v) for k, v in out.items()}, flush=True)
+
+
 if __name__ == "__main__":
     for what in sys.argv[1:]:
-        {"small": gen_small, "config0": gen_config0, "config1": gen_config1, "cli": gen_cli}[what]()
+        {"small": gen_small, "config0": gen_config0, "config1": gen_config1, "cli": gen_cli,
+         "scale": gen_scale}[what]()

@@ -336,3 +336,27 @@ def test_z1_engines_agree(gpu, monkeypatch):
     assert np.array_equal(a.l, b.l) and np.array_equal(a.diffs, b.diffs)
     row, k, l, d, _ = orc.inexact_batch(orc.OracleIndex(idx), wl.patterns, 1)
     assert np.array_equal(a.offsets, row) and np.array_equal(a.k.astype(np.int64), k)
+
+
+def test_exact_kmer_table_paths(gpu):
+    """>= 1024 patterns use the k-mer table (K = 6 here): lengths below, at and above K,
+    present and absent, packed and CSR inputs — all identical to the oracle."""
+    rng = np.random.Generator(np.random.PCG64(606))
+    text = rng.integers(0, 4, 200_000, dtype=np.uint8)
+    idx = fm.build_index(text)
+    ox = orc.OracleIndex(idx)
+    pats = []
+    for _ in range(40_000):
+        m = int(rng.integers(1, 41))
+        if rng.random() < 0.6:
+            s = int(rng.integers(0, text.size - m + 1))
+            pats.append(codes_to_str(text[s:s + m]))
+        else:
+            pats.append(codes_to_str(rng.integers(0, 4, m, dtype=np.uint8)))
+    kl, _ = fm.exact_search_batch(idx, pats)  # CSR kernel
+    assert np.array_equal(kl, orc.exact_batch(ox, pats))
+    for m in (5, 6, 7, 20):
+        arr = rng.integers(0, 4, (1 << 15, m), dtype=np.uint8)
+        arr[::2] = workloads.substrings(text, rng.integers(0, text.size - m + 1, arr[::2].shape[0]), m)
+        klp, _ = fm.exact_search_batch(idx, arr)  # packed kernel
+        assert np.array_equal(klp, orc.exact_batch(ox, arr)), m
