@@ -442,7 +442,7 @@ bool run_z1(const fmg_index* ix, const CodePatterns& cp, uint64_t count, uint64_
 fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64_t* offsets, uint64_t count,
                          uint64_t max_len, int max_diff, cudaStream_t s, const uint64_t* packed1 = nullptr) {
   FMG_REQUIRE(max_diff >= 0, "difference budget is negative");
-  FMG_REQUIRE(max_diff <= 0xFFFF, "difference budget above 65535 is not supported");
+  FMG_REQUIRE(max_diff <= 255, "difference budget above 255 is not supported (diffs are stored as u8)");
   FMG_REQUIRE(max_len < 0xFFFF, "pattern longer than 65534 is not supported");
   FMG_REQUIRE(count < 0xFFFFFFFFull, "too many patterns in one call");
   auto* res = new fmg_matches();

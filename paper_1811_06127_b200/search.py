@@ -160,6 +160,8 @@ def inexact_search_batch(index: FmIndex, patterns, max_diff: int,
     """inexact_search over many patterns; results in CSR form (see MatchSet)."""
     if max_diff < 0:
         raise ValueError(f"difference budget {max_diff} is negative")
+    if max_diff > 255:  # engine limit (diffs are u8); the reference has none
+        raise ValueError(f"difference budget {max_diff} above 255 is not supported")
     resolve_kernel(kernel)
     codes, offsets, degenerate = patterns_to_csr(patterns)
     n = offsets.size - 1
