@@ -267,6 +267,18 @@ def dist_sum(value: float, world: int, device) -> float:
     return float(t.item())
 
 
+def exact_work(lib, dix, d_pat, m: int, count: int, d_out, stream) -> tuple[int, int]:
+    """(Occ steps, lines fetched) of one packed exact search, counted on the device."""
+    fn = lib.fmgx_exact_packed_work
+    fn.argtypes = [ct.c_void_p, ct.c_void_p, ct.c_uint32, ct.c_uint64, ct.c_void_p, ct.c_void_p,
+                   ct.POINTER(ct.c_uint64), ct.POINTER(ct.c_uint64)]
+    st, ln = ct.c_uint64(), ct.c_uint64()
+    from paper_1811_06127_b200 import _lib
+
+    _lib.check(fn(dix.handle, d_pat.data_ptr(), m, count, d_out.data_ptr(), stream, ct.byref(st), ct.byref(ln)))
+    return st.value, ln.value
+
+
 def random_fetch_peak(lib, device: int) -> float | None:
     """Measured random 32-byte fetches/s over 4 GiB on this GPU (the DRAM request ceiling)."""
     fn = getattr(lib, "fmgx_random_fetch_rate", None)
@@ -390,7 +402,7 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
         d_pat = torch.from_numpy(wl.packed.view(np.int64)).to(dev)
         d_out = torch.empty((n_seeds, 2), dtype=torch.int32, device=dev)
         chunk = 1 << 24
-        steps_seen = [0]
+        work_seen = [0, 0]  # inexact Occ steps, lines fetched (device counters, per step)
 
         def step():
             _lib.check(lib.fmg_exact_packed(dix.handle, d_pat.data_ptr(), m, n_seeds, d_out.data_ptr(), sp))
@@ -398,9 +410,11 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
                 h = ct.c_void_p()
                 _lib.check(lib.fmg_inexact_packed(dix.handle, d_pat.data_ptr() + 8 * c0, m,
                                                   min(chunk, n_seeds - c0), 1, ct.byref(h), sp))
-                st_ = ct.c_uint64()
+                st_, ln_ = ct.c_uint64(), ct.c_uint64()
                 lib.fmg_matches_steps(h, ct.byref(st_))
-                steps_seen[0] += st_.value
+                lib.fmgx_matches_lines(h, ct.byref(ln_))
+                work_seen[0] += st_.value
+                work_seen[1] += ln_.value
                 lib.fmg_matches_free(h)
 
         launches_per_step = 1 + ((n_seeds + chunk - 1) // chunk) * 6
@@ -429,7 +443,16 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
 
         alg_bytes = alg_lines = None
         extra["seeds_per_step"] = n_seeds
+
+        def count_work():
+            work_seen[0] = work_seen[1] = 0
+            step()
+            torch.cuda.synchronize(dev)
+            es, el = exact_work(lib, dix, d_pat, m, n_seeds, d_out, sp)
+            return {"exact_steps": es, "exact_lines": el, "inexact_steps": work_seen[0],
+                    "inexact_lines": work_seen[1]}
     elif wl.pairs is not None:
+        count_work = None
         kl_h = np.empty((units, 2), dtype=np.uint32)
         kl_h[:, 0] = (wl.pairs[:, 0] + 1).astype(np.uint32)
         kl_h[:, 1] = wl.pairs[:, 1].astype(np.uint32)
@@ -466,6 +489,10 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
             launches_per_step = 1
             kernel_name = "k_exact"
             h2d_per, d2h_per = units * 8, units * 8
+
+            def count_work():
+                es, el = exact_work(lib, dix, d_pat, m, units, d_out, sp)
+                return {"exact_steps": es, "exact_lines": el}
             pin_in = torch.from_numpy(packed.view(np.int64)).pin_memory()
             pin_out = torch.empty((units, 2), dtype=torch.int32).pin_memory()
 
@@ -482,6 +509,16 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
                 _lib.check(lib.fmg_inexact(dix.handle, d_codes.data_ptr(), d_offs.data_ptr(), units, z,
                                            ct.byref(h), sp))
                 lib.fmg_matches_free(h)
+
+            def count_work():
+                h = ct.c_void_p()
+                _lib.check(lib.fmg_inexact(dix.handle, d_codes.data_ptr(), d_offs.data_ptr(), units, z,
+                                           ct.byref(h), sp))
+                st_, ln_ = ct.c_uint64(), ct.c_uint64()
+                lib.fmg_matches_steps(h, ct.byref(st_))
+                lib.fmgx_matches_lines(h, ct.byref(ln_))
+                lib.fmg_matches_free(h)
+                return {"inexact_steps": st_.value, "inexact_lines": ln_.value}
 
             launches_per_step = None  # counted below
             kernel_name = "k_inexact"
@@ -548,6 +585,34 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
                     "sectors_per_step": round(alg_lines / units, 4),
                     "random_sector_roofline_steps_per_s": round(peak * 1e9 / (alg_bytes / units), 1)}
 
+    # ---- search configs: device-counted work (one extra, untimed step) ----
+    work = None
+    if count_work is not None:
+        work = count_work()
+        steps_all = sum(v for k_, v in work.items() if k_.endswith("_steps"))
+        lines_all = sum(v for k_, v in work.items() if k_.endswith("_lines"))
+        step_s = ms_step / 1e3
+        peak, peak_kind = hbm_peak()
+        alg = 32 * lines_all  # one 32-byte sector per distinct line per executed Occ step
+        achieved = alg / step_s / 1e9
+        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": measured_traffic(kernel_name, args.config),
+                    "peak_kind": peak_kind, "kernel": kernel_name if launches_per_step == 1 else
+                    f"whole step ({kernel_name} dominant)",
+                    "alg_bytes_per_launch": alg, "alg_bytes_per_step": round(alg / max(steps_all, 1), 2),
+                    "sectors_per_step": round(lines_all / max(steps_all, 1), 4),
+                    "note": "algorithmic bytes = 32 B x lines fetched by the executed Occ steps, counted "
+                            "on the device; time = the timed step average"}
+        fetch_peak = random_fetch_peak(lib, local) if dix.device_bytes > (256 << 20) else None
+        if fetch_peak:
+            roofline["request_roofline"] = {
+                "bound": "dram_random_requests", "achieved": round(lines_all / step_s / 1e9, 2),
+                "peak": round(fetch_peak / 1e9, 2), "unit": "G random line fetches/s",
+                "frac": round(lines_all / step_s / fetch_peak, 4),
+                "note": "each fetched line counted as one random DRAM request; L2 hits let frac exceed 1"}
+        extra["work"] = {**work, "occ_steps_per_unit": round(steps_all / units, 2),
+                         "lines_per_unit": round(lines_all / units, 2)}
+
     # ---- end to end through the C-ABI host entry point ----
     e2e_steps = max(2, min(args.steps, 5))
     e2e_step()
@@ -577,7 +642,11 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
 
             def fn():
                 orc.exact_batch(ox, sp3, th)
-                orc.inexact_batch(ox, sp3, 1, th)
+                return orc.inexact_batch(ox, sp3, 1, th)
+
+            if work is not None:  # the reference DFS's own step count per seed, beside ours
+                extra["work"]["reference_dfs_steps_per_seed"] = round(fn()[4] / sp3.shape[0], 2)
+                extra["work"]["inexact_steps_per_seed"] = round(work["inexact_steps"] / max(1, wl.packed.size), 2)
         elif wl.pairs is not None:
             sample = min(units, 1 << 22)
             fn = lambda: orc.occ_pair_batch(ox, wl.pairs[:sample, 0], wl.pairs[:sample, 1], th)  # noqa: E731
@@ -585,6 +654,8 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
             sample = min(units, 20_000)
             sp_ = pattern_sample(wl, 0, sample)
             fn = lambda: orc.inexact_batch(ox, sp_, wl.max_diff, th)  # noqa: E731
+            if work is not None:  # the reference DFS's own step count, beside ours
+                extra["work"]["reference_dfs_steps_per_unit"] = round(fn()[4] / sample, 2)
         else:
             sample = min(units, 1 << 20)
             sp_ = pattern_sample(wl, 0, sample)

@@ -125,7 +125,7 @@ struct fmg_index {
 
 struct fmg_matches {
   int device = 0;
-  uint64_t patterns = 0, total = 0, steps = 0;
+  uint64_t patterns = 0, total = 0, steps = 0, lines = 0;  // work counters: Occ steps, lines fetched
   uint64_t* row_off = nullptr;  // device, patterns + 1
   uint32_t* k = nullptr;        // device, total
   uint32_t* l = nullptr;
@@ -413,11 +413,12 @@ bool run_z1(const fmg_index* ix, const CodePatterns& cp, uint64_t count, uint64_
   FMG_CK(cub::DeviceScan::InclusiveSum(tmp.ptr, tb, c64.ptr, res->row_off + 1, count, s));
   uint64_t total = 0;
   FMG_CK(cudaMemcpyAsync(&total, res->row_off + count, 8, cudaMemcpyDeviceToHost, s));
-  unsigned long long st = 0;
-  FMG_CK(cudaMemcpyAsync(&st, steps, 8, cudaMemcpyDeviceToHost, s));
+  unsigned long long st[2] = {0, 0};
+  FMG_CK(cudaMemcpyAsync(st, steps, sizeof(st), cudaMemcpyDeviceToHost, s));
   FMG_CK(cudaStreamSynchronize(s));
   res->total = total;
-  res->steps = st;
+  res->steps = st[0];
+  res->lines = st[1];
   FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->k), std::max<uint64_t>(total, 1) * 4, s));
   FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->l), std::max<uint64_t>(total, 1) * 4, s));
   FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->diffs), std::max<uint64_t>(total, 1), s));
@@ -468,14 +469,14 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     DevBuf<uint64_t> res_off(count, s);
     DevBuf<uint32_t> res_cnt(count, s);
     DevBuf<uint8_t> res_pass(count, s);
-    DevBuf<unsigned long long> counters(5, s);  // total, fail_count, steps, queue cursor, unsorted
+    DevBuf<unsigned long long> counters(6, s);  // total, fail_count, steps, lines, queue cursor, unsorted
     DevBuf<uint32_t> unsorted_list(count, s);
     DevBuf<uint32_t> too_big(1, s);
     FMG_CK(cudaMemsetAsync(too_big.ptr, 0, 4, s));
     bool need_cub_sort = false;
     FMG_CK(cudaMemsetAsync(res_pass.ptr, 0xFF, count, s));
-    FMG_CK(cudaMemsetAsync(counters.ptr + 2, 0, sizeof(unsigned long long), s));
-    FMG_CK(cudaMemsetAsync(counters.ptr + 4, 0, sizeof(unsigned long long), s));
+    FMG_CK(cudaMemsetAsync(counters.ptr + 2, 0, 2 * sizeof(unsigned long long), s));
+    FMG_CK(cudaMemsetAsync(counters.ptr + 5, 0, sizeof(unsigned long long), s));
 
     DevBuf<ulonglong2> packed((short_pat && !packed1) ? count : 0, s);
     if (short_pat && !packed1) {
@@ -558,7 +559,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       pass_kl.emplace_back(cap, s);
       pass_d.emplace_back(cap, s);
       FMG_CK(cudaMemsetAsync(counters.ptr, 0, 2 * sizeof(unsigned long long), s));
-      FMG_CK(cudaMemsetAsync(counters.ptr + 3, 0, sizeof(unsigned long long), s));
+      FMG_CK(cudaMemsetAsync(counters.ptr + 4, 0, sizeof(unsigned long long), s));
       InexactOut o{};
       o.kl = pass_kl.back().ptr;
       o.diffs = pass_d.back().ptr;
@@ -571,10 +572,10 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       o.fail_list = lists[pass & 1].ptr;
       o.fail_count = counters.ptr + 1;
       o.steps = counters.ptr + 2;
-      o.next = counters.ptr + 3;
-      o.unsorted = counters.ptr + 4;
+      o.next = counters.ptr + 4;
+      o.unsorted = counters.ptr + 5;
       o.unsorted_list = unsorted_list.ptr;
-      FMG_CK(cudaMemsetAsync(counters.ptr + 4, 0, sizeof(unsigned long long), s));
+      FMG_CK(cudaMemsetAsync(counters.ptr + 5, 0, sizeof(unsigned long long), s));
       const unsigned blocks = unsigned(T / nt);
       CodePatterns cp{codes, offsets, packed.ptr, packed1, uint32_t(max_len), dbits.ptr};
       static const bool trace = std::getenv("FMG_TRACE") != nullptr;
@@ -592,12 +593,12 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
           k_inexact<false, W><<<blocks, nt, smem, s>>>(ix->view(), cp, list, pending, z, sc, o);
       });
       FMG_CK(cudaGetLastError());
-      unsigned long long host_ctr[5];
+      unsigned long long host_ctr[6];
       FMG_CK(cudaMemcpyAsync(host_ctr, counters.ptr, sizeof(host_ctr), cudaMemcpyDeviceToHost, s));
       FMG_CK(cudaStreamSynchronize(s));
       const uint64_t failed = host_ctr[1];
-      if (host_ctr[4] > 0) {  // sort this pass's large result sets in place
-        k_sort_segments<<<unsigned(host_ctr[4]), 256, 0, s>>>(unsorted_list.ptr, res_off.ptr, res_cnt.ptr,
+      if (host_ctr[5] > 0) {  // sort this pass's large result sets in place
+        k_sort_segments<<<unsigned(host_ctr[5]), 256, 0, s>>>(unsorted_list.ptr, res_off.ptr, res_cnt.ptr,
                                                               pass_kl.back().ptr, pass_d.back().ptr, too_big.ptr);
         FMG_CK(cudaGetLastError());
         uint32_t tb_flag = 0;
@@ -646,12 +647,13 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     FMG_CK(cub::DeviceScan::InclusiveSum(tmp.ptr, tmp_bytes, c64.ptr, res->row_off + 1, count, s));
     uint64_t total = 0;
     FMG_CK(cudaMemcpyAsync(&total, res->row_off + count, sizeof(total), cudaMemcpyDeviceToHost, s));
-    unsigned long long steps = 0;
-    FMG_CK(cudaMemcpyAsync(&steps, counters.ptr + 2, sizeof(steps), cudaMemcpyDeviceToHost, s));
+    unsigned long long work[2] = {0, 0};
+    FMG_CK(cudaMemcpyAsync(work, counters.ptr + 2, sizeof(work), cudaMemcpyDeviceToHost, s));
     FMG_CK(cudaStreamSynchronize(s));
     const bool unsorted = need_cub_sort;
     res->total = total;
-    res->steps = steps;
+    res->steps = work[0];
+    res->lines = work[1];
     FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->k), std::max<uint64_t>(total, 1) * sizeof(uint32_t), s));
     FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->l), std::max<uint64_t>(total, 1) * sizeof(uint32_t), s));
     FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->diffs), std::max<uint64_t>(total, 1), s));
@@ -876,6 +878,35 @@ int fmgx_occ_pair_tuned(const fmg_index* ix, const uint32_t* kl, uint64_t count,
     check_index(ix);
     fmg::DeviceScope scope(ix->device);
     launch_occ_pair(ix, kl, count, out, as_stream(stream), per, threads);
+  });
+}
+
+// Work-counting variant of fmg_exact_packed (not part of include/fmgpu.h;
+// bench.py's algorithmic-bytes figure): synchronous, returns the Occ steps
+// executed and the 32-byte lines they fetched.
+int fmgx_exact_packed_work(const fmg_index* ix, const uint64_t* packed, uint32_t m, uint64_t count,
+                           uint32_t* kl_out, void* stream, uint64_t* steps, uint64_t* lines) {
+  return fmg::guard([&] {
+    check_index(ix);
+    FMG_REQUIRE(m >= 1 && m <= 32, "packed patterns need 1 <= m <= 32");
+    fmg::DeviceScope scope(ix->device);
+    cudaStream_t s = as_stream(stream);
+    DevBuf<unsigned long long> ctr(2, s);
+    FMG_CK(cudaMemsetAsync(ctr.ptr, 0, 2 * sizeof(unsigned long long), s));
+    launch_exact_packed(ix, packed, m, count, kl_out, s, ctr.ptr);
+    unsigned long long h[2];
+    FMG_CK(cudaMemcpyAsync(h, ctr.ptr, sizeof(h), cudaMemcpyDeviceToHost, s));
+    FMG_CK(cudaStreamSynchronize(s));
+    if (steps) *steps = h[0];
+    if (lines) *lines = h[1];
+  });
+}
+
+// Lines fetched by a bounded-difference search (companion of fmg_matches_steps).
+int fmgx_matches_lines(const fmg_matches* m, uint64_t* lines) {
+  return fmg::guard([&] {
+    FMG_REQUIRE(m != nullptr && lines != nullptr, "null argument");
+    *lines = m->lines;
   });
 }
 

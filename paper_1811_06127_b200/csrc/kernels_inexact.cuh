@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(256) k_dbound(IndexView ix, CodePatterns cp, u
   uint64_t bits = 0;
   uint32_t k = 0, l = ix.n;
   int seg_end = m - 1;
-  uint32_t my_steps = 0;
+  uint64_t work = 0;
   for (int pos = m - 1; pos >= 0; --pos) {
     const uint32_t b = uint32_t((pos < 32 ? pw0 : pw1) >> ((pos & 31) << 1)) & 3u;
     const uint32_t cb = c_of(ix, b);
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) k_dbound(IndexView ix, CodePatterns cp, u
       }
       k2 = cb + ol + 1u;
       l2 = cb + occ1_from_line<W>(ix, bh, wh, l, rh, b);
-      ++my_steps;
+      work += work_unit(jl != jh ? 2u : 1u);
     }
     if (k2 > l2) {  // W[pos..seg_end] is absent from the text
       bits |= 1ull << seg_end;
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256) k_dbound(IndexView ix, CodePatterns cp, u
     }
   }
   dbits_out[q] = bits;
-  if (steps) atomicAdd(steps, (unsigned long long)my_steps);
+  flush_work(steps, work);
 }
 
 // Per-thread global scratch for the inexact engine, warp-blocked (element e
@@ -334,8 +334,7 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
 
     // ---- one Occ step: the eight values at (k-1, l) ----
     uint32_t lo[4], hi[4];
-    occ_step<W, false>(ix, k, l, lo, hi);
-    ++my_steps;
+    my_steps += work_unit(occ_step<W, false>(ix, k, l, lo, hi));
 
     if (phase == 0) {
       const uint32_t b = sym_at(pos);
@@ -422,7 +421,7 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
     }
     cur_valid = false;  // the next iteration pops the top (the last child pushed)
   }
-  if (out.steps) atomicAdd(out.steps, (unsigned long long)my_steps);
+  flush_work(out.steps, my_steps);
 }
 
 // Sort the results of patterns that had more than S of them (written
@@ -554,14 +553,13 @@ __global__ void __launch_bounds__(256) k_spine(IndexView ix, CodePatterns cp, ui
   int m;
   z1_pattern(cp, q, pw0, pw1, m);
   const uint64_t dbits = cp.dbits[q];
-  uint32_t my_steps = 0;
+  uint64_t my_steps = 0;
   int i = m - 1;
   uint32_t k = 0, l = ix.n;
   bool alive = z1_dlb(dbits, m - 1) <= 1u;  // root (m-1, 1, 0, n), search.py:125
   while (alive) {
     uint32_t lo[4], hi[4];
-    occ_step<W, false>(ix, k, l, lo, hi);
-    ++my_steps;
+    my_steps += work_unit(occ_step<W, false>(ix, k, l, lo, hi));
     const uint32_t want = z1_sym(pw0, pw1, i);
     uint32_t k2[4], l2[4];
 #pragma unroll
@@ -635,7 +633,7 @@ __global__ void __launch_bounds__(256) k_spine(IndexView ix, CodePatterns cp, ui
     l = lw;
     --i;
   }
-  if (steps) atomicAdd(steps, (unsigned long long)my_steps);
+  flush_work(steps, my_steps);
 }
 
 template <int W>
@@ -647,7 +645,7 @@ __global__ void __launch_bounds__(256) k_chain(IndexView ix, CodePatterns cp, co
   constexpr uint32_t kC = LineTraits<W>::kChars;
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  uint32_t my_steps = 0;
+  uint64_t my_steps = 0;
   uint64_t pw0 = 0, pw1 = 0, dbits = 0;
   int i = -1;
   uint32_t k = 0, l = 0, q = 0;
@@ -689,7 +687,7 @@ __global__ void __launch_bounds__(256) k_chain(IndexView ix, CodePatterns cp, co
       const uint32_t cs = c_of(ix, sym);
       k2 = cs + ol + 1u;
       l2 = cs + occ1_from_line<W>(ix, bh, wh, l, rh, sym);
-      ++my_steps;
+      my_steps += work_unit(jl != jh ? 2u : 1u);
     }
     const bool empty = k2 > l2;
     const bool found = !empty && i == 0;
@@ -705,7 +703,7 @@ __global__ void __launch_bounds__(256) k_chain(IndexView ix, CodePatterns cp, co
     l = l2;
     --i;
   }
-  if (steps) atomicAdd(steps, (unsigned long long)my_steps);
+  flush_work(steps, my_steps);
 }
 
 // counting sort of raw results by pattern

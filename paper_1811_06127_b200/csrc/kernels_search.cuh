@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(256) k_exact(IndexView ix, PackedPatterns pp, 
                                                KmerTable kt) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  uint64_t my_steps = 0;
+  uint64_t work = 0;  // work_unit per step
   uint64_t pat = 0;          // packed form
   const uint8_t* codes = nullptr;  // general form
   int i = -1;
@@ -111,9 +111,9 @@ __global__ void __launch_bounds__(256) k_exact(IndexView ix, PackedPatterns pp, 
     const uint32_t cs = c_of(ix, sym);
     k = cs + ol + 1u;
     l = cs + oh;
-    ++my_steps;
+    work += work_unit(jl != jh ? 2u : 1u);
   }
-  if (steps) atomicAdd(steps, (unsigned long long)my_steps);
+  flush_work(steps, work);
 }
 
 

@@ -192,15 +192,15 @@ __device__ __forceinline__ uint32_t occ1_from_line(const IndexView& ix, const ui
 // needs no memory at all (Occ(b, n) = c[b+1] - c[b]).  When both ends share a
 // line it is fetched once (occ.py:86-96 does the same per bucket).
 template <int W, bool kStream>
-__device__ __forceinline__ void occ_step(const IndexView& ix, uint32_t k, uint32_t l, uint32_t lo[4],
-                                         uint32_t hi[4]) {
+__device__ __forceinline__ uint32_t occ_step(const IndexView& ix, uint32_t k, uint32_t l, uint32_t lo[4],
+                                             uint32_t hi[4]) {
   if (k == 0u && l == ix.n) {
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       lo[s] = 0u;
       hi[s] = ix.c[s + 1] - ix.c[s];
     }
-    return;
+    return 0u;
   }
   constexpr uint32_t kC = LineTraits<W>::kChars;
   const uint32_t jh = line_of<W>(l), rh = l - jh * kC;
@@ -221,6 +221,24 @@ __device__ __forceinline__ void occ_step(const IndexView& ix, uint32_t k, uint32
     for (int s = 0; s < 4; ++s) lo[s] = 0u;
   }
   occ4_from_line<W>(ix, bh, wh, l, rh, hi);
+  return jl != jh ? 2u : 1u;  // lines fetched
+}
+
+// Work counters (reporting only; the pointer is null on production calls).
+// A thread accumulates one u64: Occ steps in the high half, lines fetched in
+// the low half; flush_work adds them warp-reduced into ctr[0] (steps) and
+// ctr[1] (lines), so a launch costs a handful of same-address atomics.
+__device__ __forceinline__ uint64_t work_unit(uint32_t lines) { return (1ull << 32) | lines; }
+
+__device__ __forceinline__ void flush_work(unsigned long long* ctr, uint64_t v) {
+  if (ctr == nullptr) return;
+  const unsigned mask = __activemask();
+  const unsigned st = __reduce_add_sync(mask, unsigned(v >> 32));
+  const unsigned ln = __reduce_add_sync(mask, unsigned(v));
+  if ((threadIdx.x & 31u) == unsigned(__ffs(mask) - 1)) {
+    atomicAdd(ctr, (unsigned long long)st);
+    atomicAdd(ctr + 1, (unsigned long long)ln);
+  }
 }
 
 }  // namespace fmg

@@ -360,3 +360,38 @@ def test_exact_kmer_table_paths(gpu):
         arr[::2] = workloads.substrings(text, rng.integers(0, text.size - m + 1, arr[::2].shape[0]), m)
         klp, _ = fm.exact_search_batch(idx, arr)  # packed kernel
         assert np.array_equal(klp, orc.exact_batch(ox, arr)), m
+
+
+def _scale_cases():
+    path = GOLDEN / "scale_cases.json"
+    assert path.exists(), "tests/golden/scale_cases.json missing (make_golden.py scale)"
+    return json.loads(path.read_text())
+
+
+def test_scale_golden_config4_config1h(gpu):
+    """Reference outputs (fmpm run on this text, tests/golden/make_golden.py scale) on the
+    1 Gbp config-4 / 1-H text, GPU-built index: the first 16k config-4 seeds (exact) and
+    the first 4k config-1-H Occ pairs."""
+    cases = _scale_cases()
+    wl4 = workloads.config4(count=1 << 14)
+    idx = fm.build_index(wl4.text, builder="gpu")
+    seeds = workloads.unpack_patterns(wl4.packed, 20)
+    kl, _ = fm.exact_search_batch(idx, seeds)  # 16k >= 1024: k-mer table path
+    assert np.array_equal(kl.astype(np.int64), np.array(cases["config4_first16k_kl"], dtype=np.int64))
+    wl1h = workloads.config1h(count=1 << 12)
+    got = fm.occ_pair_batch(idx, wl1h.pairs[:, 0], wl1h.pairs[:, 1])
+    assert np.array_equal(got.astype(np.int64), np.array(cases["config1h_first4k_occ"], dtype=np.int64))
+    idx.release_device()
+
+
+def test_scale_golden_config2(gpu):
+    """Reference z = 1 result lists for the first 2000 config-2 seeds (1M-read workload)."""
+    cases = _scale_cases()["config2_first2k_z1"]
+    wl = workloads.config2()
+    idx = fm.build_index(wl.text)
+    ms = fm.inexact_search_batch(idx, wl.patterns[:2000], 1)
+    off = ms.offsets.astype(np.int64)
+    for q, want in enumerate(cases):
+        a, b = off[q], off[q + 1]
+        got = list(zip(ms.k[a:b].tolist(), ms.l[a:b].tolist(), ms.diffs[a:b].tolist()))
+        assert got == [tuple(x) for x in want], q

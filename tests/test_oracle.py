@@ -131,3 +131,15 @@ def test_oracle_inexact_is_order_free_dedup(small_cases):
         kk, ll = k[row[j]:row[j + 1]], l[row[j]:row[j + 1]]
         keys = list(zip(kk, ll))
         assert keys == sorted(set(keys))
+
+
+def test_oracle_config2_scale_golden():
+    """Pins the oracle on the 64 Mbp config-2 genome: reference z = 1 result lists for the
+    first 2000 seeds (tests/golden/make_golden.py scale, fmpm run on this text)."""
+    cases = json.loads((GOLDEN / "scale_cases.json").read_text())["config2_first2k_z1"]
+    wl = workloads.config2()
+    ox = orc.OracleIndex(build_index(wl.text, builder="host"))
+    row, k, l, d, _ = orc.inexact_batch(ox, wl.patterns[:2000], 1)
+    for q, want in enumerate(cases):
+        a, b = row[q], row[q + 1]
+        assert list(zip(k[a:b].tolist(), l[a:b].tolist(), d[a:b].tolist())) == [tuple(x) for x in want], q

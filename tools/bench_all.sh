@@ -5,8 +5,8 @@ out=gpurun_out/bench_all.jsonl
 : > $out
 for c in config1 config0 config1h config2 config4 config3; do
   steps=10; [ $c = config3 ] && steps=2
-  timeout 1500 python bench.py --config $c --steps $steps --warmup 3 --no-hbm-extra 2>/dev/null | tail -1 >> $out
-  timeout 900 python bench.py --impl reference --config $c --steps 3 --warmup 3 2>/dev/null | tail -1 >> $out
+  timeout 1500 python bench.py --config $c --steps $steps --warmup 3 --no-hbm-extra 2>gpurun_out/bench_$c.err | tail -1 >> $out
+  timeout 900 python bench.py --impl reference --config $c --steps 3 --warmup 3 2>gpurun_out/ref_$c.err | tail -1 >> $out
 done
 python - <<'PY'
 import json
