@@ -43,19 +43,29 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > built for p in deps)
 
 
-def build_native(force: bool = False, verbose: bool = False) -> Path:
-    """Build libfmgpu.so if any source is newer than the library."""
-    if not force and not _stale():
+def build_native(force: bool = False, verbose: bool = False, out: Path | None = None,
+                 extra: list[str] | None = None) -> Path:
+    """Build libfmgpu.so if any source is newer than the library.
+
+    `out` / `extra` (extra nvcc flags, e.g. -D switches) are for A/B variant
+    builds only (tools/ab/); the package always loads LIB_PATH.
+    """
+    target = Path(out) if out else LIB_PATH
+    if out is None and not force and not _stale():
         return LIB_PATH
-    tmp = LIB_PATH.with_suffix(".so.tmp")
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", str(REPO_DIR / "include"),
+    tmp = target.with_suffix(".so.tmp")
+    cmd = [_nvcc(), *NVCC_FLAGS, *(extra or []), "-I", str(REPO_DIR / "include"),
            *[str(CSRC / s) for s in SOURCES], "-o", str(tmp)]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True, cwd=str(CSRC))
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build_native(force=True, verbose=True))
+    import sys
+
+    # python -m paper_1811_06127_b200._build [out.so -DFLAG ...]   (variant builds for A/B)
+    args = sys.argv[1:]
+    print(build_native(force=True, verbose=True, out=Path(args[0]).resolve() if args else None, extra=args[1:]))

@@ -245,10 +245,13 @@ unsigned wave_blocks(const fmg_index* ix, const void* kernel, int threads, uint6
   return unsigned(std::min<uint64_t>(std::max<uint64_t>(resident, waves), 1u << 30));
 }
 
-// The exact-search k-mer table of the index, built on first use by a large
-// call (>= 1024 patterns): K = clamp(floor(log4 n) - 2, 4, 12), 8 * 4^K bytes
-// (128 MiB at 1 Gbp).  FMG_EXACT_LUT=0 disables it (A/B).
-KmerTable kmer_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
+// The prefix interval table of the index (PrefixTable), built on first use
+// by a large call (>= 1024 patterns): levels 1..K with
+// K = clamp(floor(log4 n) - 2, 4, 13), 8 * (4^(K+1) - 4) / 3 bytes (179 MB at
+// K = 12 for 1 Gbp, 716 MB at K = 13 for 3.1 Gbp).  Level K is the exact-search k-mer table (KmerTable): its entries
+// are what exact_search returns for each K-mer, first empty interval
+// included.  FMG_EXACT_LUT=0 disables both uses (A/B).
+PrefixTable prefix_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
   static const bool enabled = [] {
     const char* e = std::getenv("FMG_EXACT_LUT");
     return e == nullptr || std::atoi(e) != 0;
@@ -259,23 +262,33 @@ KmerTable kmer_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
   if (!ix->lut) {
     uint32_t k = 0;
     while ((uint64_t(1) << (2 * (k + 1))) <= ix->n) ++k;  // floor(log4 n)
-    k = std::min<uint32_t>(12, std::max<uint32_t>(4, k >= 2 ? k - 2 : 0));
-    const uint64_t entries = uint64_t(1) << (2 * k);
+    k = std::min<uint32_t>(13, std::max<uint32_t>(4, k >= 2 ? k - 2 : 0));
+    if (const char* e = std::getenv("FMG_LUT_K")) k = std::min<uint32_t>(14, std::max<uint32_t>(1, std::atoi(e)));  // A/B
+    const uint64_t entries = PrefixTable::off(k + 1);
     uint2* lut = nullptr;
     FMG_CK(cudaMalloc(&lut, entries * sizeof(uint2)));
-    PackedPatterns pp{nullptr, k};  // words == nullptr: search x = 0 .. 4^K - 1
     CodePatterns cp{nullptr, nullptr};
-    with_words(ix, [&](auto wt) {
-      constexpr int W = decltype(wt)::value;
-      k_exact<true, W><<<unsigned((entries + 255) / 256), 256, 0, s>>>(ix->view(), pp, cp, entries, lut, nullptr,
-                                                                        KmerTable{});
-    });
-    FMG_CK(cudaGetLastError());
+    for (uint32_t j = 1; j <= k; ++j) {
+      PackedPatterns pp{nullptr, j};  // words == nullptr: search x = 0 .. 4^j - 1
+      const uint64_t cnt = uint64_t(1) << (2 * j);
+      with_words(ix, [&](auto wt) {
+        constexpr int W = decltype(wt)::value;
+        k_exact<true, W><<<unsigned((cnt + 255) / 256), 256, 0, s>>>(ix->view(), pp, cp, cnt,
+                                                                      lut + PrefixTable::off(j), nullptr, KmerTable{});
+      });
+      FMG_CK(cudaGetLastError());
+    }
     FMG_CK(cudaStreamSynchronize(s));
     ix->lut = lut;
     ix->lut_k = k;
   }
-  return KmerTable{ix->lut, ix->lut_k};
+  return PrefixTable{ix->lut, ix->lut_k};
+}
+
+KmerTable kmer_table(const fmg_index* ix, uint64_t count, cudaStream_t s) {
+  const PrefixTable pt = prefix_table(ix, count, s);
+  if (!pt.base) return {};
+  return KmerTable{pt.base + PrefixTable::off(pt.k), pt.k};
 }
 
 void launch_exact_packed(const fmg_index* ix, const uint64_t* packed, uint32_t m, uint64_t count, uint32_t* kl_out,
@@ -505,6 +518,12 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       if (run_z1(ix, cpz, count, max_len, s, counters.ptr + 2, res)) return res;
       // queues overflowed: fall through to the DFS engine (same results)
     }
+    // shallow DFS nodes step through the prefix table (FMG_INEXACT_LUT=0: off, A/B)
+    const bool lut_off = [] {
+      const char* e = std::getenv("FMG_INEXACT_LUT");
+      return e != nullptr && std::atoi(e) == 0;
+    }();
+    const PrefixTable pt = lut_off ? PrefixTable{} : prefix_table(ix, count, s);
     std::vector<DevBuf<uint2>> pass_kl;
     std::vector<DevBuf<uint8_t>> pass_d;
     DevBuf<uint32_t> lists[2] = {DevBuf<uint32_t>(count, s), DevBuf<uint32_t>(count, s)};
@@ -588,9 +607,9 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       with_words(ix, [&](auto wt) {
         constexpr int W = decltype(wt)::value;
         if (short_pat)
-          k_inexact<true, W><<<blocks, nt, smem, s>>>(ix->view(), cp, list, pending, z, sc, o);
+          k_inexact<true, W><<<blocks, nt, smem, s>>>(ix->view(), cp, list, pending, z, sc, o, pt);
         else
-          k_inexact<false, W><<<blocks, nt, smem, s>>>(ix->view(), cp, list, pending, z, sc, o);
+          k_inexact<false, W><<<blocks, nt, smem, s>>>(ix->view(), cp, list, pending, z, sc, o, pt);
       });
       FMG_CK(cudaGetLastError());
       unsigned long long host_ctr[6];

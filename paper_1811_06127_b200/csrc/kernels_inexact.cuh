@@ -106,6 +106,24 @@ struct InexactOut {
   uint32_t* unsorted_list;       // their pattern ids (capacity: count)
 };
 
+#ifndef FMG_LUT_HINT
+#define FMG_LUT_HINT 0  // 1: prefix-table loads with an L2 evict_last policy
+#endif
+#ifndef FMG_INEX_LINE_HINT
+#define FMG_INEX_LINE_HINT 0  // 2: DFS index-line loads with an L2 evict_first policy
+#endif
+
+// Prefix interval table: level j (1 <= j <= k) holds the interval of every
+// string x of length j, key(x) = sum x_t 4^t (x_0 = first character), at
+// base[off(j) + key]; absent strings hold some k > l.  Prepending b to S
+// gives key(bS) = b + 4 key(S), so the four children of a node whose string
+// S is shorter than k sit in ONE aligned 32-byte sector of level |S| + 1.
+struct PrefixTable {
+  const uint2* base = nullptr;
+  uint32_t k = 0;
+  __host__ __device__ static uint32_t off(uint32_t j) { return ((1u << (2 * j)) - 4u) / 3u; }
+};
+
 // Reference semantics (search.py:120-159): nodes (i, budget, k, l) from the
 // root (m-1, z, 0, n); a node with i < 0 is a result with z - budget diffs;
 // otherwise one Occ step at (k-1, l) and children skip (i-1, budget-1, k, l),
@@ -127,9 +145,17 @@ struct InexactOut {
 // turning W[0..i] into a substring of the text must touch each absent
 // segment with its own edit, so a node with D(i) > budget yields nothing and
 // is never pushed.  (BWA's D array, computed with the forward index only.)
+//
+// Shallow nodes (prefix table present): a node whose string S (the text
+// characters its path consumed) is shorter than pt.k is held as (key(S), |S|)
+// instead of (k, l); its Occ step is one 32-byte table sector giving all four
+// child intervals.  Shallow strings are shared by every pattern, so these
+// sectors stay in L2, where the index lines of the same wide intervals —
+// two random DRAM fetches per step — do not.
 template <bool kShort, int W>
 __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, const uint32_t* __restrict__ list,
-                                                 uint64_t count, uint32_t z, InexactScratch sc, InexactOut out) {
+                                                 uint64_t count, uint32_t z, InexactScratch sc, InexactOut out,
+                                                 PrefixTable pt) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t S = sc.S, nt = blockDim.x, tid = threadIdx.x;
   uint2* s_kl = reinterpret_cast<uint2*>(smem);               // [S][nt]
@@ -157,7 +183,8 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
   bool overflow = false;
   bool cur_valid = false;  // DFS node held in registers
   int ci = 0;
-  uint32_t cb = 0, ck = 0, cl = 0;
+  uint32_t cb = 0, ck = 0, cl = 0;  // budget; (k, l), or (key, depth) when csh
+  bool csh = false;
 
   auto sym_at = [&](int i) -> uint32_t {
     if (kShort) return uint32_t((i < 32 ? pw0 : pw1) >> ((i & 31) << 1)) & 3u;
@@ -297,8 +324,9 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
           cur_valid = dlb(m - 1) <= z;
           ci = m - 1;
           cb = z;
+          csh = pt.base != nullptr;  // the root's string is empty: key 0, depth 0
           ck = 0u;
-          cl = ix.n;
+          cl = csh ? 0u : ix.n;
           continue;
         }
         k = kd;
@@ -320,7 +348,8 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
           const uint2 e = s_kl[sp * nt + tid];
           const uint32_t ib = s_ib[sp * nt + tid];
           ci = int(ib >> 16) - 1;
-          cb = ib & 0xFFFFu;
+          cb = ib & 0xFFu;
+          csh = (ib >> 15) & 1u;
           ck = e.x;
           cl = e.y;
           cur_valid = true;
@@ -332,15 +361,37 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
     }
     if (!stepping) break;
 
-    // ---- one Occ step: the eight values at (k-1, l) ----
-    uint32_t lo[4], hi[4];
-    my_steps += work_unit(occ_step<W, false>(ix, k, l, lo, hi));
+    // ---- one Occ step: the four child intervals of (k, l) ----
+    uint32_t k2[4], l2[4];
+    if (phase == 1 && csh) {  // shallow node: one prefix-table sector
+      const uint2* p = pt.base + PrefixTable::off(l + 1u) + 4u * k;
+      uint64_t a0, a1, a2, a3;
+#if FMG_LUT_HINT
+      uint64_t pol;
+      asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+      asm("ld.global.nc.L2::cache_hint.v4.u64 {%0,%1,%2,%3}, [%4], %5;"
+          : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3)
+          : "l"(p), "l"(pol));
+#else
+      ld256<0>(reinterpret_cast<const uint8_t*>(p), a0, a1, a2, a3);
+#endif
+      k2[0] = uint32_t(a0), l2[0] = uint32_t(a0 >> 32), k2[1] = uint32_t(a1), l2[1] = uint32_t(a1 >> 32);
+      k2[2] = uint32_t(a2), l2[2] = uint32_t(a2 >> 32), k2[3] = uint32_t(a3), l2[3] = uint32_t(a3 >> 32);
+      my_steps += work_unit(1u);
+    } else {
+      uint32_t lo[4], hi[4];
+      my_steps += work_unit(occ_step<W, FMG_INEX_LINE_HINT>(ix, k, l, lo, hi));
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        k2[b] = ix.c[b] + lo[b] + 1u;
+        l2[b] = ix.c[b] + hi[b];
+      }
+    }
 
     if (phase == 0) {
       const uint32_t b = sym_at(pos);
-      const uint32_t cbase = c_of(ix, b);
-      const uint32_t k2 = cbase + sel4(lo, b) + 1u, l2 = cbase + sel4(hi, b);
-      if (k2 > l2) {  // W[pos..seg_end] is absent from the text
+      const uint32_t kb = sel4(k2, b), lb = sel4(l2, b);
+      if (kb > lb) {  // W[pos..seg_end] is absent from the text
         if (kShort)
           dbits |= 1ull << seg_end;
         else
@@ -349,8 +400,8 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
         ld = ix.n;
         seg_end = pos - 1;
       } else {
-        kd = k2;
-        ld = l2;
+        kd = kb;
+        ld = lb;
       }
       --pos;
       continue;
@@ -360,8 +411,9 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
     const int i = ci;
     const uint32_t budget = cb;
     const uint32_t want = sym_at(i);
-    const uint32_t cw = c_of(ix, want);
-    const uint32_t kw = cw + sel4(lo, want) + 1u, lw = cw + sel4(hi, want);
+    const uint32_t kw = sel4(k2, want), lw = sel4(l2, want);
+    // children stay shallow while their strings are shorter than pt.k
+    const bool child_sh = csh && cl + 1u < pt.k;
     if (budget == 0) {
       // budget-0 node: only the match child, continued in registers
       if (kw > lw) {
@@ -371,8 +423,9 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
         cur_valid = false;
       } else {
         ci = i - 1;
-        ck = kw;
-        cl = lw;
+        ck = child_sh ? want + 4u * ck : kw;
+        cl = child_sh ? cl + 1u : lw;
+        csh = child_sh;
         cur_valid = dlb(i - 1) == 0;
       }
       continue;
@@ -387,37 +440,45 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
     const bool ok_match = !at0 && d_prev <= budget;  // (i-1, budget)
     const bool ok_prev = !at0 && d_prev <= bm1;      // skip / mismatch: (i-1, budget-1)
     const bool ok_cur = d_cur <= bm1;                // insert: (i, budget-1)
-    uint32_t k2[4], l2[4];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      k2[b] = ix.c[b] + lo[b] + 1u;
-      l2[b] = ix.c[b] + hi[b];
-    }
     if (at0) {  // children with i - 1 < 0 are results (rare)
       if (kw <= lw) record(kw, lw, z - budget);
-      record(k, l, z - bm1);  // skip
+      uint32_t sk = ck, sl = cl;  // skip: this node's own interval
+      if (csh) {
+        if (cl == 0u) {
+          sk = 0u;
+          sl = ix.n;
+        } else {
+          const uint2 e = __ldg(pt.base + PrefixTable::off(cl) + ck);
+          sk = e.x;
+          sl = e.y;
+        }
+      }
+      record(sk, sl, z - bm1);
 #pragma unroll
       for (uint32_t b = 0; b < 4; ++b)
         if (b != want && k2[b] <= l2[b]) record(k2[b], l2[b], z - bm1);  // mismatch
     }
-    auto push_if = [&](bool cond, int pi, uint32_t pb, uint32_t pk, uint32_t pl) {
+    auto push_if = [&](bool cond, int pi, uint32_t pb, uint32_t pk, uint32_t pl, bool psh) {
       if (cond) {
         if (sp == S) {
           overflow = true;
         } else {
           s_kl[sp * nt + tid] = make_uint2(pk, pl);
-          s_ib[sp * nt + tid] = (uint32_t(pi + 1) << 16) | pb;
+          s_ib[sp * nt + tid] = (uint32_t(pi + 1) << 16) | (psh ? 0x8000u : 0u) | pb;
           ++sp;
         }
       }
     };
-    push_if(ok_match && kw <= lw, i - 1, budget, kw, lw);  // match
-    push_if(ok_prev, i - 1, bm1, k, l);                      // skip
+    const uint32_t ckey = 4u * ck, cdep = cl + 1u;  // shallow children: key b + 4 key(S), depth + 1
+    push_if(ok_match && kw <= lw, i - 1, budget, child_sh ? want + ckey : kw, child_sh ? cdep : lw,
+            child_sh);                                  // match
+    push_if(ok_prev, i - 1, bm1, ck, cl, csh);           // skip: same string
 #pragma unroll
     for (uint32_t b = 0; b < 4; ++b) {
       const bool ne = k2[b] <= l2[b];
-      push_if(ok_cur && ne, i, bm1, k2[b], l2[b]);                 // insert
-      push_if(ok_prev && ne && b != want, i - 1, bm1, k2[b], l2[b]);  // mismatch
+      const uint32_t px = child_sh ? b + ckey : k2[b], py = child_sh ? cdep : l2[b];
+      push_if(ok_cur && ne, i, bm1, px, py, child_sh);                 // insert
+      push_if(ok_prev && ne && b != want, i - 1, bm1, px, py, child_sh);  // mismatch
     }
     cur_valid = false;  // the next iteration pops the top (the last child pushed)
   }
@@ -611,7 +672,7 @@ __global__ void __launch_bounds__(256) k_spine(IndexView ix, CodePatterns cp, ui
 #pragma unroll
       for (int b = 0; b < 4; ++b)
         if (uint32_t(b) != want && k2[b] <= l2[b]) ++rc;
-      if (k2[want & 3u] <= l2[want & 3u]) ++rc;  // match with budget kept
+      if (sel4(k2, want) <= sel4(l2, want)) ++rc;  // match with budget kept
     }
     uint64_t rs = warp_reserve(qu.n_raws, rc);
     if (at0) {
@@ -623,7 +684,7 @@ __global__ void __launch_bounds__(256) k_spine(IndexView ix, CodePatterns cp, ui
 #pragma unroll
       for (int b = 0; b < 4; ++b)
         if (uint32_t(b) != want && k2[b] <= l2[b]) rput(k2[b], l2[b], 1u);
-      if (k2[want & 3u] <= l2[want & 3u]) rput(k2[want & 3u], l2[want & 3u], 0u);
+      if (sel4(k2, want) <= sel4(l2, want)) rput(sel4(k2, want), sel4(l2, want), 0u);
       break;
     }
     // continue along the match child (i-1, 1)

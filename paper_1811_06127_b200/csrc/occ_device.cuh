@@ -62,12 +62,21 @@ struct IndexView {
 
 constexpr uint64_t kFieldLo = 0x5555555555555555ull;
 
-template <bool kStream>
+// kStream: 0 = default caching; 1 = L1::no_allocate (gathers without reuse);
+// 2 = L2 evict_first (lines that must not push a hot working set — the
+// prefix table — out of L2).
+template <int kStream>
 __device__ __forceinline__ void ld256(const uint8_t* p, uint64_t& a0, uint64_t& a1, uint64_t& a2, uint64_t& a3) {
-  if (kStream) {
+  if (kStream == 1) {
     asm("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
         : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3)
         : "l"(p));
+  } else if (kStream == 2) {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm("ld.global.nc.L2::cache_hint.v4.u64 {%0,%1,%2,%3}, [%4], %5;"
+        : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3)
+        : "l"(p), "l"(pol));
   } else {
     asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3) : "l"(p));
   }
@@ -83,7 +92,7 @@ __device__ __forceinline__ uint32_t line_of(uint32_t p) {
 // kStream selects L1::no_allocate for gathers without reuse (Occ
 // microbenchmark); search kernels keep L1 allocation so the hot top-of-BWT
 // lines every query starts from are L1 hits.
-template <int W, bool kStream>
+template <int W, int kStream>
 __device__ __forceinline__ void load_line(const IndexView& ix, uint32_t j, uint32_t rmax, uint32_t b[4],
                                           uint64_t w[W]) {
   const uint8_t* p = ix.lines + size_t(j) * LineTraits<W>::kBytes;
@@ -191,7 +200,7 @@ __device__ __forceinline__ uint32_t occ1_from_line(const IndexView& ix, const ui
 // Occ(., l).  k == 0 gives lo = 0 (occ.py:74-77); the root interval (0, n)
 // needs no memory at all (Occ(b, n) = c[b+1] - c[b]).  When both ends share a
 // line it is fetched once (occ.py:86-96 does the same per bucket).
-template <int W, bool kStream>
+template <int W, int kStream>
 __device__ __forceinline__ uint32_t occ_step(const IndexView& ix, uint32_t k, uint32_t l, uint32_t lo[4],
                                              uint32_t hi[4]) {
   if (k == 0u && l == ix.n) {

@@ -395,3 +395,36 @@ def test_scale_golden_config2(gpu):
         a, b = off[q], off[q + 1]
         got = list(zip(ms.k[a:b].tolist(), ms.l[a:b].tolist(), ms.diffs[a:b].tolist()))
         assert got == [tuple(x) for x in want], q
+
+
+@pytest.mark.parametrize("z,lens", [(1, (1, 2, 3, 7, 19, 32, 40)), (2, (1, 2, 5, 12, 20)), (3, (1, 3, 6, 9)),
+                                    (1, (70, 90))])
+def test_inexact_prefix_table_paths(gpu, monkeypatch, z, lens):
+    """The DFS engine with the prefix table (>= 1024 patterns; K = 6 here): shallow nodes
+    stepped through the table, the depth-K hand-over to index lines, length-1..3 patterns
+    whose results come from shallow nodes (root skip), long (> 64) patterns — identical to
+    the oracle and to the table-less engine."""
+    monkeypatch.setenv("FMG_INEXACT_DFS", "1")
+    rng = np.random.Generator(np.random.PCG64(777 + z))
+    text = rng.integers(0, 4, 200_000, dtype=np.uint8)
+    idx = fm.build_index(text)
+    ox = orc.OracleIndex(idx)
+    pats = []
+    for _ in range(1200):
+        m = int(rng.choice(lens))
+        if rng.random() < 0.6:
+            s = int(rng.integers(0, text.size - m + 1))
+            p = text[s:s + m].copy()
+            if m > 4 and rng.random() < 0.5:
+                p[int(rng.integers(0, m))] = rng.integers(0, 4)
+        else:
+            p = rng.integers(0, 4, m, dtype=np.uint8)
+        pats.append(codes_to_str(p))
+    ms = fm.inexact_search_batch(idx, pats, z)
+    row, k, l, d, _ = orc.inexact_batch(ox, pats, z)
+    assert np.array_equal(ms.offsets, row)
+    assert np.array_equal(ms.k.astype(np.int64), k) and np.array_equal(ms.l.astype(np.int64), l)
+    assert np.array_equal(ms.diffs, d)
+    monkeypatch.setenv("FMG_INEXACT_LUT", "0")
+    b = fm.inexact_search_batch(idx, pats, z)
+    assert np.array_equal(b.offsets, ms.offsets) and np.array_equal(b.k, ms.k) and np.array_equal(b.diffs, ms.diffs)

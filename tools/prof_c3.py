@@ -30,9 +30,15 @@ for r in range(reps):
     h = ct.c_void_p()
     _lib.check(lib.fmg_inexact_packed(dix.handle, d.data_ptr(), 19, wl.packed.size, 1, ct.byref(h), s.cuda_stream))
     t2 = time.perf_counter()
-    tot, steps = ct.c_uint64(), ct.c_uint64()
+    tot, steps, lines = ct.c_uint64(), ct.c_uint64(), ct.c_uint64()
     lib.fmg_matches_size(h, ct.byref(tot), None)
     lib.fmg_matches_steps(h, ct.byref(steps))
+    lib.fmgx_matches_lines(h, ct.byref(lines))
+    kk = np.empty(tot.value, np.uint32)
+    dd = np.empty(tot.value, np.uint8)
+    row = np.empty(wl.packed.size + 1, np.uint64)
+    lib.fmg_matches_copy(h, row.ctypes.data, kk.ctypes.data, None, dd.ctypes.data, 1)
     lib.fmg_matches_free(h)
     print(f"rep {r}: {1e3 * (t2 - t1):.1f} ms, {wl.packed.size / (t2 - t1) / 1e6:.2f} M seeds/s, results {tot.value}, "
-          f"steps/seed {steps.value / wl.packed.size:.0f}", flush=True)
+          f"steps/seed {steps.value / wl.packed.size:.0f}, lines/seed {lines.value / wl.packed.size:.0f}, "
+          f"checksum {int(kk.astype(np.uint64).sum()) ^ int(row.sum()) ^ int(dd.sum())}", flush=True)
