@@ -551,7 +551,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       FMG_REQUIRE(pass < 250, "inexact search did not converge");
       int nt = 128;
       while (nt > 32 && size_t(S) * 12 * nt > size_t(96) << 10) nt /= 2;
-      const size_t smem = size_t(S) * 12 * nt;
+      const size_t smem = size_t(S + 1) * 12 * nt;  // + the push dump slot
       FMG_REQUIRE(smem <= size_t(smem_optin), "inexact search stack does not fit in shared memory");
       FMG_CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       int per_sm = 0;

@@ -158,8 +158,8 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
                                                  PrefixTable pt) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t S = sc.S, nt = blockDim.x, tid = threadIdx.x;
-  uint2* s_kl = reinterpret_cast<uint2*>(smem);               // [S][nt]
-  uint32_t* s_ib = reinterpret_cast<uint32_t*>(s_kl + S * nt);  // [S][nt]
+  uint2* s_kl = reinterpret_cast<uint2*>(smem);                     // [S + 1][nt]
+  uint32_t* s_ib = reinterpret_cast<uint32_t*>(s_kl + (S + 1) * nt);  // [S + 1][nt]; slot S: push dump
   const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= sc.T) return;
   uint64_t my_steps = 0;
@@ -458,16 +458,15 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
       for (uint32_t b = 0; b < 4; ++b)
         if (b != want && k2[b] <= l2[b]) record(k2[b], l2[b], z - bm1);  // mismatch
     }
+    // Branch-free push: every candidate is stored, a rejected one into the
+    // dump slot S (the stack has S + 1 entries), and sp advances by `ok`.
     auto push_if = [&](bool cond, int pi, uint32_t pb, uint32_t pk, uint32_t pl, bool psh) {
-      if (cond) {
-        if (sp == S) {
-          overflow = true;
-        } else {
-          s_kl[sp * nt + tid] = make_uint2(pk, pl);
-          s_ib[sp * nt + tid] = (uint32_t(pi + 1) << 16) | (psh ? 0x8000u : 0u) | pb;
-          ++sp;
-        }
-      }
+      const bool ok = cond && sp < S;
+      overflow |= cond && sp >= S;
+      const uint32_t slot = ok ? sp : S;
+      s_kl[slot * nt + tid] = make_uint2(pk, pl);
+      s_ib[slot * nt + tid] = (uint32_t(pi + 1) << 16) | (psh ? 0x8000u : 0u) | pb;
+      sp += ok ? 1u : 0u;
     };
     const uint32_t ckey = 4u * ck, cdep = cl + 1u;  // shallow children: key b + 4 key(S), depth + 1
     push_if(ok_match && kw <= lw, i - 1, budget, child_sh ? want + ckey : kw, child_sh ? cdep : lw,

@@ -115,11 +115,12 @@ __device__ __forceinline__ void load_line(const IndexView& ix, uint32_t j, uint3
 }
 
 // Mask of the fields of word k that lie in 0..r.
+// Branch-free: PTX clamps shift counts above 64 (all fields out -> 0).
 __device__ __forceinline__ uint64_t word_mask(uint32_t r, int k) {
-  const int d = int(r) - 32 * k;
-  if (d < 0) return 0ull;
-  if (d >= 31) return ~0ull;
-  return ~0ull >> (62 - 2 * d);
+  const int s = max(62 - 2 * (int(r) - 32 * k), 0);
+  uint64_t m;
+  asm("shr.b64 %0, %1, %2;" : "=l"(m) : "l"(~0ull), "r"(s));
+  return m;
 }
 
 // Counts of A, C, G, T among fields 0..r of the line (raw: '$' counts as A).
@@ -217,19 +218,17 @@ __device__ __forceinline__ uint32_t occ_step(const IndexView& ix, uint32_t k, ui
   const uint32_t low = k - 1u;
   const uint32_t jl = has_low ? line_of<W>(low) : jh;
   const uint32_t rl = has_low ? low - jl * kC : 0u;
+  // Branch-free: the low line is loaded unconditionally (the same line again
+  // — an L1 hit — when k-1 and l share it), so lanes taking one or two lines
+  // never split the warp and both counts run as one straight-line block.
   uint32_t bh[4], bl[4];
   uint64_t wh[W], wl[W];
   load_line<W, kStream>(ix, jh, rh, bh, wh);
-  if (jl != jh) {
-    load_line<W, kStream>(ix, jl, rl, bl, wl);
-    occ4_from_line<W>(ix, bl, wl, low, rl, lo);
-  } else if (has_low) {
-    occ4_from_line<W>(ix, bh, wh, low, rl, lo);
-  } else {
-#pragma unroll
-    for (int s = 0; s < 4; ++s) lo[s] = 0u;
-  }
+  load_line<W, kStream>(ix, jl, rl, bl, wl);
+  occ4_from_line<W>(ix, bl, wl, low, rl, lo);
   occ4_from_line<W>(ix, bh, wh, l, rh, hi);
+#pragma unroll
+  for (int s = 0; s < 4; ++s) lo[s] = has_low ? lo[s] : 0u;
   return jl != jh ? 2u : 1u;  // lines fetched
 }
 

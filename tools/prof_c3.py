@@ -24,6 +24,7 @@ lib = _lib.load()
 dix = idx.device_index(0)
 d = torch.from_numpy(wl.packed.view(np.int64)).cuda()
 s = torch.cuda.Stream()
+times = []
 for r in range(reps):
     torch.cuda.synchronize()
     t1 = time.perf_counter()
@@ -39,6 +40,10 @@ for r in range(reps):
     row = np.empty(wl.packed.size + 1, np.uint64)
     lib.fmg_matches_copy(h, row.ctypes.data, kk.ctypes.data, None, dd.ctypes.data, 1)
     lib.fmg_matches_free(h)
+    times.append(t2 - t1)
     print(f"rep {r}: {1e3 * (t2 - t1):.1f} ms, {wl.packed.size / (t2 - t1) / 1e6:.2f} M seeds/s, results {tot.value}, "
           f"steps/seed {steps.value / wl.packed.size:.0f}, lines/seed {lines.value / wl.packed.size:.0f}, "
           f"checksum {int(kk.astype(np.uint64).sum()) ^ int(row.sum()) ^ int(dd.sum())}", flush=True)
+ts = sorted(times[1:] or times)
+print(f"summary: median {1e3 * ts[len(ts) // 2]:.1f} ms, min {1e3 * ts[0]:.1f} ms over {len(ts)} reps after the first",
+      flush=True)
