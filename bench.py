@@ -395,6 +395,15 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
     units = unit_count(wl)
     metric, unit = metric_of(args.config)
     extra: dict = {"index_build_s": round(t_build, 2), "index_device_bytes": dix.device_bytes}
+    if wl.pairs is None:  # search configs: the k-mer / prefix interval table, built before timing
+        fn = lib.fmgx_prefix_table
+        fn.argtypes = [ct.c_void_p, ct.POINTER(ct.c_uint32), ct.POINTER(ct.c_uint64)]
+        kk, nb = ct.c_uint32(), ct.c_uint64()
+        torch.cuda.synchronize(dev)
+        t_lut = time.perf_counter()
+        _lib.check(fn(dix.handle, ct.byref(kk), ct.byref(nb)))
+        extra["prefix_table"] = {"k": kk.value, "bytes": nb.value,
+                                 "build_s": round(time.perf_counter() - t_lut, 4)}
 
     if wl.name == "config3":
         m = wl.meta["m"]

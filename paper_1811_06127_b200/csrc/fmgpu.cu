@@ -246,11 +246,19 @@ unsigned wave_blocks(const fmg_index* ix, const void* kernel, int threads, uint6
 }
 
 // The prefix interval table of the index (PrefixTable), built on first use
-// by a large call (>= 1024 patterns): levels 1..K with
-// K = clamp(floor(log4 n) - 2, 4, 13), 8 * (4^(K+1) - 4) / 3 bytes (179 MB at
-// K = 12 for 1 Gbp, 716 MB at K = 13 for 3.1 Gbp).  Level K is the exact-search k-mer table (KmerTable): its entries
-// are what exact_search returns for each K-mer, first empty interval
-// included.  FMG_EXACT_LUT=0 disables both uses (A/B).
+// by a large call (>= 1024 patterns): levels 1..K, level j built from level
+// j-1 with one Occ step per entry (k_lut_level), 8 * (4^(K+1) - 4) / 3 bytes.
+// K = clamp(floor(log4 n) + 1, 4, 15), lowered while the table would take
+// more than a quarter of the free device memory: 11.5 GB at K = 15 (1 and
+// 3.1 Gbp), 716 MB at K = 13 (64 Mbp).  Measured on config 4 (2^28 20-mers,
+// 1 Gbp): K = 12 / 13 / 14 / 15 -> 6.45 / 7.40 / 8.54 / 10.04 G seeds/s,
+// table build 13 ms at K = 15 — HBM capacity spent to skip dependent steps.  Level K is the
+// exact-search k-mer table (KmerTable): its entries are what exact_search
+// returns for each K-mer, first empty interval included.  FMG_EXACT_LUT=0
+// disables both uses, FMG_LUT_K=j forces K (A/B).
+constexpr int kLutBias = 1;
+constexpr uint32_t kLutMax = 15;
+
 PrefixTable prefix_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
   static const bool enabled = [] {
     const char* e = std::getenv("FMG_EXACT_LUT");
@@ -260,27 +268,29 @@ PrefixTable prefix_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
   auto* ix = const_cast<fmg_index*>(cix);  // the table is a cache; the index itself never changes
   std::lock_guard<std::mutex> lock(ix->lut_mu);
   if (!ix->lut) {
-    uint32_t k = 0;
+    int k = 0;
     while ((uint64_t(1) << (2 * (k + 1))) <= ix->n) ++k;  // floor(log4 n)
-    k = std::min<uint32_t>(13, std::max<uint32_t>(4, k >= 2 ? k - 2 : 0));
-    if (const char* e = std::getenv("FMG_LUT_K")) k = std::min<uint32_t>(14, std::max<uint32_t>(1, std::atoi(e)));  // A/B
-    const uint64_t entries = PrefixTable::off(k + 1);
+    k = std::min<int>(int(kLutMax), std::max<int>(4, k + kLutBias));
+    if (const char* e = std::getenv("FMG_LUT_K")) k = std::min<int>(15, std::max<int>(1, std::atoi(e)));  // A/B
+    size_t free_b = 0, total_b = 0;
+    FMG_CK(cudaMemGetInfo(&free_b, &total_b));
+    while (k > 1 && PrefixTable::off64(k + 1) * sizeof(uint2) > free_b / 4) --k;
+    const uint64_t entries = PrefixTable::off64(k + 1);
     uint2* lut = nullptr;
     FMG_CK(cudaMalloc(&lut, entries * sizeof(uint2)));
-    CodePatterns cp{nullptr, nullptr};
-    for (uint32_t j = 1; j <= k; ++j) {
-      PackedPatterns pp{nullptr, j};  // words == nullptr: search x = 0 .. 4^j - 1
+    for (int j = 1; j <= k; ++j) {
       const uint64_t cnt = uint64_t(1) << (2 * j);
+      const uint2* parent = j == 1 ? nullptr : lut + PrefixTable::off64(j - 1);
       with_words(ix, [&](auto wt) {
         constexpr int W = decltype(wt)::value;
-        k_exact<true, W><<<unsigned((cnt + 255) / 256), 256, 0, s>>>(ix->view(), pp, cp, cnt,
-                                                                      lut + PrefixTable::off(j), nullptr, KmerTable{});
+        k_lut_level<W><<<unsigned((cnt + 255) / 256), 256, 0, s>>>(ix->view(), parent, lut + PrefixTable::off64(j),
+                                                                   cnt);
       });
       FMG_CK(cudaGetLastError());
     }
     FMG_CK(cudaStreamSynchronize(s));
     ix->lut = lut;
-    ix->lut_k = k;
+    ix->lut_k = uint32_t(k);
   }
   return PrefixTable{ix->lut, ix->lut_k};
 }
@@ -288,7 +298,7 @@ PrefixTable prefix_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
 KmerTable kmer_table(const fmg_index* ix, uint64_t count, cudaStream_t s) {
   const PrefixTable pt = prefix_table(ix, count, s);
   if (!pt.base) return {};
-  return KmerTable{pt.base + PrefixTable::off(pt.k), pt.k};
+  return KmerTable{pt.base + PrefixTable::off64(pt.k), pt.k};
 }
 
 void launch_exact_packed(const fmg_index* ix, const uint64_t* packed, uint32_t m, uint64_t count, uint32_t* kl_out,
@@ -926,6 +936,18 @@ int fmgx_matches_lines(const fmg_matches* m, uint64_t* lines) {
   return fmg::guard([&] {
     FMG_REQUIRE(m != nullptr && lines != nullptr, "null argument");
     *lines = m->lines;
+  });
+}
+
+// Builds the prefix / k-mer table now instead of on the first large call
+// (bench.py reports its build time and size apart from the timed region).
+int fmgx_prefix_table(const fmg_index* ix, uint32_t* k_out, uint64_t* bytes_out) {
+  return fmg::guard([&] {
+    check_index(ix);
+    fmg::DeviceScope scope(ix->device);
+    const PrefixTable pt = prefix_table(ix, 1u << 20, nullptr);
+    if (k_out) *k_out = pt.k;
+    if (bytes_out) *bytes_out = pt.base ? PrefixTable::off64(pt.k + 1) * sizeof(uint2) : 0;
   });
 }
 

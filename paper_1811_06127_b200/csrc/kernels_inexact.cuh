@@ -121,7 +121,8 @@ struct InexactOut {
 struct PrefixTable {
   const uint2* base = nullptr;
   uint32_t k = 0;
-  __host__ __device__ static uint32_t off(uint32_t j) { return ((1u << (2 * j)) - 4u) / 3u; }
+  __host__ __device__ static uint32_t off(uint32_t j) { return ((1u << (2 * j)) - 4u) / 3u; }  // j <= 15
+  static uint64_t off64(uint32_t j) { return ((uint64_t(1) << (2 * j)) - 4u) / 3u; }
 };
 
 // Reference semantics (search.py:120-159): nodes (i, budget, k, l) from the

@@ -117,6 +117,39 @@ __global__ void __launch_bounds__(256) k_exact(IndexView ix, PackedPatterns pp, 
 }
 
 
+// Level j of the k-mer / prefix interval table from level j-1 (`parent`,
+// null for j = 1): entry x (x_0 = first character in bits 0..1) is the
+// interval exact_search returns for x — extend_backward of the entry of
+// x[1..] = x >> 2 by x_0, or that entry unchanged when it is already the
+// first empty interval (search.py:88-93).  One Occ step per entry; the four
+// siblings share their parent's lines (L1 hits).
+template <int W>
+__global__ void __launch_bounds__(256) k_lut_level(IndexView ix, const uint2* __restrict__ parent,
+                                                   uint2* __restrict__ out, uint64_t cnt) {
+  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= cnt) return;
+  const uint32_t sym = uint32_t(q & 3u);
+  const uint32_t cs = c_of(ix, sym);
+  if (parent == nullptr) {  // init_interval, search.py:50-57
+    out[q] = make_uint2(cs + 1u, c_of(ix, sym + 1u));
+    return;
+  }
+  const uint2 e = parent[q >> 2];
+  if (e.x > e.y) {
+    out[q] = e;
+    return;
+  }
+  constexpr uint32_t kC = LineTraits<W>::kChars;
+  const uint32_t low = e.x - 1u, l = e.y;  // e.x >= 1 on every non-empty interval
+  const uint32_t jh = line_of<W>(l), jl = line_of<W>(low);
+  uint32_t bh[4], bl[4];
+  uint64_t wh[W], wl[W];
+  load_line<W, 0>(ix, jh, l - jh * kC, bh, wh);
+  load_line<W, 0>(ix, jl, low - jl * kC, bl, wl);
+  out[q] = make_uint2(cs + occ1_from_line<W>(ix, bl, wl, low, low - jl * kC, sym) + 1u,
+                      cs + occ1_from_line<W>(ix, bh, wh, l, l - jh * kC, sym));
+}
+
 // ----- position recovery ---------------------------------------------------
 
 // psi_inverse_fused (search.py:172-186): symbol at row i and its

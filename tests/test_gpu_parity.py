@@ -339,8 +339,8 @@ def test_z1_engines_agree(gpu, monkeypatch):
 
 
 def test_exact_kmer_table_paths(gpu):
-    """>= 1024 patterns use the k-mer table (K = 6 here): lengths below, at and above K,
-    present and absent, packed and CSR inputs — all identical to the oracle."""
+    """>= 1024 patterns use the k-mer table (K = floor(log4 n) + 1 = 9 here): lengths below,
+    at and above K, present and absent, packed and CSR inputs — all identical to the oracle."""
     rng = np.random.Generator(np.random.PCG64(606))
     text = rng.integers(0, 4, 200_000, dtype=np.uint8)
     idx = fm.build_index(text)
@@ -355,7 +355,7 @@ def test_exact_kmer_table_paths(gpu):
             pats.append(codes_to_str(rng.integers(0, 4, m, dtype=np.uint8)))
     kl, _ = fm.exact_search_batch(idx, pats)  # CSR kernel
     assert np.array_equal(kl, orc.exact_batch(ox, pats))
-    for m in (5, 6, 7, 20):
+    for m in (5, 8, 9, 10, 20):
         arr = rng.integers(0, 4, (1 << 15, m), dtype=np.uint8)
         arr[::2] = workloads.substrings(text, rng.integers(0, text.size - m + 1, arr[::2].shape[0]), m)
         klp, _ = fm.exact_search_batch(idx, arr)  # packed kernel
@@ -397,10 +397,10 @@ def test_scale_golden_config2(gpu):
         assert got == [tuple(x) for x in want], q
 
 
-@pytest.mark.parametrize("z,lens", [(1, (1, 2, 3, 7, 19, 32, 40)), (2, (1, 2, 5, 12, 20)), (3, (1, 3, 6, 9)),
+@pytest.mark.parametrize("z,lens", [(1, (1, 2, 3, 8, 9, 10, 19, 32, 40)), (2, (1, 2, 5, 9, 10, 20)), (3, (1, 3, 6, 9, 10)),
                                     (1, (70, 90))])
 def test_inexact_prefix_table_paths(gpu, monkeypatch, z, lens):
-    """The DFS engine with the prefix table (>= 1024 patterns; K = 6 here): shallow nodes
+    """The DFS engine with the prefix table (>= 1024 patterns; K = 9 here): shallow nodes
     stepped through the table, the depth-K hand-over to index lines, length-1..3 patterns
     whose results come from shallow nodes (root skip), long (> 64) patterns — identical to
     the oracle and to the table-less engine."""
