@@ -83,6 +83,14 @@ int fmb_build_gpu(int device, const uint8_t* codes, uint64_t n, uint8_t* bucket_
  * ------------------------------------------------------------------------- */
 int fmg_index_create(int device, const void* bucket_records, uint64_t n_buckets, uint64_t n,
                      uint64_t sentinel_row, const uint64_t c[5], fmg_index** out);
+/* Optional index of the REVERSED text (its .fmi bucket records and sentinel
+ * row; same n and C).  With it attached, fmg_inexact[_packed] at
+ * max_diff = 1 runs the bidirectional engine (identical results, fewer Occ
+ * steps: each half of the pattern is matched exactly before the edit is
+ * placed in the other half).  No reference counterpart (an engine cache). */
+int fmg_index_set_reverse(fmg_index* index, const void* bucket_records, uint64_t n_buckets,
+                          uint64_t sentinel_row);
+int fmg_index_has_reverse(const fmg_index* index, int* has);
 /* Suffix-array samples for locate (index.py:93); count must be n/32 + 1. */
 int fmg_index_set_samples(fmg_index* index, const uint64_t* sa_samples, uint64_t count);
 /* n, the device ordinal and the device bytes the handle owns. */

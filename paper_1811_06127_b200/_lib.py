@@ -30,6 +30,8 @@ PROTOTYPES: dict[str, tuple] = {
     "fmg_index_create": (ct.c_int, [ct.c_int, _vp, ct.c_uint64, ct.c_uint64, ct.c_uint64, _vp,
                                     ct.POINTER(_vp)]),
     "fmg_index_set_samples": (ct.c_int, [_vp, _vp, ct.c_uint64]),
+    "fmg_index_set_reverse": (ct.c_int, [_vp, _vp, ct.c_uint64, ct.c_uint64]),
+    "fmg_index_has_reverse": (ct.c_int, [_vp, ct.POINTER(ct.c_int)]),
     "fmg_index_info": (ct.c_int, [_vp, _u64p, ct.POINTER(ct.c_int), _u64p]),
     "fmg_index_destroy": (None, [_vp]),
     "fmg_occ_pair": (ct.c_int, [_vp, _vp, ct.c_uint64, _vp, _vp]),

@@ -83,6 +83,7 @@ struct DevBuf {
 #include "kernels_occ.cuh"
 #include "kernels_search.cuh"
 #include "kernels_inexact.cuh"
+#include "kernels_bidir.cuh"
 
 namespace fmg {
 
@@ -111,6 +112,20 @@ struct fmg_index {
   std::mutex lut_mu;
   uint2* lut = nullptr;
   uint32_t lut_k = 0;
+  // optional index of the reversed text (fmg_index_set_reverse): the
+  // bidirectional z = 1 engine (kernels_bidir.cuh) and its prefix table
+  uint8_t* rev_lines = nullptr;
+  uint64_t rev_sentinel_row = 0;
+  uint2* lut_r = nullptr;
+  uint32_t tail[16] = {};
+
+  fmg::IndexView view_rev() const {
+    fmg::IndexView v = view();
+    v.lines = rev_lines;
+    v.samples = nullptr;
+    v.sentinel_row = uint32_t(rev_sentinel_row);
+    return v;
+  }
 
   fmg::IndexView view() const {
     fmg::IndexView v;
@@ -259,6 +274,18 @@ unsigned wave_blocks(const fmg_index* ix, const void* kernel, int threads, uint6
 constexpr int kLutBias = 1;
 constexpr uint32_t kLutMax = 15;
 
+void build_prefix_levels(const fmg_index* ix, const fmg::IndexView& v, uint2* lut, int k, cudaStream_t s) {
+  for (int j = 1; j <= k; ++j) {
+    const uint64_t cnt = uint64_t(1) << (2 * j);
+    const uint2* parent = j == 1 ? nullptr : lut + PrefixTable::off64(j - 1);
+    with_words(ix, [&](auto wt) {
+      constexpr int W = decltype(wt)::value;
+      k_lut_level<W><<<unsigned((cnt + 255) / 256), 256, 0, s>>>(v, parent, lut + PrefixTable::off64(j), cnt);
+    });
+    FMG_CK(cudaGetLastError());
+  }
+}
+
 PrefixTable prefix_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
   static const bool enabled = [] {
     const char* e = std::getenv("FMG_EXACT_LUT");
@@ -275,24 +302,35 @@ PrefixTable prefix_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
     size_t free_b = 0, total_b = 0;
     FMG_CK(cudaMemGetInfo(&free_b, &total_b));
     while (k > 1 && PrefixTable::off64(k + 1) * sizeof(uint2) > free_b / 4) --k;
-    const uint64_t entries = PrefixTable::off64(k + 1);
     uint2* lut = nullptr;
-    FMG_CK(cudaMalloc(&lut, entries * sizeof(uint2)));
-    for (int j = 1; j <= k; ++j) {
-      const uint64_t cnt = uint64_t(1) << (2 * j);
-      const uint2* parent = j == 1 ? nullptr : lut + PrefixTable::off64(j - 1);
-      with_words(ix, [&](auto wt) {
-        constexpr int W = decltype(wt)::value;
-        k_lut_level<W><<<unsigned((cnt + 255) / 256), 256, 0, s>>>(ix->view(), parent, lut + PrefixTable::off64(j),
-                                                                   cnt);
-      });
-      FMG_CK(cudaGetLastError());
-    }
+    FMG_CK(cudaMalloc(&lut, PrefixTable::off64(k + 1) * sizeof(uint2)));
+    build_prefix_levels(ix, ix->view(), lut, k, s);
     FMG_CK(cudaStreamSynchronize(s));
     ix->lut = lut;
     ix->lut_k = uint32_t(k);
   }
   return PrefixTable{ix->lut, ix->lut_k};
+}
+
+// The reverse index's prefix table, same K as the forward one (empty when
+// there is no reverse index, no forward table, or no room for it).
+PrefixTable prefix_table_rev(const fmg_index* cix, uint64_t count, cudaStream_t s) {
+  const PrefixTable tf = prefix_table(cix, count, s);
+  if (!tf.base || !cix->rev_lines) return {};
+  auto* ix = const_cast<fmg_index*>(cix);
+  std::lock_guard<std::mutex> lock(ix->lut_mu);
+  if (!ix->lut_r) {
+    const uint64_t bytes = PrefixTable::off64(tf.k + 1) * sizeof(uint2);
+    size_t free_b = 0, total_b = 0;
+    FMG_CK(cudaMemGetInfo(&free_b, &total_b));
+    if (bytes > free_b / 3) return {};
+    uint2* lut = nullptr;
+    FMG_CK(cudaMalloc(&lut, bytes));
+    build_prefix_levels(ix, ix->view_rev(), lut, int(tf.k), s);
+    FMG_CK(cudaStreamSynchronize(s));
+    ix->lut_r = lut;
+  }
+  return PrefixTable{ix->lut_r, tf.k};
 }
 
 KmerTable kmer_table(const fmg_index* ix, uint64_t count, cudaStream_t s) {
@@ -534,6 +572,23 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       return e != nullptr && std::atoi(e) == 0;
     }();
     const PrefixTable pt = lut_off ? PrefixTable{} : prefix_table(ix, count, s);
+    // z = 1 with a reverse index attached: the bidirectional engine for the
+    // first pass (FMG_INEXACT_BIDIR=0: off, A/B); retries use the DFS engine.
+    const bool bidir_off = [] {
+      const char* e = std::getenv("FMG_INEXACT_BIDIR");
+      return e != nullptr && std::atoi(e) == 0;
+    }();
+    BiIndex bi{};
+    bool bidir = false;
+    if (z == 1 && short_pat && ix->rev_lines && pt.base && !bidir_off) {
+      bi.rev = ix->view_rev();
+      bi.tf = pt;
+      bi.tr = prefix_table_rev(ix, count, s);
+      for (int d = 0; d < 16; ++d) bi.tail[d] = ix->tail[d];
+      bidir = bi.tr.base != nullptr;
+    }
+    const void* kfn_bi = nullptr;
+    with_words(ix, [&](auto wt) { kfn_bi = (const void*)k_inexact_bi<decltype(wt)::value>; });
     std::vector<DevBuf<uint2>> pass_kl;
     std::vector<DevBuf<uint8_t>> pass_d;
     DevBuf<uint32_t> lists[2] = {DevBuf<uint32_t>(count, s), DevBuf<uint32_t>(count, s)};
@@ -559,13 +614,17 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     if (const char* e = std::getenv("FMG_STACK_S")) S = std::max<uint32_t>(2, uint32_t(std::atoi(e)));  // A/B
     for (int pass = 0; pending > 0; ++pass) {
       FMG_REQUIRE(pass < 250, "inexact search did not converge");
+      const bool use_bi = bidir && pass == 0;
+      const uint32_t Sp = use_bi ? 9u : S;  // z = 1: one budget-1 node's children at a time
+      const size_t ebytes = use_bi ? 20 : 12;
+      const void* kf = use_bi ? kfn_bi : kfn;
       int nt = 128;
-      while (nt > 32 && size_t(S) * 12 * nt > size_t(96) << 10) nt /= 2;
-      const size_t smem = size_t(S + 1) * 12 * nt;  // + the push dump slot
+      while (nt > 32 && size_t(Sp) * ebytes * nt > size_t(96) << 10) nt /= 2;
+      const size_t smem = size_t(Sp + 1) * ebytes * nt;  // + the push dump slot
       FMG_REQUIRE(smem <= size_t(smem_optin), "inexact search stack does not fit in shared memory");
-      FMG_CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      FMG_CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       int per_sm = 0;
-      FMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, nt, smem));
+      FMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, nt, smem));
       per_sm = std::max(per_sm, 1);
       // threads: full residency, bounded by a scratch budget of ~2 GiB
       const uint64_t per_thread = uint64_t(R) * (2 * 16 + 4) + (short_pat ? 0 : max_len);
@@ -581,7 +640,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       sc.table = table.ptr;
       sc.slots = slots.ptr;
       sc.dlb = dl.ptr;
-      sc.S = S;
+      sc.S = Sp;
       sc.R = R;
       sc.Mmax = uint32_t(max_len);
       sc.T = T;
@@ -616,7 +675,9 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       }
       with_words(ix, [&](auto wt) {
         constexpr int W = decltype(wt)::value;
-        if (short_pat)
+        if (use_bi)
+          k_inexact_bi<W><<<blocks, nt, smem, s>>>(ix->view(), bi, cp, list, pending, sc, o);
+        else if (short_pat)
           k_inexact<true, W><<<blocks, nt, smem, s>>>(ix->view(), cp, list, pending, z, sc, o, pt);
         else
           k_inexact<false, W><<<blocks, nt, smem, s>>>(ix->view(), cp, list, pending, z, sc, o, pt);
@@ -788,6 +849,33 @@ int fmg_device_count(int* count) {
   });
 }
 
+// .fmi bucket records (n_buckets x 64 B, host) -> device lines of ix's layout.
+static uint8_t* upload_lines(fmg_index* ix, const void* bucket_records) {
+  uint8_t* lines = nullptr;
+  const uint64_t n_buckets = ix->n_buckets;
+  with_words(ix, [&](auto wt) {
+    constexpr int W = decltype(wt)::value;
+    ix->n_lines = (n_buckets * 128 + fmg::LineTraits<W>::kChars - 1) / fmg::LineTraits<W>::kChars;
+    FMG_CK(cudaMalloc(&lines, ix->n_lines * fmg::LineTraits<W>::kBytes));
+    uint64_t* staging = nullptr;
+    FMG_CK(cudaMalloc(&staging, n_buckets * 64));
+    FMG_CK(cudaMemcpy(staging, bucket_records, n_buckets * 64, cudaMemcpyHostToDevice));
+    FMG_CK(cudaMemset(ix->err, 0, sizeof(uint32_t)));
+    fmg::k_build_lines<W><<<unsigned((ix->n_lines + 255) / 256), 256>>>(staging, n_buckets, lines, ix->n_lines,
+                                                                         ix->err);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    cudaFree(staging);
+    if (e != cudaSuccess) cudaFree(lines);
+    FMG_CK(e);
+  });
+  uint32_t bad = 0;
+  FMG_CK(cudaMemcpy(&bad, ix->err, sizeof(bad), cudaMemcpyDeviceToHost));
+  if (bad != 0) cudaFree(lines);
+  FMG_REQUIRE(bad == 0, "bucket base does not fit 32 bits");
+  return lines;
+}
+
 int fmg_index_create(int device, const void* bucket_records, uint64_t n_buckets, uint64_t n, uint64_t sentinel_row,
                      const uint64_t c[5], fmg_index** out) {
   return fmg::guard([&] {
@@ -812,25 +900,9 @@ int fmg_index_create(int device, const void* bucket_records, uint64_t n_buckets,
       ix->n_buckets = n_buckets;
       ix->words = choose_words(n_buckets);
       ix->sms = fmg::sm_count(device);
-      with_words(ix, [&](auto wt) {
-        constexpr int W = decltype(wt)::value;
-        ix->n_lines = (n_buckets * 128 + fmg::LineTraits<W>::kChars - 1) / fmg::LineTraits<W>::kChars;
-        FMG_CK(cudaMalloc(&ix->lines, ix->n_lines * fmg::LineTraits<W>::kBytes));
-        FMG_CK(cudaMalloc(&ix->err, sizeof(uint32_t)));
-        FMG_CK(cudaMemset(ix->err, 0, sizeof(uint32_t)));
-        uint64_t* staging = nullptr;
-        FMG_CK(cudaMalloc(&staging, n_buckets * 64));
-        FMG_CK(cudaMemcpy(staging, bucket_records, n_buckets * 64, cudaMemcpyHostToDevice));
-        fmg::k_build_lines<W><<<unsigned((ix->n_lines + 255) / 256), 256>>>(staging, n_buckets, ix->lines,
-                                                                             ix->n_lines, ix->err);
-        cudaError_t e = cudaGetLastError();
-        if (e == cudaSuccess) e = cudaDeviceSynchronize();
-        cudaFree(staging);
-        FMG_CK(e);
-      });
-      uint32_t bad = 0;
-      FMG_CK(cudaMemcpy(&bad, ix->err, sizeof(bad), cudaMemcpyDeviceToHost));
-      FMG_REQUIRE(bad == 0, "bucket base does not fit 32 bits");
+      FMG_CK(cudaMalloc(&ix->err, sizeof(uint32_t)));
+      FMG_CK(cudaMemset(ix->err, 0, sizeof(uint32_t)));
+      ix->lines = upload_lines(ix, bucket_records);
       // Allow the stream-ordered pool to keep freed blocks (host entry points
       // allocate per call).
       cudaMemPool_t pool;
@@ -843,6 +915,38 @@ int fmg_index_create(int device, const void* bucket_records, uint64_t n_buckets,
       fmg_index_destroy(ix);
       throw;
     }
+  });
+}
+
+int fmg_index_set_reverse(fmg_index* ix, const void* bucket_records, uint64_t n_buckets, uint64_t sentinel_row) {
+  return fmg::guard([&] {
+    check_index(ix);
+    FMG_REQUIRE(bucket_records != nullptr, "null argument");
+    FMG_REQUIRE(n_buckets == ix->n_buckets, "reverse index bucket count does not match the index");
+    FMG_REQUIRE(sentinel_row <= ix->n, "sentinel row outside [0, n]");
+    fmg::DeviceScope scope(ix->device);
+    std::lock_guard<std::mutex> lock(ix->lut_mu);
+    if (ix->rev_lines) cudaFree(ix->rev_lines);
+    if (ix->lut_r) cudaFree(ix->lut_r);
+    ix->rev_lines = nullptr;
+    ix->lut_r = nullptr;
+    ix->rev_lines = upload_lines(ix, bucket_records);
+    ix->rev_sentinel_row = sentinel_row;
+    DevBuf<uint32_t> tail(16, nullptr);
+    with_words(ix, [&](auto wt) {
+      constexpr int W = decltype(wt)::value;
+      fmg::k_tail_keys<W><<<1, 32>>>(ix->view(), 16u, tail.ptr);
+    });
+    FMG_CK(cudaGetLastError());
+    FMG_CK(cudaMemcpy(ix->tail, tail.ptr, sizeof(ix->tail), cudaMemcpyDeviceToHost));
+  });
+}
+
+int fmg_index_has_reverse(const fmg_index* ix, int* has) {
+  return fmg::guard([&] {
+    check_index(ix);
+    FMG_REQUIRE(has != nullptr, "null argument");
+    *has = ix->rev_lines != nullptr;
   });
 }
 
@@ -873,7 +977,7 @@ int fmg_index_info(const fmg_index* ix, uint64_t* n, int* device, uint64_t* devi
     if (device_bytes) {
       uint64_t lb = 0;
       with_words(ix, [&](auto wt) { lb = fmg::LineTraits<decltype(wt)::value>::kBytes; });
-      *device_bytes = ix->n_lines * lb + ix->n_samples * 4;
+      *device_bytes = ix->n_lines * lb * (ix->rev_lines ? 2 : 1) + ix->n_samples * 4;
     }
   });
 }
@@ -885,6 +989,8 @@ void fmg_index_destroy(fmg_index* ix) {
   cudaSetDevice(ix->device);
   if (ix->lines) cudaFree(ix->lines);
   if (ix->lut) cudaFree(ix->lut);
+  if (ix->lut_r) cudaFree(ix->lut_r);
+  if (ix->rev_lines) cudaFree(ix->rev_lines);
   if (ix->samples) cudaFree(ix->samples);
   if (ix->err) cudaFree(ix->err);
   if (prev >= 0) cudaSetDevice(prev);

@@ -1,0 +1,468 @@
+// Bidirectional z = 1 engine for the bounded-difference search
+// (search.py:97-159).  Part of libfmgpu.so (sm_100a); included once by
+// fmgpu.cu after kernels_inexact.cuh.
+//
+// For z = 1 the reference's DFS reports (interval(S), diffs) for every
+// string S in the one-edit neighbourhood of W that occurs in the text:
+// W itself (diffs 0), one substitution, one deletion (skip), or one
+// insertion after W[p] for p in [0, m-1] (never before W[0]); equal
+// intervals keep the smallest diffs.  The order of exploration is free, so
+// instead of one backward DFS from the empty string — whose wrong-edit
+// chains near the right end survive for ~log4(n) characters — the set is
+// enumerated in two halves (h = m / 2):
+//   case A: edits in W[0..h-1] (and insertion after W[h-1]): the right
+//     part W[h..m-1] is matched exactly first, then the usual backward DFS
+//     runs over the left part on the forward index;
+//   case B: edits in W[h..m-1] (insertions after W[p], p >= h): the left
+//     part W[0..h-1] is matched exactly first, then a forward DFS runs over
+//     the right part on the index of the REVERSED text, with the forward
+//     index's interval of S kept in step arithmetically (2BWT):
+//     extending S by c on the right, Sc's rows are the rows of S whose next
+//     character is c, ordered after "S$" (S a suffix of the text) and after
+//     every Sb with b < c, so k(Sc) = k(S) + [S is a text suffix] +
+//     sum_{b<c} |Sb| with |Sb| read off the reverse index's Occ step.
+// Every chain therefore starts from an already-long exact string and dies
+// within a few characters.  Results are the forward-index intervals, so the
+// output is bit-identical to the one-directional engines.
+#pragma once
+
+#include <cstdint>
+
+#include "occ_device.cuh"
+
+namespace fmg {
+
+struct BiIndex {
+  IndexView rev;       // index of the reversed text (same n and C)
+  PrefixTable tf, tr;  // prefix tables of the forward / reverse index (same k)
+  uint32_t tail[16];   // tail[d]: key of the reversed text's first d characters (d < k), ~0u if d > n
+};
+
+// key of W[a .. a+len-1] with W[a] in bits 0..1 (len <= 15)
+__device__ __forceinline__ uint32_t pat_key(uint64_t pw0, uint64_t pw1, int a, int len) {
+  uint64_t x;
+  if (a == 0) {
+    x = pw0;
+  } else if (a < 32) {
+    x = (pw0 >> (2 * a)) | (pw1 << (64 - 2 * a));
+  } else {
+    x = pw1 >> (2 * (a - 32));
+  }
+  return uint32_t(x) & ((1u << (2 * len)) - 1u);
+}
+
+__device__ __forceinline__ uint32_t pat_sym(uint64_t pw0, uint64_t pw1, int i) {
+  return uint32_t((i < 32 ? pw0 : pw1) >> ((i & 31) << 1)) & 3u;
+}
+
+// key of reverse(W[a .. a+len-1]): W[a+len-1] in bits 0..1
+__device__ __forceinline__ uint32_t pat_rkey(uint64_t pw0, uint64_t pw1, int a, int len) {
+  uint32_t key = 0;
+  for (int t = 0; t < len; ++t) key |= pat_sym(pw0, pw1, a + len - 1 - t) << (2 * t);
+  return key;
+}
+
+// The four child intervals of (k, l) on index v: from the prefix table
+// (shallow: key, depth) or by one Occ step on the index lines.
+template <int W>
+__device__ __forceinline__ void children4(const IndexView& v, const PrefixTable& pt, bool shallow, uint32_t x,
+                                          uint32_t y, uint32_t ck[4], uint32_t cl[4], uint64_t& work) {
+  if (shallow) {
+    const uint2* p = pt.base + PrefixTable::off(y + 1u) + 4u * x;
+    uint64_t a0, a1, a2, a3;
+    ld256<0>(reinterpret_cast<const uint8_t*>(p), a0, a1, a2, a3);
+    ck[0] = uint32_t(a0), cl[0] = uint32_t(a0 >> 32), ck[1] = uint32_t(a1), cl[1] = uint32_t(a1 >> 32);
+    ck[2] = uint32_t(a2), cl[2] = uint32_t(a2 >> 32), ck[3] = uint32_t(a3), cl[3] = uint32_t(a3 >> 32);
+    work += work_unit(1u);
+  } else {
+    uint32_t lo[4], hi[4];
+    work += work_unit(occ_step<W, 0>(v, x, y, lo, hi));
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      ck[b] = v.c[b] + lo[b] + 1u;
+      cl[b] = v.c[b] + hi[b];
+    }
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(128) k_inexact_bi(IndexView ix, BiIndex bi, CodePatterns cp,
+                                                    const uint32_t* __restrict__ list, uint64_t count,
+                                                    InexactScratch sc, InexactOut out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t S = sc.S, nt = blockDim.x, tid = threadIdx.x;
+  uint4* s_x = reinterpret_cast<uint4*>(smem);                      // [S + 1][nt]
+  uint32_t* s_ib = reinterpret_cast<uint32_t*>(s_x + (S + 1) * nt);  // [S + 1][nt]; slot S: push dump
+  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= sc.T) return;
+  uint64_t my_steps = 0;
+  const uint64_t wbase = t >> 5, lane = t & 31u;
+  auto HI = [&](uint32_t e) -> uint64_t { return (wbase * (2u * sc.R) + e) * 32u + lane; };
+  auto LI = [&](uint32_t e) -> uint64_t { return (wbase * sc.R + e) * 32u + lane; };
+  uint32_t epoch = 0;
+  const uint32_t K = bi.tf.k;
+  const uint32_t sent_r = bi.rev.sentinel_row;
+
+  bool have = false;
+  uint64_t q = 0;
+  int m = 0, h = 0;
+  uint64_t pw0 = 0, pw1 = 0, dbits = 0;
+  int phase = 1;  // 1: case A (backward, forward index), 3: case B (forward, reverse index)
+  uint32_t sp = 0, nres = 0;
+  bool overflow = false;
+  bool cur_valid = false;
+  int ci = 0;                               // i (case A) / j (case B)
+  uint32_t cb = 0;                          // budget
+  uint32_t cx = 0, cy = 0, cz = 0, cw = 0;  // A: (k, l) or (key, depth); B: F (k, l) + R (k', l') or (rkey, depth)
+  bool csh = false;
+
+  auto sym_at = [&](int i) -> uint32_t { return pat_sym(pw0, pw1, i); };
+  auto dlb = [&](int i) -> uint32_t { return __popcll(dbits & ((2ull << i) - 1ull)); };
+  auto record = [&](uint32_t k, uint32_t l, uint32_t used) {
+    const uint32_t H = 2u * sc.R;
+    uint32_t hh = (k * 0x9E3779B1u ^ l * 0x85EBCA77u) & (H - 1u);
+    for (uint32_t probe = 0; probe < H; ++probe, hh = (hh + 1u) & (H - 1u)) {
+      uint4 e = sc.table[HI(hh)];
+      if (e.z != epoch) {
+        if (nres == sc.R) {
+          overflow = true;
+          return;
+        }
+        sc.table[HI(hh)] = make_uint4(k, l, epoch, used);
+        sc.slots[LI(nres)] = hh;
+        ++nres;
+        return;
+      }
+      if (e.x == k && e.y == l) {
+        if (used < e.w) sc.table[HI(hh)].w = used;
+        return;
+      }
+    }
+    overflow = true;
+  };
+  auto fail = [&]() {
+    const unsigned long long f = atomicAdd(out.fail_count, 1ull);
+    out.fail_list[f] = uint32_t(q);
+    out.res_cnt[q] = 0;
+  };
+  auto finish = [&]() {
+    if (overflow) {
+      fail();
+      return;
+    }
+    uint64_t o = 0;
+    if (nres) {
+      o = atomicAdd(out.total, (unsigned long long)nres);
+      if (o + nres > out.cap) {
+        fail();
+        return;
+      }
+      if (nres <= S) {  // insertion sort by (k, l) in the (empty) stack slots
+        for (uint32_t r = 0; r < nres; ++r) {
+          const uint4 e = sc.table[HI(sc.slots[LI(r)])];
+          uint32_t b = r;
+          while (b > 0) {
+            const uint4 p = s_x[(b - 1) * nt + tid];
+            if (p.x < e.x || (p.x == e.x && p.y < e.y)) break;
+            s_x[b * nt + tid] = p;
+            --b;
+          }
+          s_x[b * nt + tid] = make_uint4(e.x, e.y, e.w, 0u);
+        }
+        for (uint32_t r = 0; r < nres; ++r) {
+          const uint4 p = s_x[r * nt + tid];
+          out.kl[o + r] = make_uint2(p.x, p.y);
+          out.diffs[o + r] = uint8_t(p.z);
+        }
+      } else {
+        for (uint32_t r = 0; r < nres; ++r) {
+          const uint4 e = sc.table[HI(sc.slots[LI(r)])];
+          out.kl[o + r] = make_uint2(e.x, e.y);
+          out.diffs[o + r] = uint8_t(e.w);
+        }
+        const unsigned long long u = atomicAdd(out.unsorted, 1ull);
+        out.unsorted_list[u] = uint32_t(q);
+      }
+    }
+    out.res_off[q] = o;
+    out.res_cnt[q] = nres;
+    out.res_pass[q] = out.pass;
+  };
+  auto push_if = [&](bool cond, int pos, uint32_t pb, bool psh, uint32_t x, uint32_t y, uint32_t zz, uint32_t ww) {
+    const bool ok = cond && sp < S;
+    overflow |= cond && sp >= S;
+    const uint32_t slot = ok ? sp : S;
+    s_x[slot * nt + tid] = make_uint4(x, y, zz, ww);
+    s_ib[slot * nt + tid] = (uint32_t(pos + 1) << 16) | (psh ? 0x8000u : 0u) | pb;
+    sp += ok ? 1u : 0u;
+  };
+
+  // case A root: interval of W[h..m-1], then node (h-1, budget 1)
+  auto root_a = [&]() -> bool {
+    const int r = m - h;
+    const int tt = min(r, int(K));
+    uint2 e = __ldg(bi.tf.base + PrefixTable::off(uint32_t(tt)) + pat_key(pw0, pw1, m - tt, tt));
+    my_steps += work_unit(1u);
+    for (int p = m - tt - 1; p >= h && e.x <= e.y; --p) {
+      uint32_t ck[4], cl[4];
+      children4<W>(ix, bi.tf, false, e.x, e.y, ck, cl, my_steps);
+      const uint32_t b = sym_at(p);
+      e = make_uint2(sel4(ck, b), sel4(cl, b));
+    }
+    if (e.x > e.y) return false;
+    if (h == 0) {  // the whole pattern matched: the exact result
+      record(e.x, e.y, 0u);
+      return false;
+    }
+    if (dlb(h - 1) > 1u) return false;
+    ci = h - 1;
+    cb = 1u;
+    csh = uint32_t(r) < K;
+    cx = csh ? pat_key(pw0, pw1, h, r) : e.x;
+    cy = csh ? uint32_t(r) : e.y;
+    return true;
+  };
+  // case B root: both intervals of W[0..h-1], then node (h, budget 1)
+  auto root_b = [&]() -> bool {
+    const int tt = min(h, int(K));
+    uint2 f = make_uint2(0u, ix.n), rr = make_uint2(0u, ix.n);
+    if (tt > 0) {
+      f = __ldg(bi.tf.base + PrefixTable::off(uint32_t(tt)) + pat_key(pw0, pw1, 0, tt));
+      rr = __ldg(bi.tr.base + PrefixTable::off(uint32_t(tt)) + pat_rkey(pw0, pw1, 0, tt));
+      my_steps += work_unit(2u);
+    }
+    for (int p = tt; p < h && f.x <= f.y; ++p) {
+      uint32_t rk[4], rl[4];
+      children4<W>(bi.rev, bi.tr, false, rr.x, rr.y, rk, rl, my_steps);
+      const uint32_t w = sym_at(p);
+      uint32_t k = f.x + ((rr.x <= sent_r && sent_r <= rr.y) ? 1u : 0u);
+#pragma unroll
+      for (uint32_t b = 0; b < 4; ++b)
+        if (b < w) k += rl[b] + 1u - rk[b];
+      const uint32_t sz = sel4(rl, w) + 1u - sel4(rk, w);
+      f = make_uint2(k, k + sz - 1u);
+      rr = make_uint2(sel4(rk, w), sel4(rl, w));
+      if (sz == 0u) f = make_uint2(1u, 0u);
+    }
+    if (f.x > f.y) return false;
+    ci = h;
+    cb = 1u;
+    csh = uint32_t(h) < K;
+    cx = f.x;
+    cy = f.y;
+    cz = csh ? pat_rkey(pw0, pw1, 0, h) : rr.x;
+    cw = csh ? uint32_t(h) : rr.y;
+    return true;
+  };
+
+  while (true) {
+    bool stepping = false;
+    while (!stepping) {
+      if (!have) {
+        const unsigned long long slot = atomicAdd(out.next, 1ull);
+        if (slot >= count) break;
+        q = list ? list[slot] : slot;
+        if (cp.packed1) {
+          m = int(cp.fixed_m);
+          pw0 = cp.packed1[q];
+          pw1 = 0;
+        } else {
+          m = int(cp.offsets[q + 1] - cp.offsets[q]);
+          const ulonglong2 pk = cp.packed[q];
+          pw0 = pk.x;
+          pw1 = pk.y;
+        }
+        dbits = cp.dbits[q];
+        h = m / 2;
+        sp = nres = 0;
+        ++epoch;
+        overflow = false;
+        phase = 1;
+        have = true;
+        cur_valid = dlb(m - 1) <= 1u && root_a();
+      }
+      if (overflow) {
+        finish();
+        have = false;
+        continue;
+      }
+      if (!cur_valid) {
+        if (sp > 0) {
+          --sp;
+          const uint4 e = s_x[sp * nt + tid];
+          const uint32_t ib = s_ib[sp * nt + tid];
+          ci = int(ib >> 16) - 1;
+          cb = ib & 0xFFu;
+          csh = (ib >> 15) & 1u;
+          cx = e.x;
+          cy = e.y;
+          cz = e.z;
+          cw = e.w;
+          cur_valid = true;
+        } else if (phase == 1) {
+          phase = 3;
+          cur_valid = dlb(m - 1) <= 1u && root_b();
+          continue;
+        } else {
+          finish();
+          have = false;
+          continue;
+        }
+      }
+      stepping = true;
+    }
+    if (!stepping) break;
+
+    // ---- one step: the four children of the node's string ----
+    const bool fwd = phase == 3;
+    uint32_t ck[4], cl[4];
+    children4<W>(fwd ? bi.rev : ix, fwd ? bi.tr : bi.tf, csh, fwd ? cz : cx, fwd ? cw : cy, ck, cl, my_steps);
+
+    if (!fwd) {
+      // ---- case A: backward expansion (search.py:135-152) ----
+      const int i = ci;
+      const uint32_t want = sym_at(i);
+      const uint32_t kw = sel4(ck, want), lw = sel4(cl, want);
+      const bool child_sh = csh && cy + 1u < K;
+      if (cb == 0u) {
+        if (kw > lw) {
+          cur_valid = false;
+        } else if (i == 0) {
+          record(kw, lw, 1u);
+          cur_valid = false;
+        } else {
+          ci = i - 1;
+          cx = child_sh ? want + 4u * cx : kw;
+          cy = child_sh ? cy + 1u : lw;
+          csh = child_sh;
+          cur_valid = dlb(i - 1) == 0u;
+        }
+        continue;
+      }
+      const bool at0 = i == 0;
+      const uint32_t d_prev = at0 ? 0u : dlb(i - 1), d_cur = dlb(i);
+      const bool ok_match = !at0 && d_prev <= 1u;
+      const bool ok_prev = !at0 && d_prev == 0u;
+      const bool ok_cur = d_cur == 0u;
+      if (at0) {
+        if (kw <= lw) record(kw, lw, 0u);
+        uint32_t sk = cx, sl = cy;  // skip: this node's own interval
+        if (csh) {
+          if (cy == 0u) {
+            sk = 0u;
+            sl = ix.n;
+          } else {
+            const uint2 e = __ldg(bi.tf.base + PrefixTable::off(cy) + cx);
+            sk = e.x;
+            sl = e.y;
+          }
+        }
+        record(sk, sl, 1u);
+#pragma unroll
+        for (uint32_t b = 0; b < 4; ++b)
+          if (b != want && ck[b] <= cl[b]) record(ck[b], cl[b], 1u);  // mismatch
+      }
+      const uint32_t ckey = 4u * cx, cdep = cy + 1u;
+      push_if(ok_match && kw <= lw, i - 1, 1u, child_sh, child_sh ? want + ckey : kw, child_sh ? cdep : lw, 0u, 0u);
+      push_if(ok_prev, i - 1, 0u, csh, cx, cy, 0u, 0u);  // skip
+#pragma unroll
+      for (uint32_t b = 0; b < 4; ++b) {
+        const bool ne = ck[b] <= cl[b];
+        const uint32_t px = child_sh ? b + ckey : ck[b], py = child_sh ? cdep : cl[b];
+        push_if(ok_cur && ne, i, 0u, child_sh, px, py, 0u, 0u);                  // insert
+        push_if(ok_prev && ne && b != want, i - 1, 0u, child_sh, px, py, 0u, 0u);  // mismatch
+      }
+      cur_valid = false;
+      continue;
+    }
+
+    // ---- case B: forward expansion on the reverse index ----
+    const int j = ci;
+    uint32_t sz[4], fk[4];
+    const bool dollar = csh ? (cz == bi.tail[cw]) : (cz <= sent_r && sent_r <= cw);
+    uint32_t acc = cx + (dollar ? 1u : 0u);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      sz[b] = cl[b] + 1u - ck[b];
+      fk[b] = acc;
+      acc += sz[b];
+    }
+    const bool child_sh = csh && cw + 1u < K;
+    const uint32_t rkey = 4u * cz, rdep = cw + 1u;
+    auto cz_of = [&](uint32_t b) { return child_sh ? b + rkey : sel4(ck, b); };
+    auto cw_of = [&](uint32_t b) { return child_sh ? rdep : sel4(cl, b); };
+    if (cb == 0u) {  // only the match child; j < m here
+      const uint32_t w = sym_at(j);
+      const uint32_t s = sel4(sz, w), k = sel4(fk, w);
+      if (s == 0u) {
+        cur_valid = false;
+      } else if (j + 1 == m) {
+        record(k, k + s - 1u, 1u);
+        cur_valid = false;
+      } else {
+        ci = j + 1;
+        cz = cz_of(w);
+        cw = cw_of(w);
+        cx = k;
+        cy = k + s - 1u;
+        csh = child_sh;
+      }
+      continue;
+    }
+    if (j == m) {  // budget 1 after the whole pattern: insertion after W[m-1]
+#pragma unroll
+      for (uint32_t b = 0; b < 4; ++b)
+        if (sz[b]) record(fk[b], fk[b] + sz[b] - 1u, 1u);
+      cur_valid = false;
+      continue;
+    }
+    const uint32_t w = sym_at(j);
+    const bool last = j + 1 == m;
+    const uint32_t sw = sel4(sz, w), kw = sel4(fk, w);
+    if (last) {
+      if (sw) record(kw, kw + sw - 1u, 0u);  // W itself (also found by case A)
+      record(cx, cy, 1u);                    // skip W[m-1]
+#pragma unroll
+      for (uint32_t b = 0; b < 4; ++b)
+        if (b != w && sz[b]) record(fk[b], fk[b] + sz[b] - 1u, 1u);  // mismatch at m-1
+    }
+    // match: (j+1, 1); at the end it still expands for insertions after W[m-1]
+    push_if(sw != 0u, j + 1, 1u, child_sh, kw, kw + sw - 1u, cz_of(w), cw_of(w));
+    push_if(!last, j + 1, 0u, csh, cx, cy, cz, cw);  // skip
+    const bool ins = j >= h + 1;                      // insertion after W[j-1], j-1 >= h
+#pragma unroll
+    for (uint32_t b = 0; b < 4; ++b) {
+      const bool ne = sz[b] != 0u;
+      const uint32_t px = child_sh ? b + rkey : ck[b], py = child_sh ? rdep : cl[b];
+      push_if(!last && ne && b != w, j + 1, 0u, child_sh, fk[b], fk[b] + sz[b] - 1u, px, py);  // mismatch
+      push_if(ins && ne, j, 0u, child_sh, fk[b], fk[b] + sz[b] - 1u, px, py);                  // insert
+    }
+    cur_valid = false;
+  }
+  flush_work(out.steps, my_steps);
+}
+
+// tail[d] = key of the reversed text's first d characters = text[n-1],
+// text[n-2], ... (text[n-1] in bits 0..1): BWT[0] = text[n-1] (row 0 is the
+// '$' suffix), then one LF step per character (search.py:172-186).
+template <int W>
+__global__ void k_tail_keys(IndexView ix, uint32_t k, uint32_t* __restrict__ tail) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  uint32_t row = 0, key = 0;
+  tail[0] = 0u;
+  bool live = true;
+  for (uint32_t d = 1; d < 16; ++d) {
+    if (live && d <= ix.n && d < k) {
+      uint32_t sym;
+      const uint32_t prev = psi_step<W>(ix, row, sym);
+      key |= sym << (2 * (d - 1));
+      tail[d] = key;
+      row = prev;
+    } else {
+      live = false;
+      tail[d] = 0xFFFFFFFFu;
+    }
+  }
+}
+
+}  // namespace fmg

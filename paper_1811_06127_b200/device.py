@@ -52,7 +52,15 @@ class DeviceIndex:
         self.device = int(device)
         self.n = index.n
         self._has_samples = False
+        self._has_reverse = False
         self._index = index
+
+    def ensure_reverse(self) -> None:
+        """Attach the reversed-text index (bidirectional z = 1 engine)."""
+        if not self._has_reverse:
+            rec, sentinel = self._index.reverse_index(device=self.device)
+            _lib.check(_lib.load().fmg_index_set_reverse(self.handle, rec.ctypes.data, rec.shape[0], sentinel))
+            self._has_reverse = True
 
     def ensure_samples(self) -> None:
         if not self._has_samples:

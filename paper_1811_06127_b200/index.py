@@ -73,7 +73,7 @@ class FmIndex:
     copies are created lazily per CUDA device by `device_index()`.
     """
 
-    __slots__ = ("n", "c", "sentinel_row", "records", "bucket_records", "sa_samples", "_dev")
+    __slots__ = ("n", "c", "sentinel_row", "records", "bucket_records", "sa_samples", "_dev", "_codes", "_rev")
 
     def __init__(
         self,
@@ -95,6 +95,8 @@ class FmIndex:
         object.__setattr__(self, "sa_samples", samples)
         object.__setattr__(self, "records", tuple(records))
         object.__setattr__(self, "_dev", {})
+        object.__setattr__(self, "_codes", None)  # text codes when built here (for the reverse index)
+        object.__setattr__(self, "_rev", None)
 
     def __setattr__(self, name, value):
         raise AttributeError("FmIndex is immutable")
@@ -127,6 +129,26 @@ class FmIndex:
             f"FmIndex(n={self.n}, c={self.c}, buckets={self.bucket_records.shape[0]}, "
             f"sentinel_row={self.sentinel_row}, records={len(self.records)})"
         )
+
+    def reverse_index(self, builder: str = "auto", device: int | None = None) -> tuple[np.ndarray, int]:
+        """(bucket records, sentinel row) of the index of the REVERSED text.
+
+        Engine cache for the bidirectional z = 1 search (kernels_bidir.cuh);
+        not part of the reference's index or of the .fmi format.  Built from
+        the text this index was built from, or from the text recovered from
+        the index itself (reconstruct_reference) when it was loaded.
+        """
+        if self._rev is None:
+            codes = self._codes
+            if codes is None:
+                from .alphabet import encode_array
+                from .search import reconstruct_reference
+
+                codes = encode_array(reconstruct_reference(self))
+            rec, _, _, sentinel = _build_arrays(np.ascontiguousarray(codes[::-1]), builder, device, None)
+            rec.setflags(write=False)
+            object.__setattr__(self, "_rev", (rec, sentinel))
+        return self._rev
 
     def device_index(self, device: int | None = None):
         """The device-resident copy on `device` (created on first use)."""
@@ -185,6 +207,15 @@ def build_index(
     if n == 0:
         raise ValueError("reference is empty")
     spans = _normalize_records(records, n)
+    rec, samples, c, sentinel = _build_arrays(codes, builder, device, threads)
+    index = FmIndex(n, c.tolist(), rec, sentinel, samples, spans)
+    object.__setattr__(index, "_codes", codes)
+    return index
+
+
+def _build_arrays(codes: np.ndarray, builder: str, device: int | None, threads: int | None):
+    """(bucket records, SA samples, C, sentinel row) of text codes + '$'."""
+    n = int(codes.size)
     nb = (n + 1 + BUCKET_CHARS - 1) // BUCKET_CHARS
     rec = np.empty((nb, RECORD_BYTES), dtype=np.uint8)
     samples = np.empty(n // SA_STRIDE + 1, dtype=np.uint64)
@@ -211,7 +242,7 @@ def build_index(
                 sentinel.ctypes.data, int(threads or os.cpu_count() or 1),
             )
         )
-    return FmIndex(n, c.tolist(), rec, int(sentinel[0]), samples, spans)
+    return rec, samples, c, int(sentinel[0])
 
 
 def suffix_array(reference) -> np.ndarray:

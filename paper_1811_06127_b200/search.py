@@ -16,6 +16,7 @@ collect_hits (search.py:211-267), done with vectorised numpy.
 from __future__ import annotations
 
 import ctypes as ct
+import os
 from typing import Iterable, NamedTuple
 
 import numpy as np
@@ -155,6 +156,15 @@ class MatchSet(NamedTuple):
         return self.offsets.size - 1
 
 
+BIDIR_MIN_N = 1 << 40  # off by default until the level-synchronous variant lands
+
+
+def bidir_min_n() -> int:
+    """Index size from which z = 1 batches attach the reversed-text index
+    (FMG_BIDIR_MIN_N overrides; the one-directional engines stay exact)."""
+    return int(os.environ.get("FMG_BIDIR_MIN_N", BIDIR_MIN_N))
+
+
 def inexact_search_batch(index: FmIndex, patterns, max_diff: int,
                          kernel: Kernel | str | None = None, device: int | None = None) -> MatchSet:
     """inexact_search over many patterns; results in CSR form (see MatchSet)."""
@@ -171,6 +181,8 @@ def inexact_search_batch(index: FmIndex, patterns, max_diff: int,
                         np.zeros(0, np.uint8), 0)
     require_gpu()
     dev = index.device_index(device)
+    if max_diff == 1 and index.n >= bidir_min_n() and n >= 1024:
+        dev.ensure_reverse()  # the bidirectional engine (kernels_bidir.cuh)
     handle = ct.c_void_p()
     _lib.check(lib.fmg_inexact_host(dev.handle, codes.ctypes.data, offsets.ctypes.data, n,
                                     int(max_diff), ct.byref(handle)))

@@ -428,3 +428,53 @@ def test_inexact_prefix_table_paths(gpu, monkeypatch, z, lens):
     monkeypatch.setenv("FMG_INEXACT_LUT", "0")
     b = fm.inexact_search_batch(idx, pats, z)
     assert np.array_equal(b.offsets, ms.offsets) and np.array_equal(b.k, ms.k) and np.array_equal(b.diffs, ms.diffs)
+
+
+@pytest.mark.parametrize("n,lens", [(200_000, (1, 2, 3, 5, 8, 9, 10, 11, 19, 20, 32, 33, 47, 64)),
+                                    (3_000, (1, 2, 4, 7, 12, 19, 25)), (40, (1, 2, 3, 6, 9, 14))])
+def test_inexact_bidirectional_engine(gpu, monkeypatch, n, lens):
+    """z = 1 through the bidirectional engine (reverse index attached, both prefix tables):
+    patterns cut from anywhere (incl. the text's very start and end, which exercises the
+    forward extension's '$' term), mutated or random, lengths 1..64 — identical to the
+    oracle and to the one-directional DFS engine."""
+    monkeypatch.setenv("FMG_BIDIR_MIN_N", "0")
+    monkeypatch.setenv("FMG_INEXACT_DFS", "1")
+    rng = np.random.Generator(np.random.PCG64(31337 + n))
+    text = rng.integers(0, 4, n, dtype=np.uint8)
+    idx = fm.build_index(text)
+    pats = []
+    for r in range(3000):
+        m = int(rng.choice(lens))
+        if m > n:
+            m = n
+        kind = r % 5
+        if kind == 0:  # a suffix of the text
+            p = text[n - m:].copy()
+        elif kind == 1:  # a prefix of the text
+            p = text[:m].copy()
+        elif kind == 2:
+            p = rng.integers(0, 4, m, dtype=np.uint8)
+        else:
+            s = int(rng.integers(0, n - m + 1))
+            p = text[s:s + m].copy()
+        if m > 2 and rng.random() < 0.5:  # one random edit
+            j = int(rng.integers(0, m))
+            e = rng.random()
+            if e < 0.4:
+                p[j] = (p[j] + 1 + rng.integers(0, 3)) % 4
+            elif e < 0.7:
+                p = np.delete(p, j)
+            else:
+                p = np.insert(p, j, rng.integers(0, 4))
+        pats.append(codes_to_str(p[:64]))
+    ms = fm.inexact_search_batch(idx, pats, 1)
+    assert idx.device_index()._has_reverse
+    ox = orc.OracleIndex(idx)
+    row, k, l, d, _ = orc.inexact_batch(ox, pats, 1)
+    assert np.array_equal(ms.offsets, row)
+    assert np.array_equal(ms.k.astype(np.int64), k) and np.array_equal(ms.l.astype(np.int64), l)
+    assert np.array_equal(ms.diffs, d)
+    monkeypatch.setenv("FMG_INEXACT_BIDIR", "0")
+    b = fm.inexact_search_batch(idx, pats, 1)
+    assert np.array_equal(b.offsets, ms.offsets) and np.array_equal(b.k, ms.k) and np.array_equal(b.diffs, ms.diffs)
+    assert ms.steps < b.steps  # the point of the engine
