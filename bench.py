@@ -395,6 +395,14 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
     units = unit_count(wl)
     metric, unit = metric_of(args.config)
     extra: dict = {"index_build_s": round(t_build, 2), "index_device_bytes": dix.device_bytes}
+    if wl.max_diff == 1 and wl.pairs is None:
+        from paper_1811_06127_b200.search import bidir_min_n
+
+        if idx.n >= bidir_min_n():  # the reversed-text index of the bidirectional z = 1 engine
+            t_rev = time.perf_counter()
+            dix.ensure_reverse()
+            extra["reverse_index_build_s"] = round(time.perf_counter() - t_rev, 2)
+            extra["engine"] = "bidirectional z=1 (case-A / case-B DFS launches + merge)"
     if wl.pairs is None:  # search configs: the k-mer / prefix interval table, built before timing
         fn = lib.fmgx_prefix_table
         fn.argtypes = [ct.c_void_p, ct.POINTER(ct.c_uint32), ct.POINTER(ct.c_uint64)]

@@ -401,6 +401,55 @@ uint64_t validate_patterns_device(const uint8_t* codes, const uint64_t* offsets,
 
 // z = 1 through k_spine / k_chain; false when a queue overflowed (the caller
 // then runs the DFS engine, which has no such limit).  Fills res on success.
+// Raw (pattern, k, l, used) results -> the CSR result set of `res`:
+// counting sort by pattern, per-pattern sort by (k, l), keep the smallest
+// `used` per interval (search.py:127-134, 153-159).
+void z1_collect(Z1Raw* raws, uint64_t n_raw, uint64_t count, cudaStream_t s, unsigned long long* steps,
+                fmg_matches* res) {
+  // group raw results by pattern (counting sort), sort each segment by (k, l)
+  DevBuf<uint32_t> per_q(count, s);
+  DevBuf<uint64_t> seg(count + 1, s), cursor(count, s), c64(count, s);
+  FMG_CK(cudaMemsetAsync(per_q.ptr, 0, count * 4, s));
+  FMG_CK(cudaMemsetAsync(seg.ptr, 0, 8, s));
+  if (n_raw) k_z1_hist<<<unsigned((n_raw + 255) / 256), 256, 0, s>>>(raws, n_raw, per_q.ptr);
+  k_widen_counts<<<unsigned((count + 255) / 256), 256, 0, s>>>(count, per_q.ptr, c64.ptr);
+  size_t tb = 0;
+  FMG_CK(cub::DeviceScan::InclusiveSum(nullptr, tb, c64.ptr, seg.ptr + 1, count, s));
+  DevBuf<uint8_t> tmp(tb, s);
+  FMG_CK(cub::DeviceScan::InclusiveSum(tmp.ptr, tb, c64.ptr, seg.ptr + 1, count, s));
+  FMG_CK(cudaMemcpyAsync(cursor.ptr, seg.ptr, count * 8, cudaMemcpyDeviceToDevice, s));
+  const uint64_t nr = std::max<uint64_t>(n_raw, 1);
+  DevBuf<uint64_t> keys(nr, s), keys2(nr, s);
+  DevBuf<uint8_t> used(nr, s), used2(nr, s);
+  if (n_raw) {
+    k_z1_scatter<<<unsigned((n_raw + 255) / 256), 256, 0, s>>>(raws, n_raw, cursor.ptr, keys.ptr, used.ptr);
+    FMG_REQUIRE(n_raw < (1ull << 31), "too many inexact results for one call");
+    size_t sb = 0;
+    FMG_CK(cub::DeviceSegmentedSort::SortPairs(nullptr, sb, keys.ptr, keys2.ptr, used.ptr, used2.ptr, int(n_raw),
+                                               int(count), seg.ptr, seg.ptr + 1, s));
+    DevBuf<uint8_t> stmp(sb, s);
+    FMG_CK(cub::DeviceSegmentedSort::SortPairs(stmp.ptr, sb, keys.ptr, keys2.ptr, used.ptr, used2.ptr, int(n_raw),
+                                               int(count), seg.ptr, seg.ptr + 1, s));
+  }
+  k_z1_unique_count<<<unsigned((count + 255) / 256), 256, 0, s>>>(keys2.ptr, used2.ptr, seg.ptr, count, per_q.ptr);
+  k_widen_counts<<<unsigned((count + 255) / 256), 256, 0, s>>>(count, per_q.ptr, c64.ptr);
+  FMG_CK(cub::DeviceScan::InclusiveSum(tmp.ptr, tb, c64.ptr, res->row_off + 1, count, s));
+  uint64_t total = 0;
+  FMG_CK(cudaMemcpyAsync(&total, res->row_off + count, 8, cudaMemcpyDeviceToHost, s));
+  unsigned long long st[2] = {0, 0};
+  FMG_CK(cudaMemcpyAsync(st, steps, sizeof(st), cudaMemcpyDeviceToHost, s));
+  FMG_CK(cudaStreamSynchronize(s));
+  res->total = total;
+  res->steps = st[0];
+  res->lines = st[1];
+  FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->k), std::max<uint64_t>(total, 1) * 4, s));
+  FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->l), std::max<uint64_t>(total, 1) * 4, s));
+  FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->diffs), std::max<uint64_t>(total, 1), s));
+  k_z1_unique_write<<<unsigned((count + 255) / 256), 256, 0, s>>>(keys2.ptr, used2.ptr, seg.ptr, res->row_off,
+                                                                  count, res->k, res->l, res->diffs);
+  FMG_CK(cudaGetLastError());
+}
+
 bool run_z1(const fmg_index* ix, const CodePatterns& cp, uint64_t count, uint64_t m, cudaStream_t s,
             unsigned long long* steps, fmg_matches* res) {
   static const bool trace = std::getenv("FMG_TRACE") != nullptr;
@@ -444,47 +493,8 @@ bool run_z1(const fmg_index* ix, const CodePatterns& cp, uint64_t count, uint64_
   FMG_CK(cudaStreamSynchronize(s));
   if (n_raw > raw_cap) return false;
   if (trace) cudaEventRecord(ev[2], s);
-  // group raw results by pattern (counting sort), sort each segment by (k, l)
-  DevBuf<uint32_t> per_q(count, s);
-  DevBuf<uint64_t> seg(count + 1, s), cursor(count, s), c64(count, s);
-  FMG_CK(cudaMemsetAsync(per_q.ptr, 0, count * 4, s));
-  FMG_CK(cudaMemsetAsync(seg.ptr, 0, 8, s));
-  if (n_raw) k_z1_hist<<<unsigned((n_raw + 255) / 256), 256, 0, s>>>(raws.ptr, n_raw, per_q.ptr);
-  k_widen_counts<<<unsigned((count + 255) / 256), 256, 0, s>>>(count, per_q.ptr, c64.ptr);
-  size_t tb = 0;
-  FMG_CK(cub::DeviceScan::InclusiveSum(nullptr, tb, c64.ptr, seg.ptr + 1, count, s));
-  DevBuf<uint8_t> tmp(tb, s);
-  FMG_CK(cub::DeviceScan::InclusiveSum(tmp.ptr, tb, c64.ptr, seg.ptr + 1, count, s));
-  FMG_CK(cudaMemcpyAsync(cursor.ptr, seg.ptr, count * 8, cudaMemcpyDeviceToDevice, s));
-  const uint64_t nr = std::max<uint64_t>(n_raw, 1);
-  DevBuf<uint64_t> keys(nr, s), keys2(nr, s);
-  DevBuf<uint8_t> used(nr, s), used2(nr, s);
-  if (n_raw) {
-    k_z1_scatter<<<unsigned((n_raw + 255) / 256), 256, 0, s>>>(raws.ptr, n_raw, cursor.ptr, keys.ptr, used.ptr);
-    FMG_REQUIRE(n_raw < (1ull << 31), "too many inexact results for one call");
-    size_t sb = 0;
-    FMG_CK(cub::DeviceSegmentedSort::SortPairs(nullptr, sb, keys.ptr, keys2.ptr, used.ptr, used2.ptr, int(n_raw),
-                                               int(count), seg.ptr, seg.ptr + 1, s));
-    DevBuf<uint8_t> stmp(sb, s);
-    FMG_CK(cub::DeviceSegmentedSort::SortPairs(stmp.ptr, sb, keys.ptr, keys2.ptr, used.ptr, used2.ptr, int(n_raw),
-                                               int(count), seg.ptr, seg.ptr + 1, s));
-  }
-  k_z1_unique_count<<<unsigned((count + 255) / 256), 256, 0, s>>>(keys2.ptr, used2.ptr, seg.ptr, count, per_q.ptr);
-  k_widen_counts<<<unsigned((count + 255) / 256), 256, 0, s>>>(count, per_q.ptr, c64.ptr);
-  FMG_CK(cub::DeviceScan::InclusiveSum(tmp.ptr, tb, c64.ptr, res->row_off + 1, count, s));
-  uint64_t total = 0;
-  FMG_CK(cudaMemcpyAsync(&total, res->row_off + count, 8, cudaMemcpyDeviceToHost, s));
-  unsigned long long st[2] = {0, 0};
-  FMG_CK(cudaMemcpyAsync(st, steps, sizeof(st), cudaMemcpyDeviceToHost, s));
-  FMG_CK(cudaStreamSynchronize(s));
-  res->total = total;
-  res->steps = st[0];
-  res->lines = st[1];
-  FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->k), std::max<uint64_t>(total, 1) * 4, s));
-  FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->l), std::max<uint64_t>(total, 1) * 4, s));
-  FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->diffs), std::max<uint64_t>(total, 1), s));
-  k_z1_unique_write<<<unsigned((count + 255) / 256), 256, 0, s>>>(keys2.ptr, used2.ptr, seg.ptr, res->row_off,
-                                                                  count, res->k, res->l, res->diffs);
+  z1_collect(raws.ptr, n_raw, count, s, steps, res);
+  uint64_t total = res->total;
   FMG_CK(cudaGetLastError());
   if (trace) cudaEventRecord(ev[3], s);
   FMG_CK(cudaStreamSynchronize(s));
@@ -496,6 +506,73 @@ bool run_z1(const fmg_index* ix, const CodePatterns& cp, uint64_t count, uint64_
     fprintf(stderr, "[fmg] z1 engine: %llu patterns, spine+queue %.3f ms (%llu continuations), chains %.3f ms, "
             "dedup/sort %.3f ms (%llu raw -> %llu results)\n", (unsigned long long)count, a, n_nodes, b, c,
             n_raw, (unsigned long long)total);
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+  return true;
+}
+
+// The level-synchronous bidirectional z = 1 engine (kernels_bidir.cuh):
+// patterns in chunks sized so the worst case of 8 continuations per spine
+// node always fits the node queue; raw results of all chunks are collected
+// once.  Returns false (caller falls back to the DFS engines) only if the
+// raw-result buffer overflowed.
+bool run_z1b(const fmg_index* ix, const BiIndex& bi, const CodePatterns& cp, uint64_t count, uint64_t m,
+             cudaStream_t s, unsigned long long* steps, fmg_matches* res) {
+  static const bool trace = std::getenv("FMG_TRACE") != nullptr;
+  cudaEvent_t ev[3] = {};
+  if (trace)
+    for (auto& e : ev) cudaEventCreate(&e);
+  if (trace) cudaEventRecord(ev[0], s);
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = size_t(8) << 30;
+  const uint64_t per = 8 * (m + 1);
+  const uint64_t node_budget = std::max<uint64_t>(per, free_b / 4 / sizeof(Z1BNode));
+  const uint64_t chunk = std::min<uint64_t>(count, std::max<uint64_t>(1, node_budget / per));
+  const uint64_t node_cap = chunk * per;
+  const uint64_t raw_cap = std::min<uint64_t>(count * (per + 17), std::max<uint64_t>(1u << 20, free_b / 8 / sizeof(Z1Raw)));
+  DevBuf<Z1BNode> nodes(node_cap, s);
+  DevBuf<Z1Raw> raws(raw_cap, s);
+  DevBuf<unsigned long long> ctr(2, s);
+  FMG_CK(cudaMemsetAsync(ctr.ptr, 0, 16, s));
+  Z1BQueues qu{nodes.ptr, ctr.ptr, node_cap, raws.ptr, ctr.ptr + 1, raw_cap};
+  unsigned long long total_nodes = 0;
+  for (uint64_t q0 = 0; q0 < count; q0 += chunk) {
+    const uint64_t c = std::min<uint64_t>(chunk, count - q0);
+    FMG_CK(cudaMemsetAsync(ctr.ptr, 0, 8, s));
+    with_words(ix, [&](auto wt) {
+      constexpr int W = decltype(wt)::value;
+      k_bspine<W><<<unsigned((c + 255) / 256), 256, 0, s>>>(ix->view(), bi, cp, q0, c, qu, steps);
+    });
+    FMG_CK(cudaGetLastError());
+    unsigned long long n_nodes = 0;
+    FMG_CK(cudaMemcpyAsync(&n_nodes, ctr.ptr, 8, cudaMemcpyDeviceToHost, s));
+    FMG_CK(cudaStreamSynchronize(s));
+    FMG_REQUIRE(n_nodes <= node_cap, "bidirectional node queue overflow");  // impossible by sizing
+    total_nodes += n_nodes;
+    if (n_nodes) {
+      with_words(ix, [&](auto wt) {
+        constexpr int W = decltype(wt)::value;
+        const unsigned nb = persistent_blocks(ix, (const void*)k_bchain<W>, 256, n_nodes);
+        k_bchain<W><<<nb, 256, 0, s>>>(ix->view(), bi, cp, nodes.ptr, n_nodes, qu, steps);
+      });
+      FMG_CK(cudaGetLastError());
+    }
+  }
+  unsigned long long n_raw = 0;
+  FMG_CK(cudaMemcpyAsync(&n_raw, ctr.ptr + 1, 8, cudaMemcpyDeviceToHost, s));
+  FMG_CK(cudaStreamSynchronize(s));
+  if (n_raw > raw_cap) return false;
+  if (trace) cudaEventRecord(ev[1], s);
+  z1_collect(raws.ptr, n_raw, count, s, steps, res);
+  if (trace) {
+    cudaEventRecord(ev[2], s);
+    cudaEventSynchronize(ev[2]);
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    fprintf(stderr, "[fmg] z1 bidirectional engine: %llu patterns in chunks of %llu, spines+chains %.3f ms "
+            "(%llu continuations), dedup/sort %.3f ms (%llu raw -> %llu results)\n", (unsigned long long)count,
+            (unsigned long long)chunk, a, total_nodes, b, n_raw, (unsigned long long)res->total);
     for (auto& e : ev) cudaEventDestroy(e);
   }
   return true;
@@ -588,7 +665,22 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       bidir = bi.tr.base != nullptr;
     }
     const void* kfn_bi = nullptr;
-    with_words(ix, [&](auto wt) { kfn_bi = (const void*)k_inexact_bi<decltype(wt)::value>; });
+    with_words(ix, [&](auto wt) { kfn_bi = (const void*)k_inexact_bi<decltype(wt)::value, 0>; });
+    // bidirectional forms: "split" (default: phase-uniform case-A and case-B
+    // DFS launches + merge), "dfs" (both cases per thread), "sync"
+    // (level-synchronous spine + chain kernels); FMG_BIDIR_ENGINE selects.
+    const std::string bidir_engine = [] {
+      const char* e = std::getenv("FMG_BIDIR_ENGINE");
+      return std::string(e ? e : "split");
+    }();
+    const bool bidir_dfs = bidir_engine == "dfs";
+    bool bidir_split = bidir && bidir_engine == "split";
+    if (bidir && bidir_engine == "sync") {
+      CodePatterns cpz{codes, offsets, packed.ptr, packed1, uint32_t(max_len), dbits.ptr};
+      if (run_z1b(ix, bi, cpz, count, max_len, s, counters.ptr + 2, res)) return res;
+      // raw-result buffer overflowed: fall through (same results)
+      FMG_CK(cudaMemsetAsync(counters.ptr + 2, 0, 2 * sizeof(unsigned long long), s));
+    }
     std::vector<DevBuf<uint2>> pass_kl;
     std::vector<DevBuf<uint8_t>> pass_d;
     DevBuf<uint32_t> lists[2] = {DevBuf<uint32_t>(count, s), DevBuf<uint32_t>(count, s)};
@@ -612,9 +704,130 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     // (config 3: S = 20 -> 667 ms, S = 10 -> 447 ms per 14M seeds).
     uint32_t S = std::min<uint32_t>(S_max, 9 * z + 2);
     if (const char* e = std::getenv("FMG_STACK_S")) S = std::max<uint32_t>(2, uint32_t(std::atoi(e)));  // A/B
-    for (int pass = 0; pending > 0; ++pass) {
+    int first_pass = 0;
+    DevBuf<uint32_t> retry_list;
+    if (bidir_split) {
+      // ---- pass 0 = case-A launch + case-B launch + merge (kernels_bidir.cuh) ----
+      const uint32_t Sp = 9;  // z = 1: one budget-1 node's children at a time
+      const size_t ebytes = 20;
+      const int nt = 128;
+      const size_t smem = size_t(Sp + 1) * ebytes * nt;
+      FMG_REQUIRE(smem <= size_t(smem_optin), "inexact search stack does not fit in shared memory");
+      const void* kA = nullptr;
+      const void* kB = nullptr;
+      with_words(ix, [&](auto wt) {
+        kA = (const void*)k_inexact_bi<decltype(wt)::value, 1>;
+        kB = (const void*)k_inexact_bi<decltype(wt)::value, 3>;
+      });
+      FMG_CK(cudaFuncSetAttribute(kA, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      FMG_CK(cudaFuncSetAttribute(kB, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      int per_sm = 0;
+      FMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kA, nt, smem));
+      per_sm = std::max(per_sm, 1);
+      const uint64_t per_thread = uint64_t(R) * (2 * 16 + 4);
+      uint64_t T = uint64_t(per_sm) * ix->sms * nt;
+      T = std::min<uint64_t>(T, std::max<uint64_t>(nt, std::max<uint64_t>(2ull << 30, free_b / 8) / per_thread));
+      T = std::min<uint64_t>(T, ((count + nt - 1) / nt) * nt);
+      T = std::max<uint64_t>(nt, (T / nt) * nt);
+      DevBuf<uint4> table(uint64_t(2 * R) * T, s);
+      DevBuf<uint32_t> slots(uint64_t(R) * T, s);
+      InexactScratch sc{};
+      sc.table = table.ptr;
+      sc.slots = slots.ptr;
+      sc.S = Sp;
+      sc.R = R;
+      sc.Mmax = uint32_t(max_len);
+      sc.T = T;
+      const uint64_t cap_h = std::max<uint64_t>(1u << 20, cap / 2);
+      DevBuf<uint2> klh[2] = {DevBuf<uint2>(cap_h, s), DevBuf<uint2>(cap_h, s)};
+      DevBuf<uint8_t> dh[2] = {DevBuf<uint8_t>(cap_h, s), DevBuf<uint8_t>(cap_h, s)};
+      DevBuf<uint64_t> offh[2] = {DevBuf<uint64_t>(count, s), DevBuf<uint64_t>(count, s)};
+      DevBuf<uint32_t> cnth[2] = {DevBuf<uint32_t>(count, s), DevBuf<uint32_t>(count, s)};
+      DevBuf<uint8_t> passh(count, s);
+      CodePatterns cp{codes, offsets, packed.ptr, packed1, uint32_t(max_len), dbits.ptr};
+      bool too_big_any = false;
+      for (int half = 0; half < 2; ++half) {
+        FMG_CK(cudaMemsetAsync(table.ptr, 0, uint64_t(2 * R) * T * sizeof(uint4), s));  // epoch 0 = empty
+        FMG_CK(cudaMemsetAsync(counters.ptr, 0, 2 * sizeof(unsigned long long), s));
+        FMG_CK(cudaMemsetAsync(counters.ptr + 4, 0, 2 * sizeof(unsigned long long), s));
+        InexactOut o{};
+        o.kl = klh[half].ptr;
+        o.diffs = dh[half].ptr;
+        o.total = counters.ptr;
+        o.cap = cap_h;
+        o.res_off = offh[half].ptr;
+        o.res_cnt = cnth[half].ptr;
+        o.res_pass = passh.ptr;
+        o.pass = 0;
+        o.fail_list = lists[0].ptr;
+        o.fail_count = counters.ptr + 1;
+        o.steps = counters.ptr + 2;
+        o.next = counters.ptr + 4;
+        o.unsorted = counters.ptr + 5;
+        o.unsorted_list = unsorted_list.ptr;
+        with_words(ix, [&](auto wt) {
+          constexpr int W = decltype(wt)::value;
+          if (half == 0)
+            k_inexact_bi<W, 1><<<unsigned(T / nt), nt, smem, s>>>(ix->view(), bi, cp, nullptr, count, sc, o);
+          else
+            k_inexact_bi<W, 3><<<unsigned(T / nt), nt, smem, s>>>(ix->view(), bi, cp, nullptr, count, sc, o);
+        });
+        FMG_CK(cudaGetLastError());
+        unsigned long long host_ctr[6];
+        FMG_CK(cudaMemcpyAsync(host_ctr, counters.ptr, sizeof(host_ctr), cudaMemcpyDeviceToHost, s));
+        FMG_CK(cudaStreamSynchronize(s));
+        if (host_ctr[5] > 0) {  // sort this half's large result sets in place
+          k_sort_segments<<<unsigned(host_ctr[5]), 256, 0, s>>>(unsorted_list.ptr, offh[half].ptr, cnth[half].ptr,
+                                                                klh[half].ptr, dh[half].ptr, too_big.ptr);
+          FMG_CK(cudaGetLastError());
+          uint32_t tb_flag = 0;
+          FMG_CK(cudaMemcpyAsync(&tb_flag, too_big.ptr, 4, cudaMemcpyDeviceToHost, s));
+          FMG_CK(cudaStreamSynchronize(s));
+          too_big_any = too_big_any || tb_flag;
+        }
+      }
+      if (too_big_any) {
+        // a half-list was too long to sort in place, so the merge would be
+        // wrong: redo every pattern with the one-directional DFS engine
+        bidir_split = false;
+        bidir = false;
+        FMG_CK(cudaMemsetAsync(too_big.ptr, 0, 4, s));
+        FMG_CK(cudaMemsetAsync(res_pass.ptr, 0xFF, count, s));
+      } else {
+        DevBuf<uint64_t> c64(count, s), moff(count + 1, s);
+        DevBuf<unsigned long long> nret(1, s);
+        retry_list = DevBuf<uint32_t>(count, s);
+        FMG_CK(cudaMemsetAsync(nret.ptr, 0, 8, s));
+        FMG_CK(cudaMemsetAsync(moff.ptr, 0, 8, s));
+        const unsigned gb = unsigned((count + 255) / 256);
+        k_merge_ab<<<gb, 256, 0, s>>>(count, offh[0].ptr, cnth[0].ptr, klh[0].ptr, dh[0].ptr, offh[1].ptr,
+                                      cnth[1].ptr, klh[1].ptr, dh[1].ptr, false, c64.ptr, nullptr, nullptr, nullptr,
+                                      nullptr, nullptr, nullptr, nullptr, nullptr);
+        size_t tb = 0;
+        FMG_CK(cub::DeviceScan::InclusiveSum(nullptr, tb, c64.ptr, moff.ptr + 1, count, s));
+        DevBuf<uint8_t> tmp(tb, s);
+        FMG_CK(cub::DeviceScan::InclusiveSum(tmp.ptr, tb, c64.ptr, moff.ptr + 1, count, s));
+        uint64_t mtotal = 0;
+        FMG_CK(cudaMemcpyAsync(&mtotal, moff.ptr + count, 8, cudaMemcpyDeviceToHost, s));
+        FMG_CK(cudaStreamSynchronize(s));
+        pass_kl.emplace_back(std::max<uint64_t>(mtotal, 1), s);
+        pass_d.emplace_back(std::max<uint64_t>(mtotal, 1), s);
+        k_merge_ab<<<gb, 256, 0, s>>>(count, offh[0].ptr, cnth[0].ptr, klh[0].ptr, dh[0].ptr, offh[1].ptr,
+                                      cnth[1].ptr, klh[1].ptr, dh[1].ptr, true, nullptr, moff.ptr,
+                                      pass_kl.back().ptr, pass_d.back().ptr, res_cnt.ptr, res_off.ptr, res_pass.ptr,
+                                      retry_list.ptr, nret.ptr);
+        FMG_CK(cudaGetLastError());
+        unsigned long long n_retry = 0;
+        FMG_CK(cudaMemcpyAsync(&n_retry, nret.ptr, 8, cudaMemcpyDeviceToHost, s));
+        FMG_CK(cudaStreamSynchronize(s));
+        list = retry_list.ptr;
+        pending = n_retry;
+        first_pass = 1;
+      }
+    }
+    for (int pass = first_pass; pending > 0; ++pass) {
       FMG_REQUIRE(pass < 250, "inexact search did not converge");
-      const bool use_bi = bidir && pass == 0;
+      const bool use_bi = bidir && !bidir_split && pass == 0;
       const uint32_t Sp = use_bi ? 9u : S;  // z = 1: one budget-1 node's children at a time
       const size_t ebytes = use_bi ? 20 : 12;
       const void* kf = use_bi ? kfn_bi : kfn;
@@ -676,7 +889,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       with_words(ix, [&](auto wt) {
         constexpr int W = decltype(wt)::value;
         if (use_bi)
-          k_inexact_bi<W><<<blocks, nt, smem, s>>>(ix->view(), bi, cp, list, pending, sc, o);
+          k_inexact_bi<W, 0><<<blocks, nt, smem, s>>>(ix->view(), bi, cp, list, pending, sc, o);
         else if (short_pat)
           k_inexact<true, W><<<blocks, nt, smem, s>>>(ix->view(), cp, list, pending, z, sc, o, pt);
         else

@@ -85,8 +85,10 @@ __device__ __forceinline__ void children4(const IndexView& v, const PrefixTable&
   }
 }
 
-template <int W>
-__global__ void __launch_bounds__(128) k_inexact_bi(IndexView ix, BiIndex bi, CodePatterns cp,
+// kOnly: 0 = both cases per pattern (one result list), 1 = case A only,
+// 3 = case B only (phase-uniform launches; k_merge_ab joins the two lists).
+template <int W, int kOnly>
+__global__ void __launch_bounds__(128, 7) k_inexact_bi(IndexView ix, BiIndex bi, CodePatterns cp,
                                                     const uint32_t* __restrict__ list, uint64_t count,
                                                     InexactScratch sc, InexactOut out) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__(128) k_inexact_bi(IndexView ix, BiIndex bi, Co
   auto fail = [&]() {
     const unsigned long long f = atomicAdd(out.fail_count, 1ull);
     out.fail_list[f] = uint32_t(q);
-    out.res_cnt[q] = 0;
+    out.res_cnt[q] = kOnly == 0 ? 0u : 0xFFFFFFFFu;  // split launches: k_merge_ab routes it to a retry
   };
   auto finish = [&]() {
     if (overflow) {
@@ -277,9 +279,9 @@ __global__ void __launch_bounds__(128) k_inexact_bi(IndexView ix, BiIndex bi, Co
         sp = nres = 0;
         ++epoch;
         overflow = false;
-        phase = 1;
+        phase = kOnly == 3 ? 3 : 1;
         have = true;
-        cur_valid = dlb(m - 1) <= 1u && root_a();
+        cur_valid = dlb(m - 1) <= 1u && (kOnly == 3 ? root_b() : root_a());
       }
       if (overflow) {
         finish();
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(128) k_inexact_bi(IndexView ix, BiIndex bi, Co
           cz = e.z;
           cw = e.w;
           cur_valid = true;
-        } else if (phase == 1) {
+        } else if (kOnly == 0 && phase == 1) {
           phase = 3;
           cur_valid = dlb(m - 1) <= 1u && root_b();
           continue;
@@ -440,6 +442,406 @@ __global__ void __launch_bounds__(128) k_inexact_bi(IndexView ix, BiIndex bi, Co
     cur_valid = false;
   }
   flush_work(out.steps, my_steps);
+}
+
+// Joins the case-A and case-B result lists of each pattern (each sorted by
+// (k, l), unique within itself): merge, equal intervals keep the smaller
+// diffs.  Count pass (write == false) then write pass into one buffer.
+// A pattern whose A or B launch failed (res_cnt ~0) gets count 0 here and
+// is appended to `retry` for the one-directional DFS engine.
+__global__ void k_merge_ab(uint64_t count, const uint64_t* __restrict__ offA, const uint32_t* __restrict__ cntA,
+                           const uint2* __restrict__ klA, const uint8_t* __restrict__ dA,
+                           const uint64_t* __restrict__ offB, const uint32_t* __restrict__ cntB,
+                           const uint2* __restrict__ klB, const uint8_t* __restrict__ dB, bool write,
+                           uint64_t* __restrict__ c64, const uint64_t* __restrict__ out_off, uint2* __restrict__ kl,
+                           uint8_t* __restrict__ dd, uint32_t* __restrict__ res_cnt, uint64_t* __restrict__ res_off,
+                           uint8_t* __restrict__ res_pass, uint32_t* __restrict__ retry,
+                           unsigned long long* __restrict__ n_retry) {
+  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  const uint32_t na = cntA[q], nb = cntB[q];
+  if (na == 0xFFFFFFFFu || nb == 0xFFFFFFFFu) {
+    if (write) {
+      res_cnt[q] = 0;
+      const unsigned long long r = atomicAdd(n_retry, 1ull);
+      retry[r] = uint32_t(q);
+    } else {
+      c64[q] = 0;
+    }
+    return;
+  }
+  const uint2* a = klA + (na ? offA[q] : 0);
+  const uint2* b = klB + (nb ? offB[q] : 0);
+  const uint8_t* da = dA + (na ? offA[q] : 0);
+  const uint8_t* db = dB + (nb ? offB[q] : 0);
+  uint64_t o = write ? out_off[q] : 0;
+  uint32_t i = 0, j = 0, n = 0;
+  while (i < na || j < nb) {
+    uint2 x;
+    uint8_t d;
+    if (j >= nb || (i < na && (a[i].x < b[j].x || (a[i].x == b[j].x && a[i].y < b[j].y)))) {
+      x = a[i];
+      d = da[i++];
+    } else if (i >= na || (a[i].x != b[j].x || a[i].y != b[j].y)) {
+      x = b[j];
+      d = db[j++];
+    } else {  // the same interval from both halves
+      x = a[i];
+      d = min(da[i], db[j]);
+      ++i;
+      ++j;
+    }
+    if (write) {
+      kl[o + n] = x;
+      dd[o + n] = d;
+    }
+    ++n;
+  }
+  if (write) {
+    res_cnt[q] = n;
+    res_off[q] = o;
+    res_pass[q] = 0;
+  } else {
+    c64[q] = n;
+  }
+}
+
+// ----- level-synchronous form (the default bidirectional engine) ----------
+//
+// k_bspine: one thread per pattern walks both budget-1 spines — case A over
+// W[h-1..0] on the forward index, case B over W[h..m-1] on the reverse
+// index — queuing every budget-0 child as a Z1BNode and writing results
+// reached at the pattern ends as Z1Raw.  Patterns of equal length keep the
+// warp in lock-step.  k_bchain: persistent lane-refill over the queued
+// nodes, each an exact extension (backward for case A, forward for case B)
+// until its string leaves the text or the pattern ends.  Deduplication and
+// ordering reuse the z1 engine's kernels.
+struct Z1BNode {  // a budget-0 continuation of pattern q
+  uint32_t q;
+  uint32_t pos;  // bits 0..15: next position; bit 16: case B (forward); bit 17: shallow
+  uint32_t x, y, zz, ww;  // A: (k, l) | (key, depth); B: F (k, l) + R (k', l') | (rkey, depth)
+};
+struct Z1BQueues {
+  Z1BNode* nodes;
+  unsigned long long* n_nodes;
+  uint64_t node_cap;
+  Z1Raw* raws;
+  unsigned long long* n_raws;
+  uint64_t raw_cap;
+};
+
+__device__ __forceinline__ void z1b_pattern(const CodePatterns& cp, uint64_t q, uint64_t& pw0, uint64_t& pw1,
+                                            int& m) {
+  if (cp.packed1) {
+    pw0 = cp.packed1[q];
+    pw1 = 0;
+    m = int(cp.fixed_m);
+  } else {
+    const ulonglong2 pk = cp.packed[q];
+    pw0 = pk.x;
+    pw1 = pk.y;
+    m = int(cp.offsets[q + 1] - cp.offsets[q]);
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) k_bspine(IndexView ix, BiIndex bi, CodePatterns cp, uint64_t q0,
+                                                uint64_t count, Z1BQueues qu, unsigned long long* steps) {
+  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const uint32_t q = uint32_t(q0 + t);
+  uint64_t pw0, pw1;
+  int m;
+  z1b_pattern(cp, q, pw0, pw1, m);
+  const uint64_t dbits = cp.dbits[q];
+  auto dlb = [&](int i) -> uint32_t { return __popcll(dbits & ((2ull << i) - 1ull)); };
+  uint64_t work = 0;
+  const uint32_t K = bi.tf.k;
+  const uint32_t sent_r = bi.rev.sentinel_row;
+  const int h = m / 2;
+  auto raw = [&](bool c, uint32_t k, uint32_t l, uint32_t used, uint64_t& slot) {
+    if (c) {
+      if (slot < qu.raw_cap) qu.raws[slot] = Z1Raw{q, k, l, used};
+      ++slot;
+    }
+  };
+  auto node = [&](bool c, uint32_t pos, uint32_t x, uint32_t y, uint32_t zz, uint32_t ww, uint64_t& slot) {
+    if (c) {
+      if (slot < qu.node_cap) qu.nodes[slot] = Z1BNode{q, pos, x, y, zz, ww};
+      ++slot;
+    }
+  };
+  if (dlb(m - 1) > 1u) {  // two absent segments: no string within one edit occurs
+    flush_work(steps, work);
+    return;
+  }
+
+  // ---- case A: W[h..m-1] exactly, then the backward spine over W[h-1..0] ----
+  {
+    const int r = m - h;
+    const int tt = min(r, int(K));
+    uint2 e = __ldg(bi.tf.base + PrefixTable::off(uint32_t(tt)) + pat_key(pw0, pw1, m - tt, tt));
+    work += work_unit(1u);
+    for (int p = m - tt - 1; p >= h && e.x <= e.y; --p) {
+      uint32_t ck[4], cl[4];
+      children4<W>(ix, bi.tf, false, e.x, e.y, ck, cl, work);
+      const uint32_t b = pat_sym(pw0, pw1, p);
+      e = make_uint2(sel4(ck, b), sel4(cl, b));
+    }
+    bool alive = e.x <= e.y;
+    if (alive && h == 0) {
+      uint64_t rs = warp_reserve(qu.n_raws, 1u);
+      raw(true, e.x, e.y, 0u, rs);
+      alive = false;
+    }
+    alive = alive && dlb(h - 1) <= 1u;
+    bool sh = uint32_t(r) < K;
+    uint32_t x = sh ? pat_key(pw0, pw1, h, r) : e.x, y = sh ? uint32_t(r) : e.y;
+    int i = h - 1;
+    while (alive) {
+      uint32_t ck[4], cl[4];
+      children4<W>(ix, bi.tf, sh, x, y, ck, cl, work);
+      const uint32_t want = pat_sym(pw0, pw1, i);
+      const bool at0 = i == 0;
+      const bool ok_prev = !at0 && dlb(i - 1) == 0u, ok_cur = dlb(i) == 0u;
+      const bool child_sh = sh && y + 1u < K;
+      uint32_t e_ins = 0, e_mis = 0;
+#pragma unroll
+      for (uint32_t b = 0; b < 4; ++b) {
+        const bool ne = ck[b] <= cl[b];
+        e_ins |= (ok_cur && ne) ? (1u << b) : 0u;
+        e_mis |= (ok_prev && ne && b != want) ? (1u << b) : 0u;
+      }
+      uint64_t slot = warp_reserve(qu.n_nodes, (ok_prev ? 1u : 0u) + __popc(e_ins) + __popc(e_mis));
+      node(ok_prev, uint32_t(i - 1) | (sh ? 0x20000u : 0u), x, y, 0u, 0u, slot);  // skip
+#pragma unroll
+      for (uint32_t b = 0; b < 4; ++b) {
+        const uint32_t px = child_sh ? b + 4u * x : ck[b], py = child_sh ? y + 1u : cl[b];
+        const uint32_t fl = child_sh ? 0x20000u : 0u;
+        node((e_ins >> b) & 1u, uint32_t(i) | fl, px, py, 0u, 0u, slot);      // insert
+        node((e_mis >> b) & 1u, uint32_t(i - 1) | fl, px, py, 0u, 0u, slot);  // mismatch
+      }
+      const uint32_t kw = sel4(ck, want), lw = sel4(cl, want);
+      // results at the left end (search.py:127-134): rare
+      uint32_t n_at0 = 0;
+      if (at0) {
+        n_at0 = (kw <= lw ? 1u : 0u) + 1u;
+#pragma unroll
+        for (uint32_t b = 0; b < 4; ++b) n_at0 += (b != want && ck[b] <= cl[b]) ? 1u : 0u;
+      }
+      uint64_t rs = warp_reserve(qu.n_raws, n_at0);
+      if (at0) {
+        raw(kw <= lw, kw, lw, 0u, rs);
+        uint32_t sk = x, sl = y;  // skip: this node's own interval
+        if (sh) {
+          if (y == 0u) {
+            sk = 0u;
+            sl = ix.n;
+          } else {
+            const uint2 o = __ldg(bi.tf.base + PrefixTable::off(y) + x);
+            sk = o.x;
+            sl = o.y;
+          }
+        }
+        raw(true, sk, sl, 1u, rs);
+#pragma unroll
+        for (uint32_t b = 0; b < 4; ++b) raw(b != want && ck[b] <= cl[b], ck[b], cl[b], 1u, rs);
+        break;
+      }
+      if (kw > lw || dlb(i - 1) > 1u) break;
+      x = child_sh ? want + 4u * x : kw;
+      y = child_sh ? y + 1u : lw;
+      sh = child_sh;
+      --i;
+    }
+  }
+
+  // ---- case B: W[0..h-1] exactly, then the forward spine over W[h..m-1] ----
+  {
+    const int tt = min(h, int(K));
+    uint2 f = make_uint2(0u, ix.n), rr = make_uint2(0u, ix.n);
+    if (tt > 0) {
+      f = __ldg(bi.tf.base + PrefixTable::off(uint32_t(tt)) + pat_key(pw0, pw1, 0, tt));
+      rr = __ldg(bi.tr.base + PrefixTable::off(uint32_t(tt)) + pat_rkey(pw0, pw1, 0, tt));
+      work += work_unit(2u);
+    }
+    for (int p = tt; p < h && f.x <= f.y; ++p) {
+      uint32_t rk[4], rl[4];
+      children4<W>(bi.rev, bi.tr, false, rr.x, rr.y, rk, rl, work);
+      const uint32_t w = pat_sym(pw0, pw1, p);
+      uint32_t k = f.x + ((rr.x <= sent_r && sent_r <= rr.y) ? 1u : 0u);
+#pragma unroll
+      for (uint32_t b = 0; b < 4; ++b)
+        if (b < w) k += rl[b] + 1u - rk[b];
+      const uint32_t sz = sel4(rl, w) + 1u - sel4(rk, w);
+      f = sz ? make_uint2(k, k + sz - 1u) : make_uint2(1u, 0u);
+      rr = make_uint2(sel4(rk, w), sel4(rl, w));
+    }
+    bool alive = f.x <= f.y;
+    bool sh = uint32_t(h) < K;
+    uint32_t fx = f.x, fy = f.y;
+    uint32_t rz = sh ? pat_rkey(pw0, pw1, 0, h) : rr.x, rw = sh ? uint32_t(h) : rr.y;
+    int j = h;
+    while (alive) {
+      uint32_t ck[4], cl[4];
+      children4<W>(bi.rev, bi.tr, sh, rz, rw, ck, cl, work);
+      const bool dollar = sh ? (rz == bi.tail[rw]) : (rz <= sent_r && sent_r <= rw);
+      uint32_t sz[4], fk[4];
+      uint32_t acc = fx + (dollar ? 1u : 0u);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        sz[b] = cl[b] + 1u - ck[b];
+        fk[b] = acc;
+        acc += sz[b];
+      }
+      const bool child_sh = sh && rw + 1u < K;
+      const uint32_t fl = 0x10000u | (child_sh ? 0x20000u : 0u);
+      if (j == m) {  // insertion after W[m-1]
+        uint32_t n_ins = 0;
+#pragma unroll
+        for (uint32_t b = 0; b < 4; ++b) n_ins += sz[b] ? 1u : 0u;
+        uint64_t rs = warp_reserve(qu.n_raws, n_ins);
+#pragma unroll
+        for (uint32_t b = 0; b < 4; ++b) raw(sz[b] != 0u, fk[b], fk[b] + sz[b] - 1u, 1u, rs);
+        break;
+      }
+      const uint32_t w = pat_sym(pw0, pw1, j);
+      const bool last = j + 1 == m;
+      const bool ins = j >= h + 1;  // insertion after W[j-1], j-1 >= h
+      uint32_t e_ins = 0, e_mis = 0;
+#pragma unroll
+      for (uint32_t b = 0; b < 4; ++b) {
+        e_ins |= (ins && sz[b]) ? (1u << b) : 0u;
+        e_mis |= (!last && sz[b] && b != w) ? (1u << b) : 0u;
+      }
+      uint64_t slot = warp_reserve(qu.n_nodes, (last ? 0u : 1u) + __popc(e_ins) + __popc(e_mis));
+      node(!last, uint32_t(j + 1) | 0x10000u | (sh ? 0x20000u : 0u), fx, fy, rz, rw, slot);  // skip
+#pragma unroll
+      for (uint32_t b = 0; b < 4; ++b) {
+        const uint32_t pz = child_sh ? b + 4u * rz : ck[b], pw = child_sh ? rw + 1u : cl[b];
+        node((e_mis >> b) & 1u, uint32_t(j + 1) | fl, fk[b], fk[b] + sz[b] - 1u, pz, pw, slot);  // mismatch
+        node((e_ins >> b) & 1u, uint32_t(j) | fl, fk[b], fk[b] + sz[b] - 1u, pz, pw, slot);      // insert
+      }
+      const uint32_t sw = sel4(sz, w), kw = sel4(fk, w);
+      uint32_t n_last = 0;
+      if (last) {
+        n_last = (sw ? 1u : 0u) + 1u;
+#pragma unroll
+        for (uint32_t b = 0; b < 4; ++b) n_last += (b != w && sz[b]) ? 1u : 0u;
+      }
+      uint64_t rs = warp_reserve(qu.n_raws, n_last);
+      if (last) {
+        raw(sw != 0u, kw, kw + sw - 1u, 0u, rs);  // W itself (also found by case A)
+        raw(true, fx, fy, 1u, rs);                // skip W[m-1]
+#pragma unroll
+        for (uint32_t b = 0; b < 4; ++b) raw(b != w && sz[b], fk[b], fk[b] + sz[b] - 1u, 1u, rs);  // mismatch
+      }
+      if (sw == 0u) break;
+      // the match child; after W[m-1] it still expands once for the insertions
+      rz = child_sh ? w + 4u * rz : sel4(ck, w);
+      rw = child_sh ? rw + 1u : sel4(cl, w);
+      fx = kw;
+      fy = kw + sw - 1u;
+      sh = child_sh;
+      ++j;
+    }
+  }
+  flush_work(steps, work);
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) k_bchain(IndexView ix, BiIndex bi, CodePatterns cp,
+                                                const Z1BNode* __restrict__ nodes, uint64_t n_nodes, Z1BQueues qu,
+                                                unsigned long long* steps) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint64_t work = 0;
+  const uint32_t K = bi.tf.k;
+  const uint32_t sent_r = bi.rev.sentinel_row;
+  uint64_t pw0 = 0, pw1 = 0, dbits = 0;
+  int m = 0, pos = 0;
+  uint32_t q = 0, x = 0, y = 0, zz = 0, ww = 0;
+  bool fwd = false, sh = false, have = false;
+  while (true) {
+    if (!have) {
+      if (t >= n_nodes) break;
+      const Z1BNode nd = nodes[t];
+      t += stride;
+      q = nd.q;
+      z1b_pattern(cp, q, pw0, pw1, m);
+      dbits = cp.dbits[q];
+      pos = int(nd.pos & 0xFFFFu);
+      fwd = (nd.pos >> 16) & 1u;
+      sh = (nd.pos >> 17) & 1u;
+      x = nd.x;
+      y = nd.y;
+      zz = nd.zz;
+      ww = nd.ww;
+      have = true;
+    }
+    const uint32_t sym = pat_sym(pw0, pw1, pos);
+    if (!fwd) {  // case A: backward, one symbol
+      uint32_t k2, l2;
+      if (sh) {
+        const uint2 e = __ldg(bi.tf.base + PrefixTable::off(y + 1u) + 4u * x + sym);
+        k2 = e.x;
+        l2 = e.y;
+        work += work_unit(1u);
+      } else {
+        constexpr uint32_t kC = LineTraits<W>::kChars;
+        const uint32_t low = x - 1u;
+        const uint32_t jh = line_of<W>(y), jl = line_of<W>(low);
+        uint32_t bh[4], bl[4];
+        uint64_t wh[W], wl[W];
+        load_line<W, 0>(ix, jh, y - jh * kC, bh, wh);
+        load_line<W, 0>(ix, jl, low - jl * kC, bl, wl);
+        const uint32_t cs = c_of(ix, sym);
+        k2 = cs + occ1_from_line<W>(ix, bl, wl, low, low - jl * kC, sym) + 1u;
+        l2 = cs + occ1_from_line<W>(ix, bh, wh, y, y - jh * kC, sym);
+        work += work_unit(jl != jh ? 2u : 1u);
+      }
+      const bool empty = k2 > l2;
+      if (empty || pos == 0 || __popcll(dbits & ((1ull << pos) - 1ull)) > 0u) {
+        have = false;
+        if (!empty && pos == 0) {
+          const unsigned long long rs = atomicAdd(qu.n_raws, 1ull);
+          if (rs < qu.raw_cap) qu.raws[rs] = Z1Raw{q, k2, l2, 1u};
+        }
+        continue;
+      }
+      const bool child_sh = sh && y + 1u < K;
+      x = child_sh ? sym + 4u * x : k2;
+      y = child_sh ? y + 1u : l2;
+      sh = child_sh;
+      --pos;
+      continue;
+    }
+    // case B: forward, needs all four counts of the reverse index
+    uint32_t ck[4], cl[4];
+    children4<W>(bi.rev, bi.tr, sh, zz, ww, ck, cl, work);
+    const bool dollar = sh ? (zz == bi.tail[ww]) : (zz <= sent_r && sent_r <= ww);
+    uint32_t k = x + (dollar ? 1u : 0u);
+#pragma unroll
+    for (uint32_t b = 0; b < 4; ++b)
+      if (b < sym) k += cl[b] + 1u - ck[b];
+    const uint32_t sz = sel4(cl, sym) + 1u - sel4(ck, sym);
+    if (sz == 0u || pos + 1 == m) {
+      have = false;
+      if (sz != 0u) {
+        const unsigned long long rs = atomicAdd(qu.n_raws, 1ull);
+        if (rs < qu.raw_cap) qu.raws[rs] = Z1Raw{q, k, k + sz - 1u, 1u};
+      }
+      continue;
+    }
+    const bool child_sh = sh && ww + 1u < K;
+    zz = child_sh ? sym + 4u * zz : sel4(ck, sym);
+    ww = child_sh ? ww + 1u : sel4(cl, sym);
+    x = k;
+    y = k + sz - 1u;
+    sh = child_sh;
+    ++pos;
+  }
+  flush_work(steps, work);
 }
 
 // tail[d] = key of the reversed text's first d characters = text[n-1],

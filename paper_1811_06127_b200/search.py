@@ -156,7 +156,7 @@ class MatchSet(NamedTuple):
         return self.offsets.size - 1
 
 
-BIDIR_MIN_N = 1 << 40  # off by default until the level-synchronous variant lands
+BIDIR_MIN_N = 1 << 26
 
 
 def bidir_min_n() -> int:

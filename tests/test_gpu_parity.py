@@ -430,15 +430,17 @@ def test_inexact_prefix_table_paths(gpu, monkeypatch, z, lens):
     assert np.array_equal(b.offsets, ms.offsets) and np.array_equal(b.k, ms.k) and np.array_equal(b.diffs, ms.diffs)
 
 
+@pytest.mark.parametrize("engine", ["split", "sync", "dfs"])
 @pytest.mark.parametrize("n,lens", [(200_000, (1, 2, 3, 5, 8, 9, 10, 11, 19, 20, 32, 33, 47, 64)),
                                     (3_000, (1, 2, 4, 7, 12, 19, 25)), (40, (1, 2, 3, 6, 9, 14))])
-def test_inexact_bidirectional_engine(gpu, monkeypatch, n, lens):
+def test_inexact_bidirectional_engine(gpu, monkeypatch, n, lens, engine):
     """z = 1 through the bidirectional engine (reverse index attached, both prefix tables):
     patterns cut from anywhere (incl. the text's very start and end, which exercises the
     forward extension's '$' term), mutated or random, lengths 1..64 — identical to the
     oracle and to the one-directional DFS engine."""
     monkeypatch.setenv("FMG_BIDIR_MIN_N", "0")
     monkeypatch.setenv("FMG_INEXACT_DFS", "1")
+    monkeypatch.setenv("FMG_BIDIR_ENGINE", engine)
     rng = np.random.Generator(np.random.PCG64(31337 + n))
     text = rng.integers(0, 4, n, dtype=np.uint8)
     idx = fm.build_index(text)

@@ -20,6 +20,8 @@ lib = _lib.load()
 wl = workloads.config2(n_reads=n_reads)
 idx = fm.build_index(wl.text)
 dix = idx.device_index(0)
+if int(__import__("os").environ.get("FMG_BIDIR", "0")):
+    dix.ensure_reverse()
 m = wl.patterns.shape[1]
 codes = np.ascontiguousarray(wl.patterns.reshape(-1))
 offs = np.arange(0, (n_reads + 1) * m, m, dtype=np.uint64)
