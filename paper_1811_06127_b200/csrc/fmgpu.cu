@@ -746,7 +746,13 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       DevBuf<uint8_t> passh(count, s);
       CodePatterns cp{codes, offsets, packed.ptr, packed1, uint32_t(max_len), dbits.ptr};
       bool too_big_any = false;
+      static const bool trace_split = std::getenv("FMG_TRACE") != nullptr;
+      cudaEvent_t sev[6] = {};
+      if (trace_split)
+        for (auto& e : sev) cudaEventCreate(&e);
+      unsigned long long n_unsorted[2] = {0, 0};
       for (int half = 0; half < 2; ++half) {
+        if (trace_split) cudaEventRecord(sev[2 * half], s);
         FMG_CK(cudaMemsetAsync(table.ptr, 0, uint64_t(2 * R) * T * sizeof(uint4), s));  // epoch 0 = empty
         FMG_CK(cudaMemsetAsync(counters.ptr, 0, 2 * sizeof(unsigned long long), s));
         FMG_CK(cudaMemsetAsync(counters.ptr + 4, 0, 2 * sizeof(unsigned long long), s));
@@ -775,7 +781,9 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
         FMG_CK(cudaGetLastError());
         unsigned long long host_ctr[6];
         FMG_CK(cudaMemcpyAsync(host_ctr, counters.ptr, sizeof(host_ctr), cudaMemcpyDeviceToHost, s));
+        if (trace_split) cudaEventRecord(sev[2 * half + 1], s);
         FMG_CK(cudaStreamSynchronize(s));
+        n_unsorted[half] = host_ctr[5];
         if (host_ctr[5] > 0) {  // sort this half's large result sets in place
           k_sort_segments<<<unsigned(host_ctr[5]), 256, 0, s>>>(unsorted_list.ptr, offh[half].ptr, cnth[half].ptr,
                                                                 klh[half].ptr, dh[half].ptr, too_big.ptr);
@@ -823,6 +831,18 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
         list = retry_list.ptr;
         pending = n_retry;
         first_pass = 1;
+        if (trace_split) {
+          cudaEventRecord(sev[5], s);
+          cudaEventSynchronize(sev[5]);
+          float ta = 0, tsa = 0, tb = 0, tm = 0;
+          cudaEventElapsedTime(&ta, sev[0], sev[1]);
+          cudaEventElapsedTime(&tsa, sev[1], sev[2]);
+          cudaEventElapsedTime(&tb, sev[2], sev[3]);
+          cudaEventElapsedTime(&tm, sev[3], sev[5]);
+          fprintf(stderr, "[fmg] bidirectional split: case A %.3f ms (%llu > S sorted, %.3f ms), case B %.3f ms "
+                  "(%llu > S), B sort + merge %.3f ms, %llu merged results, %llu retried\n", ta, n_unsorted[0], tsa,
+                  tb, n_unsorted[1], tm, (unsigned long long)mtotal, n_retry);
+        }
       }
     }
     for (int pass = first_pass; pending > 0; ++pass) {

@@ -85,6 +85,10 @@ __device__ __forceinline__ void children4(const IndexView& v, const PrefixTable&
   }
 }
 
+#ifndef FMG_BI_OCC1
+#define FMG_BI_OCC1 1  // case-A budget-0 steps count one symbol instead of four
+#endif
+
 // kOnly: 0 = both cases per pattern (one result list), 1 = case A only,
 // 3 = case B only (phase-uniform launches; k_merge_ab joins the two lists).
 template <int W, int kOnly>
@@ -318,13 +322,37 @@ __global__ void __launch_bounds__(128, 7) k_inexact_bi(IndexView ix, BiIndex bi,
     // ---- one step: the four children of the node's string ----
     const bool fwd = phase == 3;
     uint32_t ck[4], cl[4];
+#if FMG_BI_OCC1
+    // case-A budget-0 node: only the symbol W[i] is needed (one-symbol count)
+    const bool one = !fwd && cb == 0u && !csh;
+    uint32_t k1 = 0, l1 = 0;
+    if (one) {
+      const uint32_t sym = sym_at(ci);
+      constexpr uint32_t kC = LineTraits<W>::kChars;
+      const uint32_t low = cx - 1u;
+      const uint32_t jh = line_of<W>(cy), jl = line_of<W>(low);
+      uint32_t bh[4], bl[4];
+      uint64_t wh[W], wl[W];
+      load_line<W, 0>(ix, jh, cy - jh * kC, bh, wh);
+      load_line<W, 0>(ix, jl, low - jl * kC, bl, wl);
+      const uint32_t cs = c_of(ix, sym);
+      k1 = cs + occ1_from_line<W>(ix, bl, wl, low, low - jl * kC, sym) + 1u;
+      l1 = cs + occ1_from_line<W>(ix, bh, wh, cy, cy - jh * kC, sym);
+      my_steps += work_unit(jl != jh ? 2u : 1u);
+    } else {
+      children4<W>(fwd ? bi.rev : ix, fwd ? bi.tr : bi.tf, csh, fwd ? cz : cx, fwd ? cw : cy, ck, cl, my_steps);
+    }
+#else
+    constexpr bool one = false;
+    uint32_t k1 = 0, l1 = 0;
     children4<W>(fwd ? bi.rev : ix, fwd ? bi.tr : bi.tf, csh, fwd ? cz : cx, fwd ? cw : cy, ck, cl, my_steps);
+#endif
 
     if (!fwd) {
       // ---- case A: backward expansion (search.py:135-152) ----
       const int i = ci;
       const uint32_t want = sym_at(i);
-      const uint32_t kw = sel4(ck, want), lw = sel4(cl, want);
+      const uint32_t kw = one ? k1 : sel4(ck, want), lw = one ? l1 : sel4(cl, want);
       const bool child_sh = csh && cy + 1u < K;
       if (cb == 0u) {
         if (kw > lw) {

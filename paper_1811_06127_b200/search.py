@@ -156,7 +156,7 @@ class MatchSet(NamedTuple):
         return self.offsets.size - 1
 
 
-BIDIR_MIN_N = 1 << 26
+BIDIR_MIN_N = 1 << 22
 
 
 def bidir_min_n() -> int:

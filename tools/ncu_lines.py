@@ -14,6 +14,7 @@ from pathlib import Path
 
 rep, lib, kname = sys.argv[1], sys.argv[2], sys.argv[3]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+launch = int(sys.argv[5]) if len(sys.argv) > 5 else 0  # which profiled launch of the report
 tmp = Path(tempfile.mkdtemp())
 subprocess.run(["cuobjdump", "-xelf", "all", str(Path(lib).resolve())], cwd=tmp, capture_output=True)
 cubin = next(p for p in tmp.glob("*.cubin") if p.name.startswith("fmgpu.") or "fmgpu" in p.name)
@@ -32,7 +33,9 @@ for l in sass[start + 1:]:
         idx2src[int(m.group(1), 16) // 16] = cur
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
-h, data = rows[1], rows[2:]
+starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] + [len(rows)]
+sec = rows[starts[launch]:starts[launch + 1]]
+h, data = sec[1], [r for r in sec[2:] if len(r) == len(sec[1])]
 ia, ta = h.index("Instructions Executed"), h.index("Thread Instructions Executed")
 sa = h.index("Warp Stall Sampling (All Samples)")
 agg = collections.defaultdict(lambda: [0.0, 0.0, 0.0])
