@@ -97,6 +97,27 @@ int sm_count(int device) {
   return v;
 }
 
+// Memory a call may size its scratch from: device free memory plus what the
+// stream-ordered pool holds but is not using.  Unlike cudaMemGetInfo alone
+// this does not shrink as the pool keeps freed blocks (release threshold is
+// unlimited), so scratch sizes stay the same from call to call and the pool
+// reuses its blocks instead of mapping fresh memory (measured on B200: the
+// config-2 z = 1 call varied 8 -> 50 ms while sizes followed cudaMemGetInfo).
+size_t available_bytes(int device) {
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return size_t(8) << 30;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t reserved = 0, used = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
+      free_b += size_t(reserved - used);
+  }
+  // round down to 1 GiB so small fluctuations keep the sizes identical
+  const size_t g = size_t(1) << 30;
+  return free_b > g ? free_b / g * g : free_b;
+}
+
 }  // namespace fmg
 
 struct fmg_index {
@@ -457,8 +478,7 @@ bool run_z1(const fmg_index* ix, const CodePatterns& cp, uint64_t count, uint64_
   if (trace)
     for (auto& e : ev) cudaEventCreate(&e);
   if (trace) cudaEventRecord(ev[0], s);
-  size_t free_b = 0, total_b = 0;
-  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = size_t(8) << 30;
+  const size_t free_b = available_bytes(ix->device);
   // worst case 8 continuations per spine node and m + 1 spine nodes; in
   // practice far fewer, so cap by memory and detect overflow
   const uint64_t worst = count * 8 * (m + 1);
@@ -523,8 +543,7 @@ bool run_z1b(const fmg_index* ix, const BiIndex& bi, const CodePatterns& cp, uin
   if (trace)
     for (auto& e : ev) cudaEventCreate(&e);
   if (trace) cudaEventRecord(ev[0], s);
-  size_t free_b = 0, total_b = 0;
-  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = size_t(8) << 30;
+  const size_t free_b = available_bytes(ix->device);
   const uint64_t per = 8 * (m + 1);
   const uint64_t node_budget = std::max<uint64_t>(per, free_b / 4 / sizeof(Z1BNode));
   const uint64_t chunk = std::min<uint64_t>(count, std::max<uint64_t>(1, node_budget / per));
@@ -631,14 +650,21 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       });
       FMG_CK(cudaGetLastError());
     }
-    // z = 1 on an L2-resident index: the level-synchronous engine (uniform
-    // warps).  On HBM-resident indexes the DFS engine wins: its chains start
-    // from intervals already in L1/L2, while queued continuations re-fetch
-    // pattern, bound and first line from DRAM (tools/prof_c3.py).
+    // z = 1 on an L2-resident index without a reverse index: the
+    // level-synchronous engine (uniform warps).  On HBM-resident indexes the
+    // DFS engine wins: its chains start from intervals already in L1/L2, while
+    // queued continuations re-fetch pattern, bound and first line from DRAM
+    // (tools/prof_c3.py).  With a reverse index attached the bidirectional
+    // split engine below beats both (config 2: 9.4 -> 6.4 ms per 1M seeds).
     const bool force_dfs = std::getenv("FMG_INEXACT_DFS") != nullptr;  // read per call (tests flip it)
+    const bool bidir_off_env = [] {
+      const char* e = std::getenv("FMG_INEXACT_BIDIR");
+      return e != nullptr && std::atoi(e) == 0;
+    }();
     uint64_t line_bytes = 0;
     with_words(ix, [&](auto wt) { line_bytes = ix->n_lines * fmg::LineTraits<decltype(wt)::value>::kBytes; });
-    if (z == 1 && short_pat && !force_dfs && line_bytes <= (uint64_t(64) << 20)) {
+    if (z == 1 && short_pat && !force_dfs && line_bytes <= (uint64_t(64) << 20) &&
+        (ix->rev_lines == nullptr || bidir_off_env)) {
       CodePatterns cpz{codes, offsets, packed.ptr, packed1, uint32_t(max_len), dbits.ptr};
       if (run_z1(ix, cpz, count, max_len, s, counters.ptr + 2, res)) return res;
       // queues overflowed: fall through to the DFS engine (same results)
@@ -690,8 +716,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     // slots).  cap: results per pass (9 bytes each) before patterns finishing
     // later are retried — sized from free memory so a pass rarely fills it.
     uint32_t R = 256;
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = size_t(8) << 30;
+    const size_t free_b = available_bytes(ix->device);
     uint64_t cap = std::max<uint64_t>(count * 16, 1u << 20);
     cap = std::min<uint64_t>(cap, std::max<uint64_t>(1u << 20, free_b / 4 / 9));
     // Stack: depth <= 8(z+1) with the budget-ordered pushes of k_inexact;

@@ -326,16 +326,23 @@ def test_config4_first_chunk_vs_oracle(gpu):
 
 
 def test_z1_engines_agree(gpu, monkeypatch):
-    """z = 1: the level-synchronous engine and the DFS engine give identical result sets."""
+    """z = 1 on an L2-resident repeat genome: the bidirectional split engine (default once a
+    reverse index is attached), the level-synchronous engine and the DFS engine give
+    identical result sets, equal to the oracle's."""
     wl = workloads.config2(n_reads=20_000, n=8_000_000)
     idx = fm.build_index(wl.text)
-    a = fm.inexact_search_batch(idx, wl.patterns, 1)
+    a = fm.inexact_search_batch(idx, wl.patterns, 1)  # >= BIDIR_MIN_N: bidirectional split
+    assert idx.device_index()._has_reverse
+    monkeypatch.setenv("FMG_INEXACT_BIDIR", "0")
+    c = fm.inexact_search_batch(idx, wl.patterns, 1)  # level-synchronous z1 engine
     monkeypatch.setenv("FMG_INEXACT_DFS", "1")
-    b = fm.inexact_search_batch(idx, wl.patterns, 1)
-    assert np.array_equal(a.offsets, b.offsets) and np.array_equal(a.k, b.k)
-    assert np.array_equal(a.l, b.l) and np.array_equal(a.diffs, b.diffs)
+    b = fm.inexact_search_batch(idx, wl.patterns, 1)  # one-directional DFS
+    for x in (b, c):
+        assert np.array_equal(a.offsets, x.offsets) and np.array_equal(a.k, x.k)
+        assert np.array_equal(a.l, x.l) and np.array_equal(a.diffs, x.diffs)
     row, k, l, d, _ = orc.inexact_batch(orc.OracleIndex(idx), wl.patterns, 1)
     assert np.array_equal(a.offsets, row) and np.array_equal(a.k.astype(np.int64), k)
+    assert np.array_equal(a.l.astype(np.int64), l) and np.array_equal(a.diffs, d)
 
 
 def test_exact_kmer_table_paths(gpu):
