@@ -412,6 +412,13 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
         _lib.check(fn(dix.handle, ct.byref(kk), ct.byref(nb)))
         extra["prefix_table"] = {"k": kk.value, "bytes": nb.value,
                                  "build_s": round(time.perf_counter() - t_lut, 4)}
+        if wl.name == "config3" or wl.max_diff == 0:  # exact search: its k-mer table (maybe one level deeper)
+            fx = lib.fmgx_kmer_table
+            fx.argtypes = [ct.c_void_p, ct.POINTER(ct.c_uint32), ct.POINTER(ct.c_uint64)]
+            t_lut = time.perf_counter()
+            _lib.check(fx(dix.handle, ct.byref(kk), ct.byref(nb)))
+            extra["kmer_table"] = {"k": kk.value, "extension_bytes": nb.value,
+                                   "build_s": round(time.perf_counter() - t_lut, 4)}
 
     if wl.name == "config3":
         m = wl.meta["m"]

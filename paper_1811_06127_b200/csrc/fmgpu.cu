@@ -139,6 +139,11 @@ struct fmg_index {
   uint64_t rev_sentinel_row = 0;
   uint2* lut_r = nullptr;
   uint32_t tail[16] = {};
+  // exact-search k-mer table one level beyond the prefix table (level
+  // lut_k + 1 alone; see kmer_table), or null
+  uint2* lut_x = nullptr;
+  uint32_t lut_x_k = 0;
+  bool lut_x_tried = false;
 
   fmg::IndexView view_rev() const {
     fmg::IndexView v = view();
@@ -354,9 +359,49 @@ PrefixTable prefix_table_rev(const fmg_index* cix, uint64_t count, cudaStream_t 
   return PrefixTable{ix->lut_r, tf.k};
 }
 
-KmerTable kmer_table(const fmg_index* ix, uint64_t count, cudaStream_t s) {
-  const PrefixTable pt = prefix_table(ix, count, s);
+// The exact search's k-mer table.  Exact search needs only the last level,
+// so it goes one level beyond the prefix table when the index is large
+// enough for that level to still skip steps (K + 1 <= floor(log4 n) + 2, at
+// most 16 so keys stay 32-bit) and the level fits in a quarter of the
+// available memory: level 16 is 34.4 GB, built from level 15 with one Occ
+// step per entry.  Measured on config 4 (2^28 x 20 bp, 1 Gbp): K = 15 -> 16
+// takes present seeds from 5 to 4 dependent steps and most random seeds to
+// an empty interval in the table.  FMG_EXACT_LUT_EXT=0 disables it (A/B).
+KmerTable kmer_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
+  const PrefixTable pt = prefix_table(cix, count, s);
   if (!pt.base) return {};
+  static const bool ext_enabled = [] {
+    const char* e = std::getenv("FMG_EXACT_LUT_EXT");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  auto* ix = const_cast<fmg_index*>(cix);  // a cache, like the prefix table
+  if (ext_enabled) {
+    std::lock_guard<std::mutex> lock(ix->lut_mu);
+    if (!ix->lut_x_tried) {
+      ix->lut_x_tried = true;
+      int lg = 0;
+      while ((uint64_t(1) << (2 * (lg + 1))) <= ix->n) ++lg;  // floor(log4 n)
+      const uint32_t kx = pt.k + 1;
+      const uint64_t cnt = uint64_t(1) << (2 * kx);
+      if (kx <= 16 && int(kx) <= lg + 2 && cnt * sizeof(uint2) <= available_bytes(ix->device) / 4) {
+        uint2* lx = nullptr;
+        if (cudaMalloc(&lx, cnt * sizeof(uint2)) == cudaSuccess) {
+          with_words(ix, [&](auto wt) {
+            constexpr int W = decltype(wt)::value;
+            k_lut_level<W><<<unsigned((cnt + 255) / 256), 256, 0, s>>>(ix->view(), pt.base + PrefixTable::off64(pt.k),
+                                                                      lx, cnt);
+          });
+          FMG_CK(cudaGetLastError());
+          FMG_CK(cudaStreamSynchronize(s));
+          ix->lut_x = lx;
+          ix->lut_x_k = kx;
+        } else {
+          cudaGetLastError();  // clear the failed allocation; keep level K
+        }
+      }
+    }
+    if (ix->lut_x) return KmerTable{ix->lut_x, ix->lut_x_k};
+  }
   return KmerTable{pt.base + PrefixTable::off64(pt.k), pt.k};
 }
 
@@ -1248,6 +1293,7 @@ void fmg_index_destroy(fmg_index* ix) {
   if (ix->lines) cudaFree(ix->lines);
   if (ix->lut) cudaFree(ix->lut);
   if (ix->lut_r) cudaFree(ix->lut_r);
+  if (ix->lut_x) cudaFree(ix->lut_x);
   if (ix->rev_lines) cudaFree(ix->rev_lines);
   if (ix->samples) cudaFree(ix->samples);
   if (ix->err) cudaFree(ix->err);
@@ -1312,6 +1358,19 @@ int fmgx_prefix_table(const fmg_index* ix, uint32_t* k_out, uint64_t* bytes_out)
     const PrefixTable pt = prefix_table(ix, 1u << 20, nullptr);
     if (k_out) *k_out = pt.k;
     if (bytes_out) *bytes_out = pt.base ? PrefixTable::off64(pt.k + 1) * sizeof(uint2) : 0;
+  });
+}
+
+// Builds the exact search's k-mer table now (kmer_table: the prefix table's
+// level K, or the level-(K + 1) extension); reports its K and the bytes of
+// the extension (0 when exact search uses level K of the prefix table).
+int fmgx_kmer_table(const fmg_index* ix, uint32_t* k_out, uint64_t* ext_bytes_out) {
+  return fmg::guard([&] {
+    check_index(ix);
+    fmg::DeviceScope scope(ix->device);
+    const KmerTable kt = kmer_table(ix, 1u << 20, nullptr);
+    if (k_out) *k_out = kt.k;
+    if (ext_bytes_out) *ext_bytes_out = ix->lut_x ? (uint64_t(1) << (2 * ix->lut_x_k)) * sizeof(uint2) : 0;
   });
 }
 

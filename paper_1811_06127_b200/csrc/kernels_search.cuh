@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(256) k_exact(IndexView ix, PackedPatterns pp, 
     if (kt.lut && m >= kt.k) {  // start after the last K characters
       uint32_t key = 0;
       if (kPacked) {
-        key = uint32_t(pat >> (2 * (m - kt.k))) & ((1u << (2 * kt.k)) - 1u);
+        key = uint32_t((pat >> (2 * (m - kt.k))) & ((uint64_t(1) << (2 * kt.k)) - 1u));  // K <= 16
       } else {
         for (uint32_t t = 0; t < kt.k; ++t) key |= uint32_t(__ldg(codes + m - kt.k + t) & 3u) << (2 * t);
       }
