@@ -91,8 +91,12 @@ __device__ __forceinline__ void children4(const IndexView& v, const PrefixTable&
 
 // kOnly: 0 = both cases per pattern (one result list), 1 = case A only,
 // 3 = case B only (phase-uniform launches; k_merge_ab joins the two lists).
+#ifndef FMG_BI_MINB
+#define FMG_BI_MINB 7  // resident blocks per SM the register budget is sized for
+#endif
+
 template <int W, int kOnly>
-__global__ void __launch_bounds__(128, 7) k_inexact_bi(IndexView ix, BiIndex bi, CodePatterns cp,
+__global__ void __launch_bounds__(128, FMG_BI_MINB) k_inexact_bi(IndexView ix, BiIndex bi, CodePatterns cp,
                                                     const uint32_t* __restrict__ list, uint64_t count,
                                                     InexactScratch sc, InexactOut out) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -261,24 +265,43 @@ __global__ void __launch_bounds__(128, 7) k_inexact_bi(IndexView ix, BiIndex bi,
     return true;
   };
 
+  // The next pattern is claimed and its words loaded while the current one
+  // is searched, so starting a pattern never waits on the queue atomic and
+  // the pattern loads (they would stall the whole warp for the lanes that
+  // start).
+  uint64_t nq = 0, npw0 = 0, npw1 = 0, ndbits = 0;
+  int nm = 0;
+  bool nvalid = false;
+  auto prefetch = [&]() {
+    const unsigned long long slot = atomicAdd(out.next, 1ull);
+    nvalid = slot < count;
+    if (!nvalid) return;
+    nq = list ? list[slot] : slot;
+    if (cp.packed1) {
+      nm = int(cp.fixed_m);
+      npw0 = cp.packed1[nq];
+      npw1 = 0;
+    } else {
+      nm = int(cp.offsets[nq + 1] - cp.offsets[nq]);
+      const ulonglong2 pk = cp.packed[nq];
+      npw0 = pk.x;
+      npw1 = pk.y;
+    }
+    ndbits = cp.dbits[nq];
+  };
+  prefetch();
+
   while (true) {
     bool stepping = false;
     while (!stepping) {
       if (!have) {
-        const unsigned long long slot = atomicAdd(out.next, 1ull);
-        if (slot >= count) break;
-        q = list ? list[slot] : slot;
-        if (cp.packed1) {
-          m = int(cp.fixed_m);
-          pw0 = cp.packed1[q];
-          pw1 = 0;
-        } else {
-          m = int(cp.offsets[q + 1] - cp.offsets[q]);
-          const ulonglong2 pk = cp.packed[q];
-          pw0 = pk.x;
-          pw1 = pk.y;
-        }
-        dbits = cp.dbits[q];
+        if (!nvalid) break;
+        q = nq;
+        m = nm;
+        pw0 = npw0;
+        pw1 = npw1;
+        dbits = ndbits;
+        prefetch();
         h = m / 2;
         sp = nres = 0;
         ++epoch;
@@ -320,8 +343,13 @@ __global__ void __launch_bounds__(128, 7) k_inexact_bi(IndexView ix, BiIndex bi,
     if (!stepping) break;
 
     // ---- one step: the four children of the node's string ----
+    // (a compile-time `fwd` for the split launches measured slower: case B
+    // 83 -> 99 ms per 14M config-3 seeds, register spills)
     const bool fwd = phase == 3;
     uint32_t ck[4], cl[4];
+    // (One shared pair of loads for every node kind, selecting addresses
+    // first, measured no faster for case A and slower for case B: 79.6 ->
+    // 79.1 ms and 83.5 -> 97 ms per 14M config-3 seeds.)
 #if FMG_BI_OCC1
     // case-A budget-0 node: only the symbol W[i] is needed (one-symbol count)
     const bool one = !fwd && cb == 0u && !csh;
