@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(256) k_exact(IndexView ix, PackedPatterns pp, 
         for (uint32_t t = 0; t < kt.k; ++t) key |= uint32_t(__ldg(codes + m - kt.k + t) & 3u) << (2 * t);
       }
       const uint2 e = __ldg(kt.lut + key);
+      work += 1u;  // one random table gather: counted as a fetched line, not as an Occ step
       k = e.x;
       l = e.y;
       i = int(m) - 1 - int(kt.k);
