@@ -779,9 +779,9 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     if (bidir_split) {
       // ---- pass 0 = case-A launch + case-B launch + merge (kernels_bidir.cuh) ----
       const uint32_t Sp = 9;  // z = 1: one budget-1 node's children at a time
-      const size_t ebytes = 20;
       const int nt = 128;
-      const size_t smem = size_t(Sp + 1) * ebytes * nt;
+      // stack entries: 12 bytes for case A (one interval), 20 for case B
+      const size_t smemA = size_t(Sp + 1) * 12 * nt, smem = size_t(Sp + 1) * 20 * nt;
       FMG_REQUIRE(smem <= size_t(smem_optin), "inexact search stack does not fit in shared memory");
       const void* kA = nullptr;
       const void* kB = nullptr;
@@ -789,11 +789,13 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
         kA = (const void*)k_inexact_bi<decltype(wt)::value, 1>;
         kB = (const void*)k_inexact_bi<decltype(wt)::value, 3>;
       });
-      FMG_CK(cudaFuncSetAttribute(kA, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      FMG_CK(cudaFuncSetAttribute(kA, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemA)));
       FMG_CK(cudaFuncSetAttribute(kB, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       int per_sm = 0;
-      FMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kA, nt, smem));
-      per_sm = std::max(per_sm, 1);
+      int per_sm_b = 0;
+      FMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kA, nt, smemA));
+      FMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_b, kB, nt, smem));
+      per_sm = std::max(std::max(per_sm, per_sm_b), 1);  // T sized for the more resident of the two
       const uint64_t per_thread = uint64_t(R) * (2 * 16 + 4);
       uint64_t T = uint64_t(per_sm) * ix->sms * nt;
       T = std::min<uint64_t>(T, std::max<uint64_t>(nt, std::max<uint64_t>(2ull << 30, free_b / 8) / per_thread));
@@ -844,7 +846,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
         with_words(ix, [&](auto wt) {
           constexpr int W = decltype(wt)::value;
           if (half == 0)
-            k_inexact_bi<W, 1><<<unsigned(T / nt), nt, smem, s>>>(ix->view(), bi, cp, nullptr, count, sc, o);
+            k_inexact_bi<W, 1><<<unsigned(T / nt), nt, smemA, s>>>(ix->view(), bi, cp, nullptr, count, sc, o);
           else
             k_inexact_bi<W, 3><<<unsigned(T / nt), nt, smem, s>>>(ix->view(), bi, cp, nullptr, count, sc, o);
         });

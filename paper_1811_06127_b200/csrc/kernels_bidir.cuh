@@ -62,6 +62,14 @@ __device__ __forceinline__ uint32_t pat_rkey(uint64_t pw0, uint64_t pw1, int a, 
   return key;
 }
 
+// The key of a len-character string read backwards: its 2-bit fields in
+// reverse order (len <= 16).
+__device__ __forceinline__ uint32_t pair_rev(uint32_t key, uint32_t len) {
+  uint32_t v = __brev(key);
+  v = ((v >> 1) & 0x55555555u) | ((v & 0x55555555u) << 1);  // bit pairs back in order
+  return len == 0u ? 0u : v >> (32u - 2u * len);
+}
+
 // The four child intervals of (k, l) on index v: from the prefix table
 // (shallow: key, depth) or by one Occ step on the index lines.
 template <int W>
@@ -91,6 +99,14 @@ __device__ __forceinline__ void children4(const IndexView& v, const PrefixTable&
 
 // kOnly: 0 = both cases per pattern (one result list), 1 = case A only,
 // 3 = case B only (phase-uniform launches; k_merge_ab joins the two lists).
+#ifndef FMG_BI_JUMP
+#define FMG_BI_JUMP 1  // budget-0 chains jump through the prefix tables in one gather
+#endif
+#ifndef FMG_BI_JUMP_B
+// case B too: measured slower (83 -> 104 ms per 14M config-3 seeds) — the
+// extra live state makes the case-B kernel spill at 72 registers
+#define FMG_BI_JUMP_B 0
+#endif
 #ifndef FMG_BI_MINB
 #define FMG_BI_MINB 7  // resident blocks per SM the register budget is sized for
 #endif
@@ -101,8 +117,46 @@ __global__ void __launch_bounds__(128, FMG_BI_MINB) k_inexact_bi(IndexView ix, B
                                                     InexactScratch sc, InexactOut out) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t S = sc.S, nt = blockDim.x, tid = threadIdx.x;
-  uint4* s_x = reinterpret_cast<uint4*>(smem);                      // [S + 1][nt]
-  uint32_t* s_ib = reinterpret_cast<uint32_t*>(s_x + (S + 1) * nt);  // [S + 1][nt]; slot S: push dump
+  // Stack entries: case A (kOnly == 1) needs only the interval (or key,
+  // depth) — 8 bytes + 4 bytes of position/budget; the other forms carry
+  // both intervals of case B — 16 + 4 bytes.  Slot S is the push dump.
+  constexpr bool kNarrow = kOnly == 1;
+  uint4* s_x = reinterpret_cast<uint4*>(smem);                                   // [S + 1][nt] (wide)
+  uint2* s_xy = reinterpret_cast<uint2*>(smem);                                  // [S + 1][nt] (narrow)
+  uint32_t* s_ib = kNarrow ? reinterpret_cast<uint32_t*>(s_xy + (S + 1) * nt)   // [S + 1][nt]
+                           : reinterpret_cast<uint32_t*>(s_x + (S + 1) * nt);
+  auto st_put = [&](uint32_t slot, uint32_t x, uint32_t y, uint32_t zz, uint32_t ww) {
+    if constexpr (kNarrow) {
+      s_xy[slot * nt + tid] = make_uint2(x, y);
+    } else {
+      s_x[slot * nt + tid] = make_uint4(x, y, zz, ww);
+    }
+  };
+  auto st_get = [&](uint32_t slot) -> uint4 {
+    if constexpr (kNarrow) {
+      const uint2 v = s_xy[slot * nt + tid];
+      return make_uint4(v.x, v.y, 0u, 0u);
+    } else {
+      return s_x[slot * nt + tid];
+    }
+  };
+  // result sort scratch (the stack is empty by then): (k, l) + diffs
+  auto so_put = [&](uint32_t slot, uint32_t k, uint32_t l, uint32_t d) {
+    if constexpr (kNarrow) {
+      s_xy[slot * nt + tid] = make_uint2(k, l);
+      s_ib[slot * nt + tid] = d;
+    } else {
+      s_x[slot * nt + tid] = make_uint4(k, l, d, 0u);
+    }
+  };
+  auto so_get = [&](uint32_t slot) -> uint4 {
+    if constexpr (kNarrow) {
+      const uint2 v = s_xy[slot * nt + tid];
+      return make_uint4(v.x, v.y, s_ib[slot * nt + tid], 0u);
+    } else {
+      return s_x[slot * nt + tid];
+    }
+  };
   const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= sc.T) return;
   uint64_t my_steps = 0;
@@ -172,15 +226,15 @@ __global__ void __launch_bounds__(128, FMG_BI_MINB) k_inexact_bi(IndexView ix, B
           const uint4 e = sc.table[HI(sc.slots[LI(r)])];
           uint32_t b = r;
           while (b > 0) {
-            const uint4 p = s_x[(b - 1) * nt + tid];
+            const uint4 p = so_get(b - 1);
             if (p.x < e.x || (p.x == e.x && p.y < e.y)) break;
-            s_x[b * nt + tid] = p;
+            so_put(b, p.x, p.y, p.z);
             --b;
           }
-          s_x[b * nt + tid] = make_uint4(e.x, e.y, e.w, 0u);
+          so_put(b, e.x, e.y, e.w);
         }
         for (uint32_t r = 0; r < nres; ++r) {
-          const uint4 p = s_x[r * nt + tid];
+          const uint4 p = so_get(r);
           out.kl[o + r] = make_uint2(p.x, p.y);
           out.diffs[o + r] = uint8_t(p.z);
         }
@@ -202,7 +256,7 @@ __global__ void __launch_bounds__(128, FMG_BI_MINB) k_inexact_bi(IndexView ix, B
     const bool ok = cond && sp < S;
     overflow |= cond && sp >= S;
     const uint32_t slot = ok ? sp : S;
-    s_x[slot * nt + tid] = make_uint4(x, y, zz, ww);
+    st_put(slot, x, y, zz, ww);
     s_ib[slot * nt + tid] = (uint32_t(pos + 1) << 16) | (psh ? 0x8000u : 0u) | pb;
     sp += ok ? 1u : 0u;
   };
@@ -318,7 +372,7 @@ __global__ void __launch_bounds__(128, FMG_BI_MINB) k_inexact_bi(IndexView ix, B
       if (!cur_valid) {
         if (sp > 0) {
           --sp;
-          const uint4 e = s_x[sp * nt + tid];
+          const uint4 e = st_get(sp);
           const uint32_t ib = s_ib[sp * nt + tid];
           ci = int(ib >> 16) - 1;
           cb = ib & 0xFFu;
@@ -341,6 +395,64 @@ __global__ void __launch_bounds__(128, FMG_BI_MINB) k_inexact_bi(IndexView ix, B
       stepping = true;
     }
     if (!stepping) break;
+
+    // ---- budget-0 node inside the prefix tables' depth range: jump ----
+    // Its string grows by known pattern characters only, so the node t =
+    // min(characters left, K - depth) levels down is ONE table gather away
+    // instead of t dependent ones.  Case A prepends W[i], W[i-1], ... (key
+    // of W[i-t+1..i] below the node's key); case B appends W[j..j+t-1]: the
+    // reverse key grows the same way and the forward interval is read from
+    // the forward table under the bit-pair-reversed key (for a non-empty
+    // string the table entry IS the interval the 2BWT update computes; an
+    // empty one ends the chain either way).  Chains that reach depth K
+    // continue on the index lines with explicit intervals.
+    constexpr bool kJumpA = FMG_BI_JUMP && kOnly != 3, kJumpB = FMG_BI_JUMP_B && kOnly != 1;
+    if (cb == 0u && csh && ((kJumpA && phase != 3) || (kJumpB && phase == 3))) {
+      if (phase != 3) {  // case A
+        const uint32_t t = min(uint32_t(ci) + 1u, K - cy);
+        const uint32_t d = cy + t;
+        const uint32_t key = pat_key(pw0, pw1, ci - int(t) + 1, int(t)) | (cx << (2u * t));
+        const uint2 e = __ldg(bi.tf.base + PrefixTable::off(d) + key);
+        my_steps += work_unit(1u);
+        if (e.x > e.y) {
+          cur_valid = false;
+        } else if (uint32_t(ci) + 1u == t) {
+          record(e.x, e.y, 1u);
+          cur_valid = false;
+        } else {
+          ci -= int(t);
+          cx = e.x;
+          cy = e.y;
+          csh = false;
+          cur_valid = dlb(ci) == 0u;
+        }
+      } else {  // case B
+        const uint32_t t = min(uint32_t(m - ci), K - cw);
+        const uint32_t d = cw + t;
+        // forward key of S = the node's reverse key with its bit pairs
+        // reversed; S' = S + W[j..j+t-1] appends the pattern's key above it
+        const uint32_t fkey = pair_rev(cz, cw) | (pat_key(pw0, pw1, ci, int(t)) << (2u * cw));
+        const uint2 f = __ldg(bi.tf.base + PrefixTable::off(d) + fkey);
+        const bool done = uint32_t(m - ci) == t;
+        uint2 r = make_uint2(0u, 0u);
+        if (!done) r = __ldg(bi.tr.base + PrefixTable::off(d) + pair_rev(fkey, d));
+        my_steps += work_unit(done ? 1u : 2u);
+        if (f.x > f.y) {
+          cur_valid = false;
+        } else if (done) {
+          record(f.x, f.y, 1u);
+          cur_valid = false;
+        } else {
+          ci += int(t);
+          cx = f.x;
+          cy = f.y;
+          cz = r.x;
+          cw = r.y;
+          csh = false;
+        }
+      }
+      continue;
+    }
 
     // ---- one step: the four children of the node's string ----
     // (a compile-time `fwd` for the split launches measured slower: case B
