@@ -509,8 +509,10 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
         d_kl = torch.from_numpy(kl_h.view(np.int32)).to(dev)
         d_out = torch.empty((units, 8), dtype=torch.int32, device=dev)
 
+        args_ = (dix.handle, d_kl.data_ptr(), units, d_out.data_ptr(), sp)  # resolved once, outside the loop
+
         def step():
-            rc = lib.fmg_occ_pair(dix.handle, d_kl.data_ptr(), units, d_out.data_ptr(), sp)
+            rc = lib.fmg_occ_pair(*args_)
             if rc:
                 _lib.check(rc)
 
@@ -531,8 +533,10 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
             d_pat = torch.from_numpy(packed.view(np.int64)).to(dev)
             d_out = torch.empty((units, 2), dtype=torch.int32, device=dev)
 
+            args_ = (dix.handle, d_pat.data_ptr(), m, units, d_out.data_ptr(), sp)  # resolved once
+
             def step():
-                rc = lib.fmg_exact_packed(dix.handle, d_pat.data_ptr(), m, units, d_out.data_ptr(), sp)
+                rc = lib.fmg_exact_packed(*args_)
                 if rc:
                     _lib.check(rc)
 

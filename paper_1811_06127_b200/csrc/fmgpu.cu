@@ -17,6 +17,7 @@
 #include <type_traits>
 #include <string>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
@@ -262,9 +263,40 @@ void launch_occ_pair(const fmg_index* ix, const uint32_t* kl, uint64_t count, ui
   }
 }
 
-unsigned persistent_blocks(const fmg_index* ix, const void* kernel, int threads, uint64_t work) {
+// Resident blocks per SM of (kernel, threads, dynamic smem), cached: the
+// occupancy query costs about a microsecond of host time, which small
+// latency-bound batches (config 0: 23 us per call) cannot hide.
+int blocks_per_sm(const void* kernel, int threads, size_t smem) {
+  struct Key {
+    const void* k;
+    int t;
+    size_t s;
+    bool operator==(const Key& o) const { return k == o.k && t == o.t && s == o.s; }
+  };
+  struct Hash {
+    size_t operator()(const Key& x) const {
+      return std::hash<const void*>()(x.k) ^ (size_t(x.t) << 40) ^ (x.s << 8);
+    }
+  };
+  static std::mutex mu;
+  static std::unordered_map<Key, int, Hash> cache;
+  int dev = 0;
+  FMG_CK(cudaGetDevice(&dev));
+  const Key key{kernel, threads * 64 + dev, smem};  // one entry per device (same GPU model in practice)
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
   int per_sm = 0;
-  FMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0));
+  FMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+  std::lock_guard<std::mutex> lock(mu);
+  cache[key] = per_sm;
+  return per_sm;
+}
+
+unsigned persistent_blocks(const fmg_index* ix, const void* kernel, int threads, uint64_t work) {
+  const int per_sm = blocks_per_sm(kernel, threads, 0);
   static const int mult = [] {
     const char* e = std::getenv("FMG_GRID_MULT");  // tuning hook: waves of the persistent grid
     return e ? std::max(1, std::atoi(e)) : 1;
@@ -405,16 +437,24 @@ KmerTable kmer_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
   return KmerTable{pt.base + PrefixTable::off64(pt.k), pt.k};
 }
 
+// Block size of the exact kernels: small batches (config 0: 10,000
+// patterns) in 64-thread blocks so every SM gets some of the dependent
+// chains instead of 40 blocks of 256 on 40 SMs.
+int exact_block_threads(const fmg_index* ix, uint64_t count) {
+  return count < uint64_t(ix->sms) * 1024u ? 64 : 256;
+}
+
 void launch_exact_packed(const fmg_index* ix, const uint64_t* packed, uint32_t m, uint64_t count, uint32_t* kl_out,
                          cudaStream_t s, unsigned long long* steps) {
   if (count == 0) return;
   PackedPatterns pp{packed, m};
   CodePatterns cp{nullptr, nullptr};
   const KmerTable kt = kmer_table(ix, count, s);
+  const int nt = exact_block_threads(ix, count);
   with_words(ix, [&](auto wt) {
     constexpr int W = decltype(wt)::value;
-    const unsigned blocks = wave_blocks(ix, (const void*)k_exact<true, W>, 256, count);
-    k_exact<true, W><<<blocks, 256, 0, s>>>(ix->view(), pp, cp, count, reinterpret_cast<uint2*>(kl_out), steps, kt);
+    const unsigned blocks = wave_blocks(ix, (const void*)k_exact<true, W>, nt, count);
+    k_exact<true, W><<<blocks, nt, 0, s>>>(ix->view(), pp, cp, count, reinterpret_cast<uint2*>(kl_out), steps, kt);
   });
   FMG_CK(cudaGetLastError());
 }
@@ -425,11 +465,12 @@ void launch_exact_codes(const fmg_index* ix, const uint8_t* codes, const uint64_
   PackedPatterns pp{nullptr, 0};
   CodePatterns cp{codes, offsets};
   const KmerTable kt = kmer_table(ix, count, s);
+  const int nt = exact_block_threads(ix, count);
   with_words(ix, [&](auto wt) {
     constexpr int W = decltype(wt)::value;
-    const unsigned blocks = wave_blocks(ix, (const void*)k_exact<false, W>, 256, count);
-    k_exact<false, W><<<blocks, 256, 0, s>>>(ix->view(), pp, cp, count, reinterpret_cast<uint2*>(kl_out), steps,
-                                             kt);
+    const unsigned blocks = wave_blocks(ix, (const void*)k_exact<false, W>, nt, count);
+    k_exact<false, W><<<blocks, nt, 0, s>>>(ix->view(), pp, cp, count, reinterpret_cast<uint2*>(kl_out), steps,
+                                            kt);
   });
   FMG_CK(cudaGetLastError());
 }
