@@ -145,6 +145,13 @@ struct fmg_index {
   uint2* lut_x = nullptr;
   uint32_t lut_x_k = 0;
   bool lut_x_tried = false;
+  // dedup hash table of the inexact engines, kept between calls with a
+  // monotone epoch so it is zeroed only when allocated or when the epochs
+  // wrap (EpochTable)
+  std::mutex ep_mu;
+  uint4* ep_table = nullptr;
+  uint64_t ep_entries = 0;
+  uint64_t ep_next = 1;
 
   fmg::IndexView view_rev() const {
     fmg::IndexView v = view();
@@ -506,6 +513,51 @@ uint64_t validate_patterns_device(const uint8_t* codes, const uint64_t* offsets,
 }
 
 
+// The inexact engines' dedup table for one launch: `entries` uint4 slots
+// whose current contents all carry epochs <= epoch0, and room for
+// `epochs` more per thread.  The index's persistent table is leased when
+// free (zeroed only when (re)allocated or when the epochs would wrap; a
+// 1.1 GB memset per launch was 10% of a config-2 call); a concurrent call
+// gets a zeroed table of its own.
+struct EpochTable {
+  uint4* ptr = nullptr;
+  uint32_t epoch0 = 0;
+  DevBuf<uint4> own;
+  std::unique_lock<std::mutex> lease;
+};
+
+void lease_epoch_table(fmg_index* ix, uint64_t entries, uint64_t epochs, cudaStream_t s, EpochTable& t) {
+  std::unique_lock<std::mutex> lk(ix->ep_mu, std::try_to_lock);
+  // only first-pass sized tables (<= 2 GiB) are kept; retry passes with
+  // grown capacities get their own
+  if (!lk.owns_lock() || epochs >= 0x7FFFFFFFull || entries * sizeof(uint4) > (size_t(2) << 30)) {
+    t.own = DevBuf<uint4>(entries, s);
+    FMG_CK(cudaMemsetAsync(t.own.ptr, 0, entries * sizeof(uint4), s));  // epoch 0 = empty
+    t.ptr = t.own.ptr;
+    t.epoch0 = 0;
+    return;
+  }
+  if (ix->ep_entries < entries) {
+    if (ix->ep_table) {
+      FMG_CK(cudaStreamSynchronize(s));  // no launch of this index may still use it (we hold the lease)
+      FMG_CK(cudaFree(ix->ep_table));
+      ix->ep_table = nullptr;
+      ix->ep_entries = 0;
+    }
+    FMG_CK(cudaMalloc(&ix->ep_table, entries * sizeof(uint4)));
+    ix->ep_entries = entries;
+    ix->ep_next = 0xFFFFFFFFull;  // forces the zeroing below
+  }
+  if (ix->ep_next + epochs >= 0xFFFFFFFFull) {
+    FMG_CK(cudaMemsetAsync(ix->ep_table, 0, ix->ep_entries * sizeof(uint4), s));
+    ix->ep_next = 0;
+  }
+  t.ptr = ix->ep_table;
+  t.epoch0 = uint32_t(ix->ep_next);
+  ix->ep_next += epochs;
+  t.lease = std::move(lk);
+}
+
 // z = 1 through k_spine / k_chain; false when a queue overflowed (the caller
 // then runs the DFS engine, which has no such limit).  Fills res on success.
 // Raw (pattern, k, l, used) results -> the CSR result set of `res`:
@@ -842,7 +894,8 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       T = std::min<uint64_t>(T, std::max<uint64_t>(nt, std::max<uint64_t>(2ull << 30, free_b / 8) / per_thread));
       T = std::min<uint64_t>(T, ((count + nt - 1) / nt) * nt);
       T = std::max<uint64_t>(nt, (T / nt) * nt);
-      DevBuf<uint4> table(uint64_t(2 * R) * T, s);
+      EpochTable table;
+      lease_epoch_table(const_cast<fmg_index*>(ix), uint64_t(2 * R) * T, 2 * (count + 1), s, table);
       DevBuf<uint32_t> slots(uint64_t(R) * T, s);
       InexactScratch sc{};
       sc.table = table.ptr;
@@ -866,7 +919,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       unsigned long long n_unsorted[2] = {0, 0};
       for (int half = 0; half < 2; ++half) {
         if (trace_split) cudaEventRecord(sev[2 * half], s);
-        FMG_CK(cudaMemsetAsync(table.ptr, 0, uint64_t(2 * R) * T * sizeof(uint4), s));  // epoch 0 = empty
+        sc.epoch0 = table.epoch0 + uint32_t(half) * uint32_t(count + 1);  // each half its own epochs
         FMG_CK(cudaMemsetAsync(counters.ptr, 0, 2 * sizeof(unsigned long long), s));
         FMG_CK(cudaMemsetAsync(counters.ptr + 4, 0, 2 * sizeof(unsigned long long), s));
         InexactOut o{};
@@ -979,11 +1032,12 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       T = std::min<uint64_t>(T, ((pending + nt - 1) / nt) * nt);
       T = std::max<uint64_t>(nt, (T / nt) * nt);
       InexactScratch sc{};
-      DevBuf<uint4> table(uint64_t(2 * R) * T, s);
+      EpochTable table;
+      lease_epoch_table(const_cast<fmg_index*>(ix), uint64_t(2 * R) * T, pending + 1, s, table);
       DevBuf<uint32_t> slots(uint64_t(R) * T, s);
       DevBuf<uint8_t> dl(short_pat ? 0 : max_len * T, s);
-      FMG_CK(cudaMemsetAsync(table.ptr, 0, uint64_t(2 * R) * T * sizeof(uint4), s));  // epoch 0 = empty
       sc.table = table.ptr;
+      sc.epoch0 = table.epoch0;
       sc.slots = slots.ptr;
       sc.dlb = dl.ptr;
       sc.S = Sp;
@@ -1337,6 +1391,7 @@ void fmg_index_destroy(fmg_index* ix) {
   if (ix->lut) cudaFree(ix->lut);
   if (ix->lut_r) cudaFree(ix->lut_r);
   if (ix->lut_x) cudaFree(ix->lut_x);
+  if (ix->ep_table) cudaFree(ix->ep_table);
   if (ix->rev_lines) cudaFree(ix->rev_lines);
   if (ix->samples) cudaFree(ix->samples);
   if (ix->err) cudaFree(ix->err);

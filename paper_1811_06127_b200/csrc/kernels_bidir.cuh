@@ -111,8 +111,12 @@ __device__ __forceinline__ void children4(const IndexView& v, const PrefixTable&
 #define FMG_BI_MINB 7  // resident blocks per SM the register budget is sized for
 #endif
 
+#ifndef FMG_BI_MINB_B
+#define FMG_BI_MINB_B FMG_BI_MINB
+#endif
+
 template <int W, int kOnly>
-__global__ void __launch_bounds__(128, FMG_BI_MINB) k_inexact_bi(IndexView ix, BiIndex bi, CodePatterns cp,
+__global__ void __launch_bounds__(128, kOnly == 3 ? FMG_BI_MINB_B : FMG_BI_MINB) k_inexact_bi(IndexView ix, BiIndex bi, CodePatterns cp,
                                                     const uint32_t* __restrict__ list, uint64_t count,
                                                     InexactScratch sc, InexactOut out) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(128, FMG_BI_MINB) k_inexact_bi(IndexView ix, B
   const uint64_t wbase = t >> 5, lane = t & 31u;
   auto HI = [&](uint32_t e) -> uint64_t { return (wbase * (2u * sc.R) + e) * 32u + lane; };
   auto LI = [&](uint32_t e) -> uint64_t { return (wbase * sc.R + e) * 32u + lane; };
-  uint32_t epoch = 0;
+  uint32_t epoch = sc.epoch0;
   const uint32_t K = bi.tf.k;
   const uint32_t sent_r = bi.rev.sentinel_row;
 

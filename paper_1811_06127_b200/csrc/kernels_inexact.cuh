@@ -87,6 +87,9 @@ struct InexactScratch {
   uint8_t* dlb;     // Mmax entries: lower bound D[i] (long patterns only)
   uint32_t S, R, Mmax;
   uint64_t T;
+  // first pattern of each thread uses epoch0 + 1; every entry already in
+  // the table carries an epoch <= epoch0 (EpochTable), so it reads as empty
+  uint32_t epoch0;
 };
 
 struct InexactOut {
@@ -167,7 +170,7 @@ __global__ void __launch_bounds__(128) k_inexact(IndexView ix, CodePatterns cp, 
   const uint64_t wbase = t >> 5, lane = t & 31u;
   auto HI = [&](uint32_t e) -> uint64_t { return (wbase * (2u * sc.R) + e) * 32u + lane; };
   auto LI = [&](uint32_t e) -> uint64_t { return (wbase * sc.R + e) * 32u + lane; };
-  uint32_t epoch = 0;  // per-thread pattern counter: table slots of older patterns read as empty
+  uint32_t epoch = sc.epoch0;  // per-thread pattern counter: table slots of older patterns read as empty
   auto DI = [&](uint32_t e) -> uint64_t { return (wbase * sc.Mmax + e) * 32u + lane; };
 
   // per-pattern state

@@ -487,3 +487,29 @@ def test_inexact_bidirectional_engine(gpu, monkeypatch, n, lens, engine):
     b = fm.inexact_search_batch(idx, pats, 1)
     assert np.array_equal(b.offsets, ms.offsets) and np.array_equal(b.k, ms.k) and np.array_equal(b.diffs, ms.diffs)
     assert ms.steps < b.steps  # the point of the engine
+
+
+def test_inexact_repeated_calls_reuse_dedup_table(gpu, monkeypatch):
+    """The dedup hash table persists in the index between calls (epoch-tagged, zeroed only on
+    allocation): back-to-back calls with different batches, budgets and engines on one index
+    must each equal the oracle — stale entries of earlier calls never read as results."""
+    monkeypatch.setenv("FMG_BIDIR_MIN_N", "0")
+    rng = np.random.Generator(np.random.PCG64(4242))
+    text = rng.integers(0, 4, 300_000, dtype=np.uint8)
+    idx = fm.build_index(text)
+    ox = orc.OracleIndex(idx)
+    for call, (z, n_pat, m, env) in enumerate([(1, 3000, 20, None), (1, 1500, 24, None), (2, 1200, 16, None),
+                                               (1, 3000, 20, "FMG_INEXACT_BIDIR"), (1, 2000, 18, None)]):
+        if env:
+            monkeypatch.setenv(env, "0")
+        pats = workloads.substrings(text, rng.integers(0, text.size - m + 1, n_pat), m).copy()
+        mut = rng.random(n_pat) < 0.5
+        pos = rng.integers(0, m, n_pat)
+        pats[mut, pos[mut]] = (pats[mut, pos[mut]] + 1) % 4
+        ms = fm.inexact_search_batch(idx, pats, z)
+        row, k, l, d, _ = orc.inexact_batch(ox, pats, z)
+        assert np.array_equal(ms.offsets, row), call
+        assert np.array_equal(ms.k.astype(np.int64), k) and np.array_equal(ms.l.astype(np.int64), l), call
+        assert np.array_equal(ms.diffs, d), call
+        if env:
+            monkeypatch.delenv(env)
