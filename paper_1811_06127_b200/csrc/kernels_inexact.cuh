@@ -859,17 +859,38 @@ __global__ void k_pack_patterns(const uint8_t* __restrict__ codes, const uint64_
 __global__ void k_check_patterns(const uint8_t* __restrict__ codes, const uint64_t* __restrict__ offsets,
                                  uint64_t count, unsigned long long* __restrict__ max_len,
                                  uint32_t* __restrict__ err) {
+  // One thread per pattern for the offsets, a grid-stride scan of the code
+  // bytes in 8-byte words, and one atomic per warp (a per-thread atomicMax
+  // on one address serialised 1M patterns into 660 us on B200).
   const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (q >= count) return;
-  const uint64_t a = offsets[q], b = offsets[q + 1];
-  if (q == 0 && a != 0) atomicOr(err, 4u);
-  if (b <= a) {
-    atomicOr(err, 1u);
-    return;
+  const unsigned lane = threadIdx.x & 31u;
+  uint32_t len = 0, flags = 0;
+  if (q < count) {
+    const uint64_t a = offsets[q], b = offsets[q + 1];
+    if (q == 0 && a != 0) flags |= 4u;
+    if (b <= a) flags |= 1u;
+    else len = uint32_t(b - a > 0xFFFFFFFFull ? 0xFFFFFFFFull : b - a);
   }
-  atomicMax(max_len, (unsigned long long)(b - a));
-  for (uint64_t j = a; j < b; ++j)
-    if (codes[j] > 3) atomicOr(err, 2u);
+  // codes[0 .. total) when offsets[0] == 0 (otherwise that error is
+  // reported and the codes are not scanned)
+  const uint64_t total = offsets[0] == 0 ? offsets[count] : 0;
+  const uint64_t nthreads = uint64_t(gridDim.x) * blockDim.x;
+  if ((reinterpret_cast<uintptr_t>(codes) & 7u) == 0) {
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(codes);
+    for (uint64_t i = q; i < total / 8; i += nthreads)
+      if (__ldg(w + i) & 0xFCFCFCFCFCFCFCFCull) flags |= 2u;  // a byte > 3
+    for (uint64_t j = total / 8 * 8 + q; j < total; j += nthreads)
+      if (codes[j] > 3) flags |= 2u;
+  } else {
+    for (uint64_t j = q; j < total; j += nthreads)
+      if (codes[j] > 3) flags |= 2u;
+  }
+  const uint32_t wl = __reduce_max_sync(0xFFFFFFFFu, len);
+  const uint32_t wf = __reduce_or_sync(0xFFFFFFFFu, flags);
+  if (lane == 0) {
+    if (wl) atomicMax(max_len, (unsigned long long)wl);
+    if (wf) atomicOr(err, wf);
+  }
 }
 
 __global__ void k_pack_keys(uint64_t n, const uint32_t* __restrict__ k, const uint32_t* __restrict__ l,

@@ -513,3 +513,50 @@ def test_inexact_repeated_calls_reuse_dedup_table(gpu, monkeypatch):
         assert np.array_equal(ms.diffs, d), call
         if env:
             monkeypatch.delenv(env)
+
+
+def test_device_pattern_validation_errors(gpu):
+    """Device-side pattern checks of the C ABI (k_check_patterns): a code > 3, an empty
+    pattern and offsets not starting at 0 are EINVAL with the reference's messages, at any
+    position in a large batch and from an unaligned codes pointer; a valid call still works."""
+    import ctypes as ct
+
+    import torch
+
+    from paper_1811_06127_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.Generator(np.random.PCG64(99))
+    text = rng.integers(0, 4, 50_000, dtype=np.uint8)
+    idx = fm.build_index(text)
+    dix = idx.device_index()
+    n, m = 100_000, 12
+    base = workloads.substrings(text, rng.integers(0, text.size - m + 1, n), m).reshape(-1)
+
+    def run(codes: np.ndarray, offs: np.ndarray, shift: int = 0, z: int = 1):
+        buf = torch.zeros(codes.size + 8, dtype=torch.uint8, device=gpu)
+        buf[shift:shift + codes.size] = torch.from_numpy(codes).to(gpu)
+        d_off = torch.from_numpy(offs.astype(np.int64)).to(gpu)
+        h = ct.c_void_p()
+        rc = lib.fmg_inexact(dix.handle, buf.data_ptr() + shift, d_off.data_ptr(), offs.size - 1, z, ct.byref(h), None)
+        if rc == 0:
+            lib.fmg_matches_free(h)
+        return rc, _lib.last_error()
+
+    offs = np.arange(0, (n + 1) * m, m, dtype=np.uint64)
+    for shift in (0, 1, 3):
+        assert run(base, offs, shift)[0] == 0
+        for pos in (0, 7, base.size // 2 + 5, base.size - 1):
+            bad = base.copy()
+            bad[pos] = 4 + pos % 200
+            rc, msg = run(bad, offs, shift)
+            assert rc == 1 and "symbol code" in msg, (shift, pos, rc, msg)
+    empty = offs.copy()
+    empty[n // 3 + 1] = empty[n // 3]  # pattern n//3 empty (and the next one twice as long)
+    rc, msg = run(base, empty)
+    assert rc == 1 and "empty" in msg, msg
+    rc, msg = run(base[m:], offs[1:] - offs[1] + m)  # offsets[0] = m != 0
+    assert rc == 1 and "start at 0" in msg, msg
+    ms = fm.inexact_search_batch(idx, base.reshape(n, m)[:2000], 1)  # still healthy
+    row, k, _, _, _ = orc.inexact_batch(orc.OracleIndex(idx), base.reshape(n, m)[:2000], 1)
+    assert np.array_equal(ms.offsets, row) and np.array_equal(ms.k.astype(np.int64), k)
