@@ -433,7 +433,9 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
             t_rev = time.perf_counter()
             dix.ensure_reverse()
             extra["reverse_index_build_s"] = round(time.perf_counter() - t_rev, 2)
-            extra["engine"] = "bidirectional z=1 (case-A / case-B DFS launches + merge)"
+            extra["engine"] = ("bidirectional z=1, level-synchronous (spine + chain kernels; L2-resident lines)"
+                               if dix.device_bytes <= (64 << 20) else
+                               "bidirectional z=1 (case-A / case-B DFS launches + merge)")
     if wl.pairs is None:  # search configs: the k-mer / prefix interval table, built before timing
         fn = lib.fmgx_prefix_table
         fn.argtypes = [ct.c_void_p, ct.POINTER(ct.c_uint32), ct.POINTER(ct.c_uint64)]

@@ -830,12 +830,15 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     }
     const void* kfn_bi = nullptr;
     with_words(ix, [&](auto wt) { kfn_bi = (const void*)k_inexact_bi<decltype(wt)::value, 0>; });
-    // bidirectional forms: "split" (default: phase-uniform case-A and case-B
-    // DFS launches + merge), "dfs" (both cases per thread), "sync"
-    // (level-synchronous spine + chain kernels); FMG_BIDIR_ENGINE selects.
-    const std::string bidir_engine = [] {
+    // bidirectional forms: "split" (phase-uniform case-A and case-B DFS
+    // launches + merge; default for HBM-resident indexes), "sync"
+    // (level-synchronous spine + chain kernels; default when the line array
+    // is L2-resident: config 2 5.9 -> 3.6 ms per 1M seeds, while on config 3
+    // its queued continuations re-fetch from DRAM), "dfs" (both cases per
+    // thread); FMG_BIDIR_ENGINE selects.
+    const std::string bidir_engine = [&] {
       const char* e = std::getenv("FMG_BIDIR_ENGINE");
-      return std::string(e ? e : "split");
+      return std::string(e ? e : line_bytes <= (uint64_t(64) << 20) ? "sync" : "split");
     }();
     const bool bidir_dfs = bidir_engine == "dfs";
     bool bidir_split = bidir && bidir_engine == "split";

@@ -326,13 +326,20 @@ def test_config4_first_chunk_vs_oracle(gpu):
 
 
 def test_z1_engines_agree(gpu, monkeypatch):
-    """z = 1 on an L2-resident repeat genome: the bidirectional split engine (default once a
-    reverse index is attached), the level-synchronous engine and the DFS engine give
-    identical result sets, equal to the oracle's."""
+    """z = 1 on an L2-resident repeat genome: the bidirectional engine (default once a
+    reverse index is attached) in its level-synchronous (default here), split and per-thread
+    forms, the one-directional level-synchronous engine and the DFS engine give identical
+    result sets, equal to the oracle's."""
     wl = workloads.config2(n_reads=20_000, n=8_000_000)
     idx = fm.build_index(wl.text)
-    a = fm.inexact_search_batch(idx, wl.patterns, 1)  # >= BIDIR_MIN_N: bidirectional split
+    a = fm.inexact_search_batch(idx, wl.patterns, 1)  # >= BIDIR_MIN_N: bidirectional, sync form
     assert idx.device_index()._has_reverse
+    for eng in ("split", "dfs"):
+        monkeypatch.setenv("FMG_BIDIR_ENGINE", eng)
+        x = fm.inexact_search_batch(idx, wl.patterns, 1)
+        assert np.array_equal(a.offsets, x.offsets) and np.array_equal(a.k, x.k), eng
+        assert np.array_equal(a.l, x.l) and np.array_equal(a.diffs, x.diffs), eng
+    monkeypatch.delenv("FMG_BIDIR_ENGINE")
     monkeypatch.setenv("FMG_INEXACT_BIDIR", "0")
     c = fm.inexact_search_batch(idx, wl.patterns, 1)  # level-synchronous z1 engine
     monkeypatch.setenv("FMG_INEXACT_DFS", "1")
