@@ -881,9 +881,15 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       FMG_REQUIRE(smem <= size_t(smem_optin), "inexact search stack does not fit in shared memory");
       const void* kA = nullptr;
       const void* kB = nullptr;
+      static const bool one_word_ok = [] {  // FMG_BI_ONEWORD=0: the two-word kernels (A/B)
+        const char* e = std::getenv("FMG_BI_ONEWORD");
+        return e == nullptr || std::atoi(e) != 0;
+      }();
+      const bool one_word = one_word_ok && max_len <= 32;  // patterns in one 64-bit word: the kOne kernels
       with_words(ix, [&](auto wt) {
-        kA = (const void*)k_inexact_bi<decltype(wt)::value, 1>;
-        kB = (const void*)k_inexact_bi<decltype(wt)::value, 3>;
+        constexpr int W = decltype(wt)::value;
+        kA = one_word ? (const void*)k_inexact_bi<W, 1, true> : (const void*)k_inexact_bi<W, 1, false>;
+        kB = (const void*)k_inexact_bi<W, 3, false>;  // (kOne for case B spills at 72 registers: 83 -> 98 ms)
       });
       FMG_CK(cudaFuncSetAttribute(kA, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemA)));
       FMG_CK(cudaFuncSetAttribute(kB, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -942,10 +948,12 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
         o.unsorted_list = unsorted_list.ptr;
         with_words(ix, [&](auto wt) {
           constexpr int W = decltype(wt)::value;
-          if (half == 0)
-            k_inexact_bi<W, 1><<<unsigned(T / nt), nt, smemA, s>>>(ix->view(), bi, cp, nullptr, count, sc, o);
+          if (half == 0 && one_word)
+            k_inexact_bi<W, 1, true><<<unsigned(T / nt), nt, smemA, s>>>(ix->view(), bi, cp, nullptr, count, sc, o);
+          else if (half == 0)
+            k_inexact_bi<W, 1, false><<<unsigned(T / nt), nt, smemA, s>>>(ix->view(), bi, cp, nullptr, count, sc, o);
           else
-            k_inexact_bi<W, 3><<<unsigned(T / nt), nt, smem, s>>>(ix->view(), bi, cp, nullptr, count, sc, o);
+            k_inexact_bi<W, 3, false><<<unsigned(T / nt), nt, smem, s>>>(ix->view(), bi, cp, nullptr, count, sc, o);
         });
         FMG_CK(cudaGetLastError());
         unsigned long long host_ctr[6];

@@ -115,7 +115,9 @@ __device__ __forceinline__ void children4(const IndexView& v, const PrefixTable&
 #define FMG_BI_MINB_B FMG_BI_MINB
 #endif
 
-template <int W, int kOnly>
+// kOne: every pattern fits one 64-bit word (m <= 32), so the second
+// pattern word is the constant 0 (four registers fewer).
+template <int W, int kOnly, bool kOne = false>
 __global__ void __launch_bounds__(128, kOnly == 3 ? FMG_BI_MINB_B : FMG_BI_MINB) k_inexact_bi(IndexView ix, BiIndex bi, CodePatterns cp,
                                                     const uint32_t* __restrict__ list, uint64_t count,
                                                     InexactScratch sc, InexactOut out) {
@@ -339,6 +341,10 @@ __global__ void __launch_bounds__(128, kOnly == 3 ? FMG_BI_MINB_B : FMG_BI_MINB)
       nm = int(cp.fixed_m);
       npw0 = cp.packed1[nq];
       npw1 = 0;
+    } else if (kOne) {
+      nm = int(cp.offsets[nq + 1] - cp.offsets[nq]);
+      npw0 = cp.packed[nq].x;
+      npw1 = 0;
     } else {
       nm = int(cp.offsets[nq + 1] - cp.offsets[nq]);
       const ulonglong2 pk = cp.packed[nq];
@@ -357,7 +363,7 @@ __global__ void __launch_bounds__(128, kOnly == 3 ? FMG_BI_MINB_B : FMG_BI_MINB)
         q = nq;
         m = nm;
         pw0 = npw0;
-        pw1 = npw1;
+        pw1 = kOne ? 0ull : npw1;
         dbits = ndbits;
         prefetch();
         h = m / 2;
