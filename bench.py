@@ -458,7 +458,10 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
         n_seeds = wl.packed.size
         d_pat = torch.from_numpy(wl.packed.view(np.int64)).to(dev)
         d_out = torch.empty((n_seeds, 2), dtype=torch.int32, device=dev)
-        chunk = 1 << 24
+        # z = 1 calls of at most 2^24 seeds, equal-sized (a rank's shard at 8 GPUs, 17.5M seeds,
+        # runs as 2 x 8.75M rather than 16.8M + 0.7M)
+        n_chunks = max(1, -(-n_seeds // (1 << 24)))
+        chunk = -(-n_seeds // n_chunks)
         work_seen = [0, 0]  # inexact Occ steps, lines fetched (device counters, per step)
 
         def step():
@@ -474,7 +477,9 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
                 work_seen[1] += ln_.value
                 lib.fmg_matches_free(h)
 
-        launches_per_step = 1 + ((n_seeds + chunk - 1) // chunk) * 6
+        # per z = 1 call: k_dbound, case A + its segment sort, case B + its sort, 2 x k_merge_ab,
+        # k_widen_counts, k_gather_matches (CUB scans not counted); + the exact pass
+        launches_per_step = 1 + ((n_seeds + chunk - 1) // chunk) * 9
         kernel_name = "k_inexact"
         h2d_per, d2h_per = n_seeds * 8 * 2, None
         pin_in = torch.from_numpy(wl.packed.view(np.int64)).pin_memory()
