@@ -827,6 +827,17 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       bi.tr = prefix_table_rev(ix, count, s);
       for (int d = 0; d < 16; ++d) bi.tail[d] = ix->tail[d];
       bidir = bi.tr.base != nullptr;
+      static const bool jump_x = [] {  // FMG_BI_JUMPX=0: case-A jumps stop at level K (A/B)
+        const char* e = std::getenv("FMG_BI_JUMPX");
+        return e == nullptr || std::atoi(e) != 0;
+      }();
+      if (bidir && jump_x) {
+        const KmerTable kt = kmer_table(ix, count, s);  // level K + 1 when it was worth building
+        if (kt.lut && kt.k == pt.k + 1) {
+          bi.tx = kt.lut;
+          bi.kx = kt.k;
+        }
+      }
     }
     const void* kfn_bi = nullptr;
     with_words(ix, [&](auto wt) { kfn_bi = (const void*)k_inexact_bi<decltype(wt)::value, 0>; });

@@ -36,6 +36,8 @@ struct BiIndex {
   IndexView rev;       // index of the reversed text (same n and C)
   PrefixTable tf, tr;  // prefix tables of the forward / reverse index (same k)
   uint32_t tail[16];   // tail[d]: key of the reversed text's first d characters (d < k), ~0u if d > n
+  const uint2* tx = nullptr;  // forward level kx = tf.k + 1 alone (the exact search's k-mer table), or null
+  uint32_t kx = 0;
 };
 
 // key of W[a .. a+len-1] with W[a] in bits 0..1 (len <= 15)
@@ -48,7 +50,7 @@ __device__ __forceinline__ uint32_t pat_key(uint64_t pw0, uint64_t pw1, int a, i
   } else {
     x = pw1 >> (2 * (a - 32));
   }
-  return uint32_t(x) & ((1u << (2 * len)) - 1u);
+  return uint32_t(x & ((uint64_t(1) << (2 * len)) - 1u));  // len <= 16
 }
 
 __device__ __forceinline__ uint32_t pat_sym(uint64_t pw0, uint64_t pw1, int i) {
@@ -418,11 +420,12 @@ __global__ void __launch_bounds__(128, kOnly == 3 ? FMG_BI_MINB_B : FMG_BI_MINB)
     // continue on the index lines with explicit intervals.
     constexpr bool kJumpA = FMG_BI_JUMP && kOnly != 3, kJumpB = FMG_BI_JUMP_B && kOnly != 1;
     if (cb == 0u && csh && ((kJumpA && phase != 3) || (kJumpB && phase == 3))) {
-      if (phase != 3) {  // case A
-        const uint32_t t = min(uint32_t(ci) + 1u, K - cy);
+      if (phase != 3) {  // case A; with the level-(K+1) table the jump lands one level deeper
+        const uint32_t kmax = bi.tx ? bi.kx : K;
+        const uint32_t t = min(uint32_t(ci) + 1u, kmax - cy);
         const uint32_t d = cy + t;
-        const uint32_t key = pat_key(pw0, pw1, ci - int(t) + 1, int(t)) | (cx << (2u * t));
-        const uint2 e = __ldg(bi.tf.base + PrefixTable::off(d) + key);
+        const uint32_t key = pat_key(pw0, pw1, ci - int(t) + 1, int(t)) | uint32_t(uint64_t(cx) << (2u * t));
+        const uint2 e = __ldg(d > K ? bi.tx + key : bi.tf.base + PrefixTable::off(d) + key);
         my_steps += work_unit(1u);
         if (e.x > e.y) {
           cur_valid = false;
