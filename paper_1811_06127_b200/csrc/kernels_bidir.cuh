@@ -475,6 +475,9 @@ __global__ void __launch_bounds__(128, kOnly == 3 ? FMG_BI_MINB_B : FMG_BI_MINB)
     // (One shared pair of loads for every node kind, selecting addresses
     // first, measured no faster for case A and slower for case B: 79.6 ->
     // 79.1 ms and 83.5 -> 97 ms per 14M config-3 seeds.)
+    // (A case-B budget-0 step from Occ of W[j] plus the count of the symbols
+    // below it, instead of all four counts, measured slower: 83 -> 137 ms
+    // per 14M config-3 seeds, spills at 72 registers.)
 #if FMG_BI_OCC1
     // case-A budget-0 node: only the symbol W[i] is needed (one-symbol count)
     const bool one = !fwd && cb == 0u && !csh;
