@@ -9,7 +9,8 @@
 // intervals keep the smallest diffs.  The order of exploration is free, so
 // instead of one backward DFS from the empty string — whose wrong-edit
 // chains near the right end survive for ~log4(n) characters — the set is
-// enumerated in two halves (h = m / 2):
+// enumerated in two parts split at h (3m/4 in the split form, m/2 in the
+// others; any 0 <= h <= m gives the same set):
 //   case A: edits in W[0..h-1] (and insertion after W[h-1]): the right
 //     part W[h..m-1] is matched exactly first, then the usual backward DFS
 //     runs over the left part on the forward index;
@@ -113,6 +114,14 @@ __device__ __forceinline__ void children4(const IndexView& v, const PrefixTable&
 #define FMG_BI_MINB 7  // resident blocks per SM the register budget is sized for
 #endif
 
+#ifndef FMG_BI_HNUM
+// split point h = m * HNUM / 16 of the split DFS form.  Case A (backward:
+// one-symbol chain steps, jumps through the tables) is cheaper per edit
+// position than case B (forward: four counts per step, no jumps), so the
+// split sits right of the middle — config 3 (m = 19), ms per 14M seeds:
+// HNUM 8 / 9 / 10 / 11 / 12 / 13 -> 157.6 / 151.3 / 146.6 / 140.9 / 139.4 / 142.5.
+#define FMG_BI_HNUM 12
+#endif
 #ifndef FMG_BI_MINB_B
 #define FMG_BI_MINB_B FMG_BI_MINB
 #endif
@@ -368,7 +377,7 @@ __global__ void __launch_bounds__(128, kOnly == 3 ? FMG_BI_MINB_B : FMG_BI_MINB)
         pw1 = kOne ? 0ull : npw1;
         dbits = ndbits;
         prefetch();
-        h = m / 2;
+        h = (m * FMG_BI_HNUM) / 16;  // split point: case A edits W[0..h-1], case B W[h..m-1]
         sp = nres = 0;
         ++epoch;
         overflow = false;
