@@ -260,8 +260,11 @@ def test_alternate_line_layouts(small_cases, gpu, words, monkeypatch):
     assert np.array_equal(kl, orc.exact_batch(orc.OracleIndex(idx), pats))
 
 
-def test_config3_small_scale_vs_oracle(gpu):
-    """Config-3 generator at 1/150 scale: exact and z=1 on packed 19-bp seeds."""
+def test_config3_small_scale_vs_oracle(gpu, monkeypatch):
+    """Config-3 generator at 1/150 scale: exact and z=1 on packed 19-bp seeds, through the
+    packed host entry point, one-directional (no reverse index) and then bidirectional in its
+    split (the config-3 default at scale: edit range split at 3m/4, case-A jumps into the
+    level-(K+1) table), level-synchronous and per-thread forms."""
     import ctypes as ct
 
     from paper_1811_06127_b200 import _lib
@@ -270,24 +273,27 @@ def test_config3_small_scale_vs_oracle(gpu):
     idx = fm.build_index(wl.text)
     seeds = workloads.unpack_patterns(wl.packed, 19)
     ox = orc.OracleIndex(idx)
-    kl, _ = fm.exact_search_batch(idx, seeds)
+    kl, _ = fm.exact_search_batch(idx, seeds)  # builds the level-(K+1) k-mer table too
     assert np.array_equal(kl, orc.exact_batch(ox, seeds))
-    # packed inexact entry point (fmg_inexact_packed_host) vs the oracle
-    lib = _lib.load()
-    h = ct.c_void_p()
-    _lib.check(lib.fmg_inexact_packed_host(idx.device_index().handle, wl.packed.ctypes.data, 19, wl.packed.size, 1,
-                                           ct.byref(h)))
-    tot = ct.c_uint64()
-    lib.fmg_matches_size(h, ct.byref(tot), None)
-    row = np.empty(wl.packed.size + 1, np.uint64)
-    k = np.empty(tot.value, np.uint32)
-    l = np.empty(tot.value, np.uint32)
-    d = np.empty(tot.value, np.uint8)
-    lib.fmg_matches_copy(h, row.ctypes.data, k.ctypes.data, l.ctypes.data, d.ctypes.data, 1)
-    lib.fmg_matches_free(h)
     orow, ok, ol, od, _ = orc.inexact_batch(ox, seeds, 1)
-    assert np.array_equal(row, orow) and np.array_equal(k.astype(np.int64), ok)
-    assert np.array_equal(l.astype(np.int64), ol) and np.array_equal(d, od)
+    lib = _lib.load()
+    dix = idx.device_index()
+    for engine in (None, "split", "sync", "dfs"):
+        if engine is not None:
+            dix.ensure_reverse()
+            monkeypatch.setenv("FMG_BIDIR_ENGINE", engine)
+        h = ct.c_void_p()
+        _lib.check(lib.fmg_inexact_packed_host(dix.handle, wl.packed.ctypes.data, 19, wl.packed.size, 1, ct.byref(h)))
+        tot = ct.c_uint64()
+        lib.fmg_matches_size(h, ct.byref(tot), None)
+        row = np.empty(wl.packed.size + 1, np.uint64)
+        k = np.empty(tot.value, np.uint32)
+        l = np.empty(tot.value, np.uint32)
+        d = np.empty(tot.value, np.uint8)
+        lib.fmg_matches_copy(h, row.ctypes.data, k.ctypes.data, l.ctypes.data, d.ctypes.data, 1)
+        lib.fmg_matches_free(h)
+        assert np.array_equal(row, orow) and np.array_equal(k.astype(np.int64), ok), engine
+        assert np.array_equal(l.astype(np.int64), ol) and np.array_equal(d, od), engine
 
 
 def test_config1h_sample_vs_oracle(gpu):
