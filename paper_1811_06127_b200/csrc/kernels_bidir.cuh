@@ -435,6 +435,8 @@ __global__ void __launch_bounds__(128, kOnly == 3 ? FMG_BI_MINB_B : FMG_BI_MINB)
         const uint32_t d = cy + t;
         const uint32_t key = pat_key(pw0, pw1, ci - int(t) + 1, int(t)) | uint32_t(uint64_t(cx) << (2u * t));
         const uint2 e = __ldg(d > K ? bi.tx + key : bi.tf.base + PrefixTable::off(d) + key);
+        // (Also gathering the final string's first K + 1 characters beside
+        // `e`, to end absent chains here, measured slower: 96.3 -> 99.9 ms.)
         my_steps += work_unit(1u);
         if (e.x > e.y) {
           cur_valid = false;
