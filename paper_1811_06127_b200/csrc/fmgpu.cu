@@ -18,6 +18,7 @@
 #include <string>
 #include <mutex>
 #include <unordered_map>
+#include <array>
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
@@ -124,9 +125,19 @@ size_t available_bytes(int device) {
         cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
       free_b += size_t(reserved - used);
   }
-  // round down to 1 GiB so small fluctuations keep the sizes identical
+  // round down to 1 GiB, and keep the previous figure unless memory got
+  // >10% tighter or >50% roomier: another process freeing its memory while
+  // this one runs (the previous test or bench on the box) must not change
+  // the sizes on every call — each change remaps GBs of pool memory
+  // (measured: config 2 at 3.6 vs 16 ms per call for a whole process)
   const size_t g = size_t(1) << 30;
-  return free_b > g ? free_b / g * g : free_b;
+  const size_t cur = free_b > g ? free_b / g * g : free_b;
+  static std::mutex mu;
+  static std::unordered_map<int, size_t> last;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& c = last[device];
+  if (c == 0 || cur < c / 10 * 9 || cur > c / 2 * 3) c = cur;
+  return c;
 }
 
 }  // namespace fmg
@@ -745,12 +756,36 @@ bool run_z1b(const fmg_index* ix, const BiIndex& bi, const CodePatterns& cp, uin
   return true;
 }
 
+// Grows the device's stream-ordered pool once per process to `bytes` of
+// reserved memory (one allocation, freed at once; the unlimited release
+// threshold keeps it), so the per-call scratch of large searches is carved
+// out of already-mapped memory instead of growing the pool mid-run
+// (config 3: 30-290 ms stalls in the calls that grew it).
+// FMG_POOL_RESERVE_GB overrides the size (0 disables).
+void pool_reserve(int device, size_t bytes, cudaStream_t s) {
+  static std::mutex mu;
+  static std::unordered_map<int, bool> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done[device]) return;
+  done[device] = true;
+  if (const char* e = std::getenv("FMG_POOL_RESERVE_GB")) bytes = size_t(std::atof(e) * double(size_t(1) << 30));
+  if (bytes == 0) return;
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) {
+    cudaGetLastError();  // no room: the pool just grows on demand
+    return;
+  }
+  FMG_CK(cudaFreeAsync(p, s));
+  FMG_CK(cudaStreamSynchronize(s));
+}
+
 fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64_t* offsets, uint64_t count,
                          uint64_t max_len, int max_diff, cudaStream_t s, const uint64_t* packed1 = nullptr) {
   FMG_REQUIRE(max_diff >= 0, "difference budget is negative");
   FMG_REQUIRE(max_diff <= 255, "difference budget above 255 is not supported (diffs are stored as u8)");
   FMG_REQUIRE(max_len < 0xFFFF, "pattern longer than 65534 is not supported");
   FMG_REQUIRE(count < 0xFFFFFFFFull, "too many patterns in one call");
+  if (count >= (1u << 20)) pool_reserve(ix->device, std::min<size_t>(available_bytes(ix->device) / 4, size_t(32) << 30), s);
   auto* res = new fmg_matches();
   res->device = ix->device;
   res->patterns = count;
@@ -1219,14 +1254,34 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
   }
 }
 
+// The calling thread's streams on `device` for the host-buffer entry points,
+// created on first use and kept (never destroyed: a thread-exit destructor
+// could run after the CUDA context is gone).  Reusing them keeps per-call
+// overhead to the copies and the kernels — creating and destroying three
+// streams per call cost more than a 10,000-pattern search (config 0 e2e) —
+// and lets the stream-ordered pool reuse the previous call's blocks on the
+// same stream.
+cudaStream_t host_stream(int device, int slot) {
+  thread_local std::unordered_map<int, std::array<cudaStream_t, 3>> cache;
+  auto it = cache.find(device);
+  if (it == cache.end()) {
+    std::array<cudaStream_t, 3> st{};
+    for (auto& x : st) FMG_CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    it = cache.emplace(device, st).first;
+  }
+  return it->second[slot];
+}
+
 // Chunked host-buffer pipeline: H2D, kernel, D2H per chunk on alternating
 // streams so the copy engines overlap each other and the kernel.
 template <typename Launch>
 void pipeline_host(int device, uint64_t count, uint64_t chunk, size_t in_bytes_per, size_t out_bytes_per,
                    const void* host_in, void* host_out, Launch&& launch) {
-  constexpr int kSlots = 3;
-  cudaStream_t st[kSlots];
-  for (int i = 0; i < kSlots; ++i) FMG_CK(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
+  if (count == 0) return;
+  constexpr int kMaxSlots = 3;
+  const int kSlots = int(std::min<uint64_t>(kMaxSlots, (count + chunk - 1) / chunk));  // slots actually used
+  cudaStream_t st[kMaxSlots];
+  for (int i = 0; i < kSlots; ++i) st[i] = host_stream(device, i);
   std::vector<void*> din(kSlots, nullptr), dout(kSlots, nullptr);
   try {
     for (int i = 0; i < kSlots; ++i) {
@@ -1250,15 +1305,12 @@ void pipeline_host(int device, uint64_t count, uint64_t chunk, size_t in_bytes_p
       if (din[i]) cudaFreeAsync(din[i], st[i]);
       if (dout[i]) cudaFreeAsync(dout[i], st[i]);
       cudaStreamSynchronize(st[i]);
-      cudaStreamDestroy(st[i]);
     }
     throw;
   }
   for (int i = 0; i < kSlots; ++i) {
     cudaFreeAsync(din[i], st[i]);
     cudaFreeAsync(dout[i], st[i]);
-    cudaStreamSynchronize(st[i]);
-    cudaStreamDestroy(st[i]);
   }
 }
 
@@ -1590,8 +1642,7 @@ int fmg_exact_host(const fmg_index* ix, const uint8_t* codes, const uint64_t* of
     if (count == 0) return;
     FMG_REQUIRE(offsets[0] == 0 && offsets[count] >= count, "pattern offsets must start at 0; patterns non-empty");
     fmg::DeviceScope scope(ix->device);
-    cudaStream_t s;
-    FMG_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cudaStream_t s = host_stream(ix->device, 0);
     try {
       DevBuf<uint8_t> dc(offsets[count], s);
       DevBuf<uint64_t> doff(count + 1, s);
@@ -1604,11 +1655,9 @@ int fmg_exact_host(const fmg_index* ix, const uint8_t* codes, const uint64_t* of
       FMG_CK(cudaStreamSynchronize(s));
     } catch (...) {
       cudaStreamSynchronize(s);
-      cudaStreamDestroy(s);
       throw;
     }
-    cudaStreamSynchronize(s);
-    cudaStreamDestroy(s);
+    FMG_CK(cudaStreamSynchronize(s));
   });
 }
 
@@ -1651,8 +1700,7 @@ int fmg_inexact_host(const fmg_index* ix, const uint8_t* codes, const uint64_t* 
     if (count > 0)
       FMG_REQUIRE(offsets[0] == 0 && offsets[count] >= count, "pattern offsets must start at 0; patterns non-empty");
     fmg::DeviceScope scope(ix->device);
-    cudaStream_t s;
-    FMG_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cudaStream_t s = host_stream(ix->device, 0);
     try {
       DevBuf<uint8_t> dc(count ? offsets[count] : 0, s);
       DevBuf<uint64_t> doff(count + 1, s);
@@ -1664,11 +1712,9 @@ int fmg_inexact_host(const fmg_index* ix, const uint8_t* codes, const uint64_t* 
       *out = run_inexact(ix, dc.ptr, doff.ptr, count, max_len, max_diff, s);
     } catch (...) {
       cudaStreamSynchronize(s);
-      cudaStreamDestroy(s);
       throw;
     }
-    cudaStreamSynchronize(s);
-    cudaStreamDestroy(s);
+    FMG_CK(cudaStreamSynchronize(s));
   });
 }
 
@@ -1693,19 +1739,16 @@ int fmg_inexact_packed_host(const fmg_index* ix, const uint64_t* packed, uint32_
     FMG_REQUIRE(m >= 1 && m <= 32, "packed pattern length must be in [1, 32]");
     FMG_REQUIRE(max_diff >= 0, "difference budget is negative");
     fmg::DeviceScope scope(ix->device);
-    cudaStream_t s;
-    FMG_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cudaStream_t s = host_stream(ix->device, 0);
     try {
       DevBuf<uint64_t> dp(count, s);
       if (count) FMG_CK(cudaMemcpyAsync(dp.ptr, packed, count * 8, cudaMemcpyHostToDevice, s));
       *out = run_inexact(ix, nullptr, nullptr, count, m, max_diff, s, dp.ptr);
     } catch (...) {
       cudaStreamSynchronize(s);
-      cudaStreamDestroy(s);
       throw;
     }
-    cudaStreamSynchronize(s);
-    cudaStreamDestroy(s);
+    FMG_CK(cudaStreamSynchronize(s));
   });
 }
 
