@@ -486,17 +486,26 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
         pin_kl = torch.empty((n_seeds, 2), dtype=torch.int32).pin_memory()
 
         host_res = PinnedResults()
+        from concurrent.futures import ThreadPoolExecutor
+
+        copier = ThreadPoolExecutor(max_workers=1)  # result copies of chunk i overlap the search of chunk i+1
+
+        def copy_out(h, cnt):
+            try:
+                return host_res.copy(lib, h, cnt)
+            finally:
+                lib.fmg_matches_free(h)
 
         def e2e_step():
             _lib.check(lib.fmg_exact_packed_host(dix.handle, pin_in.data_ptr(), m, n_seeds, pin_kl.data_ptr()))
             out_bytes = pin_kl.numel() * 4
+            pending = []
             for c0 in range(0, n_seeds, chunk):
                 h = ct.c_void_p()
                 cnt = min(chunk, n_seeds - c0)
                 _lib.check(lib.fmg_inexact_packed_host(dix.handle, pin_in.data_ptr() + 8 * c0, m, cnt, 1, ct.byref(h)))
-                out_bytes += host_res.copy(lib, h, cnt)
-                lib.fmg_matches_free(h)
-            return out_bytes
+                pending.append(copier.submit(copy_out, h, cnt))
+            return out_bytes + sum(f.result() for f in pending)
 
         alg_bytes = alg_lines = None
         extra["seeds_per_step"] = n_seeds
