@@ -760,7 +760,8 @@ bool run_z1b(const fmg_index* ix, const BiIndex& bi, const CodePatterns& cp, uin
 // reserved memory (one allocation, freed at once; the unlimited release
 // threshold keeps it), so the per-call scratch of large searches is carved
 // out of already-mapped memory instead of growing the pool mid-run
-// (config 3: 30-290 ms stalls in the calls that grew it).
+// (config 3: 30-290 ms stalls in the calls that grew it; config 2 on a
+// fresh box: 12-64 ms stalls in the level-synchronous engine's queues).
 // FMG_POOL_RESERVE_GB overrides the size (0 disables).
 void pool_reserve(int device, size_t bytes, cudaStream_t s) {
   static std::mutex mu;
@@ -785,7 +786,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
   FMG_REQUIRE(max_diff <= 255, "difference budget above 255 is not supported (diffs are stored as u8)");
   FMG_REQUIRE(max_len < 0xFFFF, "pattern longer than 65534 is not supported");
   FMG_REQUIRE(count < 0xFFFFFFFFull, "too many patterns in one call");
-  if (count >= (1u << 20)) pool_reserve(ix->device, std::min<size_t>(available_bytes(ix->device) / 4, size_t(32) << 30), s);
+  if (count >= (1u << 16)) pool_reserve(ix->device, std::min<size_t>(available_bytes(ix->device) / 4, size_t(32) << 30), s);
   auto* res = new fmg_matches();
   res->device = ix->device;
   res->patterns = count;

@@ -980,6 +980,62 @@ __global__ void __launch_bounds__(256) k_bchain(IndexView ix, BiIndex bi, CodePa
       ww = nd.ww;
       have = true;
     }
+    // A chain inside the prefix tables' depth range grows by known pattern
+    // characters only: jump to the deepest table level it reaches in one
+    // gather (case A: into the level-(K+1) table when built; case B: the
+    // forward interval from the forward table under the bit-pair-reversed
+    // key, the reverse interval only if the chain goes on).
+    if (sh && FMG_BI_JUMP) {
+      if (!fwd) {
+        const uint32_t kmax = bi.tx ? bi.kx : K;
+        const uint32_t tt = min(uint32_t(pos) + 1u, kmax - y);
+        const uint32_t d = y + tt;
+        const uint32_t key = pat_key(pw0, pw1, pos - int(tt) + 1, int(tt)) | uint32_t(uint64_t(x) << (2u * tt));
+        const uint2 e = __ldg(d > K ? bi.tx + key : bi.tf.base + PrefixTable::off(d) + key);
+        work += work_unit(1u);
+        const bool done = uint32_t(pos) + 1u == tt;
+        if (e.x > e.y || done) {
+          have = false;
+          if (e.x <= e.y) {
+            const unsigned long long rs = atomicAdd(qu.n_raws, 1ull);
+            if (rs < qu.raw_cap) qu.raws[rs] = Z1Raw{q, e.x, e.y, 1u};
+          }
+          continue;
+        }
+        pos -= int(tt);
+        if (__popcll(dbits & ((2ull << pos) - 1ull)) > 0u) {  // an absent segment in W[0..pos]
+          have = false;
+          continue;
+        }
+        x = e.x;
+        y = e.y;
+        sh = false;
+      } else {
+        const uint32_t tt = min(uint32_t(m - pos), K - ww);
+        const uint32_t d = ww + tt;
+        const uint32_t fkey = pair_rev(zz, ww) | (pat_key(pw0, pw1, pos, int(tt)) << (2u * ww));
+        const uint2 f = __ldg(bi.tf.base + PrefixTable::off(d) + fkey);
+        const bool done = uint32_t(m - pos) == tt;
+        uint2 r = make_uint2(0u, 0u);
+        if (!done) r = __ldg(bi.tr.base + PrefixTable::off(d) + pair_rev(fkey, d));
+        work += work_unit(done ? 1u : 2u);
+        if (f.x > f.y || done) {
+          have = false;
+          if (f.x <= f.y) {
+            const unsigned long long rs = atomicAdd(qu.n_raws, 1ull);
+            if (rs < qu.raw_cap) qu.raws[rs] = Z1Raw{q, f.x, f.y, 1u};
+          }
+          continue;
+        }
+        pos += int(tt);
+        x = f.x;
+        y = f.y;
+        zz = r.x;
+        ww = r.y;
+        sh = false;
+      }
+      continue;
+    }
     const uint32_t sym = pat_sym(pw0, pw1, pos);
     if (!fwd) {  // case A: backward, one symbol
       uint32_t k2, l2;
