@@ -19,6 +19,7 @@
 #include <mutex>
 #include <unordered_map>
 #include <array>
+#include <chrono>
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
@@ -786,6 +787,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
   FMG_REQUIRE(max_diff <= 255, "difference budget above 255 is not supported (diffs are stored as u8)");
   FMG_REQUIRE(max_len < 0xFFFF, "pattern longer than 65534 is not supported");
   FMG_REQUIRE(count < 0xFFFFFFFFull, "too many patterns in one call");
+  const auto t_entry = std::chrono::steady_clock::now();
   if (count >= (1u << 16)) pool_reserve(ix->device, std::min<size_t>(available_bytes(ix->device) / 4, size_t(32) << 30), s);
   auto* res = new fmg_matches();
   res->device = ix->device;
@@ -901,6 +903,12 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     bool bidir_split = bidir && bidir_engine == "split";
     if (bidir && bidir_engine == "sync") {
       CodePatterns cpz{codes, offsets, packed.ptr, packed1, uint32_t(max_len), dbits.ptr};
+      static const bool trace_pre = std::getenv("FMG_TRACE") != nullptr;
+      if (trace_pre) {  // host time spent before the engine (packing, bound pass, tables, setup)
+        FMG_CK(cudaStreamSynchronize(s));
+        fprintf(stderr, "[fmg] pre-engine host time %.3f ms\n",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_entry).count());
+      }
       if (run_z1b(ix, bi, cpz, count, max_len, s, counters.ptr + 2, res)) return res;
       // raw-result buffer overflowed: fall through (same results)
       FMG_CK(cudaMemsetAsync(counters.ptr + 2, 0, 2 * sizeof(unsigned long long), s));
@@ -1686,8 +1694,17 @@ int fmg_inexact(const fmg_index* ix, const uint8_t* codes, const uint64_t* offse
     *out = nullptr;
     fmg::DeviceScope scope(ix->device);
     cudaStream_t s = as_stream(stream);
+    static const bool trace = std::getenv("FMG_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     const uint64_t max_len = validate_patterns_device(codes, offsets, count, s);
+    const auto t1 = std::chrono::steady_clock::now();
     *out = run_inexact(ix, codes, offsets, count, max_len, max_diff, s);
+    if (trace) {
+      const auto t2 = std::chrono::steady_clock::now();
+      fprintf(stderr, "[fmg] fmg_inexact host time: validate %.3f ms, search %.3f ms\n",
+              std::chrono::duration<double, std::milli>(t1 - t0).count(),
+              std::chrono::duration<double, std::milli>(t2 - t1).count());
+    }
   });
 }
 
