@@ -650,6 +650,21 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
                     "alg_bytes_per_step": round(alg_bytes / units, 2),
                     "sectors_per_step": round(alg_lines / units, 4),
                     "random_sector_roofline_steps_per_s": round(peak * 1e9 / (alg_bytes / units), 1)}
+        if wl.pairs is not None and dix.device_bytes <= (64 << 20):
+            # L2-resident index: the bound is the SM->L2 random request rate, measured live on a
+            # buffer of the index's size (random 32-byte reads, all L2 hits)
+            fn = lib.fmgx_random_fetch_rate
+            fn.argtypes = [ct.c_int, ct.c_uint64, ct.c_uint64, ct.POINTER(ct.c_double)]
+            rate = ct.c_double()
+            if fn(local, max(int(dix.device_bytes), 1 << 20), 1 << 25, ct.byref(rate)) == 0 and rate.value > 0:
+                ach = alg_lines / launch_s
+                roofline["l2_request_roofline"] = {
+                    "bound": "l2_random_requests", "achieved": round(ach / 1e9, 2),
+                    "peak": round(rate.value / 1e9, 2), "unit": "G random 32-B line reads/s",
+                    "frac": round(ach / rate.value, 4),
+                    "note": "index lines fetched per launch / launch time, against random 32-byte reads over an "
+                            "L2-resident buffer of the index's size measured in the same run; the kernel also "
+                            "streams its pairs in and counts out"}
 
     # ---- search configs: device-counted work (one extra, untimed step) ----
     work = None
