@@ -205,6 +205,9 @@ __global__ void __launch_bounds__(128, kOnly == 3 ? FMG_BI_MINB_B : (kOnly == 1 
 
   auto sym_at = [&](int i) -> uint32_t { return pat_sym(pw0, pw1, i); };
   auto dlb = [&](int i) -> uint32_t { return __popcll(dbits & ((2ull << i) - 1ull)); };
+  // (A short contiguous per-thread result list before this table, for case
+  // A, saved its probe stalls but the larger kernel lost more to registers:
+  // 90.2 -> 97.4 ms per 14M config-3 seeds.)
   auto record = [&](uint32_t k, uint32_t l, uint32_t used) {
     const uint32_t H = 2u * sc.R;
     uint32_t hh = (k * 0x9E3779B1u ^ l * 0x85EBCA77u) & (H - 1u);

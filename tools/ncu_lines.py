@@ -50,6 +50,7 @@ tt = sum(a[1] for a in agg.values())
 print(f"warp insts {tot:.4g}, avg lanes {tt / tot:.2f}, stall samples {st:.0f}")
 csrc = Path(__file__).resolve().parent.parent / "paper_1811_06127_b200" / "csrc"
 files = {p.name: p.read_text().split("\n") for p in csrc.glob("*.cuh")}
-for s, (i, t, smp) in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
+key_i = 2 if "--by-stall" in sys.argv else 0
+for s, (i, t, smp) in sorted(agg.items(), key=lambda x: -x[1][key_i])[:top]:
     txt = files.get(s[0], [""] * (s[1] if s else 1))[s[1] - 1].strip()[:70] if s else ""
     print(f"{str(s):30s} inst {100 * i / tot:5.1f}% lanes {t / max(i, 1):5.1f} stall {100 * smp / st:5.1f}%  {txt}")
