@@ -421,11 +421,11 @@ PrefixTable prefix_table_rev(const fmg_index* cix, uint64_t count, cudaStream_t 
 }
 
 // The exact search's k-mer table.  Exact search needs only the last level,
-// so it goes one level beyond the prefix table when the index is large
-// enough for that level to still skip steps (K + 1 <= floor(log4 n) + 2, at
-// most 16 so keys stay 32-bit) and the level fits in a quarter of the
-// available memory: level 16 is 34.4 GB, built from level 15 with one Occ
-// step per entry.  Measured on config 4 (2^28 x 20 bp, 1 Gbp): K = 15 -> 16
+// so it goes beyond the prefix table (to level floor(log4 n) + 4, at most
+// 16 so keys stay 32-bit) when the level fits in a quarter of the available
+// memory: level 16 is 34.4 GB, built from level 15 with one Occ step per
+// entry.  Patterns shorter than that level use the prefix table's level of
+// their own length (the exact answer in one gather) or its level K.  Measured on config 4 (2^28 x 20 bp, 1 Gbp): K = 15 -> 16
 // takes present seeds from 5 to 4 dependent steps and most random seeds to
 // an empty interval in the table.  FMG_EXACT_LUT_EXT=0 disables it (A/B).
 KmerTable kmer_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
@@ -442,17 +442,32 @@ KmerTable kmer_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
       ix->lut_x_tried = true;
       int lg = 0;
       while ((uint64_t(1) << (2 * (lg + 1))) <= ix->n) ++lg;  // floor(log4 n)
-      const uint32_t kx = pt.k + 1;
+      // level floor(log4 n) + 4 (≤ 16): small indexes go further past the
+      // prefix table, whose K tracks log4 n for the inexact engines' sake —
+      // config 0 (1 Mbp): K = 10, exact level 13 (537 MB), two dependent
+      // steps fewer per 32-bp pattern; genome-scale indexes stop at 16
+      const uint32_t kx = std::min<uint32_t>(16, std::max<uint32_t>(pt.k + 1, uint32_t(lg + 4)));
       const uint64_t cnt = uint64_t(1) << (2 * kx);
-      if (kx <= 16 && int(kx) <= lg + 2 && cnt * sizeof(uint2) <= available_bytes(ix->device) / 4) {
+      if (kx <= 16 && cnt * sizeof(uint2) <= available_bytes(ix->device) / 4) {
         uint2* lx = nullptr;
         if (cudaMalloc(&lx, cnt * sizeof(uint2)) == cudaSuccess) {
-          with_words(ix, [&](auto wt) {
-            constexpr int W = decltype(wt)::value;
-            k_lut_level<W><<<unsigned((cnt + 255) / 256), 256, 0, s>>>(ix->view(), pt.base + PrefixTable::off64(pt.k),
-                                                                      lx, cnt);
-          });
-          FMG_CK(cudaGetLastError());
+          // levels K + 1 .. kx, each from the previous; only the last is kept
+          DevBuf<uint2> tmp[2];
+          const uint2* parent = pt.base + PrefixTable::off64(pt.k);
+          for (uint32_t j = pt.k + 1; j <= kx; ++j) {
+            const uint64_t cj = uint64_t(1) << (2 * j);
+            uint2* dst = lx;
+            if (j < kx) {
+              tmp[j & 1] = DevBuf<uint2>(cj, s);
+              dst = tmp[j & 1].ptr;
+            }
+            with_words(ix, [&](auto wt) {
+              constexpr int W = decltype(wt)::value;
+              k_lut_level<W><<<unsigned((cj + 255) / 256), 256, 0, s>>>(ix->view(), parent, dst, cj);
+            });
+            FMG_CK(cudaGetLastError());
+            parent = dst;
+          }
           FMG_CK(cudaStreamSynchronize(s));
           ix->lut_x = lx;
           ix->lut_x_k = kx;
@@ -461,9 +476,9 @@ KmerTable kmer_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
         }
       }
     }
-    if (ix->lut_x) return KmerTable{ix->lut_x, ix->lut_x_k};
+    if (ix->lut_x) return KmerTable{ix->lut_x, ix->lut_x_k, pt.base, pt.k};
   }
-  return KmerTable{pt.base + PrefixTable::off64(pt.k), pt.k};
+  return KmerTable{pt.base + PrefixTable::off64(pt.k), pt.k, pt.base, pt.k};
 }
 
 // Block size of the exact kernels: small batches (config 0: 10,000

@@ -116,18 +116,6 @@ struct InexactOut {
 #define FMG_INEX_LINE_HINT 0  // 2: DFS index-line loads with an L2 evict_first policy
 #endif
 
-// Prefix interval table: level j (1 <= j <= k) holds the interval of every
-// string x of length j, key(x) = sum x_t 4^t (x_0 = first character), at
-// base[off(j) + key]; absent strings hold some k > l.  Prepending b to S
-// gives key(bS) = b + 4 key(S), so the four children of a node whose string
-// S is shorter than k sit in ONE aligned 32-byte sector of level |S| + 1.
-struct PrefixTable {
-  const uint2* base = nullptr;
-  uint32_t k = 0;
-  __host__ __device__ static uint32_t off(uint32_t j) { return ((1u << (2 * j)) - 4u) / 3u; }  // j <= 15
-  static uint64_t off64(uint32_t j) { return ((uint64_t(1) << (2 * j)) - 4u) / 3u; }
-};
-
 // Reference semantics (search.py:120-159): nodes (i, budget, k, l) from the
 // root (m-1, z, 0, n); a node with i < 0 is a result with z - budget diffs;
 // otherwise one Occ step at (k-1, l) and children skip (i-1, budget-1, k, l),

@@ -35,9 +35,24 @@ struct CodePatterns {  // codes[offsets[q] .. offsets[q+1])
 // result is identical because the entry IS what those K steps produce.
 // pp.words == nullptr makes k_exact search the K-mers x = 0 .. count-1
 // themselves (how the table is built).
+
+// Prefix interval table: level j (1 <= j <= k) holds the interval of every
+// string x of length j, key(x) = sum x_t 4^t (x_0 = first character), at
+// base[off(j) + key]; absent strings hold some k > l.  Prepending b to S
+// gives key(bS) = b + 4 key(S), so the four children of a node whose string
+// S is shorter than k sit in ONE aligned 32-byte sector of level |S| + 1.
+struct PrefixTable {
+  const uint2* base = nullptr;
+  uint32_t k = 0;
+  __host__ __device__ static uint32_t off(uint32_t j) { return ((1u << (2 * j)) - 4u) / 3u; }  // j <= 15
+  static uint64_t off64(uint32_t j) { return ((uint64_t(1) << (2 * j)) - 4u) / 3u; }
+};
+
 struct KmerTable {
   const uint2* lut = nullptr;
   uint32_t k = 0;
+  const uint2* pbase = nullptr;  // the prefix table (levels 1..pk) for patterns shorter than k
+  uint32_t pk = 0;
 };
 
 template <bool kPacked, int W>
@@ -63,18 +78,22 @@ __global__ void __launch_bounds__(256) k_exact(IndexView ix, PackedPatterns pp, 
       m = uint32_t(o1 - o0);
       b = codes[m - 1];
     }
-    if (kt.lut && m >= kt.k) {  // start after the last K characters
+    // start after the last d characters, d = K (level-K table) or, for a
+    // shorter pattern, min(m, prefix depth) from the prefix table's level d
+    const bool full = kt.lut && m >= kt.k;
+    const uint32_t d = full ? kt.k : (kt.pbase ? min(m, kt.pk) : 0u);
+    if (d > 0) {
       uint32_t key = 0;
       if (kPacked) {
-        key = uint32_t((pat >> (2 * (m - kt.k))) & ((uint64_t(1) << (2 * kt.k)) - 1u));  // K <= 16
+        key = uint32_t((pat >> (2 * (m - d))) & ((uint64_t(1) << (2 * d)) - 1u));  // d <= 16
       } else {
-        for (uint32_t t = 0; t < kt.k; ++t) key |= uint32_t(__ldg(codes + m - kt.k + t) & 3u) << (2 * t);
+        for (uint32_t t = 0; t < d; ++t) key |= uint32_t(__ldg(codes + m - d + t) & 3u) << (2 * t);
       }
-      const uint2 e = __ldg(kt.lut + key);
+      const uint2 e = __ldg(full ? kt.lut + key : kt.pbase + PrefixTable::off(d) + key);
       work += 1u;  // one random table gather: counted as a fetched line, not as an Occ step
       k = e.x;
       l = e.y;
-      i = int(m) - 1 - int(kt.k);
+      i = int(m) - 1 - int(d);
       return;
     }
     k = c_of(ix, b) + 1u;  // init_interval, search.py:50-57
