@@ -359,8 +359,10 @@ def test_z1_engines_agree(gpu, monkeypatch):
 
 
 def test_exact_kmer_table_paths(gpu):
-    """>= 1024 patterns use the k-mer table (K = floor(log4 n) + 1 = 9 here): lengths below,
-    at and above K, present and absent, packed and CSR inputs — all identical to the oracle."""
+    """>= 1024 patterns use the tables: here prefix levels 1..9 and the exact-search level 12
+    (floor(log4 n) + 4).  Lengths below 9 (one prefix-level gather is the answer), 9..11
+    (level 9 + steps), at and above 12 (level 12 + steps), present and absent, packed and CSR
+    inputs — all identical to the oracle."""
     rng = np.random.Generator(np.random.PCG64(606))
     text = rng.integers(0, 4, 200_000, dtype=np.uint8)
     idx = fm.build_index(text)
