@@ -428,6 +428,17 @@ PrefixTable prefix_table_rev(const fmg_index* cix, uint64_t count, cudaStream_t 
 // their own length (the exact answer in one gather) or its level K.  Measured on config 4 (2^28 x 20 bp, 1 Gbp): K = 15 -> 16
 // takes present seeds from 5 to 4 dependent steps and most random seeds to
 // an empty interval in the table.  FMG_EXACT_LUT_EXT=0 disables it (A/B).
+// Level of the exact search's own k-mer table: floor(log4 n) + 4, at most 16
+// and at least K + 1.  Small indexes go further past the prefix table, whose
+// K tracks log4 n for the inexact engines' sake — config 0 (1 Mbp): K = 10,
+// exact level 13 (537 MB), two dependent steps fewer per 32-bp pattern;
+// genome-scale indexes stop at 16.
+uint32_t exact_table_level(const fmg_index* ix, const PrefixTable& pt) {
+  int lg = 0;
+  while ((uint64_t(1) << (2 * (lg + 1))) <= ix->n) ++lg;  // floor(log4 n)
+  return std::min<uint32_t>(16, std::max<uint32_t>(pt.k + 1, uint32_t(lg + 4)));
+}
+
 KmerTable kmer_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
   const PrefixTable pt = prefix_table(cix, count, s);
   if (!pt.base) return {};
@@ -440,13 +451,7 @@ KmerTable kmer_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
     std::lock_guard<std::mutex> lock(ix->lut_mu);
     if (!ix->lut_x_tried) {
       ix->lut_x_tried = true;
-      int lg = 0;
-      while ((uint64_t(1) << (2 * (lg + 1))) <= ix->n) ++lg;  // floor(log4 n)
-      // level floor(log4 n) + 4 (≤ 16): small indexes go further past the
-      // prefix table, whose K tracks log4 n for the inexact engines' sake —
-      // config 0 (1 Mbp): K = 10, exact level 13 (537 MB), two dependent
-      // steps fewer per 32-bp pattern; genome-scale indexes stop at 16
-      const uint32_t kx = std::min<uint32_t>(16, std::max<uint32_t>(pt.k + 1, uint32_t(lg + 4)));
+      const uint32_t kx = exact_table_level(ix, pt);
       const uint64_t cnt = uint64_t(1) << (2 * kx);
       if (kx <= 16 && cnt * sizeof(uint2) <= available_bytes(ix->device) / 4) {
         uint2* lx = nullptr;
@@ -894,8 +899,8 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
         const char* e = std::getenv("FMG_BI_JUMPX");
         return e == nullptr || std::atoi(e) != 0;
       }();
-      if (bidir && jump_x) {
-        const KmerTable kt = kmer_table(ix, count, s);  // level K + 1 when it was worth building
+      if (bidir && jump_x && exact_table_level(ix, pt) == pt.k + 1) {  // the jumps need exactly level K + 1
+        const KmerTable kt = kmer_table(ix, count, s);
         if (kt.lut && kt.k == pt.k + 1) {
           bi.tx = kt.lut;
           bi.kx = kt.k;
