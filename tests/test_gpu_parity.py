@@ -575,3 +575,47 @@ def test_device_pattern_validation_errors(gpu):
     ms = fm.inexact_search_batch(idx, base.reshape(n, m)[:2000], 1)  # still healthy
     row, k, _, _, _ = orc.inexact_batch(orc.OracleIndex(idx), base.reshape(n, m)[:2000], 1)
     assert np.array_equal(ms.offsets, row) and np.array_equal(ms.k.astype(np.int64), k)
+
+
+def test_concurrent_host_calls_one_index(gpu, monkeypatch):
+    """Four host threads search one index at once (exact and z = 1, host entry points on each
+    thread's own streams; the dedup-table lease falls back to per-call tables for the threads
+    that find it taken): every result equals the oracle's."""
+    import threading
+
+    monkeypatch.setenv("FMG_BIDIR_MIN_N", "0")
+    rng = np.random.Generator(np.random.PCG64(2024))
+    text = rng.integers(0, 4, 400_000, dtype=np.uint8)
+    idx = fm.build_index(text)
+    ox = orc.OracleIndex(idx)
+    batches = []
+    for t in range(4):
+        m = 18 + t
+        pats = workloads.substrings(text, rng.integers(0, text.size - m + 1, 4000), m).copy()
+        pats[::3, m // 2] = (pats[::3, m // 2] + 1) % 4
+        batches.append(pats)
+    fm.exact_search_batch(idx, batches[0])  # build the tables once before the threads race
+    fm.inexact_search_batch(idx, batches[0], 1)
+    out = [None] * 4
+    errors = []
+
+    def work(t):
+        try:
+            kl, _ = fm.exact_search_batch(idx, batches[t])
+            ms = fm.inexact_search_batch(idx, batches[t], 1)
+            out[t] = (kl, ms)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    for t in range(4):
+        kl, ms = out[t]
+        assert np.array_equal(kl, orc.exact_batch(ox, batches[t])), t
+        row, k, l, d, _ = orc.inexact_batch(ox, batches[t], 1)
+        assert np.array_equal(ms.offsets, row) and np.array_equal(ms.k.astype(np.int64), k), t
+        assert np.array_equal(ms.l.astype(np.int64), l) and np.array_equal(ms.diffs, d), t
