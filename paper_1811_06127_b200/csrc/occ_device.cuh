@@ -168,12 +168,27 @@ __device__ __forceinline__ uint32_t field_at(const uint64_t w[W], uint32_t r) {
   return uint32_t((word >> ((r & 31u) << 1)) & 3ull);
 }
 
-// a[i] for a runtime i without forcing the array into local memory.
-__device__ __forceinline__ uint32_t sel4(const uint32_t a[4], uint32_t i) {
-  return i == 0u ? a[0] : i == 1u ? a[1] : i == 2u ? a[2] : a[3];
+// Predicated select (SEL, never a branch): the selects below sit on the
+// dependent chain of every Occ step, where a branchy ?: chain cost ~100 of
+// the ~800 cycles of an exact-search step (tools/exact_latency.py,
+// tools/micro/chase.cu: an L2 hit is ~310 cycles).
+__device__ __forceinline__ uint32_t selp32(bool c, uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\tselp.b32 %0, %2, %3, p;\n\t}"
+      : "=r"(r)
+      : "r"(uint32_t(c)), "r"(a), "r"(b));
+  return r;
 }
+
+// a[i] for a runtime i in 0..3 without forcing the array into local memory.
+__device__ __forceinline__ uint32_t sel4(const uint32_t a[4], uint32_t i) {
+  const uint32_t lo = selp32(i & 1u, a[1], a[0]), hi = selp32(i & 1u, a[3], a[2]);
+  return selp32(i & 2u, hi, lo);
+}
+// C[s] for s in 0..4.
 __device__ __forceinline__ uint32_t c_of(const IndexView& ix, uint32_t s) {
-  return s == 0u ? ix.c[0] : s == 1u ? ix.c[1] : s == 2u ? ix.c[2] : s == 3u ? ix.c[3] : ix.c[4];
+  const uint32_t lo = selp32(s & 1u, ix.c[1], ix.c[0]), hi = selp32(s & 1u, ix.c[3], ix.c[2]);
+  return selp32(s & 4u, ix.c[4], selp32(s & 2u, hi, lo));
 }
 
 // All four Occ(b, p) for 0 <= p <= n given the line holding p.

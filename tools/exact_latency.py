@@ -21,8 +21,8 @@ idx = fm.build_index(text)
 dix = idx.device_index(0)
 lib = _lib.load()
 st = torch.cuda.Stream()
-for count in (10_000, 100_000):
-    for m in (8, 12, 13, 14, 16, 20, 24, 28, 32):
+for count in tuple(int(x) for x in (sys.argv[2].split(',') if len(sys.argv) > 2 else ['10000', '100000'])):
+    for m in (13, 16, 20, 24, 28, 32):
         pats = workloads.substrings(text, rng.integers(0, n - m + 1, count), m)
         packed = fm.pack_patterns_u64(pats)
         d_pat = torch.from_numpy(packed.view(np.int64)).cuda()
