@@ -114,6 +114,9 @@ __device__ __forceinline__ void children4(const IndexView& v, const PrefixTable&
 #define FMG_BI_MINB 7  // resident blocks per SM the register budget is sized for
 #endif
 
+#ifndef FMG_CHAIN_COND_LOW
+#define FMG_CHAIN_COND_LOW 1  // k_bchain: load the low line only when it differs from the high one
+#endif
 #ifndef FMG_BI_HNUM
 // split point h = m * HNUM / 16 of the split DFS form.  Case A (backward:
 // one-symbol chain steps, jumps through the tables) is cheaper per edit
@@ -1056,7 +1059,14 @@ __global__ void __launch_bounds__(256) k_bchain(IndexView ix, BiIndex bi, CodePa
         uint32_t bh[4], bl[4];
         uint64_t wh[W], wl[W];
         load_line<W, 0>(ix, jh, y - jh * kC, bh, wh);
-        load_line<W, 0>(ix, jl, low - jl * kC, bl, wl);
+        if (FMG_CHAIN_COND_LOW && jl == jh) {  // same line: no second request
+#pragma unroll
+          for (int t2 = 0; t2 < 4; ++t2) bl[t2] = bh[t2];
+#pragma unroll
+          for (int t2 = 0; t2 < W; ++t2) wl[t2] = wh[t2];
+        } else {
+          load_line<W, 0>(ix, jl, low - jl * kC, bl, wl);
+        }
         const uint32_t cs = c_of(ix, sym);
         k2 = cs + occ1_from_line<W>(ix, bl, wl, low, low - jl * kC, sym) + 1u;
         l2 = cs + occ1_from_line<W>(ix, bh, wh, y, y - jh * kC, sym);
