@@ -43,14 +43,14 @@ struct BiIndex {
 
 // key of W[a .. a+len-1] with W[a] in bits 0..1 (len <= 15)
 __device__ __forceinline__ uint32_t pat_key(uint64_t pw0, uint64_t pw1, int a, int len) {
-  uint64_t x;
-  if (a == 0) {
-    x = pw0;
-  } else if (a < 32) {
-    x = (pw0 >> (2 * a)) | (pw1 << (64 - 2 * a));
-  } else {
-    x = pw1 >> (2 * (a - 32));
-  }
+  // branch-free 128-bit funnel shift by 2a: PTX shifts clamp counts >= 64
+  // (and the unsigned wrap of a negative count) to an all-zero result
+  const uint32_t sh = uint32_t(2 * a);
+  uint64_t lo, mid, hi;
+  asm("shr.b64 %0, %1, %2;" : "=l"(lo) : "l"(pw0), "r"(sh));
+  asm("shl.b64 %0, %1, %2;" : "=l"(mid) : "l"(pw1), "r"(64u - sh));
+  asm("shr.b64 %0, %1, %2;" : "=l"(hi) : "l"(pw1), "r"(sh - 64u));
+  const uint64_t x = lo | mid | hi;
   return uint32_t(x & ((uint64_t(1) << (2 * len)) - 1u));  // len <= 16
 }
 
