@@ -942,6 +942,10 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     // slots).  cap: results per pass (9 bytes each) before patterns finishing
     // later are retried — sized from free memory so a pass rarely fills it.
     uint32_t R = 256;
+    if (const char* e = std::getenv("FMG_INEXACT_R")) {  // A/B: first-pass results per pattern (power of 2)
+      const uint32_t r = uint32_t(std::atoi(e));
+      if (r >= 16 && (r & (r - 1)) == 0) R = r;
+    }
     const size_t free_b = available_bytes(ix->device);
     uint64_t cap = std::max<uint64_t>(count * 16, 1u << 20);
     cap = std::min<uint64_t>(cap, std::max<uint64_t>(1u << 20, free_b / 4 / 9));
