@@ -117,6 +117,9 @@ __device__ __forceinline__ void children4(const IndexView& v, const PrefixTable&
 #ifndef FMG_CHAIN_COND_LOW
 #define FMG_CHAIN_COND_LOW 1  // k_bchain: load the low line only when it differs from the high one
 #endif
+#ifndef FMG_BI_PRED_LOW
+#define FMG_BI_PRED_LOW 1  // case-A chain steps: predicated low-line load (no request when the line is shared)
+#endif
 #ifndef FMG_BI_HNUM
 // split point h = m * HNUM / 16 of the split DFS form.  Case A (backward:
 // one-symbol chain steps, jumps through the tables) is cheaper per edit
@@ -515,7 +518,21 @@ __global__ void __launch_bounds__(128, kOnly == 3 ? FMG_BI_MINB_B : (kOnly == 1 
       uint32_t bh[4], bl[4];
       uint64_t wh[W], wl[W];
       load_line<W, 0>(ix, jh, cy - jh * kC, bh, wh);
-      load_line<W, 0>(ix, jl, low - jl * kC, bl, wl);
+      if constexpr (W == 2 && FMG_BI_PRED_LOW && kOnly == 1) {
+        // the low line is loaded only when it differs (deep chains: nearly
+        // always the same line, and a second load is a second request)
+        uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        ld256_pred(jl != jh, ix.lines + size_t(jl) * LineTraits<2>::kBytes, a0, a1, a2, a3);
+        const bool same = jl == jh;
+        bl[0] = same ? bh[0] : uint32_t(a0);
+        bl[1] = same ? bh[1] : uint32_t(a0 >> 32);
+        bl[2] = same ? bh[2] : uint32_t(a1);
+        bl[3] = same ? bh[3] : uint32_t(a1 >> 32);
+        wl[0] = same ? wh[0] : a2;
+        wl[1] = same ? wh[1] : a3;
+      } else {
+        load_line<W, 0>(ix, jl, low - jl * kC, bl, wl);
+      }
       const uint32_t cs = c_of(ix, sym);
       k1 = cs + occ1_from_line<W>(ix, bl, wl, low, low - jl * kC, sym) + 1u;
       l1 = cs + occ1_from_line<W>(ix, bh, wh, cy, cy - jh * kC, sym);

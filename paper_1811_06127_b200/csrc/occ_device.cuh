@@ -114,6 +114,17 @@ __device__ __forceinline__ void load_line(const IndexView& ix, uint32_t j, uint3
   }
 }
 
+// W = 2 line load issued only when `go` (a predicated-off load makes no
+// memory request and keeps the straight-line code of the step).
+__device__ __forceinline__ void ld256_pred(bool go, const uint8_t* p, uint64_t& a0, uint64_t& a1, uint64_t& a2,
+                                           uint64_t& a3) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
+      "@q ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%5];\n\t}"
+      : "+l"(a0), "+l"(a1), "+l"(a2), "+l"(a3)
+      : "r"(uint32_t(go)), "l"(p));
+}
+
 // Mask of the fields of word k that lie in 0..r.
 // Branch-free: PTX clamps shift counts above 64 (all fields out -> 0).
 __device__ __forceinline__ uint64_t word_mask(uint32_t r, int k) {
