@@ -48,6 +48,10 @@ struct PrefixTable {
   static uint64_t off64(uint32_t j) { return ((uint64_t(1) << (2 * j)) - 4u) / 3u; }
 };
 
+#ifndef FMG_EXACT_PRED_LOW
+#define FMG_EXACT_PRED_LOW 1  // k_exact (W = 2): predicated low-line load instead of a branch
+#endif
+
 struct KmerTable {
   const uint2* lut = nullptr;
   uint32_t k = 0;
@@ -121,10 +125,22 @@ __global__ void __launch_bounds__(256) k_exact(IndexView ix, PackedPatterns pp, 
     const uint32_t rh = l - jh * kC, rl = low - jl * kC;
     load_line<W, false>(ix, jh, rh, bh, wh);
     uint32_t ol;
-    // (Loading the low line unconditionally, to drop this branch, costs a
+    // (Loading the low line unconditionally, to drop the branch, costs a
     // second memory request when both ends share a line: config 4 12.0 ->
-    // 9.0 G seeds/s.)
-    if (jl != jh) {
+    // 9.0 G seeds/s.  W = 2 uses a predicated load instead: no request,
+    // no branch.)
+    if constexpr (W == 2 && FMG_EXACT_PRED_LOW) {
+      uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+      ld256_pred(jl != jh, ix.lines + size_t(jl) * LineTraits<2>::kBytes, a0, a1, a2, a3);
+      const bool same = jl == jh;
+      bl[0] = same ? bh[0] : uint32_t(a0);
+      bl[1] = same ? bh[1] : uint32_t(a0 >> 32);
+      bl[2] = same ? bh[2] : uint32_t(a1);
+      bl[3] = same ? bh[3] : uint32_t(a1 >> 32);
+      wl[0] = same ? wh[0] : a2;
+      wl[1] = same ? wh[1] : a3;
+      ol = occ1_from_line<W>(ix, bl, wl, low, rl, sym);
+    } else if (jl != jh) {
       load_line<W, false>(ix, jl, rl, bl, wl);
       ol = occ1_from_line<W>(ix, bl, wl, low, rl, sym);
     } else {
