@@ -114,6 +114,10 @@ __device__ __forceinline__ void load_line(const IndexView& ix, uint32_t j, uint3
   }
 }
 
+#ifndef FMG_OCC_PRED_LOW
+#define FMG_OCC_PRED_LOW 1  // occ_step (W = 2): predicated low-line load
+#endif
+
 // W = 2 line load issued only when `go` (a predicated-off load makes no
 // memory request and keeps the straight-line code of the step).
 __device__ __forceinline__ void ld256_pred(bool go, const uint8_t* p, uint64_t& a0, uint64_t& a1, uint64_t& a2,
@@ -250,7 +254,20 @@ __device__ __forceinline__ uint32_t occ_step(const IndexView& ix, uint32_t k, ui
   uint32_t bh[4], bl[4];
   uint64_t wh[W], wl[W];
   load_line<W, kStream>(ix, jh, rh, bh, wh);
-  load_line<W, kStream>(ix, jl, rl, bl, wl);
+  if constexpr (W == 2 && kStream == 0 && FMG_OCC_PRED_LOW) {
+    // predicated: no second request when both ends share the line
+    uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    ld256_pred(jl != jh, ix.lines + size_t(jl) * LineTraits<2>::kBytes, a0, a1, a2, a3);
+    const bool same = jl == jh;
+    bl[0] = same ? bh[0] : uint32_t(a0);
+    bl[1] = same ? bh[1] : uint32_t(a0 >> 32);
+    bl[2] = same ? bh[2] : uint32_t(a1);
+    bl[3] = same ? bh[3] : uint32_t(a1 >> 32);
+    wl[0] = same ? wh[0] : a2;
+    wl[1] = same ? wh[1] : a3;
+  } else {
+    load_line<W, kStream>(ix, jl, rl, bl, wl);
+  }
   occ4_from_line<W>(ix, bl, wl, low, rl, lo);
   occ4_from_line<W>(ix, bh, wh, l, rh, hi);
 #pragma unroll
