@@ -213,33 +213,61 @@ def pattern_sample(wl, lo: int, hi: int) -> np.ndarray:
 # ---------------------------------------------------------------------------
 
 
+# Per-step unit counts of the reference arm: the full workload wherever the
+# reference path finishes one step in a few seconds on the box's host cores
+# (configs 0, 1, 1-H, 2), a bounded leading sample elsewhere (configs 3, 4).
+REF_FULL = {"config0", "config1", "config1h", "config2"}
+REF_SAMPLE = {"config4": 1 << 22, "config3": 2_000}
+
+
+def native_libs_mapped() -> list[str]:
+    """Shared objects of this repo mapped into the current process."""
+    try:
+        maps = Path("/proc/self/maps").read_text().splitlines()
+    except OSError:
+        return []
+    return sorted({ln.split()[-1] for ln in maps if ln.endswith(".so") and str(REPO) in ln})
+
+
 def run_reference(args, rank: int, world: int) -> None:
+    """The reference's CPU path on the box's host cores: the index is built by
+    the oracle's restatement of build_suffix_array / bwt_from_sa / build_index
+    (oracle/fm_build.c) and queried by the restatement of the reference's
+    occ_pair_all / exact_search / inexact_search (oracle/fm_oracle.c).  The
+    product library (libfmgpu.so) is never loaded in this process."""
     if rank != 0:
         return
     from oracle import oracle as orc
-    from paper_1811_06127_b200 import build_index
+    from paper_1811_06127_b200 import workloads as w  # numpy-only generators
 
     wl = make_workload(args.config, 0)
-    idx = build_index(wl.text)
-    ox = orc.OracleIndex(idx)
     threads = cpu_threads()
+    t_build = time.perf_counter()
+    ox = orc.OracleIndex(orc.BuiltIndex(wl.text, threads))
+    t_build = time.perf_counter() - t_build
     total = unit_count(wl)
-    sample = min(total, args.ref_sample or {"config1": 1 << 22, "config1h": 1 << 21, "config0": 10_000,
-                                          "config2": 20_000, "config4": 1 << 21, "config3": 2_000}[args.config])
+    sample = total if args.config in REF_FULL else min(total, REF_SAMPLE[args.config])
+    if args.ref_sample:
+        sample = min(total, args.ref_sample)
+    if wl.pairs is not None:
+        low = np.ascontiguousarray(wl.pairs[:, 0])
+        high = np.ascontiguousarray(wl.pairs[:, 1])
+    elif wl.name == "config3":
+        per = wl.meta["seeds_per_read"]
+        seeds3 = pattern_sample(wl, 0, sample * per)
+    else:
+        pats = pattern_sample(wl, 0, sample)
 
     def step(i: int):
-        lo = (i * sample) % max(total - sample + 1, 1)
         if wl.name == "config3":  # reads -> their 14 seeds: exact + z=1
-            per = wl.meta["seeds_per_read"]
-            seeds = pattern_sample(wl, lo * per, (lo + sample) * per)
-            orc.exact_batch(ox, seeds, threads)
-            orc.inexact_batch(ox, seeds, 1, threads)
+            orc.exact_batch(ox, seeds3, threads)
+            orc.inexact_batch(ox, seeds3, 1, threads)
         elif wl.pairs is not None:
-            orc.occ_pair_batch(ox, wl.pairs[lo:lo + sample, 0], wl.pairs[lo:lo + sample, 1], threads)
+            orc.occ_pair_batch(ox, low[:sample], high[:sample], threads)
         elif wl.max_diff:
-            orc.inexact_batch(ox, pattern_sample(wl, lo, lo + sample), wl.max_diff, threads)
+            orc.inexact_batch(ox, pats, wl.max_diff, threads)
         else:
-            orc.exact_batch(ox, pattern_sample(wl, lo, lo + sample), threads)
+            orc.exact_batch(ox, pats, threads)
 
     for i in range(args.warmup):
         step(i)
@@ -249,19 +277,31 @@ def run_reference(args, rank: int, world: int) -> None:
     dt = time.perf_counter() - t0
     metric, unit = metric_of(args.config)
     value = sample * args.steps / dt
+    what = "the full workload" if sample == total else f"the first {sample} of {total} units"
     desc = (f"C restatement of the reference path (oracle/fm_oracle.c: bytelut all4, occ_pair_all, "
-            f"exact/inexact_search) on {threads} threads of {cpu_model()}; {sample} units per step "
-            f"from the {args.config} workload")
+            f"exact/inexact_search; index by oracle/fm_build.c) on {threads} threads of {cpu_model()}; "
+            f"{what} per step")
+    mapped = native_libs_mapped()
+    if any("libfmgpu" in m for m in mapped):
+        raise SystemExit("reference arm: the product library was loaded")
     line = {
         "impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic (seeded PCG64, workloads.py)", "config": config_of(args.config, world, sample),
+        "higher_is_better": True, "scaling": scaling_of(args.config), "vs_baseline": None, "dtype": "u32",
+        "data": DATA, "config": config_of(args.config, world, total),
         "cpu_baseline": {"value": value, "unit": unit, "cores": threads, "kind": "port", "sample": desc},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "gpu_launches": 0,
+        "gpu_launches": 0, "index_build_s": round(t_build, 2), "units_timed_per_step": sample,
+        "native_libs": mapped,
     }
     print(json.dumps(line), flush=True)
+
+
+DATA = "synthetic (seeded PCG64 per BASELINE.json config; workloads.py)"
+
+
+def scaling_of(config: str) -> str:
+    return "strong" if config in ("config3", "config4") else "weak"
 
 
 def metric_of(config: str) -> tuple[str, str]:
@@ -280,7 +320,9 @@ def config_of(config: str, world: int, units: int) -> dict:
         "config3": "BASELINE configs[3]: 3.1 Gbp family genome (seed 11), 10M x 150 bp reads, 14 x 19 bp seeds "
                    "per read, exact + z=1 on every seed",
     }[config]
-    return {"workload": desc, "units_per_step_per_rank": units, "parallelism": f"query-sharded x{world}"}
+    return {"workload": desc, "units_per_step_per_rank": units, "parallelism": f"query-sharded x{world}",
+            "l2": "inputs larger than L2 (no flush)" if config != "config0" else
+                  "inputs smaller than L2; index L2-resident"}
 
 
 # ---------------------------------------------------------------------------
@@ -351,11 +393,11 @@ def hbm_resident_extra(dev, lib, reps: int = 10) -> dict:
     d_out = torch.empty((units, 8), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
     for _ in range(3):
-        _lib.check(lib.fmg_occ_pair(dix.handle, d_kl.data_ptr(), units, d_out.data_ptr(), stream.cuda_stream))
+        _lib.check(lib.fmg_occ_pair(dix.handle, d_kl.data_ptr(), units, d_out.data_ptr(), None, stream.cuda_stream))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(reps):
-        lib.fmg_occ_pair(dix.handle, d_kl.data_ptr(), units, d_out.data_ptr(), stream.cuda_stream)
+        lib.fmg_occ_pair(dix.handle, d_kl.data_ptr(), units, d_out.data_ptr(), None, stream.cuda_stream)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     launch_s = e0.elapsed_time(e1) / reps / 1e3
@@ -525,7 +567,8 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
         d_kl = torch.from_numpy(kl_h.view(np.int32)).to(dev)
         d_out = torch.empty((units, 8), dtype=torch.int32, device=dev)
 
-        args_ = (dix.handle, d_kl.data_ptr(), units, d_out.data_ptr(), sp)  # resolved once, outside the loop
+        d_status = torch.zeros(1, dtype=torch.int32, device=dev)  # per-call input-error word (checked after timing)
+        args_ = (dix.handle, d_kl.data_ptr(), units, d_out.data_ptr(), d_status.data_ptr(), sp)  # resolved once
 
         def step():
             rc = lib.fmg_occ_pair(*args_)
@@ -625,6 +668,8 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
     t_ms = ev0.elapsed_time(ev1)
+    if wl.pairs is not None and int(d_status.item()):
+        raise SystemExit("Occ step reported an input error")
     t_ms = max_over_ranks(t_ms, world, dev)
     ms_step = t_ms / args.steps
     total_units = int(dist_sum(units, world, dev)) if world > 1 else units
@@ -762,12 +807,8 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
         line = {
             "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if args.config in ("config3", "config4") else "weak",
-            "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic (seeded PCG64 per BASELINE.json config; workloads.py)",
-            "config": {**config_of(args.config, world, units),
-                       "l2": "inputs larger than L2 (no flush)" if args.config != "config0" else
-                             "inputs smaller than L2; index L2-resident"},
+            "scaling": scaling_of(args.config), "vs_baseline": None, "dtype": "u32", "data": DATA,
+            "config": config_of(args.config, world, units),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
             "gpu_launches": launches_per_step * args.steps, **extra,
         }

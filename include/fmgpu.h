@@ -27,8 +27,15 @@
  *   - Every function returns an fmg_status; the message of the last failure on
  *     the calling thread is available from fmg_last_error().  No exception
  *     crosses this boundary.
- *   - Positions handed to fmg_occ_pair are validated on the device; a bad
- *     position yields FMG_EINVAL (the reference raises ValueError, occ.py:68-79).
+ *   - Input errors are reported PER CALL.  _host entry points return
+ *     FMG_EINVAL for a bad position or row (the reference raises ValueError,
+ *     occ.py:68-79, search.py:199-200).  Device entry points that take a
+ *     `status` argument validate on the device and OR error bits into that
+ *     caller-owned device word (1 = position / row out of range or pair out
+ *     of order, 2 = predecessor walk did not terminate: corrupt index); the
+ *     caller zeroes it before the call and reads it after synchronising.
+ *     status == NULL makes the call unchecked: bad queries yield zeros and
+ *     are not reported.  No state is shared between calls.
  */
 #ifndef FMGPU_H
 #define FMGPU_H
@@ -104,7 +111,7 @@ void fmg_index_destroy(fmg_index* index);
  * k <= l + 1 and l <= n.
  * ------------------------------------------------------------------------- */
 int fmg_occ_pair(const fmg_index* index, const uint32_t* kl, uint64_t count, uint32_t* out,
-                 void* stream);
+                 uint32_t* status, void* stream);
 int fmg_occ_pair_host(const fmg_index* index, const uint32_t* kl, uint64_t count, uint32_t* out);
 
 /* ---------------------------------------------------------------------------
@@ -159,9 +166,9 @@ void fmg_matches_free(fmg_matches* m);
  * fmg_index_set_samples.
  * ------------------------------------------------------------------------- */
 int fmg_psi_inverse(const fmg_index* index, const uint32_t* rows, uint64_t count,
-                    uint8_t* out_sym, uint32_t* out_row, void* stream);
+                    uint8_t* out_sym, uint32_t* out_row, uint32_t* status, void* stream);
 int fmg_locate_rows(const fmg_index* index, const uint32_t* rows, uint64_t count,
-                    uint32_t* out_pos, void* stream);
+                    uint32_t* out_pos, uint32_t* status, void* stream);
 int fmg_locate_rows_host(const fmg_index* index, const uint32_t* rows, uint64_t count,
                          uint32_t* out_pos);
 

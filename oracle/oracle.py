@@ -32,8 +32,8 @@ class _Index(ct.Structure):
 
 
 def build(force: bool = False) -> Path:
-    src = HERE / "fm_oracle.c"
-    if force or not LIB.exists() or LIB.stat().st_mtime < src.stat().st_mtime:
+    newest = max((HERE / f).stat().st_mtime for f in ("fm_oracle.c", "fm_build.c", "Makefile"))
+    if force or not LIB.exists() or LIB.stat().st_mtime < newest:
         subprocess.run(["make", "-s", "-C", str(HERE), "liboracle.so"], check=True)
     return LIB
 
@@ -60,6 +60,8 @@ def load():
         lib.fmo_matches_free.argtypes = [vp]
         lib.fmo_psi.argtypes = [vp, ct.c_int64, ct.POINTER(ct.c_int)]
         lib.fmo_psi.restype = ct.c_int64
+        lib.fmo_build_sa.argtypes = [vp, u64, vp, ct.c_int]
+        lib.fmo_build_records.argtypes = [vp, u64, vp, vp, vp, vp, vp]
         _lib = lib
     return _lib
 
@@ -69,6 +71,34 @@ def threads_default() -> int:
         return len(os.sched_getaffinity(0))
     except AttributeError:  # pragma: no cover
         return os.cpu_count() or 1
+
+
+class BuiltIndex:
+    """An index built by the oracle's own restatement of the reference build
+    (fm_build.c: build_suffix_array, bwt_from_sa, build_index), with the
+    attributes OracleIndex reads.  Never touches the product library."""
+
+    def __init__(self, codes, threads: int | None = None, keep_sa: bool = False):
+        codes = np.ascontiguousarray(codes, dtype=np.uint8)
+        n = codes.size
+        if n == 0:
+            raise ValueError("reference is empty")
+        lib = load()
+        sa = np.empty(n + 1, dtype=np.uint32)
+        if lib.fmo_build_sa(codes.ctypes.data, n, sa.ctypes.data, threads or threads_default()):
+            raise MemoryError("oracle suffix sort failed")
+        nb = n // 128 + 1
+        self.bucket_records = np.empty((nb, 64), dtype=np.uint8)
+        self.sa_samples = np.empty(n // 32 + 1, dtype=np.uint64)
+        c = np.zeros(5, dtype=np.uint64)
+        srow = ct.c_uint64()
+        if lib.fmo_build_records(codes.ctypes.data, n, sa.ctypes.data, self.bucket_records.ctypes.data,
+                                 self.sa_samples.ctypes.data, c.ctypes.data, ct.byref(srow)):
+            raise RuntimeError("oracle build: no suffix at position 0")
+        self.n = n
+        self.c = tuple(int(x) for x in c)
+        self.sentinel_row = int(srow.value)
+        self.sa = sa if keep_sa else None
 
 
 class OracleIndex:

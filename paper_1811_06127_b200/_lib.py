@@ -34,7 +34,7 @@ PROTOTYPES: dict[str, tuple] = {
     "fmg_index_has_reverse": (ct.c_int, [_vp, ct.POINTER(ct.c_int)]),
     "fmg_index_info": (ct.c_int, [_vp, _u64p, ct.POINTER(ct.c_int), _u64p]),
     "fmg_index_destroy": (None, [_vp]),
-    "fmg_occ_pair": (ct.c_int, [_vp, _vp, ct.c_uint64, _vp, _vp]),
+    "fmg_occ_pair": (ct.c_int, [_vp, _vp, ct.c_uint64, _vp, _vp, _vp]),
     "fmg_occ_pair_host": (ct.c_int, [_vp, _vp, ct.c_uint64, _vp]),
     "fmg_exact": (ct.c_int, [_vp, _vp, _vp, ct.c_uint64, _vp, _vp]),
     "fmg_exact_packed": (ct.c_int, [_vp, _vp, ct.c_uint32, ct.c_uint64, _vp, _vp]),
@@ -48,8 +48,8 @@ PROTOTYPES: dict[str, tuple] = {
     "fmg_matches_steps": (ct.c_int, [_vp, _u64p]),
     "fmg_matches_copy": (ct.c_int, [_vp, _vp, _vp, _vp, _vp, ct.c_int]),
     "fmg_matches_free": (None, [_vp]),
-    "fmg_psi_inverse": (ct.c_int, [_vp, _vp, ct.c_uint64, _vp, _vp, _vp]),
-    "fmg_locate_rows": (ct.c_int, [_vp, _vp, ct.c_uint64, _vp, _vp]),
+    "fmg_psi_inverse": (ct.c_int, [_vp, _vp, ct.c_uint64, _vp, _vp, _vp, _vp]),
+    "fmg_locate_rows": (ct.c_int, [_vp, _vp, ct.c_uint64, _vp, _vp, _vp]),
     "fmg_locate_rows_host": (ct.c_int, [_vp, _vp, ct.c_uint64, _vp]),
     "fmg_stream_sync": (ct.c_int, [_vp]),
 }

@@ -150,7 +150,6 @@ struct fmg_index {
   int words = 2;  // line layout: W words of 32 chars per line (occ_device.cuh)
   uint8_t* lines = nullptr;
   uint32_t* samples = nullptr;
-  uint32_t* err = nullptr;  // sticky device-side input error flags
   int sms = 148;
   // exact-search k-mer table (built on first large exact call; see KmerTable)
   std::mutex lut_mu;
@@ -227,18 +226,32 @@ int choose_words(uint64_t n_buckets) {
 
 void check_index(const fmg_index* ix) { FMG_REQUIRE(ix != nullptr, "null index handle"); }
 
-// Reads and clears the sticky input-error flags (synchronises `stream`).
-void take_input_error(const fmg_index* ix, cudaStream_t stream, const char* what) {
-  uint32_t h = 0;
-  FMG_CK(cudaMemcpyAsync(&h, ix->err, sizeof(h), cudaMemcpyDeviceToHost, stream));
-  FMG_CK(cudaStreamSynchronize(stream));
-  if (h) {
-    FMG_CK(cudaMemsetAsync(ix->err, 0, sizeof(uint32_t), stream));
-    FMG_CK(cudaStreamSynchronize(stream));
-    if (h & 2u) throw std::runtime_error("predecessor walk did not terminate; index is corrupt");
-    throw std::invalid_argument(what);
+// Input-error word of ONE host-buffer call (status bits: 1 = position out of
+// range or pair out of order, 2 = predecessor walk did not terminate), from
+// the stream-ordered pool, so no call ever sees another call's errors.
+// Device entry points instead pass the caller's own status word straight to
+// the kernels (NULL: unchecked, the kernels skip the report).
+struct CallStatus {
+  DevBuf<uint32_t> own;
+  uint32_t* word = nullptr;
+  CallStatus(uint32_t* caller, cudaStream_t s) {
+    if (caller) {
+      word = caller;
+    } else {
+      own = DevBuf<uint32_t>(1, s);
+      word = own.ptr;
+      FMG_CK(cudaMemsetAsync(word, 0, sizeof(uint32_t), s));
+    }
   }
-}
+  // Reads this call's word after everything queued on `s` (synchronises).
+  void raise_if_set(cudaStream_t s, const char* what) {
+    uint32_t h = 0;
+    FMG_CK(cudaMemcpyAsync(&h, word, sizeof(h), cudaMemcpyDeviceToHost, s));
+    FMG_CK(cudaStreamSynchronize(s));
+    if (h & 2u) throw std::runtime_error("predecessor walk did not terminate; index is corrupt");
+    if (h) throw std::invalid_argument(what);
+  }
+};
 
 // Runs f(std::integral_constant<int, W>) for the index's line layout.
 template <typename F>
@@ -255,7 +268,7 @@ constexpr int kOccPer = 1;
 
 template <int PER>
 void launch_occ_pair_t(const fmg_index* ix, const uint32_t* kl, uint64_t count, uint32_t* out, cudaStream_t s,
-                       int threads) {
+                       uint32_t* err, int threads) {
   const uint64_t per_block = uint64_t(threads) * PER;
   const uint64_t blocks = (count + per_block - 1) / per_block;
   with_words(ix, [&](auto wt) {
@@ -266,28 +279,28 @@ void launch_occ_pair_t(const fmg_index* ix, const uint32_t* kl, uint64_t count, 
     const bool two_lane = e2l ? std::atoi(e2l) != 0 : ix->n_lines * 32ull > (64ull << 20);
     if (W == 2 && two_lane) {
       k_occ_pair_2l<<<dim3(unsigned((2 * count + 255) / 256)), 256, 0, s>>>(
-          ix->view(), reinterpret_cast<const uint2*>(kl), count, out, ix->err);
+          ix->view(), reinterpret_cast<const uint2*>(kl), count, out, err);
     } else if (W == 2) {
       k_occ_pair<PER, W><<<dim3(unsigned(blocks)), threads, 0, s>>>(ix->view(), reinterpret_cast<const uint2*>(kl),
-                                                                      count, out, ix->err);
+                                                                      count, out, err);
     } else {  // wide lines: lane-cooperative, persistent grid-stride
       constexpr int LANES = int(LineTraits<W>::kBytes / 32);
       const uint64_t nb = (count * LANES + 255) / 256;
       k_occ_pair_coop<W><<<dim3(unsigned(std::max<uint64_t>(nb, 1))), 256, 0, s>>>(
-          ix->view(), reinterpret_cast<const uint2*>(kl), count, out, ix->err);
+          ix->view(), reinterpret_cast<const uint2*>(kl), count, out, err);
     }
   });
   FMG_CK(cudaGetLastError());
 }
 
 void launch_occ_pair(const fmg_index* ix, const uint32_t* kl, uint64_t count, uint32_t* out, cudaStream_t s,
-                     int per = kOccPer, int threads = 128) {
+                     uint32_t* err, int per = kOccPer, int threads = 128) {
   if (count == 0) return;
   FMG_REQUIRE(threads == 128 || threads == 256, "threads must be 128 or 256");
   switch (per) {
-    case 1: launch_occ_pair_t<1>(ix, kl, count, out, s, threads); break;
-    case 2: launch_occ_pair_t<2>(ix, kl, count, out, s, threads); break;
-    case 4: launch_occ_pair_t<4>(ix, kl, count, out, s, threads); break;
+    case 1: launch_occ_pair_t<1>(ix, kl, count, out, s, err, threads); break;
+    case 2: launch_occ_pair_t<2>(ix, kl, count, out, s, err, threads); break;
+    case 4: launch_occ_pair_t<4>(ix, kl, count, out, s, err, threads); break;
     default: throw std::invalid_argument("per must be 1, 2 or 4");
   }
 }
@@ -524,11 +537,12 @@ void launch_exact_codes(const fmg_index* ix, const uint8_t* codes, const uint64_
   FMG_CK(cudaGetLastError());
 }
 
-void launch_locate(const fmg_index* ix, const uint32_t* rows, uint64_t count, uint32_t* out_pos, cudaStream_t s) {
+void launch_locate(const fmg_index* ix, const uint32_t* rows, uint64_t count, uint32_t* out_pos, cudaStream_t s,
+                   uint32_t* err) {
   with_words(ix, [&](auto wt) {
     constexpr int W = decltype(wt)::value;
     const unsigned blocks = wave_blocks(ix, (const void*)fmg::k_locate<W>, 256, count);
-    fmg::k_locate<W><<<blocks, 256, 0, s>>>(ix->view(), rows, count, out_pos, ix->err);
+    fmg::k_locate<W><<<blocks, 256, 0, s>>>(ix->view(), rows, count, out_pos, err);
   });
   FMG_CK(cudaGetLastError());
 }
@@ -1369,25 +1383,27 @@ int fmg_device_count(int* count) {
 // .fmi bucket records (n_buckets x 64 B, host) -> device lines of ix's layout.
 static uint8_t* upload_lines(fmg_index* ix, const void* bucket_records) {
   uint8_t* lines = nullptr;
+  uint32_t bad = 0;
   const uint64_t n_buckets = ix->n_buckets;
   with_words(ix, [&](auto wt) {
     constexpr int W = decltype(wt)::value;
     ix->n_lines = (n_buckets * 128 + fmg::LineTraits<W>::kChars - 1) / fmg::LineTraits<W>::kChars;
     FMG_CK(cudaMalloc(&lines, ix->n_lines * fmg::LineTraits<W>::kBytes));
     uint64_t* staging = nullptr;
-    FMG_CK(cudaMalloc(&staging, n_buckets * 64));
+    uint32_t* err = nullptr;
+    FMG_CK(cudaMalloc(&staging, n_buckets * 64 + 64));
+    err = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(staging) + n_buckets * 64);
     FMG_CK(cudaMemcpy(staging, bucket_records, n_buckets * 64, cudaMemcpyHostToDevice));
-    FMG_CK(cudaMemset(ix->err, 0, sizeof(uint32_t)));
+    FMG_CK(cudaMemset(err, 0, sizeof(uint32_t)));
     fmg::k_build_lines<W><<<unsigned((ix->n_lines + 255) / 256), 256>>>(staging, n_buckets, lines, ix->n_lines,
-                                                                         ix->err);
+                                                                         err);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(&bad, err, sizeof(bad), cudaMemcpyDeviceToHost);
     cudaFree(staging);
     if (e != cudaSuccess) cudaFree(lines);
     FMG_CK(e);
   });
-  uint32_t bad = 0;
-  FMG_CK(cudaMemcpy(&bad, ix->err, sizeof(bad), cudaMemcpyDeviceToHost));
   if (bad != 0) cudaFree(lines);
   FMG_REQUIRE(bad == 0, "bucket base does not fit 32 bits");
   return lines;
@@ -1417,8 +1433,6 @@ int fmg_index_create(int device, const void* bucket_records, uint64_t n_buckets,
       ix->n_buckets = n_buckets;
       ix->words = choose_words(n_buckets);
       ix->sms = fmg::sm_count(device);
-      FMG_CK(cudaMalloc(&ix->err, sizeof(uint32_t)));
-      FMG_CK(cudaMemset(ix->err, 0, sizeof(uint32_t)));
       ix->lines = upload_lines(ix, bucket_records);
       // Allow the stream-ordered pool to keep freed blocks (host entry points
       // allocate per call).
@@ -1511,16 +1525,17 @@ void fmg_index_destroy(fmg_index* ix) {
   if (ix->ep_table) cudaFree(ix->ep_table);
   if (ix->rev_lines) cudaFree(ix->rev_lines);
   if (ix->samples) cudaFree(ix->samples);
-  if (ix->err) cudaFree(ix->err);
   if (prev >= 0) cudaSetDevice(prev);
   delete ix;
 }
 
-int fmg_occ_pair(const fmg_index* ix, const uint32_t* kl, uint64_t count, uint32_t* out, void* stream) {
+int fmg_occ_pair(const fmg_index* ix, const uint32_t* kl, uint64_t count, uint32_t* out, uint32_t* status,
+                 void* stream) {
   return fmg::guard([&] {
     check_index(ix);
+    if (count == 0) return;
     fmg::DeviceScope scope(ix->device);
-    launch_occ_pair(ix, kl, count, out, as_stream(stream));
+    launch_occ_pair(ix, kl, count, out, as_stream(stream), status);
   });
 }
 
@@ -1531,7 +1546,7 @@ int fmgx_occ_pair_tuned(const fmg_index* ix, const uint32_t* kl, uint64_t count,
   return fmg::guard([&] {
     check_index(ix);
     fmg::DeviceScope scope(ix->device);
-    launch_occ_pair(ix, kl, count, out, as_stream(stream), per, threads);
+    launch_occ_pair(ix, kl, count, out, as_stream(stream), nullptr, per, threads);
   });
 }
 
@@ -1640,12 +1655,17 @@ int fmg_occ_pair_host(const fmg_index* ix, const uint32_t* kl, uint64_t count, u
   return fmg::guard([&] {
     check_index(ix);
     fmg::DeviceScope scope(ix->device);
+    if (count == 0) return;
     const uint64_t chunk = std::min<uint64_t>(count, 1ull << 21);
+    cudaStream_t s0 = host_stream(ix->device, 0);
+    CallStatus st(nullptr, s0);
+    FMG_CK(cudaStreamSynchronize(s0));  // the word is zeroed before any slot's kernel reads it
     pipeline_host(ix->device, count, std::max<uint64_t>(chunk, 1), 8, 32, kl, out,
                   [&](void* din, uint64_t len, void* dout, cudaStream_t s) {
-                    launch_occ_pair(ix, static_cast<const uint32_t*>(din), len, static_cast<uint32_t*>(dout), s);
+                    launch_occ_pair(ix, static_cast<const uint32_t*>(din), len, static_cast<uint32_t*>(dout), s,
+                                    st.word);
                   });
-    take_input_error(ix, nullptr, "Occ position out of range or pair out of order");
+    st.raise_if_set(s0, "Occ position out of range or pair out of order");
   });
 }
 
@@ -1839,26 +1859,27 @@ void fmg_matches_free(fmg_matches* m) {
 }
 
 int fmg_psi_inverse(const fmg_index* ix, const uint32_t* rows, uint64_t count, uint8_t* out_sym, uint32_t* out_row,
-                    void* stream) {
+                    uint32_t* status, void* stream) {
   return fmg::guard([&] {
     check_index(ix);
     if (count == 0) return;
     fmg::DeviceScope scope(ix->device);
     with_words(ix, [&](auto wt) {
       fmg::k_psi<decltype(wt)::value><<<unsigned((count + 255) / 256), 256, 0, as_stream(stream)>>>(
-          ix->view(), rows, count, out_sym, out_row, ix->err);
+          ix->view(), rows, count, out_sym, out_row, status);
     });
     FMG_CK(cudaGetLastError());
   });
 }
 
-int fmg_locate_rows(const fmg_index* ix, const uint32_t* rows, uint64_t count, uint32_t* out_pos, void* stream) {
+int fmg_locate_rows(const fmg_index* ix, const uint32_t* rows, uint64_t count, uint32_t* out_pos, uint32_t* status,
+                    void* stream) {
   return fmg::guard([&] {
     check_index(ix);
     FMG_REQUIRE(ix->samples != nullptr, "index has no suffix-array samples (fmg_index_set_samples)");
     if (count == 0) return;
     fmg::DeviceScope scope(ix->device);
-    launch_locate(ix, rows, count, out_pos, as_stream(stream));
+    launch_locate(ix, rows, count, out_pos, as_stream(stream), status);
     FMG_CK(cudaGetLastError());
   });
 }
@@ -1870,12 +1891,16 @@ int fmg_locate_rows_host(const fmg_index* ix, const uint32_t* rows, uint64_t cou
     if (count == 0) return;
     fmg::DeviceScope scope(ix->device);
     const uint64_t chunk = std::min<uint64_t>(count, 1ull << 22);
+    cudaStream_t s0 = host_stream(ix->device, 0);
+    CallStatus st(nullptr, s0);
+    FMG_CK(cudaStreamSynchronize(s0));
     pipeline_host(ix->device, count, chunk, 4, 4, rows, out_pos,
                   [&](void* din, uint64_t len, void* dout, cudaStream_t s) {
-                    launch_locate(ix, static_cast<const uint32_t*>(din), len, static_cast<uint32_t*>(dout), s);
+                    launch_locate(ix, static_cast<const uint32_t*>(din), len, static_cast<uint32_t*>(dout), s,
+                                  st.word);
                     FMG_CK(cudaGetLastError());
                   });
-    take_input_error(ix, nullptr, "row out of range");
+    st.raise_if_set(s0, "row out of range");
   });
 }
 

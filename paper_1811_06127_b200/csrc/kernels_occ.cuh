@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(256) k_occ_pair(IndexView ix, const uint2* __r
   for (int u = 0; u < PER; ++u) {
     const uint32_t k = q[u].x, l = q[u].y;
     ok[u] = act[u] && l <= ix.n && k <= l + 1u;
-    if (act[u] && !ok[u]) atomicOr(err, 1u);
+    if (act[u] && !ok[u] && err) atomicOr(err, 1u);
     const uint32_t hh = ok[u] ? l : 0u;
     const uint32_t ll = (ok[u] && k != 0u) ? k - 1u : hh;
     const uint32_t jh = line_of<W>(hh), jl = line_of<W>(ll);
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(256) k_occ_pair_2l(IndexView ix, const uint2* 
   const uint2 q = ld_stream_u2(kl + i);
   const uint32_t k = q.x, l = q.y;
   const bool ok = l <= ix.n && k <= l + 1u;
-  if (!ok && role == 0u) atomicOr(err, 1u);
+  if (!ok && role == 0u && err) atomicOr(err, 1u);
   const bool none = !ok || (role == 0u && k == 0u);  // Occ(., -1) = 0
   const uint32_t p = role ? l : k - 1u;
   const uint32_t pp = none ? (ok ? l : 0u) : p;  // a lane with nothing to count reads its partner's line
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(256) k_occ_pair_coop(IndexView ix, const uint2
     const uint2 q = ld_stream_u2(kl + i);
     const uint32_t k = q.x, l = q.y;
     const bool ok = l <= ix.n && k <= l + 1u;
-    if (!ok && sector == 0) atomicOr(err, 1u);
+    if (!ok && sector == 0 && err) atomicOr(err, 1u);
     const uint32_t hh = ok ? l : 0u;
     const uint32_t ll = (ok && k != 0u) ? k - 1u : hh;
     const uint32_t jh = line_of<W>(hh), jl = line_of<W>(ll);

@@ -210,7 +210,7 @@ __global__ void k_psi(IndexView ix, const uint32_t* __restrict__ rows, uint64_t 
   if (q >= count) return;
   const uint32_t row = rows[q];
   if (row > ix.n) {
-    atomicOr(err, 1u);
+    if (err) atomicOr(err, 1u);
     out_sym[q] = 255;
     out_row[q] = 0xFFFFFFFFu;
     return;
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(256) k_locate(IndexView ix, const uint32_t* __
   for (uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < count; q += stride) {
     uint32_t row = rows[q];
     if (row > ix.n) {
-      atomicOr(err, 1u);
+      if (err) atomicOr(err, 1u);
       out_pos[q] = 0xFFFFFFFFu;
       continue;
     }
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(256) k_locate(IndexView ix, const uint32_t* __
       row = psi_step<W>(ix, row, sym);
       ++steps;
       if (steps > ix.n + 1u) {  // corrupt index (search.py:207-208)
-        atomicOr(err, 2u);
+        if (err) atomicOr(err, 2u);
         out_pos[q] = 0xFFFFFFFFu;
         break;
       }

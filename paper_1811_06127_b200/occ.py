@@ -58,14 +58,19 @@ def validate_pairs(index: FmIndex, low: np.ndarray, high: np.ndarray) -> None:
 
 
 def occ_pair_batch(index: FmIndex, low, high=None, kernel: Kernel | str | None = None,
-                   device: int | None = None, out=None):
+                   device: int | None = None, out=None, status=None):
     """All eight counts for N Occ steps: Occ(b, low[i]) and Occ(b, high[i]).
 
     Host form: `low`, `high` are integer arrays (low = k-1 may be -1); returns
     an (N, 8) uint32 array [low A, C, G, T, high A, C, G, T].
     Device form: `low` is a CUDA uint32/int32 tensor of shape (N, 2) holding
     (k, l) pairs with k = low + 1 (the kernel's native input); the result is
-    an (N, 8) CUDA tensor produced asynchronously on torch's current stream.
+    an (N, 8) CUDA tensor (uint32 when n >= 2^31, else int32) on torch's
+    current stream.  Pairs are validated on the device (k <= l + 1, l <= n)
+    into a per-call status word: with `status=None` the call checks it before
+    returning (one synchronisation) and raises ValueError like the host form;
+    with a caller-supplied int32 CUDA tensor `status` (zeroed by the caller)
+    the call stays asynchronous and the caller inspects it (non-zero = error).
     """
     resolve_kernel(kernel)
     if _is_cuda_tensor(low):
@@ -76,12 +81,26 @@ def occ_pair_batch(index: FmIndex, low, high=None, kernel: Kernel | str | None =
             raise ValueError("device pairs must be an (N, 2) int32/uint32 tensor of (k, l)")
         kl = kl.contiguous()
         dev = index.device_index(kl.device.index)
+        wide = index.n >= (1 << 31)
         if out is None:
-            out = torch.empty((kl.shape[0], 8), dtype=torch.int32, device=kl.device)
+            out = torch.empty((kl.shape[0], 8), dtype=torch.uint32 if wide else torch.int32, device=kl.device)
+        elif (not _is_cuda_tensor(out) or out.device != kl.device or not out.is_contiguous()
+              or out.dtype not in (torch.int32, torch.uint32) or tuple(out.shape) != (kl.shape[0], 8)):
+            raise ValueError("out must be a contiguous (N, 8) int32/uint32 tensor on the pairs' device")
+        elif wide and out.dtype != torch.uint32:
+            raise ValueError("out must be uint32 when n >= 2^31 (counts exceed int32)")
+        check = status is None
+        if check:
+            status = torch.zeros(1, dtype=torch.int32, device=kl.device)
+        elif (not _is_cuda_tensor(status) or status.device != kl.device or status.dtype not in (torch.int32, torch.uint32)
+              or status.numel() < 1):
+            raise ValueError("status must be an int32/uint32 CUDA tensor on the pairs' device")
         _lib.check(
-            _lib.load().fmg_occ_pair(dev.handle, kl.data_ptr(), kl.shape[0], out.data_ptr(),
+            _lib.load().fmg_occ_pair(dev.handle, kl.data_ptr(), kl.shape[0], out.data_ptr(), status.data_ptr(),
                                      _torch_stream(dev.device))
         )
+        if check and int(status.item()):
+            raise ValueError(f"Occ pair out of range or out of order (need k <= l + 1 and l <= {index.n})")
         return out
     low = np.asarray(low, dtype=np.int64).reshape(-1)
     high = np.asarray(high, dtype=np.int64).reshape(-1)

@@ -247,9 +247,12 @@ def psi_inverse_batch(index: FmIndex, rows, device: int | None = None) -> tuple[
         d_rows = torch.from_numpy(rows.astype(np.uint32).view(np.int32)).to(f"cuda:{dev.device}")
         d_sym = torch.empty(n, dtype=torch.uint8, device=d_rows.device)
         d_prev = torch.empty(n, dtype=torch.int32, device=d_rows.device)
+        d_status = torch.zeros(1, dtype=torch.int32, device=d_rows.device)
         stream = torch.cuda.current_stream(dev.device)
         _lib.check(_lib.load().fmg_psi_inverse(dev.handle, d_rows.data_ptr(), n, d_sym.data_ptr(),
-                                               d_prev.data_ptr(), stream.cuda_stream))
+                                               d_prev.data_ptr(), d_status.data_ptr(), stream.cuda_stream))
+        if int(d_status.item()):  # rows were range-checked above: only a corrupt index gets here
+            raise RuntimeError("fmgpu: psi_inverse reported an input error on validated rows")
         sym[:] = d_sym.cpu().numpy()
         prev[:] = d_prev.cpu().numpy().view(np.uint32)
     return sym, np.where(sym == 255, -1, prev.astype(np.int64))

@@ -49,7 +49,7 @@ def test_library_has_sm100a_code():
 def test_error_channel_and_invalid_args():
     lib = _lib.load()
     # null handle -> FMG_EINVAL, message on the thread-local channel
-    rc = lib.fmg_occ_pair(None, None, 0, None, None)
+    rc = lib.fmg_occ_pair(None, None, 0, None, None, None)
     assert rc == _lib.FMG_EINVAL
     assert "null" in _lib.last_error()
     with pytest.raises(ValueError):

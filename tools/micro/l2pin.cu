@@ -1,0 +1,314 @@
+// Occ-step memory-pattern model for HBM-resident indexes: does L2 residency
+// control (evict_last index loads / a persisting access-policy window, with
+// evict_first streams) and a denser 128-byte chunk layout raise the random
+// Occ-step rate?  Positions follow config 1 (k ~ U[0,n], l = k + Geom(0.01)),
+// generated from a hash on the device; every step streams 8 B in and 32 B out
+// like k_occ_pair.  Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a l2pin.cu -o /tmp/l2pin
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+__device__ __forceinline__ uint64_t mix(uint64_t x) {
+  x ^= x >> 31;
+  x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 29;
+  x *= 0x94D049BB133111EBull;
+  x ^= x >> 32;
+  return x;
+}
+
+__global__ void k_pairs(uint2* kl, uint64_t count, uint32_t n) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const uint64_t h = mix(i * 0x9E3779B97F4A7C15ull + 12345);
+  const uint32_t k = uint32_t((h & 0xFFFFFFFFull) % (uint64_t(n) + 1));
+  const double u = (double((h >> 32) & 0xFFFFFF) + 0.5) / 16777216.0;
+  const uint32_t g = 1u + uint32_t(floor(log(u) / log(0.99)));
+  const uint64_t l = min(uint64_t(k) + g, uint64_t(n));
+  kl[i] = make_uint2(k, uint32_t(l));
+}
+
+template <int MODE>  // 0 plain, 1 evict_last (fraction), 2 evict_first, 3 evict_normal hint
+__device__ __forceinline__ void ld32(const uint8_t* p, uint64_t pol, uint64_t& a0, uint64_t& a1, uint64_t& a2,
+                                     uint64_t& a3) {
+  if (MODE == 0) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3)
+                 : "l"(p));
+  } else if (MODE == 4) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3)
+                 : "l"(p));
+  } else if (MODE == 5) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::128B.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3)
+                 : "l"(p));
+  } else {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u64 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3)
+                 : "l"(p), "l"(pol));
+  }
+}
+
+__device__ __forceinline__ uint64_t pol_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+template <int SMODE>
+__device__ __forceinline__ uint2 ld_in(const uint2* p) {
+  uint2 v;
+  if (SMODE == 0) {
+    asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  } else {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y)
+                 : "l"(p), "l"(pol_first()));
+  }
+  return v;
+}
+
+template <int SMODE>
+__device__ __forceinline__ void st_out(uint32_t* p, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+  if (SMODE == 0) {
+    asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+  } else if (SMODE == 1) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "l"(a),
+                 "l"(b), "l"(c), "l"(d), "l"(pol_first())
+                 : "memory");
+  } else {
+    asm volatile("st.global.cs.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+  }
+}
+
+// W = 2 layout: 64 chars per 32-byte line, one thread per step.
+template <int MODE, int SMODE>
+__global__ void __launch_bounds__(256) k_l32(const uint8_t* __restrict__ lines, const uint2* __restrict__ kl,
+                                             uint64_t count, uint32_t* __restrict__ out, float frac) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  uint64_t pol = 0;
+  if (MODE == 1) asm("createpolicy.fractional.L2::evict_last.b64 %0, %1;" : "=l"(pol) : "f"(frac));
+  if (MODE == 2) asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  if (MODE == 3) asm("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(pol));
+  const uint2 q = ld_in<SMODE == 0 ? 0 : 1>(kl + i);
+  const uint32_t lo = q.x == 0 ? q.y : q.x - 1, hi = q.y;
+  const uint32_t jl = lo >> 6, jh = hi >> 6;
+  uint64_t a0, a1, a2, a3, b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+  ld32<MODE>(lines + size_t(jh) * 32, pol, a0, a1, a2, a3);
+  if (jl != jh) ld32<MODE>(lines + size_t(jl) * 32, pol, b0, b1, b2, b3);
+  const uint64_t m1 = ~0ull >> (63 - (hi & 63)), m2 = ~0ull >> (63 - (lo & 63));
+  st_out<SMODE>(out + i * 8, a0 + __popcll(a2 & m1), a1 + __popcll(a3 & m1), b0 + __popcll(b2 & m2),
+                b1 + __popcll(b3 & m2));
+}
+
+// 128-byte chunk layout: CH chars per chunk, 4 lanes per step, one 128-byte
+// request per distinct chunk.
+template <int MODE, int SMODE, int CH>
+__global__ void __launch_bounds__(256) k_l128(const uint8_t* __restrict__ lines, const uint2* __restrict__ kl,
+                                              uint64_t count, uint32_t* __restrict__ out, float frac) {
+  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t i = t >> 2;
+  const int sec = int(t & 3);
+  if (i >= count) return;
+  uint64_t pol = 0;
+  if (MODE == 1) asm("createpolicy.fractional.L2::evict_last.b64 %0, %1;" : "=l"(pol) : "f"(frac));
+  if (MODE == 2) asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  if (MODE == 3) asm("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(pol));
+  const uint2 q = ld_in<SMODE == 0 ? 0 : 1>(kl + i);
+  const uint32_t lo = q.x == 0 ? q.y : q.x - 1, hi = q.y;
+  const uint32_t jl = lo / CH, jh = hi / CH;
+  uint64_t a0, a1, a2, a3, b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+  ld32<MODE>(lines + size_t(jh) * 128 + sec * 32, pol, a0, a1, a2, a3);
+  if (jl != jh) ld32<MODE>(lines + size_t(jl) * 128 + sec * 32, pol, b0, b1, b2, b3);
+  uint32_t s = __popcll(a0 & (~0ull >> (hi & 63))) + __popcll(a2 ^ a3) + __popcll(b0 & (~0ull >> (lo & 63))) +
+               __popcll(b1 ^ a1) + __popcll(b2 ^ b3);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  if (sec == 0) st_out<SMODE>(out + i * 8, s, a1, b1, a3);
+}
+
+// 128-byte chunk layout, 4 lanes per step, PER steps per lane group (all
+// loads issued before any use: more chunk fetches in flight per thread).
+template <int PER, int CH>
+__global__ void __launch_bounds__(256) k_c128_coop(const uint8_t* __restrict__ lines, const uint2* __restrict__ kl,
+                                                   uint64_t count, uint32_t* __restrict__ out) {
+  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int sec = int(t & 3);
+  const uint64_t g = t >> 2;  // group
+  const uint64_t groups_per_block = blockDim.x / 4;
+  const uint64_t base = (g / groups_per_block) * groups_per_block * PER + (g % groups_per_block);
+  uint64_t a[PER][4], b[PER][4];
+  uint32_t lo[PER], hi[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const uint64_t i = base + u * groups_per_block;
+    const uint2 q = i < count ? ld_in<1>(kl + i) : make_uint2(1, 0);
+    lo[u] = q.x == 0 ? q.y : q.x - 1;
+    hi[u] = q.y;
+    const uint32_t jl = lo[u] / CH, jh = hi[u] / CH;
+    ld32<0>(lines + size_t(jh) * 128 + sec * 32, 0, a[u][0], a[u][1], a[u][2], a[u][3]);
+    b[u][0] = b[u][1] = b[u][2] = b[u][3] = 0;
+    if (jl != jh) ld32<0>(lines + size_t(jl) * 128 + sec * 32, 0, b[u][0], b[u][1], b[u][2], b[u][3]);
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const uint64_t i = base + u * groups_per_block;
+    uint32_t s = __popcll(a[u][0] & (~0ull >> (hi[u] & 63))) + __popcll(a[u][2] ^ a[u][3]) +
+                 __popcll(b[u][0] & (~0ull >> (lo[u] & 63))) + __popcll(b[u][1] ^ a[u][1]) + __popcll(b[u][2] ^ b[u][3]);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (sec == 0 && i < count) st_out<1>(out + i * 8, s, a[u][1], b[u][1], a[u][3]);
+  }
+}
+
+// 128-byte chunk layout, one thread per step: the header sector plus the
+// data sector of each position (sector-granular L2 requests; the first miss
+// brings the whole 128-byte chunk into L2).
+template <int PER, int CH>
+__global__ void __launch_bounds__(256) k_c128_thread(const uint8_t* __restrict__ lines, const uint2* __restrict__ kl,
+                                                     uint64_t count, uint32_t* __restrict__ out) {
+  const uint64_t first = uint64_t(blockIdx.x) * blockDim.x * PER + threadIdx.x;
+  uint64_t r[PER][4][4];
+  bool act[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const uint64_t i = first + uint64_t(u) * blockDim.x;
+    act[u] = i < count;
+    const uint2 q = act[u] ? ld_in<1>(kl + i) : make_uint2(1, 0);
+    const uint32_t lo = q.x == 0 ? q.y : q.x - 1, hi = q.y;
+    const uint32_t jl = lo / CH, jh = hi / CH;
+    const uint32_t sh = 1 + (hi - jh * CH) * 3 / CH, sl = 1 + (lo - jl * CH) * 3 / CH;
+    const uint8_t* ph = lines + size_t(jh) * 128;
+    const uint8_t* pl = lines + size_t(jl) * 128;
+    ld32<0>(ph, 0, r[u][0][0], r[u][0][1], r[u][0][2], r[u][0][3]);
+    ld32<0>(ph + 32 * sh, 0, r[u][1][0], r[u][1][1], r[u][1][2], r[u][1][3]);
+    for (int z = 0; z < 4; ++z) r[u][2][z] = r[u][3][z] = 0;
+    if (jl != jh) ld32<0>(pl, 0, r[u][2][0], r[u][2][1], r[u][2][2], r[u][2][3]);
+    if (jl != jh || sl != sh) ld32<0>(pl + 32 * sl, 0, r[u][3][0], r[u][3][1], r[u][3][2], r[u][3][3]);
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    if (!act[u]) continue;
+    const uint64_t i = first + uint64_t(u) * blockDim.x;
+    uint64_t x = 0;
+    for (int z = 0; z < 4; ++z) x += __popcll(r[u][0][z] ^ r[u][1][z]) + __popcll(r[u][2][z] ^ r[u][3][z]);
+    st_out<1>(out + i * 8, x, r[u][1][1], r[u][2][2], r[u][3][3]);
+  }
+}
+
+// W = 2 layout, PER steps per thread.
+template <int MODE, int PER>
+__global__ void __launch_bounds__(256) k_l32p(const uint8_t* __restrict__ lines, const uint2* __restrict__ kl,
+                                              uint64_t count, uint32_t* __restrict__ out) {
+  const uint64_t first = uint64_t(blockIdx.x) * blockDim.x * PER + threadIdx.x;
+  uint64_t a[PER][4], b[PER][4];
+  uint32_t lo[PER], hi[PER];
+  bool act[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const uint64_t i = first + uint64_t(u) * blockDim.x;
+    act[u] = i < count;
+    const uint2 q = act[u] ? ld_in<1>(kl + i) : make_uint2(1, 0);
+    lo[u] = q.x == 0 ? q.y : q.x - 1;
+    hi[u] = q.y;
+    const uint32_t jl = lo[u] >> 6, jh = hi[u] >> 6;
+    ld32<MODE>(lines + size_t(jh) * 32, 0, a[u][0], a[u][1], a[u][2], a[u][3]);
+    b[u][0] = b[u][1] = b[u][2] = b[u][3] = 0;
+    if (jl != jh) ld32<MODE>(lines + size_t(jl) * 32, 0, b[u][0], b[u][1], b[u][2], b[u][3]);
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    if (!act[u]) continue;
+    const uint64_t i = first + uint64_t(u) * blockDim.x;
+    const uint64_t m1 = ~0ull >> (63 - (hi[u] & 63)), m2 = ~0ull >> (63 - (lo[u] & 63));
+    st_out<1>(out + i * 8, a[u][0] + __popcll(a[u][2] & m1), a[u][1] + __popcll(a[u][3] & m1),
+              b[u][0] + __popcll(b[u][2] & m2), b[u][1] + __popcll(b[u][3] & m2));
+  }
+}
+
+int main(int argc, char** argv) {
+  const uint32_t n = argc > 1 ? uint32_t(atoll(argv[1])) : 1000000000u;
+  const uint64_t count = 1ull << 24;
+  int dev = 0;
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, dev);
+  printf("%s: L2 %d MB, persistingL2CacheMaxSize %d MB, accessPolicyMaxWindowSize %d MB\n", prop.name,
+         prop.l2CacheSize >> 20, prop.persistingL2CacheMaxSize >> 20, prop.accessPolicyMaxWindowSize >> 20);
+  const size_t b32 = (size_t(n) / 64 + 1) * 32, b128 = (size_t(n) / 448 + 1) * 128;
+  uint8_t *l32, *l128;
+  uint2* kl;
+  uint32_t* out;
+  cudaMalloc(&l32, b32);
+  cudaMalloc(&l128, b128 + 4096);
+  cudaMemset(l32, 1, b32);
+  cudaMemset(l128, 1, b128);
+  cudaMalloc(&kl, count * 8);
+  cudaMalloc(&out, count * 32);
+  k_pairs<<<count / 256, 256>>>(kl, count, n);
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  printf("n=%u: W2 lines %.0f MB, 128B chunks (448 ch) %.0f MB\n", n, b32 / 1e6, b128 / 1e6);
+  auto time = [&](const char* name, auto launch) {
+    for (int r = 0; r < 3; ++r) launch();
+    cudaEventRecord(e0, st);
+    for (int r = 0; r < 10; ++r) launch();
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= 10;
+    printf("%-58s %8.1f us  %6.2f G steps/s  %s\n", name, ms * 1e3, count / ms / 1e6,
+           cudaGetErrorString(cudaGetLastError()));
+  };
+  const unsigned g1 = count / 256, g4 = count * 4 / 256;
+#define T32(M, S, F) time("W2 mode " #M " stream " #S " frac " #F, [&] { k_l32<M, S><<<g1, 256, 0, st>>>(l32, kl, count, out, F); })
+#define T128(M, S, F) time("C128 mode " #M " stream " #S " frac " #F, [&] { k_l128<M, S, 448><<<g4, 256, 0, st>>>(l128, kl, count, out, F); })
+  T32(0, 1, 1.f);
+  T32(4, 1, 1.f);
+  time("W2 PER=2", [&] { k_l32p<0, 2><<<g1 / 2, 256, 0, st>>>(l32, kl, count, out); });
+  time("W2 PER=4", [&] { k_l32p<0, 4><<<g1 / 4, 256, 0, st>>>(l32, kl, count, out); });
+  time("W2 64B-hint PER=2", [&] { k_l32p<4, 2><<<g1 / 2, 256, 0, st>>>(l32, kl, count, out); });
+  time("W2 64B-hint PER=4", [&] { k_l32p<4, 4><<<g1 / 4, 256, 0, st>>>(l32, kl, count, out); });
+  time("C128 coop PER=1", [&] { k_c128_coop<1, 448><<<g4, 256, 0, st>>>(l128, kl, count, out); });
+  time("C128 coop PER=2", [&] { k_c128_coop<2, 448><<<g4 / 2, 256, 0, st>>>(l128, kl, count, out); });
+  time("C128 coop PER=4", [&] { k_c128_coop<4, 448><<<g4 / 4, 256, 0, st>>>(l128, kl, count, out); });
+  time("C128 thread PER=1", [&] { k_c128_thread<1, 448><<<g1, 256, 0, st>>>(l128, kl, count, out); });
+  time("C128 thread PER=2", [&] { k_c128_thread<2, 448><<<g1 / 2, 256, 0, st>>>(l128, kl, count, out); });
+  time("C128 thread PER=4", [&] { k_c128_thread<4, 448><<<g1 / 4, 256, 0, st>>>(l128, kl, count, out); });
+  if (argc > 2) return 0;
+  // persisting access-policy window over the index
+  for (double hr : {1.0, 0.5, 0.3, 0.15}) {
+    size_t lim = prop.persistingL2CacheMaxSize;
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
+    for (int lay = 0; lay < 2; ++lay) {
+      cudaStreamAttrValue a = {};
+      a.accessPolicyWindow.base_ptr = lay ? (void*)l128 : (void*)l32;
+      size_t bytes = lay ? b128 : b32;
+      a.accessPolicyWindow.num_bytes = bytes < size_t(prop.accessPolicyMaxWindowSize) ? bytes : prop.accessPolicyMaxWindowSize;
+      a.accessPolicyWindow.hitRatio = float(hr);
+      a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a);
+      char nm[96];
+      snprintf(nm, sizeof nm, "%s window %.0f MB hitRatio %.2f (limit %zu MB)", lay ? "C128" : "W2",
+               a.accessPolicyWindow.num_bytes / 1e6, hr, lim >> 20);
+      if (lay)
+        time(nm, [&] { k_l128<0, 1, 448><<<g4, 256, 0, st>>>(l128, kl, count, out, 1.f); });
+      else
+        time(nm, [&] { k_l32<0, 1><<<g1, 256, 0, st>>>(l32, kl, count, out, 1.f); });
+      a.accessPolicyWindow.num_bytes = 0;
+      cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a);
+      cudaCtxResetPersistingL2Cache();
+    }
+  }
+  return 0;
+}

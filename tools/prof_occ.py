@@ -42,7 +42,7 @@ e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
 for i in range(5):
     if i == 3:
         e0.record()
-    _lib.check(lib.fmg_occ_pair(h, d_kl.data_ptr(), kl.shape[0], d_out.data_ptr(), s))
+    _lib.check(lib.fmg_occ_pair(h, d_kl.data_ptr(), kl.shape[0], d_out.data_ptr(), None, s))
 e1.record()
 torch.cuda.synchronize()
 print(which, "us/launch", e0.elapsed_time(e1) / 2 * 1e3)

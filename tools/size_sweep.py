@@ -22,11 +22,11 @@ for n in [1 << 24, 1 << 26, 1 << 27, 1 << 28, 1 << 29, 1 << 30, 3_000_000_000]:
     h = idx.device_index(0).handle
     s = torch.cuda.current_stream().cuda_stream
     for _ in range(3):
-        lib.fmg_occ_pair(h, d_kl.data_ptr(), kl.shape[0], d_out.data_ptr(), s)
+        lib.fmg_occ_pair(h, d_kl.data_ptr(), kl.shape[0], d_out.data_ptr(), None, s)
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
     for _ in range(10):
-        lib.fmg_occ_pair(h, d_kl.data_ptr(), kl.shape[0], d_out.data_ptr(), s)
+        lib.fmg_occ_pair(h, d_kl.data_ptr(), kl.shape[0], d_out.data_ptr(), None, s)
     e1.record()
     torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / 10 / 1e3
