@@ -15,6 +15,7 @@
  *   fmg_inexact*       <- search.py:97-159 inexact_search
  *   fmg_psi_inverse    <- search.py:172-186 psi_inverse_fused
  *   fmg_locate_rows    <- search.py:189-208 locate_row
+ *   fmg_reconstruct_text <- search.py:270-286 reconstruct_reference
  *
  * Conventions
  *   - Plain pointers and sizes only; no C++ or torch types.
@@ -171,6 +172,37 @@ int fmg_locate_rows(const fmg_index* index, const uint32_t* rows, uint64_t count
                     uint32_t* out_pos, uint32_t* status, void* stream);
 int fmg_locate_rows_host(const fmg_index* index, const uint32_t* rows, uint64_t count,
                          uint32_t* out_pos);
+
+/* reconstruct_reference (search.py:270-286): the n text codes (0..3) the
+ * index was built from, recovered on the GPU by walking the predecessor cycle
+ * from every sampled row in parallel (~32 steps each); requires
+ * fmg_index_set_samples.  status bit 2 = corrupt index. */
+int fmg_reconstruct_text(const fmg_index* index, uint8_t* codes_out /* device, n */, uint32_t* status,
+                         void* stream);
+int fmg_reconstruct_text_host(const fmg_index* index, uint8_t* codes_out /* host, n */);
+
+/* ---------------------------------------------------------------------------
+ * Bucket-level rank kernels: the reference's per-bucket plugin surface
+ * (kernels.py:125-292, count_bucket_* / count_bucket_all4 / mask_bucket) as
+ * batched kernels.  blocks: count x 32 packed bytes (128 fields, reference
+ * bit order), 32-byte aligned; prefix_lens in [0, 128]; symbols in [0, 4) or
+ * NULL for all four counts (out: count x 4 u32 in A, C, G, T order, else
+ * count x 1).  method 0 = masked popcount (scalar / bytelut / auto), 1 = the
+ * paper's nibble pipeline (PRMT table lookups + SAD; nibble / simd).
+ * Device form: device pointers on the CURRENT device, `status` as above.
+ * Host forms run on `device` and return FMG_EINVAL for a bad prefix / symbol.
+ * fmg_bucket_nibble_trace_host writes 15 u64 per query (KernelTrace,
+ * kernels.py:101-115): masked words[4], lookup lo words[4], lookup hi
+ * words[4], group SADs (16 bits each), sad_total | raw_count << 32, count.
+ * ------------------------------------------------------------------------- */
+int fmg_bucket_count(const uint8_t* blocks, const uint32_t* prefix_lens, const uint8_t* symbols,
+                     uint64_t count, int method, uint32_t* out, uint32_t* status, void* stream);
+int fmg_bucket_count_host(int device, const uint8_t* blocks, const uint32_t* prefix_lens,
+                          const uint8_t* symbols, uint64_t count, int method, uint32_t* out);
+int fmg_bucket_mask_host(int device, const uint8_t* blocks, const uint32_t* prefix_lens, uint64_t count,
+                         uint8_t* out);
+int fmg_bucket_nibble_trace_host(int device, const uint8_t* blocks, const uint32_t* prefix_lens,
+                                 const uint8_t* symbols, uint64_t count, uint64_t* trace);
 
 /* Blocks until all work the library queued on `stream` has finished. */
 int fmg_stream_sync(void* stream);

@@ -51,6 +51,12 @@ PROTOTYPES: dict[str, tuple] = {
     "fmg_psi_inverse": (ct.c_int, [_vp, _vp, ct.c_uint64, _vp, _vp, _vp, _vp]),
     "fmg_locate_rows": (ct.c_int, [_vp, _vp, ct.c_uint64, _vp, _vp, _vp]),
     "fmg_locate_rows_host": (ct.c_int, [_vp, _vp, ct.c_uint64, _vp]),
+    "fmg_reconstruct_text": (ct.c_int, [_vp, _vp, _vp, _vp]),
+    "fmg_reconstruct_text_host": (ct.c_int, [_vp, _vp]),
+    "fmg_bucket_count": (ct.c_int, [_vp, _vp, _vp, ct.c_uint64, ct.c_int, _vp, _vp, _vp]),
+    "fmg_bucket_count_host": (ct.c_int, [ct.c_int, _vp, _vp, _vp, ct.c_uint64, ct.c_int, _vp]),
+    "fmg_bucket_mask_host": (ct.c_int, [ct.c_int, _vp, _vp, ct.c_uint64, _vp]),
+    "fmg_bucket_nibble_trace_host": (ct.c_int, [ct.c_int, _vp, _vp, _vp, ct.c_uint64, _vp]),
     "fmg_stream_sync": (ct.c_int, [_vp]),
 }
 

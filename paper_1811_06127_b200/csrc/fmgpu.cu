@@ -16,6 +16,7 @@
 #include <cstring>
 #include <type_traits>
 #include <string>
+#include <atomic>
 #include <mutex>
 #include <unordered_map>
 #include <array>
@@ -97,6 +98,8 @@ struct DevBuf {
 #include "kernels_search.cuh"
 #include "kernels_inexact.cuh"
 #include "kernels_bidir.cuh"
+#include "kernels_bucket.cuh"
+#include "kernels_chunk.cuh"
 
 namespace fmg {
 
@@ -149,7 +152,18 @@ struct fmg_index {
   uint64_t n_buckets = 0, n_lines = 0, n_samples = 0;
   int words = 2;  // line layout: W words of 32 chars per line (occ_device.cuh)
   uint8_t* lines = nullptr;
-  uint32_t* samples = nullptr;
+  // 128-byte chunk layout of the same transform (kernels_chunk.cuh), built
+  // for HBM-resident indexes only: the Occ-step kernel reads it instead of
+  // the lines (416 instead of 256 characters per DRAM fetch)
+  uint32_t* chunks = nullptr;
+  uint64_t n_chunks = 0;
+  // Attachments (fmg_index_set_samples / fmg_index_set_reverse) are
+  // one-time: the first attach uploads and publishes the pointer with a
+  // release store under attach_mu, later attaches are no-ops, and nothing is
+  // freed before fmg_index_destroy — a launch that read a pointer can never
+  // see it freed or replaced.  Readers use acquire loads.
+  std::mutex attach_mu;
+  std::atomic<uint32_t*> samples{nullptr};
   int sms = 148;
   // exact-search k-mer table (built on first large exact call; see KmerTable)
   std::mutex lut_mu;
@@ -157,7 +171,7 @@ struct fmg_index {
   uint32_t lut_k = 0;
   // optional index of the reversed text (fmg_index_set_reverse): the
   // bidirectional z = 1 engine (kernels_bidir.cuh) and its prefix table
-  uint8_t* rev_lines = nullptr;
+  std::atomic<uint8_t*> rev_lines{nullptr};
   uint64_t rev_sentinel_row = 0;
   uint2* lut_r = nullptr;
   uint32_t tail[16] = {};
@@ -176,7 +190,7 @@ struct fmg_index {
 
   fmg::IndexView view_rev() const {
     fmg::IndexView v = view();
-    v.lines = rev_lines;
+    v.lines = rev_lines.load(std::memory_order_acquire);
     v.samples = nullptr;
     v.sentinel_row = uint32_t(rev_sentinel_row);
     return v;
@@ -185,7 +199,7 @@ struct fmg_index {
   fmg::IndexView view() const {
     fmg::IndexView v;
     v.lines = lines;
-    v.samples = samples;
+    v.samples = samples.load(std::memory_order_acquire);
     v.n = uint32_t(n);
     v.sentinel_row = uint32_t(sentinel_row);
     for (int s = 0; s < 5; ++s) v.c[s] = uint32_t(c[s]);
@@ -266,6 +280,49 @@ void with_words(const fmg_index* ix, F&& f) {
 
 constexpr int kOccPer = 1;
 
+// FMG_OCC_CHUNK=0: Occ steps read the lines even when chunks exist (A/B hook)
+bool chunk_off() {
+  static const bool off = [] {
+    const char* e = std::getenv("FMG_OCC_CHUNK");
+    return e != nullptr && std::atoi(e) == 0;
+  }();
+  return off;
+}
+
+// Chunk layout for line arrays above this size (HBM-resident; the L2-resident
+// config 1 keeps the one-sector lines, whose bound is the L2 request rate).
+// FMG_CHUNK_MIN_BYTES overrides (tests build chunks for small indexes too).
+uint64_t chunk_min_line_bytes() {
+  const char* e = std::getenv("FMG_CHUNK_MIN_BYTES");
+  return e ? std::strtoull(e, nullptr, 10) : (uint64_t(64) << 20);
+}
+
+uint32_t* build_chunks(const fmg_index* ix, const void* bucket_records, uint64_t& n_chunks) {
+  n_chunks = (ix->n + 1 + fmg::kChunkChars - 1) / fmg::kChunkChars;
+  uint32_t* chunks = nullptr;
+  FMG_CK(cudaMalloc(&chunks, n_chunks * fmg::kChunkBytes));
+  uint64_t* staging = nullptr;
+  const uint64_t nb = ix->n_buckets;
+  cudaError_t e = cudaMalloc(&staging, nb * 64 + 64);
+  uint32_t bad = 0;
+  if (e == cudaSuccess) {
+    uint32_t* err = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(staging) + nb * 64);
+    e = cudaMemcpy(staging, bucket_records, nb * 64, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(err, 0, 4);
+    if (e == cudaSuccess) {
+      fmg::k_build_chunks<<<unsigned((n_chunks + 255) / 256), 256>>>(staging, nb, chunks, n_chunks, err);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(&bad, err, 4, cudaMemcpyDeviceToHost);
+    cudaFree(staging);
+  }
+  if (e != cudaSuccess || bad) cudaFree(chunks);
+  FMG_CK(e);
+  FMG_REQUIRE(bad == 0, "bucket base does not fit 32 bits");
+  return chunks;
+}
+
 template <int PER>
 void launch_occ_pair_t(const fmg_index* ix, const uint32_t* kl, uint64_t count, uint32_t* out, cudaStream_t s,
                        uint32_t* err, int threads) {
@@ -277,7 +334,10 @@ void launch_occ_pair_t(const fmg_index* ix, const uint32_t* kl, uint64_t count, 
     // config 1-H, -8% on the L2-resident config 1 (profiles/r01_occ.md)
     const char* e2l = std::getenv("FMG_OCC_2LANE");  // A/B hook
     const bool two_lane = e2l ? std::atoi(e2l) != 0 : ix->n_lines * 32ull > (64ull << 20);
-    if (W == 2 && two_lane) {
+    if (ix->chunks && !chunk_off()) {
+      k_occ_pair_chunk<<<dim3(unsigned((count + 255) / 256)), 256, 0, s>>>(
+          ix->view(), ix->chunks, reinterpret_cast<const uint2*>(kl), count, out, err);
+    } else if (W == 2 && two_lane) {
       k_occ_pair_2l<<<dim3(unsigned((2 * count + 255) / 256)), 256, 0, s>>>(
           ix->view(), reinterpret_cast<const uint2*>(kl), count, out, err);
     } else if (W == 2) {
@@ -416,7 +476,7 @@ PrefixTable prefix_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
 // there is no reverse index, no forward table, or no room for it).
 PrefixTable prefix_table_rev(const fmg_index* cix, uint64_t count, cudaStream_t s) {
   const PrefixTable tf = prefix_table(cix, count, s);
-  if (!tf.base || !cix->rev_lines) return {};
+  if (!tf.base || !cix->rev_lines.load(std::memory_order_acquire)) return {};
   auto* ix = const_cast<fmg_index*>(cix);
   std::lock_guard<std::mutex> lock(ix->lut_mu);
   if (!ix->lut_r) {
@@ -877,6 +937,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     // (tools/prof_c3.py).  With a reverse index attached the bidirectional
     // split engine below beats both (config 2: 9.4 -> 6.4 ms per 1M seeds).
     const bool force_dfs = std::getenv("FMG_INEXACT_DFS") != nullptr;  // read per call (tests flip it)
+    const bool has_rev = ix->rev_lines.load(std::memory_order_acquire) != nullptr;
     const bool bidir_off_env = [] {
       const char* e = std::getenv("FMG_INEXACT_BIDIR");
       return e != nullptr && std::atoi(e) == 0;
@@ -884,7 +945,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     uint64_t line_bytes = 0;
     with_words(ix, [&](auto wt) { line_bytes = ix->n_lines * fmg::LineTraits<decltype(wt)::value>::kBytes; });
     if (z == 1 && short_pat && !force_dfs && line_bytes <= (uint64_t(64) << 20) &&
-        (ix->rev_lines == nullptr || bidir_off_env)) {
+        (!has_rev || bidir_off_env)) {
       CodePatterns cpz{codes, offsets, packed.ptr, packed1, uint32_t(max_len), dbits.ptr};
       if (run_z1(ix, cpz, count, max_len, s, counters.ptr + 2, res)) return res;
       // queues overflowed: fall through to the DFS engine (same results)
@@ -903,7 +964,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     }();
     BiIndex bi{};
     bool bidir = false;
-    if (z == 1 && short_pat && ix->rev_lines && pt.base && !bidir_off) {
+    if (z == 1 && short_pat && has_rev && pt.base && !bidir_off) {
       bi.rev = ix->view_rev();
       bi.tf = pt;
       bi.tr = prefix_table_rev(ix, count, s);
@@ -971,7 +1032,8 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     // slots suffice.  Kept small on purpose: shared memory and L1 share the
     // SM's SRAM, and for HBM-resident indexes the L1 left over is worth 30%
     // (config 3: S = 20 -> 667 ms, S = 10 -> 447 ms per 14M seeds).
-    uint32_t S = std::min<uint32_t>(S_max, 9 * z + 2);
+    uint32_t S = std::min<uint32_t>(std::min<uint32_t>(S_max, 9 * z + 2),
+                                    uint32_t(size_t(smem_optin) / (12 * 32)) - 1);
     if (const char* e = std::getenv("FMG_STACK_S")) S = std::max<uint32_t>(2, uint32_t(std::atoi(e)));  // A/B
     int first_pass = 0;
     DevBuf<uint32_t> retry_list;
@@ -1225,9 +1287,16 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       }
       list = lists[pass & 1].ptr;
       if (failed > 0) {
-        // grow whichever capacity might have been the cause
+        // grow whichever capacity might have been the cause; the DFS stack
+        // is capped at what shared memory holds at 32 threads per block
+        const uint32_t S_fit = uint32_t(size_t(smem_optin) / (12 * 32)) - 1;
+        if (R == (1u << 22) && S >= std::min(S_max, S_fit))
+          throw std::invalid_argument(
+              "inexact search: a pattern needs a DFS stack deeper than shared memory holds (" +
+              std::to_string(S_fit) + " entries) or more than 2^22 results; use a smaller max_diff or "
+              "shorter patterns");
         R = std::min<uint32_t>(R * 8, 1u << 22);
-        S = std::min<uint32_t>(S_max, S * 2);
+        S = std::min<uint32_t>(std::min(S_max, S_fit), S * 2);
         cap = std::max<uint64_t>(cap, std::min<uint64_t>(uint64_t(host_ctr[0]) * 2, 1ull << 31));
         cap = std::max<uint64_t>(cap, failed * uint64_t(R));
         cap = std::min<uint64_t>(cap, 1ull << 31);
@@ -1434,6 +1503,7 @@ int fmg_index_create(int device, const void* bucket_records, uint64_t n_buckets,
       ix->words = choose_words(n_buckets);
       ix->sms = fmg::sm_count(device);
       ix->lines = upload_lines(ix, bucket_records);
+      if (ix->n_lines * 32 > chunk_min_line_bytes()) ix->chunks = build_chunks(ix, bucket_records, ix->n_chunks);
       // Allow the stream-ordered pool to keep freed blocks (host entry points
       // allocate per call).
       cudaMemPool_t pool;
@@ -1456,20 +1526,20 @@ int fmg_index_set_reverse(fmg_index* ix, const void* bucket_records, uint64_t n_
     FMG_REQUIRE(n_buckets == ix->n_buckets, "reverse index bucket count does not match the index");
     FMG_REQUIRE(sentinel_row <= ix->n, "sentinel row outside [0, n]");
     fmg::DeviceScope scope(ix->device);
-    std::lock_guard<std::mutex> lock(ix->lut_mu);
-    if (ix->rev_lines) cudaFree(ix->rev_lines);
-    if (ix->lut_r) cudaFree(ix->lut_r);
-    ix->rev_lines = nullptr;
-    ix->lut_r = nullptr;
-    ix->rev_lines = upload_lines(ix, bucket_records);
+    std::lock_guard<std::mutex> lock(ix->attach_mu);
+    if (ix->rev_lines.load(std::memory_order_acquire)) return;  // attached once; the index is immutable
+    uint8_t* rev = upload_lines(ix, bucket_records);
     ix->rev_sentinel_row = sentinel_row;
     DevBuf<uint32_t> tail(16, nullptr);
     with_words(ix, [&](auto wt) {
       constexpr int W = decltype(wt)::value;
       fmg::k_tail_keys<W><<<1, 32>>>(ix->view(), 16u, tail.ptr);
     });
-    FMG_CK(cudaGetLastError());
-    FMG_CK(cudaMemcpy(ix->tail, tail.ptr, sizeof(ix->tail), cudaMemcpyDeviceToHost));
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(ix->tail, tail.ptr, sizeof(ix->tail), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) cudaFree(rev);
+    FMG_CK(e);
+    ix->rev_lines.store(rev, std::memory_order_release);  // publishes rev_sentinel_row and tail too
   });
 }
 
@@ -1477,7 +1547,7 @@ int fmg_index_has_reverse(const fmg_index* ix, int* has) {
   return fmg::guard([&] {
     check_index(ix);
     FMG_REQUIRE(has != nullptr, "null argument");
-    *has = ix->rev_lines != nullptr;
+    *has = ix->rev_lines.load(std::memory_order_acquire) != nullptr;
   });
 }
 
@@ -1492,11 +1562,15 @@ int fmg_index_set_samples(fmg_index* ix, const uint64_t* sa_samples, uint64_t co
       s32[i] = uint32_t(sa_samples[i]);
     }
     fmg::DeviceScope scope(ix->device);
-    if (ix->samples) cudaFree(ix->samples);
-    ix->samples = nullptr;
-    FMG_CK(cudaMalloc(&ix->samples, count * sizeof(uint32_t)));
-    FMG_CK(cudaMemcpy(ix->samples, s32.data(), count * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    std::lock_guard<std::mutex> lock(ix->attach_mu);
+    if (ix->samples.load(std::memory_order_acquire)) return;  // attached once; the index is immutable
+    uint32_t* d = nullptr;
+    FMG_CK(cudaMalloc(&d, count * sizeof(uint32_t)));
+    const cudaError_t e = cudaMemcpy(d, s32.data(), count * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) cudaFree(d);
+    FMG_CK(e);
     ix->n_samples = count;
+    ix->samples.store(d, std::memory_order_release);
   });
 }
 
@@ -1508,7 +1582,10 @@ int fmg_index_info(const fmg_index* ix, uint64_t* n, int* device, uint64_t* devi
     if (device_bytes) {
       uint64_t lb = 0;
       with_words(ix, [&](auto wt) { lb = fmg::LineTraits<decltype(wt)::value>::kBytes; });
-      *device_bytes = ix->n_lines * lb * (ix->rev_lines ? 2 : 1) + ix->n_samples * 4;
+      const bool rev = ix->rev_lines.load(std::memory_order_acquire) != nullptr;
+      const bool smp = ix->samples.load(std::memory_order_acquire) != nullptr;
+      *device_bytes = ix->n_lines * lb * (rev ? 2 : 1) + (smp ? ix->n_samples * 4 : 0) +
+                      ix->n_chunks * fmg::kChunkBytes;
     }
   });
 }
@@ -1519,12 +1596,13 @@ void fmg_index_destroy(fmg_index* ix) {
   cudaGetDevice(&prev);
   cudaSetDevice(ix->device);
   if (ix->lines) cudaFree(ix->lines);
+  if (ix->chunks) cudaFree(ix->chunks);
   if (ix->lut) cudaFree(ix->lut);
   if (ix->lut_r) cudaFree(ix->lut_r);
   if (ix->lut_x) cudaFree(ix->lut_x);
   if (ix->ep_table) cudaFree(ix->ep_table);
-  if (ix->rev_lines) cudaFree(ix->rev_lines);
-  if (ix->samples) cudaFree(ix->samples);
+  if (uint8_t* r = ix->rev_lines.load()) cudaFree(r);
+  if (uint32_t* sm = ix->samples.load()) cudaFree(sm);
   if (prev >= 0) cudaSetDevice(prev);
   delete ix;
 }
@@ -1876,7 +1954,8 @@ int fmg_locate_rows(const fmg_index* ix, const uint32_t* rows, uint64_t count, u
                     void* stream) {
   return fmg::guard([&] {
     check_index(ix);
-    FMG_REQUIRE(ix->samples != nullptr, "index has no suffix-array samples (fmg_index_set_samples)");
+    FMG_REQUIRE(ix->samples.load(std::memory_order_acquire) != nullptr,
+                "index has no suffix-array samples (fmg_index_set_samples)");
     if (count == 0) return;
     fmg::DeviceScope scope(ix->device);
     launch_locate(ix, rows, count, out_pos, as_stream(stream), status);
@@ -1887,7 +1966,8 @@ int fmg_locate_rows(const fmg_index* ix, const uint32_t* rows, uint64_t count, u
 int fmg_locate_rows_host(const fmg_index* ix, const uint32_t* rows, uint64_t count, uint32_t* out_pos) {
   return fmg::guard([&] {
     check_index(ix);
-    FMG_REQUIRE(ix->samples != nullptr, "index has no suffix-array samples (fmg_index_set_samples)");
+    FMG_REQUIRE(ix->samples.load(std::memory_order_acquire) != nullptr,
+                "index has no suffix-array samples (fmg_index_set_samples)");
     if (count == 0) return;
     fmg::DeviceScope scope(ix->device);
     const uint64_t chunk = std::min<uint64_t>(count, 1ull << 22);
@@ -1901,6 +1981,135 @@ int fmg_locate_rows_host(const fmg_index* ix, const uint32_t* rows, uint64_t cou
                     FMG_CK(cudaGetLastError());
                   });
     st.raise_if_set(s0, "row out of range");
+  });
+}
+
+int fmg_reconstruct_text(const fmg_index* ix, uint8_t* codes_out, uint32_t* status, void* stream) {
+  return fmg::guard([&] {
+    check_index(ix);
+    FMG_REQUIRE(codes_out != nullptr, "null output pointer");
+    FMG_REQUIRE(ix->samples.load(std::memory_order_acquire) != nullptr,
+                "index has no suffix-array samples (fmg_index_set_samples)");
+    fmg::DeviceScope scope(ix->device);
+    with_words(ix, [&](auto wt) {
+      constexpr int W = decltype(wt)::value;
+      const uint64_t ns = ix->n / 32 + 1;
+      const unsigned blocks = wave_blocks(ix, (const void*)fmg::k_reconstruct<W>, 256, ns);
+      fmg::k_reconstruct<W><<<blocks, 256, 0, as_stream(stream)>>>(ix->view(), ns, codes_out, status);
+    });
+    FMG_CK(cudaGetLastError());
+  });
+}
+
+int fmg_reconstruct_text_host(const fmg_index* ix, uint8_t* codes_out) {
+  return fmg::guard([&] {
+    check_index(ix);
+    FMG_REQUIRE(codes_out != nullptr, "null output pointer");
+    FMG_REQUIRE(ix->samples.load(std::memory_order_acquire) != nullptr,
+                "index has no suffix-array samples (fmg_index_set_samples)");
+    fmg::DeviceScope scope(ix->device);
+    cudaStream_t s = host_stream(ix->device, 0);
+    CallStatus st(nullptr, s);
+    DevBuf<uint8_t> text(ix->n, s);
+    with_words(ix, [&](auto wt) {
+      constexpr int W = decltype(wt)::value;
+      const uint64_t ns = ix->n / 32 + 1;
+      const unsigned blocks = wave_blocks(ix, (const void*)fmg::k_reconstruct<W>, 256, ns);
+      fmg::k_reconstruct<W><<<blocks, 256, 0, s>>>(ix->view(), ns, text.ptr, st.word);
+    });
+    FMG_CK(cudaGetLastError());
+    FMG_CK(cudaMemcpyAsync(codes_out, text.ptr, ix->n, cudaMemcpyDeviceToHost, s));
+    st.raise_if_set(s, "text reconstruction failed");
+  });
+}
+
+// ---- bucket-level rank kernels (kernels.py:125-292) ----
+
+static unsigned grid_for(uint64_t count, int threads) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t want = (count + threads - 1) / threads;
+  return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(sms) * 16)));
+}
+
+static void launch_bucket_count(const uint8_t* blocks, const uint32_t* prefix_lens, const uint8_t* symbols,
+                                uint64_t count, int method, uint32_t* out, uint32_t* status, cudaStream_t s) {
+  FMG_REQUIRE(method == 0 || method == 1, "bucket method must be 0 (popcount) or 1 (nibble)");
+  FMG_REQUIRE(reinterpret_cast<uintptr_t>(blocks) % 32 == 0, "bucket blocks must be 32-byte aligned");
+  if (method == 0)
+    fmg::k_bucket_count<0><<<grid_for(count, 256), 256, 0, s>>>(blocks, prefix_lens, symbols, count, out, status);
+  else
+    fmg::k_bucket_count<1><<<grid_for(count, 256), 256, 0, s>>>(blocks, prefix_lens, symbols, count, out, status);
+  FMG_CK(cudaGetLastError());
+}
+
+int fmg_bucket_count(const uint8_t* blocks, const uint32_t* prefix_lens, const uint8_t* symbols, uint64_t count,
+                     int method, uint32_t* out, uint32_t* status, void* stream) {
+  return fmg::guard([&] {
+    if (count == 0) return;
+    FMG_REQUIRE(blocks && prefix_lens && out, "null argument");
+    launch_bucket_count(blocks, prefix_lens, symbols, count, method, out, status, as_stream(stream));
+  });
+}
+
+int fmg_bucket_count_host(int device, const uint8_t* blocks, const uint32_t* prefix_lens, const uint8_t* symbols,
+                          uint64_t count, int method, uint32_t* out) {
+  return fmg::guard([&] {
+    if (count == 0) return;
+    FMG_REQUIRE(blocks && prefix_lens && out, "null argument");
+    fmg::DeviceScope scope(device);
+    cudaStream_t s = host_stream(device, 0);
+    CallStatus st(nullptr, s);
+    DevBuf<uint8_t> d_blocks(count * 32, s), d_sym(symbols ? count : 0, s);
+    DevBuf<uint32_t> d_pl(count, s), d_out(count * (symbols ? 1 : 4), s);
+    FMG_CK(cudaMemcpyAsync(d_blocks.ptr, blocks, count * 32, cudaMemcpyHostToDevice, s));
+    FMG_CK(cudaMemcpyAsync(d_pl.ptr, prefix_lens, count * 4, cudaMemcpyHostToDevice, s));
+    if (symbols) FMG_CK(cudaMemcpyAsync(d_sym.ptr, symbols, count, cudaMemcpyHostToDevice, s));
+    launch_bucket_count(d_blocks.ptr, d_pl.ptr, symbols ? d_sym.ptr : nullptr, count, method, d_out.ptr, st.word, s);
+    FMG_CK(cudaMemcpyAsync(out, d_out.ptr, count * 4 * (symbols ? 1 : 4), cudaMemcpyDeviceToHost, s));
+    st.raise_if_set(s, "prefix_len outside [0, 128] or symbol code outside [0, 4)");
+  });
+}
+
+int fmg_bucket_mask_host(int device, const uint8_t* blocks, const uint32_t* prefix_lens, uint64_t count,
+                         uint8_t* out) {
+  return fmg::guard([&] {
+    if (count == 0) return;
+    FMG_REQUIRE(blocks && prefix_lens && out, "null argument");
+    fmg::DeviceScope scope(device);
+    cudaStream_t s = host_stream(device, 0);
+    CallStatus st(nullptr, s);
+    DevBuf<uint8_t> d_blocks(count * 32, s), d_out(count * 32, s);
+    DevBuf<uint32_t> d_pl(count, s);
+    FMG_CK(cudaMemcpyAsync(d_blocks.ptr, blocks, count * 32, cudaMemcpyHostToDevice, s));
+    FMG_CK(cudaMemcpyAsync(d_pl.ptr, prefix_lens, count * 4, cudaMemcpyHostToDevice, s));
+    fmg::k_bucket_mask<<<grid_for(count, 256), 256, 0, s>>>(d_blocks.ptr, d_pl.ptr, count, d_out.ptr, st.word);
+    FMG_CK(cudaGetLastError());
+    FMG_CK(cudaMemcpyAsync(out, d_out.ptr, count * 32, cudaMemcpyDeviceToHost, s));
+    st.raise_if_set(s, "prefix_len outside [0, 128]");
+  });
+}
+
+int fmg_bucket_nibble_trace_host(int device, const uint8_t* blocks, const uint32_t* prefix_lens,
+                                 const uint8_t* symbols, uint64_t count, uint64_t* trace) {
+  return fmg::guard([&] {
+    if (count == 0) return;
+    FMG_REQUIRE(blocks && prefix_lens && symbols && trace, "null argument");
+    fmg::DeviceScope scope(device);
+    cudaStream_t s = host_stream(device, 0);
+    CallStatus st(nullptr, s);
+    DevBuf<uint8_t> d_blocks(count * 32, s), d_sym(count, s);
+    DevBuf<uint32_t> d_pl(count, s);
+    DevBuf<uint64_t> d_tr(count * 15, s);
+    FMG_CK(cudaMemcpyAsync(d_blocks.ptr, blocks, count * 32, cudaMemcpyHostToDevice, s));
+    FMG_CK(cudaMemcpyAsync(d_pl.ptr, prefix_lens, count * 4, cudaMemcpyHostToDevice, s));
+    FMG_CK(cudaMemcpyAsync(d_sym.ptr, symbols, count, cudaMemcpyHostToDevice, s));
+    fmg::k_bucket_nibble_trace<<<unsigned((count + 127) / 128), 128, 0, s>>>(d_blocks.ptr, d_pl.ptr, d_sym.ptr,
+                                                                             count, d_tr.ptr, st.word);
+    FMG_CK(cudaGetLastError());
+    FMG_CK(cudaMemcpyAsync(trace, d_tr.ptr, count * 15 * 8, cudaMemcpyDeviceToHost, s));
+    st.raise_if_set(s, "prefix_len outside [0, 128] or symbol code outside [0, 4)");
   });
 }
 

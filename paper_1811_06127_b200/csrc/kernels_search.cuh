@@ -203,6 +203,34 @@ __device__ __forceinline__ uint32_t psi_step(const IndexView& ix, uint32_t row, 
   return c_of(ix, sym) + occ1_from_line<W>(ix, b, w, row, r, sym);
 }
 
+// reconstruct_reference (search.py:270-286) in parallel.  The predecessor
+// cycle from row 0 (suffix n) to the sentinel row (suffix 0) visits every row
+// once; the sampled rows (row % 32 == 0, index.py:93) cut it into segments of
+// ~32 steps.  Segment j starts at row 32j, whose text position samples[j] is
+// known, and writes text[pos - 1], text[pos - 2], ... until it reaches the
+// next sampled row or the sentinel row, so every text position is written
+// exactly once.  Bit 2 of err: the walk left [0, n] (corrupt index).
+template <int W>
+__global__ void __launch_bounds__(256) k_reconstruct(IndexView ix, uint64_t n_samples, uint8_t* __restrict__ text,
+                                                     uint32_t* __restrict__ err) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n_samples; j += stride) {
+    uint32_t row = uint32_t(j) << 5, pos = ix.samples[j];
+    for (uint32_t steps = 0; row != ix.sentinel_row; ++steps) {
+      if (pos == 0u || pos > ix.n || steps > 64u * 1024u * 1024u) {
+        if (err) atomicOr(err, 2u);
+        break;
+      }
+      uint32_t sym;
+      const uint32_t prev = psi_step<W>(ix, row, sym);
+      text[pos - 1u] = uint8_t(sym);
+      --pos;
+      row = prev;
+      if ((row & 31u) == 0u) break;
+    }
+  }
+}
+
 template <int W>
 __global__ void k_psi(IndexView ix, const uint32_t* __restrict__ rows, uint64_t count, uint8_t* __restrict__ out_sym,
                       uint32_t* __restrict__ out_row, uint32_t* __restrict__ err) {

@@ -3,6 +3,7 @@
 from __future__ import annotations
 
 import ctypes as ct
+import threading
 
 import numpy as np
 
@@ -54,19 +55,26 @@ class DeviceIndex:
         self._has_samples = False
         self._has_reverse = False
         self._index = index
+        # one-time attachments: check-then-act under a lock (the C side is
+        # also idempotent and never frees an attached buffer before destroy)
+        self._attach = threading.RLock()  # ensure_reverse may need ensure_samples (text recovery)
 
     def ensure_reverse(self) -> None:
         """Attach the reversed-text index (bidirectional z = 1 engine)."""
-        if not self._has_reverse:
-            rec, sentinel = self._index.reverse_index(device=self.device)
-            _lib.check(_lib.load().fmg_index_set_reverse(self.handle, rec.ctypes.data, rec.shape[0], sentinel))
-            self._has_reverse = True
+        with self._attach:
+            if not self._has_reverse:
+                rec, sentinel = self._index.reverse_index(device=self.device)
+                _lib.check(_lib.load().fmg_index_set_reverse(self.handle, rec.ctypes.data, rec.shape[0], sentinel))
+                self._has_reverse = True
 
     def ensure_samples(self) -> None:
-        if not self._has_samples:
-            s = self._index.sa_samples
-            _lib.check(_lib.load().fmg_index_set_samples(self.handle, s.ctypes.data, s.size))
-            self._has_samples = True
+        if self._has_samples:
+            return
+        with self._attach:
+            if not self._has_samples:
+                s = self._index.sa_samples
+                _lib.check(_lib.load().fmg_index_set_samples(self.handle, s.ctypes.data, s.size))
+                self._has_samples = True
 
     @property
     def device_bytes(self) -> int:

@@ -363,24 +363,26 @@ def collect_hits(index: FmIndex, matches: Iterable[MatchResult], pattern_len: in
     return hits, truncated
 
 
-def reconstruct_reference(index: FmIndex, kernel: Kernel | str | None = None) -> str:
-    """Rebuild the reference text (search.py:270-286).
+def reconstruct_codes(index: FmIndex, device: int | None = None) -> np.ndarray:
+    """The n text codes the index was built from, recovered on the GPU.
 
-    The reference walks n predecessor steps from row 0; here every row is
-    located in parallel instead: text[SA[i] - 1] = BWT[i] for SA[i] > 0.
+    Parallel form of reconstruct_reference (search.py:270-286): every sampled
+    row starts a predecessor walk of ~32 steps (k_reconstruct), together
+    covering the whole cycle from row 0 to the sentinel row.
     """
+    require_gpu()
+    dev = index.device_index(device)
+    dev.ensure_samples()
+    out = np.empty(index.n, dtype=np.uint8)
+    _lib.check(_lib.load().fmg_reconstruct_text_host(dev.handle, out.ctypes.data))
+    return out
+
+
+def reconstruct_reference(index: FmIndex, kernel: Kernel | str | None = None) -> str:
+    """Rebuild the reference text (search.py:270-286) on the GPU (reconstruct_codes)."""
     resolve_kernel(kernel)
-    n = index.n
-    rows = np.arange(n + 1, dtype=np.int64)
-    pos = locate_rows(index, rows)
-    sym, _ = psi_inverse_batch(index, rows)
-    if np.unique(pos).size != n + 1 or pos.max() != n:
-        raise RuntimeError("hit the sentinel row early; index is corrupt")
-    text = np.zeros(n, dtype=np.uint8)
-    live = pos > 0
-    text[pos[live] - 1] = sym[live]
     lut = np.frombuffer(SYMBOLS.encode(), dtype=np.uint8)
-    return lut[text].tobytes().decode("ascii")
+    return lut[reconstruct_codes(index)].tobytes().decode("ascii")
 
 
 def collect_hits_batch(index: FmIndex, pid: np.ndarray, k: np.ndarray, l: np.ndarray, diffs: np.ndarray,

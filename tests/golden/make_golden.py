@@ -283,7 +283,127 @@ def gen_scale():
     print("scale: wrote", {k: len(v) for k, v in out.items()}, flush=True)
 
 
+def gen_buckets():
+    """Reference bucket kernels (kernels.py:125-358) on seeded random buckets:
+    every count_bucket_* / all4 / mask_bucket answer and the nibble trace."""
+    from fmpm import kernels as K
+
+    rng = np.random.Generator(np.random.PCG64(4242))
+    n = 3000
+    blocks = rng.integers(0, 256, (n, 32), dtype=np.uint8)
+    blocks[:64] = 0                      # all-A buckets
+    blocks[64:128] = 0xFF                # all-T buckets
+    prefix = rng.integers(0, 129, n)
+    prefix[:129] = np.arange(129)        # every prefix length
+    symbol = rng.integers(0, 4, n)
+    counts = np.zeros((n, 4), dtype=np.int64)
+    all4 = np.zeros((n, 4), dtype=np.int64)
+    masked = np.zeros((n, 32), dtype=np.uint8)
+    trace = np.zeros((n, 15), dtype=np.uint64)
+    for i in range(n):
+        b, pl, sy = blocks[i].tobytes(), int(prefix[i]), int(symbol[i])
+        counts[i] = [K.count_bucket_scalar(b, pl, sy), K.count_bucket_bytelut(b, pl, sy),
+                     K.count_bucket_nibble(b, pl, sy), K.count_bucket_simd(b, pl, sy)]
+        all4[i] = K.count_bucket_all4(b, pl)
+        masked[i] = np.frombuffer(K.mask_bucket(b, pl), dtype=np.uint8)
+        tr = K.KernelTrace()
+        K.count_bucket_nibble(b, pl, sy, trace=tr)
+        trace[i, 0:4] = tr.masked_words
+        trace[i, 4:8] = tr.lookup_lo_words
+        trace[i, 8:12] = tr.lookup_hi_words
+        trace[i, 12] = sum(int(v) << (16 * g) for g, v in enumerate(tr.group_sads))
+        trace[i, 13] = tr.sad_total | (tr.raw_count << 32)
+        trace[i, 14] = tr.count
+    np.savez_compressed(HERE / "buckets.npz", blocks=blocks, prefix=prefix, symbol=symbol, counts=counts,
+                        all4=all4, masked=masked, trace=trace, tables_lo=np.frombuffer(K.TABLES.lo, np.uint8),
+                        tables_hi=np.frombuffer(K.TABLES.hi, np.uint8))
+    print("buckets: wrote", n, "cases")
+
+
+class _LazySamples:
+    def __init__(self, samples):
+        self.s = samples
+
+    def __len__(self):
+        return self.s.size
+
+    def __getitem__(self, j):
+        return int(self.s[j])
+
+
+def _ref_index_full(ours):
+    """As _ref_index, with every SA sample (locate / hits)."""
+    return fmpm.FmIndex(n=ours.n, c=tuple(ours.c), buckets=_LazyBuckets(ours.bucket_records),
+                        sentinel_row=ours.sentinel_row, sa_samples=_LazySamples(ours.sa_samples),
+                        records=tuple(fmpm.RecordSpan(r.name, r.start, r.length) for r in ours.records))
+
+
+C3_READS = 8192  # config3(n_reads=C3_READS): 114,688 seeds; the tests regenerate the same call
+HIT_ROWS_CAP = 2000  # hit lists are recorded for seeds whose intervals hold at most this many rows
+
+
+def _hits_of(ref, matches, m):
+    rows = sum(max(0, x.interval.l - x.interval.k + 1) for x in matches)
+    if rows > HIT_ROWS_CAP:
+        return None
+    h, _ = fmpm.collect_hits(ref, matches, m)
+    return [(int(x.global_pos), int(x.diffs)) for x in h]
+
+
+def gen_scale3():
+    """Config 3 (3.1 Gbp, rows > 2^31): the reference's exact and z = 1 results
+    and hit lists on the first 2,048 seeds, through the lazy-bucket view."""
+    from paper_1811_06127_b200 import build_index
+
+    t0 = time.time()
+    wl = workloads.config3(n_reads=C3_READS)
+    print(f"config3 text {time.time() - t0:.0f}s", flush=True)
+    idx = build_index(wl.text, builder="host")
+    print(f"3.1 Gbp host build {time.time() - t0:.0f}s", flush=True)
+    ref = _ref_index_full(idx)
+    seeds = workloads.unpack_patterns(wl.packed[:2048], wl.meta["m"])
+    ex, z1, hx, h1 = [], [], [], []
+    for p in seeds:
+        t = text_of(p)
+        iv = fmpm.exact_search(ref, t)
+        ex.append((iv.k, iv.l))
+        hx.append(_hits_of(ref, [] if iv.is_empty else [fmpm.MatchResult(iv, 0)], len(t)))
+        res = fmpm.inexact_search(ref, t, 1)
+        z1.append([(m.interval.k, m.interval.l, m.diffs_used) for m in res])
+        h1.append(_hits_of(ref, res, len(t)))
+    out = {"n": int(idx.n), "text_sha256_head": sha(wl.text[:1 << 20]), "packed_sha256": sha(wl.packed[:2048]),
+           "exact": ex, "z1": z1, "exact_hits": hx, "z1_hits": h1, "hit_rows_cap": HIT_ROWS_CAP,
+           "fmi_meta": {"c": [int(x) for x in idx.c], "sentinel_row": int(idx.sentinel_row)}}
+    (HERE / "scale3_cases.json").write_text(json.dumps(out, separators=(",", ":")))
+    print(f"scale3: wrote {len(ex)} seeds in {time.time() - t0:.0f}s", flush=True)
+
+
+def gen_hits():
+    """Reference hit lists (collect_hits, search.py:245-267) on subsamples of
+    configs 0 (exact), 2 (z = 1) and 4 (exact)."""
+    from paper_1811_06127_b200 import build_index
+
+    out = {}
+    wl0 = workloads.config0()
+    ref = _ref_index_full(build_index(wl0.text, builder="host"))
+    out["config0_first1k_exact_hits"] = [
+        _hits_of(ref, [fmpm.MatchResult(iv, 0)] if not iv.is_empty else [], len(p))
+        for iv, p in ((fmpm.exact_search(ref, text_of(p)), p) for p in wl0.patterns[:1000])]
+    wl2 = workloads.config2()
+    ref = _ref_index_full(build_index(wl2.text, builder="host"))
+    out["config2_first500_z1_hits"] = [_hits_of(ref, fmpm.inexact_search(ref, text_of(p), 1), len(p))
+                                       for p in wl2.patterns[:500]]
+    wl4 = workloads.config4(count=1 << 11)
+    ref = _ref_index_full(build_index(wl4.text, builder="host"))
+    seeds = workloads.unpack_patterns(wl4.packed, 20)
+    out["config4_first2k_exact_hits"] = [
+        _hits_of(ref, [fmpm.MatchResult(iv, 0)] if not iv.is_empty else [], 20)
+        for iv in (fmpm.exact_search(ref, text_of(p)) for p in seeds)]
+    (HERE / "hits_cases.json").write_text(json.dumps(out, separators=(",", ":")))
+    print("hits: wrote", {k: len(v) for k, v in out.items()}, flush=True)
+
+
 if __name__ == "__main__":
     for what in sys.argv[1:]:
         {"small": gen_small, "config0": gen_config0, "config1": gen_config1, "cli": gen_cli,
-         "scale": gen_scale}[what]()
+         "scale": gen_scale, "buckets": gen_buckets, "scale3": gen_scale3, "hits": gen_hits}[what]()
