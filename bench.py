@@ -119,6 +119,33 @@ def occ_step_bytes(pairs: np.ndarray) -> tuple[int, int]:
     return lines * 32 + low.size * 40, lines
 
 
+CHUNK_CHARS = 416  # csrc/kernels_chunk.cuh
+
+
+def chunk_sector_of(r: np.ndarray) -> np.ndarray:
+    return np.where(r < 80, 0, 1 + (r - 80) // 112)
+
+
+def chunk_step_bytes(pairs: np.ndarray) -> tuple[int, int, int]:
+    """Algorithmic bytes of Occ steps on the 128-byte chunk layout (kernels_chunk.cuh).
+
+    Per step: 32 B x |S(k-1) U S(l)| with S(p) = {sector 0 of p's chunk, the
+    sector holding p} + 8 B (k, l) in + 32 B out.  Returns (total bytes,
+    total distinct sectors, total distinct 128-byte chunks)."""
+    low, high = pairs[:, 0], pairs[:, 1]
+    jh, jl = high // CHUNK_CHARS, np.maximum(low, 0) // CHUNK_CHARS
+    sh = chunk_sector_of(high - jh * CHUNK_CHARS)
+    sl = chunk_sector_of(np.maximum(low, 0) - jl * CHUNK_CHARS)
+    has_low = low >= 0
+    other = has_low & (jl != jh)
+    sect = 1 + (sh != 0)                                       # high end: base + its sector
+    sect = sect + np.where(other, 1 + (sl != 0), 0)            # low end in another chunk
+    sect = sect + (has_low & ~other & (sl != 0) & (sl != sh))  # low end in another sector of the same chunk
+    sectors = int(sect.sum())
+    chunks = int(low.size + other.sum())
+    return sectors * 32 + low.size * 40, sectors, chunks
+
+
 def cpu_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -189,6 +216,117 @@ def make_workload(config: str, rank: int):
         return w.config3(n_reads=int(os.environ.get("FMG_C3_READS", 10_000_000)),
                          n=int(os.environ.get("FMG_C3_BASES", 3_100_000_000)))
     raise SystemExit(f"unknown config {config}")
+
+
+# ---------------------------------------------------------------------------
+# multi-rank plumbing: one shared workload, self-launch, result digests
+# ---------------------------------------------------------------------------
+
+SHM = Path(os.environ.get("FMG_SHM_DIR", "/dev/shm"))
+
+
+def shared_workload(config: str, rank: int, world: int, barrier):
+    """The workload of `config`, generated ONCE per node: rank 0 writes its
+    arrays under /dev/shm, the other ranks memory-map them after the barrier
+    (config 3 is a 3.1 Gbp text plus 140M packed seeds: generating it on
+    every rank would cost N x the host memory and CPU).  Config 1 draws an
+    independent pair set per rank (weak scaling) and is generated locally."""
+    from paper_1811_06127_b200.workloads import Workload
+
+    if world == 1 or config == "config1":
+        return make_workload(config, rank)
+    key = f"{config}_{os.environ.get('FMG_C3_READS', '')}_{os.environ.get('FMG_C3_BASES', '')}"
+    d = SHM / f"fmg_wl_{key}_{os.environ.get('MASTER_PORT', '0')}"
+    fields = ("text", "patterns", "packed", "pairs")
+    if rank == 0:
+        wl = make_workload(config, 0)
+        d.mkdir(parents=True, exist_ok=True)
+        for f in fields:
+            a = getattr(wl, f)
+            if a is not None:
+                np.save(d / f"{f}.npy", a)
+        (d / "meta.json").write_text(json.dumps({"name": wl.name, "max_diff": wl.max_diff, "meta": wl.meta}))
+    barrier()
+    if rank != 0:
+        m = json.loads((d / "meta.json").read_text())
+        # the text is only read (by the index build): memory-mapped; query arrays are copied in
+        arrs = {f: (np.load(d / f"{f}.npy", mmap_mode="r" if f == "text" else None)
+                    if (d / f"{f}.npy").exists() else None) for f in fields}
+        wl = Workload(m["name"], arrs["text"], patterns=arrs["patterns"], packed=arrs["packed"],
+                      pairs=arrs["pairs"], max_diff=m["max_diff"], meta=m["meta"])
+    barrier()  # every rank has mapped the arrays: the files can go (the mappings stay valid)
+    if rank == 0:
+        for f in d.glob("*"):
+            f.unlink()
+        d.rmdir()
+    return wl
+
+
+def self_launch(args) -> None:
+    """`bench.py --gpus N` without a torchrun environment: re-exec under
+    torch.distributed.run with N ranks on this node (127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
+def sha_update(h, *arrays) -> None:
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+
+
+def digest_pairs(fm, idx, pairs) -> str:
+    import hashlib
+
+    h = hashlib.sha256()
+    for c0 in range(0, pairs.shape[0], 1 << 22):
+        sha_update(h, fm.occ_pair_batch(idx, pairs[c0:c0 + (1 << 22), 0], pairs[c0:c0 + (1 << 22), 1]))
+    return h.hexdigest()
+
+
+def digest_patterns(lib, dix, wl, lo: int, hi: int) -> str:
+    """SHA-256 over exact intervals (and z = 1 result counts / k / l / diffs for
+    inexact workloads) of patterns [lo, hi), in chunks of 2^22 patterns."""
+    import hashlib
+
+    from paper_1811_06127_b200 import _lib
+
+    h = hashlib.sha256()
+    m = wl.meta["m"] if wl.packed is not None else wl.patterns.shape[1]
+    step = 1 << 22
+    for c0 in range(lo, hi, step):
+        c1 = min(hi, c0 + step)
+        if wl.packed is not None:
+            packed = np.ascontiguousarray(wl.packed[c0:c1])
+        else:
+            from paper_1811_06127_b200 import pack_patterns_u64
+
+            packed = pack_patterns_u64(np.ascontiguousarray(wl.patterns[c0:c1]))
+        if wl.max_diff == 0 or wl.name == "config3":
+            kl = np.empty((c1 - c0, 2), dtype=np.uint32)
+            _lib.check(lib.fmg_exact_packed_host(dix.handle, packed.ctypes.data, m, c1 - c0, kl.ctypes.data))
+            sha_update(h, kl)
+        if wl.max_diff:
+            hd = ct.c_void_p()
+            _lib.check(lib.fmg_inexact_packed_host(dix.handle, packed.ctypes.data, m, c1 - c0, wl.max_diff,
+                                                   ct.byref(hd)))
+            try:
+                tot = ct.c_uint64()
+                lib.fmg_matches_size(hd, ct.byref(tot), None)
+                row = np.empty(c1 - c0 + 1, dtype=np.uint64)
+                k = np.empty(tot.value, dtype=np.uint32)
+                l_ = np.empty(tot.value, dtype=np.uint32)
+                d = np.empty(tot.value, dtype=np.uint8)
+                _lib.check(lib.fmg_matches_copy(hd, row.ctypes.data, k.ctypes.data, l_.ctypes.data, d.ctypes.data, 1))
+            finally:
+                lib.fmg_matches_free(hd)
+            sha_update(h, np.diff(row.astype(np.int64)), k, l_, d)
+    return h.hexdigest()
 
 
 def unit_count(wl) -> int:
@@ -372,6 +510,73 @@ def fetch_chunks(pairs: np.ndarray, chars_per_chunk: int = 256) -> int:
     return int(low.size + two.sum())
 
 
+def occ_layout(lib, dix) -> str:
+    """Layout the Occ-step kernel reads for this index: 'lines' (32-byte lines,
+    one sector per position) or 'chunks' (128-byte chunks, HBM-resident)."""
+    fn = lib.fmgx_occ_layout
+    fn.argtypes = [ct.c_void_p, ct.POINTER(ct.c_int)]
+    c = ct.c_int()
+    from paper_1811_06127_b200 import _lib
+
+    _lib.check(fn(dix.handle, ct.byref(c)))
+    return "chunks" if c.value else "lines"
+
+
+def occ_roofline(lib, dix, pairs: np.ndarray, launch_s: float, device: int, config: str) -> dict:
+    """Roofline of one Occ-step launch over `pairs`, for the layout
+    the kernel actually reads.  L2-resident index (config 1): the bound is the
+    random L2 read rate, measured live on a buffer of the index's size; the
+    HBM figure rides along (its frac exceeds 1: index bytes come from L2).
+    HBM-resident (config 1-H): HBM bytes at 32-byte sector granularity, plus
+    the DRAM random-fetch rate (128-byte fetches) measured live."""
+    units = pairs.shape[0]
+    layout = occ_layout(lib, dix)
+    peak, kind = hbm_peak()
+    line_bytes, lines = occ_step_bytes(pairs)
+    if layout == "chunks":
+        alg, sectors, chunks = chunk_step_bytes(pairs)
+        kernel = "k_occ_pair_chunk"
+    else:
+        alg, sectors, chunks = line_bytes, lines, fetch_chunks(pairs)
+        kernel = "k_occ_pair"
+    achieved = alg / launch_s / 1e9
+    hbm = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+           "frac": round(achieved / peak, 4), "traffic": measured_traffic(kernel, config), "peak_kind": kind,
+           "kernel": kernel, "layout": layout, "alg_bytes_per_launch": alg,
+           "alg_bytes_per_step": round(alg / units, 2), "sectors_per_step": round(sectors / units, 4),
+           "random_sector_roofline_steps_per_s": round(peak * 1e9 / (alg / units), 1),
+           "line_layout_bytes_per_step": round(line_bytes / units, 2),
+           "frac_line_layout_bytes": round(line_bytes / launch_s / 1e9 / peak, 4),
+           "note": "algorithmic bytes = 32 B x the distinct sectors the layout must read per step "
+                   "(|S(k-1) U S(l)|, exact replay of the pair list) + 8 B in + 32 B out; "
+                   "frac_line_layout_bytes: the same time against the 32-byte-line layout's bytes "
+                   "(one sector per position, the fewest any layout with in-sector checkpoints reads)"}
+    if dix.device_bytes <= (64 << 20) and layout == "lines":
+        fn = lib.fmgx_random_fetch_rate
+        fn.argtypes = [ct.c_int, ct.c_uint64, ct.c_uint64, ct.POINTER(ct.c_double)]
+        rate = ct.c_double()
+        if fn(device, max(int(dix.device_bytes), 1 << 20), 1 << 25, ct.byref(rate)) == 0 and rate.value > 0:
+            ach = lines / launch_s
+            return {"bound": "l2", "achieved": round(ach / 1e9, 2), "peak": round(rate.value / 1e9, 2),
+                    "unit": "G random 32-B L2 line reads/s", "frac": round(ach / rate.value, 4),
+                    "traffic": measured_traffic(kernel, config), "kernel": kernel, "layout": layout,
+                    "peak_kind": "measured live (random 32-B reads over an L2-resident buffer of the index's size)",
+                    "lines_per_step": round(lines / units, 4),
+                    "note": "the 8.4 MB index is L2-resident, so the Occ step is bound by the SM->L2 random "
+                            "request rate, not HBM; the kernel also streams its pairs in and counts out",
+                    "hbm": hbm}
+        return hbm
+    fetch_peak = random_fetch_peak(lib, device)
+    if fetch_peak:
+        hbm["request_roofline"] = {
+            "bound": "dram_random_requests", "achieved": round(chunks / launch_s / 1e9, 2),
+            "peak": round(fetch_peak / 1e9, 2), "unit": "G random 128-B fetches/s",
+            "frac": round(chunks / launch_s / fetch_peak, 4), "chunks_per_step": round(chunks / units, 4),
+            "note": "distinct 128-byte chunks per step (exact replay); peak measured live: random 32-B reads "
+                    "over 4 GiB, each fetching 128 B from DRAM; L2 hits let frac exceed 1"}
+    return hbm
+
+
 def hbm_resident_extra(dev, lib, reps: int = 10) -> dict:
     """Config 1-H on the same GPU: the config-1 pair distribution over the 1 Gbp
     config-4 text, whose 500 MB line array cannot live in the 126 MB L2."""
@@ -401,29 +606,12 @@ def hbm_resident_extra(dev, lib, reps: int = 10) -> dict:
     e1.record(stream)
     torch.cuda.synchronize(dev)
     launch_s = e0.elapsed_time(e1) / reps / 1e3
-    alg, lines = occ_step_bytes(wl.pairs)
-    peak, kind = hbm_peak()
-    achieved = alg / launch_s / 1e9
+    roof = occ_roofline(lib, dix, wl.pairs, launch_s, dev.index, "config1h")
     idx.release_device()
-    chunks = fetch_chunks(wl.pairs)
-    fetch_peak = random_fetch_peak(lib, dev.index)
-    request = None
-    if fetch_peak:
-        request = {"bound": "dram_random_requests", "achieved": round(chunks / launch_s / 1e9, 2),
-                   "peak": round(fetch_peak / 1e9, 2), "unit": "G random 128-B fetches/s",
-                   "frac": round(chunks / launch_s / fetch_peak, 4),
-                   "chunks_per_step": round(chunks / units, 4),
-                   "note": "peak measured live: random 32-B reads over 4 GiB (each fetches 128 B from DRAM); "
-                           "L2 hits let frac exceed 1"}
     return {"workload": "config 1-H: 2^24 config-1 pairs over the 1 Gbp config-4 text (seed 5), "
-                        "500 MB line array, HBM-resident",
+                        "HBM-resident index (lines 500 MB + chunks 308 MB)",
             "value": units / launch_s, "unit": "occ_steps/s", "index_build_s_gpu": round(build_s, 2),
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": measured_traffic("k_occ_pair", "config1h"),
-                         "peak_kind": kind, "alg_bytes_per_step": round(alg / units, 2),
-                         "sectors_per_step": round(lines / units, 4),
-                         "random_sector_roofline_steps_per_s": round(peak * 1e9 / (alg / units), 1)},
-            "request_roofline": request}
+            "roofline": roof}
 
 
 def run_ours(args, rank: int, local: int, world: int) -> None:
@@ -433,14 +621,32 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
     from paper_1811_06127_b200 import _lib
     from paper_1811_06127_b200.dist import max_over_ranks
 
+    # one rank per GPU; more ranks than GPUs (a parity run of the N-rank path on
+    # a smaller box) share devices round-robin and talk over gloo, since NCCL
+    # refuses two ranks on one device — no rank ever waits on another's kernels
+    n_dev = torch.cuda.device_count()
+    oversubscribed = world > n_dev
+    local = local % n_dev
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
+    gloo = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if oversubscribed:
+            dist.init_process_group("gloo")
+            gloo = None
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+            gloo = dist.new_group(backend="gloo")  # host-side digest gather (off the timed path)
     lib = _lib.load()
-    wl = make_workload(args.config, rank)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    wl = shared_workload(args.config, rank, world, barrier)
+    full_wl = wl
     # Configs 3 and 4 define one fixed query set "sharded over 1, 2, 4 and 8
     # GPUs" (strong scaling): rank r keeps its contiguous shard.  The others
     # are weak-scaled (config 1: an independent pair set per rank).
@@ -448,14 +654,18 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
     if strong:
         from paper_1811_06127_b200.dist import shard_range
 
+        import copy
+
+        wl = copy.copy(full_wl)
+        wl.meta = dict(full_wl.meta)
         if wl.name == "config3":
             per = wl.meta["seeds_per_read"]
             lo, hi = shard_range(wl.meta["reads"], rank, world)
-            wl.packed = wl.packed[lo * per:hi * per]
+            wl.packed = np.array(full_wl.packed[lo * per:hi * per])
             wl.meta["reads"] = hi - lo
         else:
-            lo, hi = shard_range(wl.packed.size, rank, world)
-            wl.packed = wl.packed[lo:hi]
+            lo, hi = shard_range(full_wl.packed.size, rank, world)
+            wl.packed = np.array(full_wl.packed[lo:hi])
     t_build = time.perf_counter()
     idx = fm.build_index(wl.text)
     t_build = time.perf_counter() - t_build
@@ -576,7 +786,6 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
                 _lib.check(rc)
 
         launches_per_step = 1
-        alg_bytes, alg_lines = occ_step_bytes(wl.pairs)
         kernel_name = "k_occ_pair"
         h2d_per, d2h_per = units * 8, units * 32
         pin_in = torch.from_numpy(kl_h.view(np.int32)).pin_memory()
@@ -677,7 +886,7 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
 
     # ---- per-launch kernel time for the roofline (same stream, CUDA events) ----
     roofline = None
-    if alg_bytes is not None:
+    if wl.pairs is not None:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = max(3, min(args.steps, 20))
         e0.record(stream)
@@ -686,30 +895,8 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
         e1.record(stream)
         torch.cuda.synchronize(dev)
         launch_s = e0.elapsed_time(e1) / reps / 1e3
-        peak, peak_kind = hbm_peak()
-        achieved = alg_bytes / launch_s / 1e9
-        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(achieved / peak, 4), "traffic": measured_traffic(kernel_name, args.config),
-                    "peak_kind": peak_kind, "kernel": kernel_name,
-                    "alg_bytes_per_launch": alg_bytes,
-                    "alg_bytes_per_step": round(alg_bytes / units, 2),
-                    "sectors_per_step": round(alg_lines / units, 4),
-                    "random_sector_roofline_steps_per_s": round(peak * 1e9 / (alg_bytes / units), 1)}
-        if wl.pairs is not None and dix.device_bytes <= (64 << 20):
-            # L2-resident index: the bound is the SM->L2 random request rate, measured live on a
-            # buffer of the index's size (random 32-byte reads, all L2 hits)
-            fn = lib.fmgx_random_fetch_rate
-            fn.argtypes = [ct.c_int, ct.c_uint64, ct.c_uint64, ct.POINTER(ct.c_double)]
-            rate = ct.c_double()
-            if fn(local, max(int(dix.device_bytes), 1 << 20), 1 << 25, ct.byref(rate)) == 0 and rate.value > 0:
-                ach = alg_lines / launch_s
-                roofline["l2_request_roofline"] = {
-                    "bound": "l2_random_requests", "achieved": round(ach / 1e9, 2),
-                    "peak": round(rate.value / 1e9, 2), "unit": "G random 32-B line reads/s",
-                    "frac": round(ach / rate.value, 4),
-                    "note": "index lines fetched per launch / launch time, against random 32-byte reads over an "
-                            "L2-resident buffer of the index's size measured in the same run; the kernel also "
-                            "streams its pairs in and counts out"}
+        roofline = occ_roofline(lib, dix, wl.pairs, launch_s, local, args.config)
+        kernel_name = roofline["kernel"]
 
     # ---- search configs: device-counted work (one extra, untimed step) ----
     work = None
@@ -800,6 +987,36 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
     if args.config == "config1" and rank == 0 and world == 1 and not args.no_hbm_extra:
         extra["hbm_resident"] = hbm_resident_extra(dev, lib)
 
+    # ---- N > 1: every rank's results, as digests, against rank 0 recomputing
+    # that rank's queries on its own GPU (off the timed path) ----
+    parity = None
+    if world > 1 and not args.no_parity:
+        import torch.distributed as dist
+
+        def shard_digest(r: int) -> str:
+            if wl.pairs is not None:
+                pr = wl.pairs if r == rank else make_workload("config1", r).pairs
+                return digest_pairs(fm, idx, pr)
+            if strong:
+                per = full_wl.meta.get("seeds_per_read", 1)
+                total_q = full_wl.meta["reads"] if full_wl.name == "config3" else full_wl.packed.size
+                lo_, hi_ = shard_range(total_q, r, world)
+                return digest_patterns(lib, dix, full_wl, lo_ * per, hi_ * per)
+            return digest_patterns(lib, dix, wl, 0, unit_count(wl))  # weak: every rank runs the same set
+
+        mine = shard_digest(rank)
+        got = [None] * world
+        dist.all_gather_object(got, mine, group=gloo)
+        if rank == 0:
+            want = [mine] + [shard_digest(r) for r in range(1, world)]
+            parity = {"ok": got == want, "ranks": world,
+                      "method": "SHA-256 of each rank's full results (intervals / CSR counts, k, l, diffs / "
+                                "Occ counts) gathered to rank 0 and compared with rank 0 recomputing that "
+                                "rank's queries with the same engine"}
+            if not parity["ok"]:
+                print(json.dumps({"error": "multi-rank parity check failed", "got": got, "want": want}),
+                      file=sys.stderr, flush=True)
+
     # ---- launch count: our kernels inside the timed region ----
     if launches_per_step is None:
         launches_per_step = 4  # k_inexact pass + widen + scan + gather (first pass only)
@@ -811,6 +1028,9 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
             "config": config_of(args.config, world, units),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
             "gpu_launches": launches_per_step * args.steps, **extra,
+            **({"parity": parity} if parity is not None else {}),
+            **({"oversubscribed": f"{world} ranks on {n_dev} GPU(s): a parity run, not a scaling number"}
+               if oversubscribed else {}),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -828,9 +1048,12 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-hbm-extra", action="store_true", help="skip the config 1-H side measurement")
+    ap.add_argument("--no-parity", action="store_true", help="N > 1: skip the gathered-digest parity check")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)  # does not return
     rank, local, world = (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
                           int(os.environ.get("WORLD_SIZE", 1)))
     if args.impl == "reference":

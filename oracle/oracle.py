@@ -196,3 +196,38 @@ def psi(ox: OracleIndex, i: int):
     if r == -2:
         raise ValueError(f"row {i} outside [0, {ox.n}]")
     return None if r == -1 else (sym.value, int(r))
+
+
+def collect_hits(ox: OracleIndex, pid, k, l, diffs, pattern_len, record_starts=(0,), record_lens=None,
+                 threads: int | None = None):
+    """collect_hits over many patterns (search.py:211-267, locate_all + collect_hits):
+    every row of every non-empty interval located with the oracle's locate_row;
+    hits at positions >= n dropped; a hit is kept only if offset + max(m - d, 0)
+    fits its record; the fewest diffs per (pattern, position); sorted by
+    (pattern, position).  Returns (pid, pos, diffs) int64 arrays."""
+    pid = np.asarray(pid, dtype=np.int64)
+    k = np.asarray(k, dtype=np.int64)
+    l = np.asarray(l, dtype=np.int64)
+    diffs = np.asarray(diffs, dtype=np.int64)
+    live = l >= k
+    pid, k, l, diffs = pid[live], k[live], l[live], diffs[live]
+    width = l - k + 1
+    owner = np.repeat(np.arange(width.size), width)
+    first = np.zeros(width.size, dtype=np.int64)
+    np.cumsum(width[:-1], out=first[1:])
+    rows = k[owner] + (np.arange(int(width.sum()), dtype=np.int64) - first[owner])
+    pos = locate_batch(ox, rows, threads)
+    hp, hd = pid[owner], diffs[owner]
+    keep = pos < ox.n
+    pos, hp, hd = pos[keep], hp[keep], hd[keep]
+    starts = np.asarray(record_starts, dtype=np.int64)
+    lens = np.asarray(record_lens if record_lens is not None else [ox.n], dtype=np.int64)
+    which = np.searchsorted(starts, pos, side="right") - 1
+    plen = np.asarray(pattern_len, dtype=np.int64)[hp]
+    ok = pos - starts[which] + np.maximum(plen - hd, 0) <= lens[which]
+    pos, hp, hd = pos[ok], hp[ok], hd[ok]
+    order = np.lexsort((hd, pos, hp))
+    pos, hp, hd = pos[order], hp[order], hd[order]
+    uniq = np.ones(pos.size, dtype=bool)
+    uniq[1:] = (pos[1:] != pos[:-1]) | (hp[1:] != hp[:-1])
+    return hp[uniq], pos[uniq], hd[uniq]

@@ -1649,6 +1649,16 @@ int fmgx_exact_packed_work(const fmg_index* ix, const uint64_t* packed, uint32_t
   });
 }
 
+// Layout the Occ-step kernel reads (not part of include/fmgpu.h; bench.py's
+// algorithmic-bytes figure): 0 = 32-byte lines, 1 = 128-byte chunks.
+int fmgx_occ_layout(const fmg_index* ix, int* chunked) {
+  return fmg::guard([&] {
+    check_index(ix);
+    FMG_REQUIRE(chunked != nullptr, "null argument");
+    *chunked = (ix->chunks != nullptr && !chunk_off()) ? 1 : 0;
+  });
+}
+
 // Lines fetched by a bounded-difference search (companion of fmg_matches_steps).
 int fmgx_matches_lines(const fmg_matches* m, uint64_t* lines) {
   return fmg::guard([&] {

@@ -284,6 +284,32 @@ int main(int argc, char** argv) {
   time("C128 thread PER=1", [&] { k_c128_thread<1, 448><<<g1, 256, 0, st>>>(l128, kl, count, out); });
   time("C128 thread PER=2", [&] { k_c128_thread<2, 448><<<g1 / 2, 256, 0, st>>>(l128, kl, count, out); });
   time("C128 thread PER=4", [&] { k_c128_thread<4, 448><<<g1 / 4, 256, 0, st>>>(l128, kl, count, out); });
+  if (argc > 2 && argv[2][0] == 'p') {
+    // persisting-L2 variants on the chunk-layout thread kernel
+    const size_t maxlim = prop.persistingL2CacheMaxSize;
+    struct V { size_t limit; size_t win; float hr; };
+    const V vs[] = {{0, 0, 0.f}, {maxlim, 0, 0.f}, {maxlim, 64u << 20, 1.f}, {maxlim, 128u << 20, 0.6f},
+                    {maxlim, 128u << 20, 0.3f}, {maxlim / 2, 128u << 20, 0.3f}, {maxlim, 32u << 20, 1.f}};
+    for (const V& v : vs) {
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, v.limit);
+      cudaStreamAttrValue a = {};
+      a.accessPolicyWindow.base_ptr = (void*)l128;
+      a.accessPolicyWindow.num_bytes = v.win;
+      a.accessPolicyWindow.hitRatio = v.hr;
+      a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a);
+      char nm[128];
+      snprintf(nm, sizeof nm, "C128 thread: limit %zu MB window %zu MB hitRatio %.2f", v.limit >> 20, v.win >> 20,
+               v.hr);
+      time(nm, [&] { k_c128_thread<1, 448><<<g1, 256, 0, st>>>(l128, kl, count, out); });
+      a.accessPolicyWindow.num_bytes = 0;
+      cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a);
+      cudaCtxResetPersistingL2Cache();
+    }
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+    return 0;
+  }
   if (argc > 2) return 0;
   // persisting access-policy window over the index
   for (double hr : {1.0, 0.5, 0.3, 0.15}) {
