@@ -213,7 +213,9 @@ struct fmg_matches {
   uint64_t* row_off = nullptr;  // device, patterns + 1
   uint32_t* k = nullptr;        // device, total
   uint32_t* l = nullptr;
+  uint64_t* kl = nullptr;       // or: device, k << 32 | l packed (host-sync-free engine); split on copy
   uint8_t* diffs = nullptr;
+  cudaStream_t stream = nullptr;  // the stream the search ran on (buffers are freed on it)
 };
 
 namespace {
@@ -785,11 +787,15 @@ bool run_z1(const fmg_index* ix, const CodePatterns& cp, uint64_t count, uint64_
   return true;
 }
 
-// The level-synchronous bidirectional z = 1 engine (kernels_bidir.cuh):
-// patterns in chunks sized so the worst case of 8 continuations per spine
-// node always fits the node queue; raw results of all chunks are collected
-// once.  Returns false (caller falls back to the DFS engines) only if the
-// raw-result buffer overflowed.
+// The level-synchronous bidirectional z = 1 engine (kernels_bidir.cuh),
+// host-sync-free: patterns in chunks sized so the worst case of 8
+// continuations per spine node always fits the node queue; the chain kernel
+// reads the queue length from the device counter; results are grouped by
+// pattern (counting sort over device-counted raws), sorted and deduplicated
+// per pattern inside one kernel, and written to capacity-sized buffers.  The
+// call synchronises ONCE, at the end, to learn the result count, the work
+// counters and whether the raw buffer overflowed (then the caller falls back
+// to the DFS engine, which gives the same results).
 bool run_z1b(const fmg_index* ix, const BiIndex& bi, const CodePatterns& cp, uint64_t count, uint64_t m,
              cudaStream_t s, unsigned long long* steps, fmg_matches* res) {
   static const bool trace = std::getenv("FMG_TRACE") != nullptr;
@@ -802,50 +808,79 @@ bool run_z1b(const fmg_index* ix, const BiIndex& bi, const CodePatterns& cp, uin
   const uint64_t node_budget = std::max<uint64_t>(per, free_b / 4 / sizeof(Z1BNode));
   const uint64_t chunk = std::min<uint64_t>(count, std::max<uint64_t>(1, node_budget / per));
   const uint64_t node_cap = chunk * per;
-  const uint64_t raw_cap = std::min<uint64_t>(count * (per + 17), std::max<uint64_t>(1u << 20, free_b / 8 / sizeof(Z1Raw)));
+  // raws: 16 B each, plus 2 x 9 B of keys / used and 9 B of results below
+  const uint64_t raw_cap = std::min<uint64_t>(count * (per + 17), std::max<uint64_t>(1u << 20, free_b / 8 / 43));
   DevBuf<Z1BNode> nodes(node_cap, s);
   DevBuf<Z1Raw> raws(raw_cap, s);
   DevBuf<unsigned long long> ctr(2, s);
   FMG_CK(cudaMemsetAsync(ctr.ptr, 0, 16, s));
   Z1BQueues qu{nodes.ptr, ctr.ptr, node_cap, raws.ptr, ctr.ptr + 1, raw_cap};
-  unsigned long long total_nodes = 0;
   for (uint64_t q0 = 0; q0 < count; q0 += chunk) {
     const uint64_t c = std::min<uint64_t>(chunk, count - q0);
     FMG_CK(cudaMemsetAsync(ctr.ptr, 0, 8, s));
     with_words(ix, [&](auto wt) {
       constexpr int W = decltype(wt)::value;
       k_bspine<W><<<unsigned((c + 255) / 256), 256, 0, s>>>(ix->view(), bi, cp, q0, c, qu, steps);
+      // one full-residency wave; lanes refill from the queue length on the device
+      const unsigned nb = persistent_blocks(ix, (const void*)k_bchain<W>, 256, c * per);
+      k_bchain<W><<<nb, 256, 0, s>>>(ix->view(), bi, cp, nodes.ptr, ctr.ptr, qu, steps);
     });
     FMG_CK(cudaGetLastError());
-    unsigned long long n_nodes = 0;
-    FMG_CK(cudaMemcpyAsync(&n_nodes, ctr.ptr, 8, cudaMemcpyDeviceToHost, s));
-    FMG_CK(cudaStreamSynchronize(s));
-    FMG_REQUIRE(n_nodes <= node_cap, "bidirectional node queue overflow");  // impossible by sizing
-    total_nodes += n_nodes;
-    if (n_nodes) {
-      with_words(ix, [&](auto wt) {
-        constexpr int W = decltype(wt)::value;
-        const unsigned nb = persistent_blocks(ix, (const void*)k_bchain<W>, 256, n_nodes);
-        k_bchain<W><<<nb, 256, 0, s>>>(ix->view(), bi, cp, nodes.ptr, n_nodes, qu, steps);
-      });
-      FMG_CK(cudaGetLastError());
-    }
   }
-  unsigned long long n_raw = 0;
-  FMG_CK(cudaMemcpyAsync(&n_raw, ctr.ptr + 1, 8, cudaMemcpyDeviceToHost, s));
-  FMG_CK(cudaStreamSynchronize(s));
-  if (n_raw > raw_cap) return false;
   if (trace) cudaEventRecord(ev[1], s);
-  z1_collect(raws.ptr, n_raw, count, s, steps, res);
+  // ---- group by pattern, sort + dedup per pattern, CSR rows ----
+  DevBuf<uint32_t> per_q(count, s);
+  DevBuf<uint64_t> seg(count + 1, s), cursor(count, s), c64(count, s);
+  DevBuf<uint64_t> keys(raw_cap, s);
+  DevBuf<uint8_t> used(raw_cap, s);
+  FMG_CK(cudaMemsetAsync(per_q.ptr, 0, count * 4, s));
+  FMG_CK(cudaMemsetAsync(seg.ptr, 0, 8, s));
+  const unsigned gs = unsigned(std::max(1, blocks_per_sm((const void*)k_z1_scatter_dev, 256, 0)) * ix->sms);
+  k_z1_hist_dev<<<gs, 256, 0, s>>>(raws.ptr, ctr.ptr + 1, raw_cap, per_q.ptr);
+  const unsigned gq = unsigned((count + 255) / 256);
+  k_widen_counts<<<gq, 256, 0, s>>>(count, per_q.ptr, c64.ptr);
+  size_t tb = 0;
+  FMG_CK(cub::DeviceScan::InclusiveSum(nullptr, tb, c64.ptr, seg.ptr + 1, count, s));
+  DevBuf<uint8_t> tmp(tb, s);
+  FMG_CK(cub::DeviceScan::InclusiveSum(tmp.ptr, tb, c64.ptr, seg.ptr + 1, count, s));
+  FMG_CK(cudaMemcpyAsync(cursor.ptr, seg.ptr, count * 8, cudaMemcpyDeviceToDevice, s));
+  k_z1_scatter_dev<<<gs, 256, 0, s>>>(raws.ptr, ctr.ptr + 1, raw_cap, cursor.ptr, keys.ptr, used.ptr);
+  k_z1_sort_unique<<<gq, 256, 0, s>>>(keys.ptr, used.ptr, seg.ptr, count, per_q.ptr);
+  k_widen_counts<<<gq, 256, 0, s>>>(count, per_q.ptr, c64.ptr);
+  FMG_CK(cub::DeviceScan::InclusiveSum(tmp.ptr, tb, c64.ptr, res->row_off + 1, count, s));
+  FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->kl), pool_bytes(raw_cap * 8), s));
+  FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->diffs), pool_bytes(raw_cap), s));
+  k_z1_write_kl<<<gq, 256, 0, s>>>(keys.ptr, used.ptr, seg.ptr, res->row_off, count, res->kl, res->diffs);
+  FMG_CK(cudaGetLastError());
+  // ---- the one synchronisation: result count, work counters, overflow ----
+  struct Info {
+    unsigned long long n_raw, total, steps, lines;
+  };
+  static thread_local Info* info = nullptr;  // pinned, per host thread
+  if (!info) FMG_CK(cudaMallocHost(reinterpret_cast<void**>(&info), sizeof(Info)));
+  FMG_CK(cudaMemcpyAsync(&info->n_raw, ctr.ptr + 1, 8, cudaMemcpyDeviceToHost, s));
+  FMG_CK(cudaMemcpyAsync(&info->total, res->row_off + count, 8, cudaMemcpyDeviceToHost, s));
+  FMG_CK(cudaMemcpyAsync(&info->steps, steps, 16, cudaMemcpyDeviceToHost, s));
+  if (trace) cudaEventRecord(ev[2], s);
+  FMG_CK(cudaStreamSynchronize(s));
+  if (info->n_raw > raw_cap) {  // overflow: drop these results, the DFS engine redoes the batch
+    cudaFreeAsync(res->kl, s);
+    cudaFreeAsync(res->diffs, s);
+    res->kl = nullptr;
+    res->diffs = nullptr;
+    return false;
+  }
+  res->total = info->total;
+  res->steps = info->steps;
+  res->lines = info->lines;
+  res->stream = s;
   if (trace) {
-    cudaEventRecord(ev[2], s);
-    cudaEventSynchronize(ev[2]);
     float a = 0, b = 0;
     cudaEventElapsedTime(&a, ev[0], ev[1]);
     cudaEventElapsedTime(&b, ev[1], ev[2]);
-    fprintf(stderr, "[fmg] z1 bidirectional engine: %llu patterns in chunks of %llu, spines+chains %.3f ms "
-            "(%llu continuations), dedup/sort %.3f ms (%llu raw -> %llu results)\n", (unsigned long long)count,
-            (unsigned long long)chunk, a, total_nodes, b, n_raw, (unsigned long long)res->total);
+    fprintf(stderr, "[fmg] z1 bidirectional engine: %llu patterns in chunks of %llu, spines+chains %.3f ms, "
+            "group/sort/dedup %.3f ms (%llu raw -> %llu results)\n", (unsigned long long)count,
+            (unsigned long long)chunk, a, b, info->n_raw, (unsigned long long)res->total);
     for (auto& e : ev) cudaEventDestroy(e);
   }
   return true;
@@ -1924,11 +1959,22 @@ int fmg_matches_copy(const fmg_matches* m, uint64_t* row_offsets, uint32_t* k, u
     fmg::DeviceScope scope(m->device);
     const cudaMemcpyKind kind = to_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     if (row_offsets) FMG_CK(cudaMemcpy(row_offsets, m->row_off, (m->patterns + 1) * 8, kind));
-    if (m->total) {
+    if (m->total && m->kl && (k || l)) {  // packed k | l: split on the device, then copy
+      cudaStream_t s = host_stream(m->device, 1);
+      DevBuf<uint32_t> dk(to_host && k ? m->total : 0, s), dl(to_host && l ? m->total : 0, s);
+      uint32_t* ok = to_host ? dk.ptr : k;
+      uint32_t* ol = to_host ? dl.ptr : l;
+      fmg::k_split_kl<<<unsigned(std::min<uint64_t>((m->total + 255) / 256, 148 * 16)), 256, 0, s>>>(
+          m->kl, m->total, k ? ok : nullptr, l ? ol : nullptr);
+      FMG_CK(cudaGetLastError());
+      if (to_host && k) FMG_CK(cudaMemcpyAsync(k, dk.ptr, m->total * 4, cudaMemcpyDeviceToHost, s));
+      if (to_host && l) FMG_CK(cudaMemcpyAsync(l, dl.ptr, m->total * 4, cudaMemcpyDeviceToHost, s));
+      FMG_CK(cudaStreamSynchronize(s));
+    } else if (m->total) {
       if (k) FMG_CK(cudaMemcpy(k, m->k, m->total * 4, kind));
       if (l) FMG_CK(cudaMemcpy(l, m->l, m->total * 4, kind));
-      if (diffs) FMG_CK(cudaMemcpy(diffs, m->diffs, m->total, kind));
     }
+    if (m->total && diffs) FMG_CK(cudaMemcpy(diffs, m->diffs, m->total, kind));
   });
 }
 
@@ -1941,6 +1987,7 @@ void fmg_matches_free(fmg_matches* m) {
   if (m->row_off) cudaFreeAsync(m->row_off, 0);
   if (m->k) cudaFreeAsync(m->k, 0);
   if (m->l) cudaFreeAsync(m->l, 0);
+  if (m->kl) cudaFreeAsync(m->kl, 0);
   if (m->diffs) cudaFreeAsync(m->diffs, 0);
   if (prev >= 0) cudaSetDevice(prev);
   delete m;

@@ -977,8 +977,11 @@ __global__ void __launch_bounds__(256) k_bspine(IndexView ix, BiIndex bi, CodePa
 
 template <int W>
 __global__ void __launch_bounds__(256) k_bchain(IndexView ix, BiIndex bi, CodePatterns cp,
-                                                const Z1BNode* __restrict__ nodes, uint64_t n_nodes, Z1BQueues qu,
+                                                const Z1BNode* __restrict__ nodes,
+                                                const unsigned long long* __restrict__ n_nodes_dev, Z1BQueues qu,
                                                 unsigned long long* steps) {
+  // the queue length k_bspine left on the device (no host round trip)
+  const uint64_t n_nodes = min(uint64_t(*n_nodes_dev), qu.node_cap);
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   uint64_t work = 0;

@@ -897,6 +897,86 @@ __global__ void k_unpack_keys(uint64_t n, const uint64_t* __restrict__ keys, con
   }
 }
 
+// ---- host-sync-free result collection (run_z1b): sizes come from device
+// counters, every kernel is grid-stride, the dedup sort runs per pattern ----
+
+__global__ void k_z1_hist_dev(const Z1Raw* __restrict__ raws, const unsigned long long* __restrict__ n_raw,
+                              uint64_t cap, uint32_t* __restrict__ per_q) {
+  const uint64_t n = min(uint64_t(*n_raw), cap);
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n; t += stride)
+    atomicAdd(&per_q[raws[t].q], 1u);
+}
+
+__global__ void k_z1_scatter_dev(const Z1Raw* __restrict__ raws, const unsigned long long* __restrict__ n_raw,
+                                 uint64_t cap, uint64_t* __restrict__ cursor, uint64_t* __restrict__ keys,
+                                 uint8_t* __restrict__ used) {
+  const uint64_t n = min(uint64_t(*n_raw), cap);
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n; t += stride) {
+    const Z1Raw r = raws[t];
+    const unsigned long long p = atomicAdd(reinterpret_cast<unsigned long long*>(&cursor[r.q]), 1ull);
+    keys[p] = (uint64_t(r.k) << 32) | r.l;
+    used[p] = uint8_t(r.used);
+  }
+}
+
+// Per pattern: sort its raw results by (k, l, diffs) in place (insertion
+// sort: segments hold a handful of entries), then keep the first of each
+// (k, l) — the smallest diffs — compacted at the segment start
+// (search.py:128-134, 153-159).  ucnt[q] = the unique count.
+__global__ void k_z1_sort_unique(uint64_t* __restrict__ keys, uint8_t* __restrict__ used,
+                                 const uint64_t* __restrict__ seg, uint64_t count, uint32_t* __restrict__ ucnt) {
+  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  const uint64_t a = seg[q], b = seg[q + 1];
+  for (uint64_t i = a + 1; i < b; ++i) {
+    const uint64_t kk = keys[i];
+    const uint8_t uu = used[i];
+    uint64_t j = i;
+    while (j > a && (keys[j - 1] > kk || (keys[j - 1] == kk && used[j - 1] > uu))) {
+      keys[j] = keys[j - 1];
+      used[j] = used[j - 1];
+      --j;
+    }
+    keys[j] = kk;
+    used[j] = uu;
+  }
+  uint32_t c = 0;
+  for (uint64_t i = a; i < b; ++i) {
+    if (i == a || keys[i] != keys[i - 1]) {
+      keys[a + c] = keys[i];
+      used[a + c] = used[i];
+      ++c;
+    }
+  }
+  ucnt[q] = c;
+}
+
+// Unique results of pattern q to their CSR rows (k | l packed in one u64).
+__global__ void k_z1_write_kl(const uint64_t* __restrict__ keys, const uint8_t* __restrict__ used,
+                              const uint64_t* __restrict__ seg, const uint64_t* __restrict__ row_off, uint64_t count,
+                              uint64_t* __restrict__ kl_out, uint8_t* __restrict__ d_out) {
+  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  const uint64_t a = seg[q], o = row_off[q], c = row_off[q + 1] - o;
+  for (uint64_t i = 0; i < c; ++i) {
+    kl_out[o + i] = keys[a + i];
+    d_out[o + i] = used[a + i];
+  }
+}
+
+// k | l packed results -> separate k and l arrays (fmg_matches_copy).
+__global__ void k_split_kl(const uint64_t* __restrict__ kl, uint64_t n, uint32_t* __restrict__ k,
+                           uint32_t* __restrict__ l) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n; t += stride) {
+    const uint64_t v = kl[t];
+    if (k) k[t] = uint32_t(v >> 32);
+    if (l) l[t] = uint32_t(v);
+  }
+}
+
 __global__ void k_widen_counts(uint64_t count, const uint32_t* __restrict__ c32, uint64_t* __restrict__ c64) {
   const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (q < count) c64[q] = c32[q];

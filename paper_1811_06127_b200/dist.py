@@ -38,7 +38,13 @@ def gather_fixed(local: np.ndarray, world: int) -> np.ndarray:
 
     if world == 1:
         return local
-    t = torch.from_numpy(np.ascontiguousarray(local))
+    local = np.ascontiguousarray(local)
+    dtype = local.dtype
+    # gloo carries no unsigned 32/64-bit tensors: ship the same bytes as signed
+    wire = {np.dtype(np.uint32): np.int32, np.dtype(np.uint64): np.int64, np.dtype(np.uint16): np.int16}
+    if dtype in wire:
+        local = local.view(wire[dtype])
+    t = torch.from_numpy(local)
     sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
     dist.all_gather(sizes, torch.tensor([t.shape[0]], dtype=torch.int64))
     mx = int(max(s.item() for s in sizes))
@@ -46,7 +52,7 @@ def gather_fixed(local: np.ndarray, world: int) -> np.ndarray:
     pad[: t.shape[0]] = t
     bufs = [torch.zeros_like(pad) for _ in range(world)]
     dist.all_gather(bufs, pad)
-    return np.concatenate([b[: int(s.item())].numpy() for b, s in zip(bufs, sizes)])
+    return np.concatenate([b[: int(s.item())].numpy() for b, s in zip(bufs, sizes)]).view(dtype)
 
 
 def gather_csr(offsets: np.ndarray, values: list[np.ndarray], world: int):

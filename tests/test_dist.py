@@ -51,6 +51,8 @@ def _worker(rank, world, port, out_dir):
         lo, hi = shard_range(pats.shape[0], rank, world)
         kl = orc.exact_batch(ox, pats[lo:hi], threads=1)
         all_kl = gather_fixed(kl, world)
+        u32 = gather_fixed(kl.astype(np.uint32), world)  # gloo has no uint32: shipped as int32 bytes
+        assert u32.dtype == np.uint32 and np.array_equal(u32, all_kl.astype(np.uint32))
         row, k, l, d, _ = orc.inexact_batch(ox, pats[lo:hi], 1, threads=1)
         all_row, (all_k, all_l, all_d) = gather_csr(row, [k, l, d], world)
         t = max_over_ranks(float(rank + 1), world)
