@@ -119,23 +119,23 @@ def occ_step_bytes(pairs: np.ndarray) -> tuple[int, int]:
     return lines * 32 + low.size * 40, lines
 
 
-CHUNK_CHARS = 416  # csrc/kernels_chunk.cuh
+CHUNK_CHARS = {2: 192, 4: 416}  # sectors per chunk -> characters (csrc/kernels_chunk.cuh)
 
 
 def chunk_sector_of(r: np.ndarray) -> np.ndarray:
     return np.where(r < 80, 0, 1 + (r - 80) // 112)
 
 
-def chunk_step_bytes(pairs: np.ndarray) -> tuple[int, int, int]:
+def chunk_step_bytes(pairs: np.ndarray, chars: int = 416) -> tuple[int, int, int]:
     """Algorithmic bytes of Occ steps on the 128-byte chunk layout (kernels_chunk.cuh).
 
     Per step: 32 B x |S(k-1) U S(l)| with S(p) = {sector 0 of p's chunk, the
     sector holding p} + 8 B (k, l) in + 32 B out.  Returns (total bytes,
-    total distinct sectors, total distinct 128-byte chunks)."""
+    total distinct sectors, total distinct chunks)."""
     low, high = pairs[:, 0], pairs[:, 1]
-    jh, jl = high // CHUNK_CHARS, np.maximum(low, 0) // CHUNK_CHARS
-    sh = chunk_sector_of(high - jh * CHUNK_CHARS)
-    sl = chunk_sector_of(np.maximum(low, 0) - jl * CHUNK_CHARS)
+    jh, jl = high // chars, np.maximum(low, 0) // chars
+    sh = chunk_sector_of(high - jh * chars)
+    sl = chunk_sector_of(np.maximum(low, 0) - jl * chars)
     has_low = low >= 0
     other = has_low & (jl != jh)
     sect = 1 + (sh != 0)                                       # high end: base + its sector
@@ -519,7 +519,7 @@ def occ_layout(lib, dix) -> str:
     from paper_1811_06127_b200 import _lib
 
     _lib.check(fn(dix.handle, ct.byref(c)))
-    return "chunks" if c.value else "lines"
+    return f"chunks{c.value}" if c.value else "lines"
 
 
 def occ_roofline(lib, dix, pairs: np.ndarray, launch_s: float, device: int, config: str) -> dict:
@@ -533,9 +533,10 @@ def occ_roofline(lib, dix, pairs: np.ndarray, launch_s: float, device: int, conf
     layout = occ_layout(lib, dix)
     peak, kind = hbm_peak()
     line_bytes, lines = occ_step_bytes(pairs)
-    if layout == "chunks":
-        alg, sectors, chunks = chunk_step_bytes(pairs)
-        kernel = "k_occ_pair_chunk"
+    if layout.startswith("chunks"):
+        ns = int(layout[6:])
+        alg, sectors, chunks = chunk_step_bytes(pairs, CHUNK_CHARS[ns])
+        kernel = f"k_occ_pair_chunk<{ns}>"
     else:
         alg, sectors, chunks = line_bytes, lines, fetch_chunks(pairs)
         kernel = "k_occ_pair"
@@ -570,7 +571,8 @@ def occ_roofline(lib, dix, pairs: np.ndarray, launch_s: float, device: int, conf
     if fetch_peak:
         hbm["request_roofline"] = {
             "bound": "dram_random_requests", "achieved": round(chunks / launch_s / 1e9, 2),
-            "peak": round(fetch_peak / 1e9, 2), "unit": "G random 128-B fetches/s",
+            "peak": round(fetch_peak / 1e9, 2),
+            "unit": f"G random {32 * int(layout[6:]) if layout.startswith('chunks') else 128}-B fetches/s",
             "frac": round(chunks / launch_s / fetch_peak, 4), "chunks_per_step": round(chunks / units, 4),
             "note": "distinct 128-byte chunks per step (exact replay); peak measured live: random 32-B reads "
                     "over 4 GiB, each fetching 128 B from DRAM; L2 hits let frac exceed 1"}
@@ -609,7 +611,7 @@ def hbm_resident_extra(dev, lib, reps: int = 10) -> dict:
     roof = occ_roofline(lib, dix, wl.pairs, launch_s, dev.index, "config1h")
     idx.release_device()
     return {"workload": "config 1-H: 2^24 config-1 pairs over the 1 Gbp config-4 text (seed 5), "
-                        "HBM-resident index (lines 500 MB + chunks 308 MB)",
+                        "HBM-resident index (500 MB of lines + the chunk layout the Occ kernel reads)",
             "value": units / launch_s, "unit": "occ_steps/s", "index_build_s_gpu": round(build_s, 2),
             "roofline": roof}
 

@@ -157,6 +157,7 @@ struct fmg_index {
   // the lines (416 instead of 256 characters per DRAM fetch)
   uint32_t* chunks = nullptr;
   uint64_t n_chunks = 0;
+  int chunk_sectors = 4;  // 4: 128-byte chunks; 2: 64-byte chunks read with the L2::64B hint
   // Attachments (fmg_index_set_samples / fmg_index_set_reverse) are
   // one-time: the first attach uploads and publishes the pointer with a
   // release store under attach_mu, later attaches are no-ops, and nothing is
@@ -299,10 +300,29 @@ uint64_t chunk_min_line_bytes() {
   return e ? std::strtoull(e, nullptr, 10) : (uint64_t(64) << 20);
 }
 
+// ... and up to this size: beyond ~2 Gbp the chunk kernel's four sector
+// requests per step lose to the lines' one or two (3.1 Gbp synthetic, 2^24
+// config-1 pairs: chunks 723-774 us, lines 535 us; profiles/r02_occ_layout.md).
+// FMG_CHUNK_MAX_BYTES overrides.
+uint64_t chunk_max_line_bytes() {
+  const char* e = std::getenv("FMG_CHUNK_MAX_BYTES");
+  return e ? std::strtoull(e, nullptr, 10) : (uint64_t(1) << 30);
+}
+
+// Sectors per chunk of the Occ-step layout: FMG_CHUNK_SECTORS=2|4 (A/B).
+int chunk_sectors_default() {
+  const char* e = std::getenv("FMG_CHUNK_SECTORS");
+  const int v = e ? std::atoi(e) : 4;
+  FMG_REQUIRE(v == 2 || v == 4, "FMG_CHUNK_SECTORS must be 2 or 4");
+  return v;
+}
+
 uint32_t* build_chunks(const fmg_index* ix, const void* bucket_records, uint64_t& n_chunks) {
-  n_chunks = (ix->n + 1 + fmg::kChunkChars - 1) / fmg::kChunkChars;
+  const int ns = ix->chunk_sectors;
+  const uint64_t chars = ns == 2 ? fmg::ChunkTraits<2>::kChars : fmg::ChunkTraits<4>::kChars;
+  n_chunks = (ix->n + 1 + chars - 1) / chars;
   uint32_t* chunks = nullptr;
-  FMG_CK(cudaMalloc(&chunks, n_chunks * fmg::kChunkBytes));
+  FMG_CK(cudaMalloc(&chunks, n_chunks * 32 * ns));
   uint64_t* staging = nullptr;
   const uint64_t nb = ix->n_buckets;
   cudaError_t e = cudaMalloc(&staging, nb * 64 + 64);
@@ -312,7 +332,10 @@ uint32_t* build_chunks(const fmg_index* ix, const void* bucket_records, uint64_t
     e = cudaMemcpy(staging, bucket_records, nb * 64, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(err, 0, 4);
     if (e == cudaSuccess) {
-      fmg::k_build_chunks<<<unsigned((n_chunks + 255) / 256), 256>>>(staging, nb, chunks, n_chunks, err);
+      if (ns == 2)
+        fmg::k_build_chunks<2><<<unsigned((n_chunks + 255) / 256), 256>>>(staging, nb, chunks, n_chunks, err);
+      else
+        fmg::k_build_chunks<4><<<unsigned((n_chunks + 255) / 256), 256>>>(staging, nb, chunks, n_chunks, err);
       e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -337,8 +360,12 @@ void launch_occ_pair_t(const fmg_index* ix, const uint32_t* kl, uint64_t count, 
     const char* e2l = std::getenv("FMG_OCC_2LANE");  // A/B hook
     const bool two_lane = e2l ? std::atoi(e2l) != 0 : ix->n_lines * 32ull > (64ull << 20);
     if (ix->chunks && !chunk_off()) {
-      k_occ_pair_chunk<<<dim3(unsigned((count + 255) / 256)), 256, 0, s>>>(
-          ix->view(), ix->chunks, reinterpret_cast<const uint2*>(kl), count, out, err);
+      if (ix->chunk_sectors == 2)
+        k_occ_pair_chunk<2><<<dim3(unsigned((count + 255) / 256)), 256, 0, s>>>(
+            ix->view(), ix->chunks, reinterpret_cast<const uint2*>(kl), count, out, err);
+      else
+        k_occ_pair_chunk<4><<<dim3(unsigned((count + 255) / 256)), 256, 0, s>>>(
+            ix->view(), ix->chunks, reinterpret_cast<const uint2*>(kl), count, out, err);
     } else if (W == 2 && two_lane) {
       k_occ_pair_2l<<<dim3(unsigned((2 * count + 255) / 256)), 256, 0, s>>>(
           ix->view(), reinterpret_cast<const uint2*>(kl), count, out, err);
@@ -1538,7 +1565,10 @@ int fmg_index_create(int device, const void* bucket_records, uint64_t n_buckets,
       ix->words = choose_words(n_buckets);
       ix->sms = fmg::sm_count(device);
       ix->lines = upload_lines(ix, bucket_records);
-      if (ix->n_lines * 32 > chunk_min_line_bytes()) ix->chunks = build_chunks(ix, bucket_records, ix->n_chunks);
+      if (ix->n_lines * 32 > chunk_min_line_bytes() && ix->n_lines * 32 <= chunk_max_line_bytes()) {
+        ix->chunk_sectors = chunk_sectors_default();
+        ix->chunks = build_chunks(ix, bucket_records, ix->n_chunks);
+      }
       // Allow the stream-ordered pool to keep freed blocks (host entry points
       // allocate per call).
       cudaMemPool_t pool;
@@ -1620,7 +1650,7 @@ int fmg_index_info(const fmg_index* ix, uint64_t* n, int* device, uint64_t* devi
       const bool rev = ix->rev_lines.load(std::memory_order_acquire) != nullptr;
       const bool smp = ix->samples.load(std::memory_order_acquire) != nullptr;
       *device_bytes = ix->n_lines * lb * (rev ? 2 : 1) + (smp ? ix->n_samples * 4 : 0) +
-                      ix->n_chunks * fmg::kChunkBytes;
+                      ix->n_chunks * 32ull * uint64_t(ix->chunk_sectors);
     }
   });
 }
@@ -1685,12 +1715,13 @@ int fmgx_exact_packed_work(const fmg_index* ix, const uint64_t* packed, uint32_t
 }
 
 // Layout the Occ-step kernel reads (not part of include/fmgpu.h; bench.py's
-// algorithmic-bytes figure): 0 = 32-byte lines, 1 = 128-byte chunks.
+// algorithmic-bytes figure): 0 = 32-byte lines, else the sectors per chunk
+// of the chunk layout (2: 64-byte, 4: 128-byte chunks).
 int fmgx_occ_layout(const fmg_index* ix, int* chunked) {
   return fmg::guard([&] {
     check_index(ix);
     FMG_REQUIRE(chunked != nullptr, "null argument");
-    *chunked = (ix->chunks != nullptr && !chunk_off()) ? 1 : 0;
+    *chunked = (ix->chunks != nullptr && !chunk_off()) ? ix->chunk_sectors : 0;
   });
 }
 

@@ -30,8 +30,16 @@
 
 namespace fmg {
 
-constexpr uint32_t kChunkChars = 416;
-constexpr uint32_t kChunkBytes = 128;
+// NS sectors per chunk: 4 (128 bytes, 416 characters; the DRAM fetch
+// granularity) or 2 (64 bytes, 192 characters: the first two sectors of the
+// same format, read with the L2::64B fetch hint so a miss moves 64 bytes).
+template <int NS>
+struct ChunkTraits {
+  static_assert(NS == 2 || NS == 4, "2 or 4 sectors per chunk");
+  static constexpr uint32_t kChars = NS == 4 ? 416u : 192u;
+  static constexpr uint32_t kBytes = 32u * NS;
+  static constexpr uint32_t kWords = 8u * NS;  // u32
+};
 
 // first character of sector s inside its chunk, and its data field offset
 // inside the sector's 128 two-bit fields
@@ -45,11 +53,12 @@ __device__ __forceinline__ uint32_t chunk_sector_of(uint32_t r) {
 
 // Build: bucket records (4 x u64 LE base + 32 B chars per 128 characters,
 // serialize.py:87-92) -> chunks.  One thread per chunk.
+template <int NS>
 __global__ void k_build_chunks(const uint64_t* __restrict__ rec, uint64_t nb, uint32_t* __restrict__ chunks,
                                uint64_t n_chunks, uint32_t* __restrict__ err) {
   const uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= n_chunks) return;
-  const uint64_t c0 = j * kChunkChars;  // multiple of 32: a word boundary of its bucket
+  const uint64_t c0 = j * ChunkTraits<NS>::kChars;  // multiple of 32: a word boundary of its bucket
   const uint64_t b0 = c0 >> 7;
   const uint64_t* r = rec + b0 * 8;
   uint32_t cgt[3];
@@ -74,13 +83,13 @@ __global__ void k_build_chunks(const uint64_t* __restrict__ rec, uint64_t nb, ui
     const uint32_t* chars = reinterpret_cast<const uint32_t*>(rec + b * 8 + 4);
     return chars[(c & 127u) >> 4];
   };
-  uint32_t out[32];
+  uint32_t out[8 * NS];
   out[0] = cgt[0];
   out[1] = cgt[1];
   out[2] = cgt[2];
   uint32_t dc = 0, dg = 0, dt = 0;  // running counts inside the chunk
 #pragma unroll
-  for (int s = 0; s < 4; ++s) {
+  for (int s = 0; s < NS; ++s) {
     const uint32_t first = s == 0 ? 3u : 1u;
     if (s > 0) out[8 * s] = dc | (dg << 10) | (dt << 20);
 #pragma unroll
@@ -93,9 +102,9 @@ __global__ void k_build_chunks(const uint64_t* __restrict__ rec, uint64_t nb, ui
       dt += t;
     }
   }
-  uint4* dst = reinterpret_cast<uint4*>(chunks + j * 32);
+  uint4* dst = reinterpret_cast<uint4*>(chunks + j * ChunkTraits<NS>::kWords);
 #pragma unroll
-  for (int q = 0; q < 8; ++q) dst[q] = make_uint4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
+  for (int q = 0; q < 2 * NS; ++q) dst[q] = make_uint4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
 }
 
 // C, G, T among the sector's data fields up to and including chunk character
@@ -124,24 +133,33 @@ __device__ __forceinline__ void chunk_count3(const uint64_t v[4], uint32_t s, ui
   c = ll - tt;
 }
 
-__device__ __forceinline__ void ld_sector(const uint32_t* chunks, uint64_t j, uint32_t s, uint64_t v[4]) {
-  ld256<1>(reinterpret_cast<const uint8_t*>(chunks + j * 32 + 8 * s), v[0], v[1], v[2], v[3]);
-}
-
+// Sector s of chunk j, predicated (no request when !go).  Two-sector chunks
+// carry the L2::64B hint: the miss fetches the 64-byte chunk, not 128 bytes.
+template <int NS>
 __device__ __forceinline__ void ld_sector_pred(bool go, const uint32_t* chunks, uint64_t j, uint32_t s,
                                                uint64_t v[4]) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
-      "@q ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%5];\n\t}"
-      : "+l"(v[0]), "+l"(v[1]), "+l"(v[2]), "+l"(v[3])
-      : "r"(uint32_t(go)), "l"(chunks + j * 32 + 8 * s));
+  const uint32_t* p = chunks + j * ChunkTraits<NS>::kWords + 8 * s;
+  if constexpr (NS == 2) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
+        "@q ld.global.nc.L1::no_allocate.L2::64B.v4.u64 {%0,%1,%2,%3}, [%5];\n\t}"
+        : "+l"(v[0]), "+l"(v[1]), "+l"(v[2]), "+l"(v[3])
+        : "r"(uint32_t(go)), "l"(p));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
+        "@q ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%5];\n\t}"
+        : "+l"(v[0]), "+l"(v[1]), "+l"(v[2]), "+l"(v[3])
+        : "r"(uint32_t(go)), "l"(p));
+  }
 }
 
 // Occ(., p) for 0 <= p <= n from sector 0 (h) and p's own sector (d; equal
 // to h when p lies in sector 0).
+template <int NS>
 __device__ __forceinline__ void chunk_occ4(const IndexView& ix, const uint64_t h[4], const uint64_t d[4], uint32_t p,
                                            uint32_t j, uint32_t out[4]) {
-  const uint32_t r = p - j * kChunkChars;
+  const uint32_t r = p - j * ChunkTraits<NS>::kChars;
   const uint32_t s = chunk_sector_of(r);
   uint32_t c, g, t;
   chunk_count3(d, s, r, c, g, t);
@@ -165,6 +183,7 @@ __device__ __forceinline__ void chunk_occ4(const IndexView& ix, const uint64_t h
 // end, each predicated off when it is already loaded), so a warp keeps
 // ~2.5 random 32-byte requests per step in flight against one or two
 // 128-byte DRAM fetches.
+template <int NS>
 __global__ void __launch_bounds__(256) k_occ_pair_chunk(IndexView ix, const uint32_t* __restrict__ chunks,
                                                         const uint2* __restrict__ kl, uint64_t count,
                                                         uint32_t* __restrict__ out, uint32_t* __restrict__ err) {
@@ -177,15 +196,15 @@ __global__ void __launch_bounds__(256) k_occ_pair_chunk(IndexView ix, const uint
   const uint32_t hp = ok ? l : 0u;
   const bool has_low = ok && k != 0u;
   const uint32_t lp = has_low ? k - 1u : hp;
-  const uint32_t jh = hp / kChunkChars, jl = lp / kChunkChars;
-  const uint32_t sh = chunk_sector_of(hp - jh * kChunkChars), sl = chunk_sector_of(lp - jl * kChunkChars);
-  uint64_t h_hi[4], d_hi[4], h_lo[4] = {0, 0, 0, 0}, d_lo[4] = {0, 0, 0, 0};
-  ld_sector(chunks, jh, 0, h_hi);
-  for (int z = 0; z < 4; ++z) d_hi[z] = 0;
-  ld_sector_pred(sh != 0u, chunks, jh, sh, d_hi);
+  constexpr uint32_t kC = ChunkTraits<NS>::kChars;
+  const uint32_t jh = hp / kC, jl = lp / kC;
+  const uint32_t sh = chunk_sector_of(hp - jh * kC), sl = chunk_sector_of(lp - jl * kC);
+  uint64_t h_hi[4] = {0, 0, 0, 0}, d_hi[4] = {0, 0, 0, 0}, h_lo[4] = {0, 0, 0, 0}, d_lo[4] = {0, 0, 0, 0};
+  ld_sector_pred<NS>(true, chunks, jh, 0, h_hi);
+  ld_sector_pred<NS>(sh != 0u, chunks, jh, sh, d_hi);
   const bool other = jl != jh;
-  ld_sector_pred(other, chunks, jl, 0, h_lo);
-  ld_sector_pred(sl != 0u && (other || sl != sh), chunks, jl, sl, d_lo);
+  ld_sector_pred<NS>(other, chunks, jl, 0, h_lo);
+  ld_sector_pred<NS>(sl != 0u && (other || sl != sh), chunks, jl, sl, d_lo);
   // resolve aliases: the low end shares whatever the high end loaded
 #pragma unroll
   for (int z = 0; z < 4; ++z) {
@@ -194,8 +213,8 @@ __global__ void __launch_bounds__(256) k_occ_pair_chunk(IndexView ix, const uint
     d_lo[z] = sl == 0u ? h_lo[z] : ((!other && sl == sh) ? d_hi[z] : d_lo[z]);
   }
   uint32_t lo4[4] = {0u, 0u, 0u, 0u}, hi4[4] = {0u, 0u, 0u, 0u};
-  if (ok) chunk_occ4(ix, h_hi, d_hi, hp, jh, hi4);
-  if (has_low) chunk_occ4(ix, h_lo, d_lo, lp, jl, lo4);
+  if (ok) chunk_occ4<NS>(ix, h_hi, d_hi, hp, jh, hi4);
+  if (has_low) chunk_occ4<NS>(ix, h_lo, d_lo, lp, jl, lo4);
   st_stream_256(out + i * 8, lo4, hi4);
 }
 

@@ -62,6 +62,12 @@ struct IndexView {
 
 constexpr uint64_t kFieldLo = 0x5555555555555555ull;
 
+#ifndef FMG_SEARCH_L2_64B
+// 1: the search kernels' line loads carry the L2::64B hint (a miss fetches
+// 64 bytes from DRAM instead of 128; A/B switch)
+#define FMG_SEARCH_L2_64B 0
+#endif
+
 // kStream: 0 = default caching; 1 = L1::no_allocate (gathers without reuse);
 // 2 = L2 evict_first (lines that must not push a hot working set — the
 // prefix table — out of L2).
@@ -78,7 +84,11 @@ __device__ __forceinline__ void ld256(const uint8_t* p, uint64_t& a0, uint64_t& 
         : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3)
         : "l"(p), "l"(pol));
   } else {
+#if FMG_SEARCH_L2_64B
+    asm("ld.global.nc.L2::64B.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3) : "l"(p));
+#else
     asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3) : "l"(p));
+#endif
   }
 }
 
@@ -124,7 +134,11 @@ __device__ __forceinline__ void ld256_pred(bool go, const uint8_t* p, uint64_t& 
                                            uint64_t& a3) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
+#if FMG_SEARCH_L2_64B
+      "@q ld.global.nc.L2::64B.v4.u64 {%0,%1,%2,%3}, [%5];\n\t}"
+#else
       "@q ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%5];\n\t}"
+#endif
       : "+l"(a0), "+l"(a1), "+l"(a2), "+l"(a3)
       : "r"(uint32_t(go)), "l"(p));
 }

@@ -13,9 +13,12 @@ from paper_1811_06127_b200 import workloads
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("n", [1, 2, 79, 80, 81, 191, 192, 303, 304, 415, 416, 417, 831, 832, 833, 5000, 20011])
-def test_chunk_layout_every_position(gpu, monkeypatch, n):
+@pytest.mark.parametrize("sectors", [2, 4])
+@pytest.mark.parametrize("n", [1, 2, 79, 80, 81, 191, 192, 193, 303, 304, 383, 384, 415, 416, 417, 831, 832, 833,
+                               5000, 20011])
+def test_chunk_layout_every_position(gpu, monkeypatch, n, sectors):
     monkeypatch.setenv("FMG_CHUNK_MIN_BYTES", "0")
+    monkeypatch.setenv("FMG_CHUNK_SECTORS", str(sectors))
     text = small_text(n, 7000 + n)
     idx = fm.build_index(text, builder="host")
     assert idx.device_index(0).device_bytes > (n + 1) // 2  # lines + chunks
@@ -51,8 +54,10 @@ def test_chunk_layout_device_status(gpu, monkeypatch):
     assert np.array_equal(out[[0, 2]].cpu().numpy().view(np.uint32), want)
 
 
-def test_config1h_full_vs_oracle(gpu):
+@pytest.mark.parametrize("sectors", [2, 4])
+def test_config1h_full_vs_oracle(gpu, monkeypatch, sectors):
     """Config 1-H (1 Gbp text, HBM-resident: chunk layout): all 2^24 bench pairs."""
+    monkeypatch.setenv("FMG_CHUNK_SECTORS", str(sectors))
     wl = workloads.config1h()
     idx = fm.build_index(wl.text, builder="gpu")
     got = fm.occ_pair_batch(idx, wl.pairs[:, 0], wl.pairs[:, 1])
