@@ -63,9 +63,12 @@ struct IndexView {
 constexpr uint64_t kFieldLo = 0x5555555555555555ull;
 
 #ifndef FMG_SEARCH_L2_64B
-// 1: the search kernels' line loads carry the L2::64B hint (a miss fetches
-// 64 bytes from DRAM instead of 128; A/B switch)
-#define FMG_SEARCH_L2_64B 0
+// 1: the search kernels' line and table loads carry the L2::64B hint, so a
+// miss fetches 64 bytes from DRAM instead of 128 (a dependent search step
+// uses one 32-byte line).  Measured on B200: config 4 exact 12.44 -> 13.30 G
+// seeds/s (it is DRAM-saturated at 128-byte fetches), config 3 z = 1 130.8
+// -> 129.9 ms per 14M seeds (latency-bound).  0 restores plain loads (A/B).
+#define FMG_SEARCH_L2_64B 1
 #endif
 
 // kStream: 0 = default caching; 1 = L1::no_allocate (gathers without reuse);
