@@ -26,6 +26,7 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC,-O3",
     "-shared",
+    "-ldl",  # guard mode resolves the driver API (libcuda) at run time: no link-time dependency
 ]
 
 

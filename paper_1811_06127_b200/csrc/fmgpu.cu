@@ -7,7 +7,9 @@
 //   kernels_inexact.cuh  k_dbound, k_inexact (DFS), k_spine / k_chain (z = 1),
 //                        sort / dedup / gather                 (search.py:97-159)
 
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -70,14 +72,161 @@ inline size_t pool_bytes(size_t bytes) {
   return bytes >= g ? (bytes + g - 1) / g * g : bytes;
 }
 
-// Stream-ordered device allocation (pool-backed, cheap after warm-up).
+// ---------------------------------------------------------------------------
+// Guard mode (FMG_GUARD=1): every library allocation gets its own virtual
+// address range with unmapped guard space on both sides, and ends exactly at
+// its mapped end, so an out-of-bounds access by any kernel faults (illegal
+// address) instead of reading a neighbour.  The bounds-checking substitute
+// for compute-sanitizer, which this pool does not allow (tools/guard_check.sh).
+// Allocation and free become synchronous; production runs never set it.
+// ---------------------------------------------------------------------------
+bool guard_mode() {
+  static const bool on = [] {
+    const char* e = std::getenv("FMG_GUARD");
+    return e != nullptr && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+struct GuardRec {
+  CUdeviceptr va;
+  size_t reserved, mapped;
+  CUmemGenericAllocationHandle h;
+};
+std::mutex g_guard_mu;
+std::unordered_map<void*, GuardRec> g_guard;
+
+// The driver's virtual-memory API, resolved from libcuda at run time (the
+// library must load on hosts without a driver, e.g. the CPU build check).
+struct CuVmm {
+  CUresult (*gran)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags);
+  CUresult (*reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+  CUresult (*create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long);
+  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+  CUresult (*access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+  CUresult (*unmap)(CUdeviceptr, size_t);
+  CUresult (*release)(CUmemGenericAllocationHandle);
+  CUresult (*addr_free)(CUdeviceptr, size_t);
+};
+const CuVmm& cu_vmm() {
+  static const CuVmm v = [] {
+    CuVmm r{};
+    void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw std::runtime_error("FMG_GUARD=1 needs libcuda.so.1");
+    auto sym = [&](const char* n) {
+      void* f = dlsym(h, n);
+      if (!f) throw std::runtime_error(std::string("libcuda lacks ") + n);
+      return f;
+    };
+    r.gran = reinterpret_cast<decltype(r.gran)>(sym("cuMemGetAllocationGranularity"));
+    r.reserve = reinterpret_cast<decltype(r.reserve)>(sym("cuMemAddressReserve"));
+    r.create = reinterpret_cast<decltype(r.create)>(sym("cuMemCreate"));
+    r.map = reinterpret_cast<decltype(r.map)>(sym("cuMemMap"));
+    r.access = reinterpret_cast<decltype(r.access)>(sym("cuMemSetAccess"));
+    r.unmap = reinterpret_cast<decltype(r.unmap)>(sym("cuMemUnmap"));
+    r.release = reinterpret_cast<decltype(r.release)>(sym("cuMemRelease"));
+    r.addr_free = reinterpret_cast<decltype(r.addr_free)>(sym("cuMemAddressFree"));
+    return r;
+  }();
+  return v;
+}
+
+#define FMG_CU(expr)                                                                  \
+  do {                                                                                \
+    CUresult r_ = (expr);                                                             \
+    if (r_ != CUDA_SUCCESS) throw ::fmg::CudaError(std::string(#expr) + " failed"); \
+  } while (0)
+
+void* guarded_alloc(size_t bytes) {
+  int dev = 0;
+  FMG_CK(cudaGetDevice(&dev));
+  CUmemAllocationProp prop = {};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = dev;
+  size_t gran = 0;
+  const CuVmm& cu = cu_vmm();
+  FMG_CU(cu.gran(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM));
+  const size_t want = std::max<size_t>((bytes + 255) / 256 * 256, 256);
+  const size_t mapped = (want + gran - 1) / gran * gran;
+  GuardRec r{};
+  r.reserved = mapped + 2 * gran;
+  r.mapped = mapped;
+  FMG_CU(cu.reserve(&r.va, r.reserved, gran, 0, 0));
+  FMG_CU(cu.create(&r.h, mapped, &prop, 0));
+  FMG_CU(cu.map(r.va + gran, mapped, 0, r.h, 0));
+  CUmemAccessDesc acc = {};
+  acc.location = prop.location;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  FMG_CU(cu.access(r.va + gran, mapped, &acc, 1));
+  void* p = reinterpret_cast<void*>(r.va + gran + (mapped - want));  // ends at the guard page
+  std::lock_guard<std::mutex> lock(g_guard_mu);
+  g_guard[p] = r;
+  return p;
+}
+
+void guarded_free(void* p) {
+  GuardRec r;
+  {
+    std::lock_guard<std::mutex> lock(g_guard_mu);
+    auto it = g_guard.find(p);
+    if (it == g_guard.end()) return;
+    r = it->second;
+    g_guard.erase(it);
+  }
+  const CuVmm& cu = cu_vmm();
+  cu.unmap(r.va + (r.reserved - r.mapped) / 2, r.mapped);
+  cu.release(r.h);
+  cu.addr_free(r.va, r.reserved);
+}
+
+// Synchronous allocations of the index structures (lines, chunks, tables).
+cudaError_t dmalloc_v(void** p, size_t bytes) {
+  if (!guard_mode()) return cudaMalloc(p, bytes);
+  try {
+    *p = guarded_alloc(bytes);
+    return cudaSuccess;
+  } catch (...) {
+    return cudaErrorMemoryAllocation;
+  }
+}
+template <typename T>
+cudaError_t dmalloc(T** p, size_t bytes) {
+  return dmalloc_v(reinterpret_cast<void**>(p), bytes);
+}
+void dfree(void* p) {
+  if (!p) return;
+  if (!guard_mode()) {
+    cudaFree(p);
+    return;
+  }
+  cudaDeviceSynchronize();
+  guarded_free(p);
+}
+
+// Stream-ordered scratch / result allocations (pool-backed, cheap after warm-up).
+cudaError_t amalloc(void** p, size_t bytes, cudaStream_t s) {
+  if (!guard_mode()) return cudaMallocAsync(p, pool_bytes(bytes), s);
+  cudaStreamSynchronize(s);
+  return dmalloc_v(p, bytes);
+}
+void afree(void* p, cudaStream_t s) {
+  if (!p) return;
+  if (!guard_mode()) {
+    cudaFreeAsync(p, s);
+    return;
+  }
+  cudaDeviceSynchronize();
+  guarded_free(p);
+}
+
 template <typename T>
 struct DevBuf {
   T* ptr = nullptr;
   cudaStream_t stream = nullptr;
   DevBuf() = default;
   DevBuf(size_t count, cudaStream_t s) : stream(s) {
-    if (count) FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&ptr), pool_bytes(count * sizeof(T)), s));
+    if (count) FMG_CK(amalloc(reinterpret_cast<void**>(&ptr), count * sizeof(T), s));
   }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
@@ -88,7 +237,7 @@ struct DevBuf {
     return *this;
   }
   ~DevBuf() {
-    if (ptr) cudaFreeAsync(ptr, stream);
+    if (ptr) afree(ptr, stream);
   }
 };
 
@@ -322,7 +471,7 @@ uint32_t* build_chunks(const fmg_index* ix, const void* bucket_records, uint64_t
   const uint64_t chars = ns == 2 ? fmg::ChunkTraits<2>::kChars : fmg::ChunkTraits<4>::kChars;
   n_chunks = (ix->n + 1 + chars - 1) / chars;
   uint32_t* chunks = nullptr;
-  FMG_CK(cudaMalloc(&chunks, n_chunks * 32 * ns));
+  FMG_CK(dmalloc(&chunks, n_chunks * 32 * ns));
   uint64_t* staging = nullptr;
   const uint64_t nb = ix->n_buckets;
   cudaError_t e = cudaMalloc(&staging, nb * 64 + 64);
@@ -342,7 +491,7 @@ uint32_t* build_chunks(const fmg_index* ix, const void* bucket_records, uint64_t
     if (e == cudaSuccess) e = cudaMemcpy(&bad, err, 4, cudaMemcpyDeviceToHost);
     cudaFree(staging);
   }
-  if (e != cudaSuccess || bad) cudaFree(chunks);
+  if (e != cudaSuccess || bad) dfree(chunks);
   FMG_CK(e);
   FMG_REQUIRE(bad == 0, "bucket base does not fit 32 bits");
   return chunks;
@@ -492,7 +641,7 @@ PrefixTable prefix_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
     FMG_CK(cudaMemGetInfo(&free_b, &total_b));
     while (k > 1 && PrefixTable::off64(k + 1) * sizeof(uint2) > free_b / 4) --k;
     uint2* lut = nullptr;
-    FMG_CK(cudaMalloc(&lut, PrefixTable::off64(k + 1) * sizeof(uint2)));
+    FMG_CK(dmalloc(&lut, PrefixTable::off64(k + 1) * sizeof(uint2)));
     build_prefix_levels(ix, ix->view(), lut, k, s);
     FMG_CK(cudaStreamSynchronize(s));
     ix->lut = lut;
@@ -514,7 +663,7 @@ PrefixTable prefix_table_rev(const fmg_index* cix, uint64_t count, cudaStream_t 
     FMG_CK(cudaMemGetInfo(&free_b, &total_b));
     if (bytes > free_b / 3) return {};
     uint2* lut = nullptr;
-    FMG_CK(cudaMalloc(&lut, bytes));
+    FMG_CK(dmalloc(&lut, bytes));
     build_prefix_levels(ix, ix->view_rev(), lut, int(tf.k), s);
     FMG_CK(cudaStreamSynchronize(s));
     ix->lut_r = lut;
@@ -557,7 +706,7 @@ KmerTable kmer_table(const fmg_index* cix, uint64_t count, cudaStream_t s) {
       const uint64_t cnt = uint64_t(1) << (2 * kx);
       if (kx <= 16 && cnt * sizeof(uint2) <= available_bytes(ix->device) / 4) {
         uint2* lx = nullptr;
-        if (cudaMalloc(&lx, cnt * sizeof(uint2)) == cudaSuccess) {
+        if (dmalloc(&lx, cnt * sizeof(uint2)) == cudaSuccess) {
           // levels K + 1 .. kx, each from the previous; only the last is kept
           DevBuf<uint2> tmp[2];
           const uint2* parent = pt.base + PrefixTable::off64(pt.k);
@@ -685,11 +834,11 @@ void lease_epoch_table(fmg_index* ix, uint64_t entries, uint64_t epochs, cudaStr
   if (ix->ep_entries < entries) {
     if (ix->ep_table) {
       FMG_CK(cudaStreamSynchronize(s));  // no launch of this index may still use it (we hold the lease)
-      FMG_CK(cudaFree(ix->ep_table));
+      dfree(ix->ep_table);
       ix->ep_table = nullptr;
       ix->ep_entries = 0;
     }
-    FMG_CK(cudaMalloc(&ix->ep_table, entries * sizeof(uint4)));
+    FMG_CK(dmalloc(&ix->ep_table, entries * sizeof(uint4)));
     ix->ep_entries = entries;
     ix->ep_next = 0xFFFFFFFFull;  // forces the zeroing below
   }
@@ -746,9 +895,9 @@ void z1_collect(Z1Raw* raws, uint64_t n_raw, uint64_t count, cudaStream_t s, uns
   res->total = total;
   res->steps = st[0];
   res->lines = st[1];
-  FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->k), pool_bytes(std::max<uint64_t>(total, 1) * 4), s));
-  FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->l), pool_bytes(std::max<uint64_t>(total, 1) * 4), s));
-  FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->diffs), pool_bytes(std::max<uint64_t>(total, 1)), s));
+  FMG_CK(amalloc(reinterpret_cast<void**>(&res->k), std::max<uint64_t>(total, 1) * 4, s));
+  FMG_CK(amalloc(reinterpret_cast<void**>(&res->l), std::max<uint64_t>(total, 1) * 4, s));
+  FMG_CK(amalloc(reinterpret_cast<void**>(&res->diffs), std::max<uint64_t>(total, 1), s));
   k_z1_unique_write<<<unsigned((count + 255) / 256), 256, 0, s>>>(keys2.ptr, used2.ptr, seg.ptr, res->row_off,
                                                                   count, res->k, res->l, res->diffs);
   FMG_CK(cudaGetLastError());
@@ -875,8 +1024,8 @@ bool run_z1b(const fmg_index* ix, const BiIndex& bi, const CodePatterns& cp, uin
   k_z1_sort_unique<<<gq, 256, 0, s>>>(keys.ptr, used.ptr, seg.ptr, count, per_q.ptr);
   k_widen_counts<<<gq, 256, 0, s>>>(count, per_q.ptr, c64.ptr);
   FMG_CK(cub::DeviceScan::InclusiveSum(tmp.ptr, tb, c64.ptr, res->row_off + 1, count, s));
-  FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->kl), pool_bytes(raw_cap * 8), s));
-  FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->diffs), pool_bytes(raw_cap), s));
+  FMG_CK(amalloc(reinterpret_cast<void**>(&res->kl), raw_cap * 8, s));
+  FMG_CK(amalloc(reinterpret_cast<void**>(&res->diffs), raw_cap, s));
   k_z1_write_kl<<<gq, 256, 0, s>>>(keys.ptr, used.ptr, seg.ptr, res->row_off, count, res->kl, res->diffs);
   FMG_CK(cudaGetLastError());
   // ---- the one synchronisation: result count, work counters, overflow ----
@@ -891,8 +1040,8 @@ bool run_z1b(const fmg_index* ix, const BiIndex& bi, const CodePatterns& cp, uin
   if (trace) cudaEventRecord(ev[2], s);
   FMG_CK(cudaStreamSynchronize(s));
   if (info->n_raw > raw_cap) {  // overflow: drop these results, the DFS engine redoes the batch
-    cudaFreeAsync(res->kl, s);
-    cudaFreeAsync(res->diffs, s);
+    afree(res->kl, s);
+    afree(res->diffs, s);
     res->kl = nullptr;
     res->diffs = nullptr;
     return false;
@@ -924,7 +1073,7 @@ void pool_reserve(int device, size_t bytes, cudaStream_t s) {
   static std::mutex mu;
   static std::unordered_map<int, bool> done;
   std::lock_guard<std::mutex> lock(mu);
-  if (done[device]) return;
+  if (done[device] || guard_mode()) return;
   done[device] = true;
   if (const char* e = std::getenv("FMG_POOL_RESERVE_GB")) bytes = size_t(std::atof(e) * double(size_t(1) << 30));
   if (bytes == 0) return;
@@ -949,7 +1098,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
   res->device = ix->device;
   res->patterns = count;
   try {
-    FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->row_off), pool_bytes((count + 1) * sizeof(uint64_t)), s));
+    FMG_CK(amalloc(reinterpret_cast<void**>(&res->row_off), (count + 1) * sizeof(uint64_t), s));
     FMG_CK(cudaMemsetAsync(res->row_off, 0, sizeof(uint64_t), s));
     if (count == 0) {
       FMG_CK(cudaStreamSynchronize(s));
@@ -1389,9 +1538,9 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     res->total = total;
     res->steps = work[0];
     res->lines = work[1];
-    FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->k), pool_bytes(std::max<uint64_t>(total, 1) * sizeof(uint32_t)), s));
-    FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->l), pool_bytes(std::max<uint64_t>(total, 1) * sizeof(uint32_t)), s));
-    FMG_CK(cudaMallocAsync(reinterpret_cast<void**>(&res->diffs), pool_bytes(std::max<uint64_t>(total, 1)), s));
+    FMG_CK(amalloc(reinterpret_cast<void**>(&res->k), std::max<uint64_t>(total, 1) * sizeof(uint32_t), s));
+    FMG_CK(amalloc(reinterpret_cast<void**>(&res->l), std::max<uint64_t>(total, 1) * sizeof(uint32_t), s));
+    FMG_CK(amalloc(reinterpret_cast<void**>(&res->diffs), std::max<uint64_t>(total, 1), s));
     for (size_t p = 0; p < pass_kl.size(); ++p) {
       k_gather_matches<<<unsigned((count + 255) / 256), 256, 0, s>>>(count, res_off.ptr, res_cnt.ptr, res_pass.ptr,
                                                                      uint8_t(p), pass_kl[p].ptr, pass_d[p].ptr,
@@ -1463,8 +1612,8 @@ void pipeline_host(int device, uint64_t count, uint64_t chunk, size_t in_bytes_p
   std::vector<void*> din(kSlots, nullptr), dout(kSlots, nullptr);
   try {
     for (int i = 0; i < kSlots; ++i) {
-      FMG_CK(cudaMallocAsync(&din[i], std::max<size_t>(chunk * in_bytes_per, 1), st[i]));
-      FMG_CK(cudaMallocAsync(&dout[i], std::max<size_t>(chunk * out_bytes_per, 1), st[i]));
+      FMG_CK(amalloc(&din[i], std::max<size_t>(chunk * in_bytes_per, 1), st[i]));
+      FMG_CK(amalloc(&dout[i], std::max<size_t>(chunk * out_bytes_per, 1), st[i]));
     }
     uint64_t c = 0;
     for (uint64_t off = 0; off < count; off += chunk, ++c) {
@@ -1480,15 +1629,15 @@ void pipeline_host(int device, uint64_t count, uint64_t chunk, size_t in_bytes_p
   } catch (...) {
     for (int i = 0; i < kSlots; ++i) cudaStreamSynchronize(st[i]);
     for (int i = 0; i < kSlots; ++i) {
-      if (din[i]) cudaFreeAsync(din[i], st[i]);
-      if (dout[i]) cudaFreeAsync(dout[i], st[i]);
+      if (din[i]) afree(din[i], st[i]);
+      if (dout[i]) afree(dout[i], st[i]);
       cudaStreamSynchronize(st[i]);
     }
     throw;
   }
   for (int i = 0; i < kSlots; ++i) {
-    cudaFreeAsync(din[i], st[i]);
-    cudaFreeAsync(dout[i], st[i]);
+    afree(din[i], st[i]);
+    afree(dout[i], st[i]);
   }
 }
 
@@ -1519,7 +1668,7 @@ static uint8_t* upload_lines(fmg_index* ix, const void* bucket_records) {
   with_words(ix, [&](auto wt) {
     constexpr int W = decltype(wt)::value;
     ix->n_lines = (n_buckets * 128 + fmg::LineTraits<W>::kChars - 1) / fmg::LineTraits<W>::kChars;
-    FMG_CK(cudaMalloc(&lines, ix->n_lines * fmg::LineTraits<W>::kBytes));
+    FMG_CK(dmalloc(&lines, ix->n_lines * fmg::LineTraits<W>::kBytes));
     uint64_t* staging = nullptr;
     uint32_t* err = nullptr;
     FMG_CK(cudaMalloc(&staging, n_buckets * 64 + 64));
@@ -1532,10 +1681,10 @@ static uint8_t* upload_lines(fmg_index* ix, const void* bucket_records) {
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e == cudaSuccess) e = cudaMemcpy(&bad, err, sizeof(bad), cudaMemcpyDeviceToHost);
     cudaFree(staging);
-    if (e != cudaSuccess) cudaFree(lines);
+    if (e != cudaSuccess) dfree(lines);
     FMG_CK(e);
   });
-  if (bad != 0) cudaFree(lines);
+  if (bad != 0) dfree(lines);
   FMG_REQUIRE(bad == 0, "bucket base does not fit 32 bits");
   return lines;
 }
@@ -1602,7 +1751,7 @@ int fmg_index_set_reverse(fmg_index* ix, const void* bucket_records, uint64_t n_
     });
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpy(ix->tail, tail.ptr, sizeof(ix->tail), cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) cudaFree(rev);
+    if (e != cudaSuccess) dfree(rev);
     FMG_CK(e);
     ix->rev_lines.store(rev, std::memory_order_release);  // publishes rev_sentinel_row and tail too
   });
@@ -1630,9 +1779,9 @@ int fmg_index_set_samples(fmg_index* ix, const uint64_t* sa_samples, uint64_t co
     std::lock_guard<std::mutex> lock(ix->attach_mu);
     if (ix->samples.load(std::memory_order_acquire)) return;  // attached once; the index is immutable
     uint32_t* d = nullptr;
-    FMG_CK(cudaMalloc(&d, count * sizeof(uint32_t)));
+    FMG_CK(dmalloc(&d, count * sizeof(uint32_t)));
     const cudaError_t e = cudaMemcpy(d, s32.data(), count * sizeof(uint32_t), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) cudaFree(d);
+    if (e != cudaSuccess) dfree(d);
     FMG_CK(e);
     ix->n_samples = count;
     ix->samples.store(d, std::memory_order_release);
@@ -1660,14 +1809,14 @@ void fmg_index_destroy(fmg_index* ix) {
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(ix->device);
-  if (ix->lines) cudaFree(ix->lines);
-  if (ix->chunks) cudaFree(ix->chunks);
-  if (ix->lut) cudaFree(ix->lut);
-  if (ix->lut_r) cudaFree(ix->lut_r);
-  if (ix->lut_x) cudaFree(ix->lut_x);
-  if (ix->ep_table) cudaFree(ix->ep_table);
-  if (uint8_t* r = ix->rev_lines.load()) cudaFree(r);
-  if (uint32_t* sm = ix->samples.load()) cudaFree(sm);
+  dfree(ix->lines);
+  dfree(ix->chunks);
+  dfree(ix->lut);
+  dfree(ix->lut_r);
+  dfree(ix->lut_x);
+  dfree(ix->ep_table);
+  dfree(ix->rev_lines.load());
+  dfree(ix->samples.load());
   if (prev >= 0) cudaSetDevice(prev);
   delete ix;
 }
@@ -2015,11 +2164,11 @@ void fmg_matches_free(fmg_matches* m) {
   cudaGetDevice(&prev);
   cudaSetDevice(m->device);
   // pool allocations (run_inexact synchronised its stream before returning)
-  if (m->row_off) cudaFreeAsync(m->row_off, 0);
-  if (m->k) cudaFreeAsync(m->k, 0);
-  if (m->l) cudaFreeAsync(m->l, 0);
-  if (m->kl) cudaFreeAsync(m->kl, 0);
-  if (m->diffs) cudaFreeAsync(m->diffs, 0);
+  afree(m->row_off, 0);
+  afree(m->k, 0);
+  afree(m->l, 0);
+  afree(m->kl, 0);
+  afree(m->diffs, 0);
   if (prev >= 0) cudaSetDevice(prev);
   delete m;
 }
@@ -2198,6 +2347,27 @@ int fmg_bucket_nibble_trace_host(int device, const uint8_t* blocks, const uint32
     FMG_CK(cudaGetLastError());
     FMG_CK(cudaMemcpyAsync(trace, d_tr.ptr, count * 15 * 8, cudaMemcpyDeviceToHost, s));
     st.raise_if_set(s, "prefix_len outside [0, 128] or symbol code outside [0, 4)");
+  });
+}
+
+// Guard-mode self test (not part of include/fmgpu.h): reads one u32 past
+// the end of a guarded 1000-byte buffer.  Under FMG_GUARD=1 the read must
+// fault; *faulted = 1 when the launch reported an error.  The fault poisons
+// the CUDA context, so callers run this in a throwaway process.
+__global__ void k_guard_probe(const uint32_t* p, uint32_t idx, uint32_t* sink) { *sink = p[idx]; }
+
+int fmgx_guard_selftest(int device, int* faulted) {
+  return fmg::guard([&] {
+    FMG_REQUIRE(faulted != nullptr, "null argument");
+    fmg::DeviceScope scope(device);
+    uint32_t* buf = nullptr;
+    uint32_t* sink = nullptr;
+    FMG_CK(dmalloc(&buf, 1000));
+    FMG_CK(cudaMalloc(&sink, 4));
+    FMG_CK(cudaMemset(buf, 0, 1000));
+    k_guard_probe<<<1, 1>>>(buf, 250, sink);  // byte 1000..1003: first byte past the end
+    cudaError_t e = cudaDeviceSynchronize();
+    *faulted = e != cudaSuccess;
   });
 }
 

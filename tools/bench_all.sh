@@ -7,7 +7,7 @@ for c in config1 config0 config1h config2 config4 config3; do
   # enough steps for a timed region of tens of ms (config 0 steps are ~12 us each)
   steps=10; [ $c = config3 ] && steps=2; [ $c = config0 ] && steps=2000; [ $c = config2 ] && steps=50
   timeout 1500 python bench.py --config $c --steps $steps --warmup 3 --no-hbm-extra 2>gpurun_out/bench_$c.err | tail -1 >> $out
-  timeout 900 python bench.py --impl reference --config $c --steps 3 --warmup 3 2>gpurun_out/ref_$c.err | tail -1 >> $out
+  timeout 2400 python bench.py --impl reference --config $c --steps 3 --warmup 3 2>gpurun_out/ref_$c.err | tail -1 >> $out
 done
 python - <<'PY'
 import json
