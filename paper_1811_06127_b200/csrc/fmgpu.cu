@@ -147,7 +147,9 @@ void* guarded_alloc(size_t bytes) {
   size_t gran = 0;
   const CuVmm& cu = cu_vmm();
   FMG_CU(cu.gran(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM));
-  const size_t want = std::max<size_t>((bytes + 255) / 256 * 256, 256);
+  // 32-byte granularity keeps the 256-bit vector loads aligned; an access
+  // past the 32-byte-rounded end of the buffer faults
+  const size_t want = std::max<size_t>((bytes + 31) / 32 * 32, 32);
   const size_t mapped = (want + gran - 1) / gran * gran;
   GuardRec r{};
   r.reserved = mapped + 2 * gran;
@@ -2350,8 +2352,8 @@ int fmg_bucket_nibble_trace_host(int device, const uint8_t* blocks, const uint32
   });
 }
 
-// Guard-mode self test (not part of include/fmgpu.h): reads one u32 past
-// the end of a guarded 1000-byte buffer.  Under FMG_GUARD=1 the read must
+// Guard-mode self test (not part of include/fmgpu.h): reads the first u32
+// past the (32-byte-rounded) end of a guarded 1000-byte buffer.  Under FMG_GUARD=1 the read must
 // fault; *faulted = 1 when the launch reported an error.  The fault poisons
 // the CUDA context, so callers run this in a throwaway process.
 __global__ void k_guard_probe(const uint32_t* p, uint32_t idx, uint32_t* sink) { *sink = p[idx]; }
@@ -2365,7 +2367,7 @@ int fmgx_guard_selftest(int device, int* faulted) {
     FMG_CK(dmalloc(&buf, 1000));
     FMG_CK(cudaMalloc(&sink, 4));
     FMG_CK(cudaMemset(buf, 0, 1000));
-    k_guard_probe<<<1, 1>>>(buf, 250, sink);  // byte 1000..1003: first byte past the end
+    k_guard_probe<<<1, 1>>>(buf, 256, sink);  // bytes 1024..1027: the first word past the rounded end
     cudaError_t e = cudaDeviceSynchronize();
     *faulted = e != cudaSuccess;
   });
