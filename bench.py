@@ -358,6 +358,16 @@ REF_FULL = {"config0", "config1", "config1h", "config2"}
 REF_SAMPLE = {"config4": 1 << 22, "config3": 2_000}
 
 
+def mem_available() -> int:
+    try:
+        for ln in Path("/proc/meminfo").read_text().splitlines():
+            if ln.startswith("MemAvailable:"):
+                return int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
 def native_libs_mapped() -> list[str]:
     """Shared objects of this repo mapped into the current process."""
     try:
@@ -380,6 +390,12 @@ def run_reference(args, rank: int, world: int) -> None:
 
     wl = make_workload(args.config, 0)
     threads = cpu_threads()
+    need = 14 * wl.text.size  # fm_build.c: sa + rank + key (u32) + records + samples
+    avail = mem_available()
+    if avail and need > 0.8 * avail:
+        print(json.dumps({"impl": "reference", "unavailable": f"the oracle's index build needs ~{need >> 30} GiB, "
+                          f"{avail >> 30} GiB available on this host"}), flush=True)
+        return
     t_build = time.perf_counter()
     ox = orc.OracleIndex(orc.BuiltIndex(wl.text, threads))
     t_build = time.perf_counter() - t_build
