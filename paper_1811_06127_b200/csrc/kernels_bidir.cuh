@@ -113,6 +113,21 @@ __device__ __forceinline__ void children4(const IndexView& v, const PrefixTable&
 #ifndef FMG_BI_MINB
 #define FMG_BI_MINB 7  // resident blocks per SM the register budget is sized for
 #endif
+#ifndef FMG_BI_NODUP
+// Edit paths that spell the same string are expanded once.  Case A (node i,
+// string S = edited W[i+1..]): inserting b = W[i] after W[i] gives
+// W[0..i] W[i] S, which the match child's insertion of W[i] after W[i-1]
+// also gives, so for i >= 1 it is left to node i-1 (at i = 0 there is no
+// insertion before W[0]); skipping W[i] when W[i] == W[i-1] gives the string
+// that skipping W[i-1] after matching W[i] gives.  Case B mirrors it:
+// inserting b = W[j] before W[j] is left to node j+1 (after matching W[j]),
+// skipping W[j] when W[j] == W[j+1] is left to node j+1.  The deferred path
+// always exists (its lower-bound conditions are weaker, and if its match
+// child is empty so is the dropped string), both carry one difference, and
+// the result SET is unchanged — the reference's DFS reaches the same strings
+// along both paths and keeps one (search.py:128-134).
+#define FMG_BI_NODUP 1
+#endif
 
 #ifndef FMG_CHAIN_COND_LOW
 #define FMG_CHAIN_COND_LOW 1  // k_bchain: load the low line only when it differs from the high one
@@ -592,12 +607,14 @@ __global__ void __launch_bounds__(128, kOnly == 3 ? FMG_BI_MINB_B : (kOnly == 1 
       }
       const uint32_t ckey = 4u * cx, cdep = cy + 1u;
       push_if(ok_match && kw <= lw, i - 1, 1u, child_sh, child_sh ? want + ckey : kw, child_sh ? cdep : lw, 0u, 0u);
-      push_if(ok_prev, i - 1, 0u, csh, cx, cy, 0u, 0u);  // skip
+      const bool skip_ok = ok_prev && (!FMG_BI_NODUP || want != sym_at(i - 1));
+      push_if(skip_ok, i - 1, 0u, csh, cx, cy, 0u, 0u);  // skip
 #pragma unroll
       for (uint32_t b = 0; b < 4; ++b) {
         const bool ne = ck[b] <= cl[b];
         const uint32_t px = child_sh ? b + ckey : ck[b], py = child_sh ? cdep : cl[b];
-        push_if(ok_cur && ne, i, 0u, child_sh, px, py, 0u, 0u);                  // insert
+        const bool ins_ok = !FMG_BI_NODUP || b != want || at0;
+        push_if(ok_cur && ne && ins_ok, i, 0u, child_sh, px, py, 0u, 0u);        // insert
         push_if(ok_prev && ne && b != want, i - 1, 0u, child_sh, px, py, 0u, 0u);  // mismatch
       }
       cur_valid = false;
@@ -656,14 +673,15 @@ __global__ void __launch_bounds__(128, kOnly == 3 ? FMG_BI_MINB_B : (kOnly == 1 
     }
     // match: (j+1, 1); at the end it still expands for insertions after W[m-1]
     push_if(sw != 0u, j + 1, 1u, child_sh, kw, kw + sw - 1u, cz_of(w), cw_of(w));
-    push_if(!last, j + 1, 0u, csh, cx, cy, cz, cw);  // skip
+    push_if(!last && (!FMG_BI_NODUP || w != sym_at(j + 1)), j + 1, 0u, csh, cx, cy, cz, cw);  // skip
     const bool ins = j >= h + 1;                      // insertion after W[j-1], j-1 >= h
 #pragma unroll
     for (uint32_t b = 0; b < 4; ++b) {
       const bool ne = sz[b] != 0u;
       const uint32_t px = child_sh ? b + rkey : ck[b], py = child_sh ? rdep : cl[b];
       push_if(!last && ne && b != w, j + 1, 0u, child_sh, fk[b], fk[b] + sz[b] - 1u, px, py);  // mismatch
-      push_if(ins && ne, j, 0u, child_sh, fk[b], fk[b] + sz[b] - 1u, px, py);                  // insert
+      push_if(ins && ne && (!FMG_BI_NODUP || b != w), j, 0u, child_sh, fk[b], fk[b] + sz[b] - 1u, px,
+              py);  // insert
     }
     cur_valid = false;
   }
@@ -835,11 +853,12 @@ __global__ void __launch_bounds__(256) k_bspine(IndexView ix, BiIndex bi, CodePa
 #pragma unroll
       for (uint32_t b = 0; b < 4; ++b) {
         const bool ne = ck[b] <= cl[b];
-        e_ins |= (ok_cur && ne) ? (1u << b) : 0u;
+        e_ins |= (ok_cur && ne && (!FMG_BI_NODUP || b != want || at0)) ? (1u << b) : 0u;
         e_mis |= (ok_prev && ne && b != want) ? (1u << b) : 0u;
       }
-      uint64_t slot = warp_reserve(qu.n_nodes, (ok_prev ? 1u : 0u) + __popc(e_ins) + __popc(e_mis));
-      node(ok_prev, uint32_t(i - 1) | (sh ? 0x20000u : 0u), x, y, 0u, 0u, slot);  // skip
+      const bool skip_ok = ok_prev && (!FMG_BI_NODUP || want != pat_sym(pw0, pw1, i - 1));
+      uint64_t slot = warp_reserve(qu.n_nodes, (skip_ok ? 1u : 0u) + __popc(e_ins) + __popc(e_mis));
+      node(skip_ok, uint32_t(i - 1) | (sh ? 0x20000u : 0u), x, y, 0u, 0u, slot);  // skip
 #pragma unroll
       for (uint32_t b = 0; b < 4; ++b) {
         const uint32_t px = child_sh ? b + 4u * x : ck[b], py = child_sh ? y + 1u : cl[b];
@@ -937,11 +956,12 @@ __global__ void __launch_bounds__(256) k_bspine(IndexView ix, BiIndex bi, CodePa
       uint32_t e_ins = 0, e_mis = 0;
 #pragma unroll
       for (uint32_t b = 0; b < 4; ++b) {
-        e_ins |= (ins && sz[b]) ? (1u << b) : 0u;
+        e_ins |= (ins && sz[b] && (!FMG_BI_NODUP || b != w)) ? (1u << b) : 0u;
         e_mis |= (!last && sz[b] && b != w) ? (1u << b) : 0u;
       }
-      uint64_t slot = warp_reserve(qu.n_nodes, (last ? 0u : 1u) + __popc(e_ins) + __popc(e_mis));
-      node(!last, uint32_t(j + 1) | 0x10000u | (sh ? 0x20000u : 0u), fx, fy, rz, rw, slot);  // skip
+      const bool skip_ok = !last && (!FMG_BI_NODUP || w != pat_sym(pw0, pw1, j + 1));
+      uint64_t slot = warp_reserve(qu.n_nodes, (skip_ok ? 1u : 0u) + __popc(e_ins) + __popc(e_mis));
+      node(skip_ok, uint32_t(j + 1) | 0x10000u | (sh ? 0x20000u : 0u), fx, fy, rz, rw, slot);  // skip
 #pragma unroll
       for (uint32_t b = 0; b < 4; ++b) {
         const uint32_t pz = child_sh ? b + 4u * rz : ck[b], pw = child_sh ? rw + 1u : cl[b];
