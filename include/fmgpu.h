@@ -156,6 +156,8 @@ int fmg_matches_steps(const fmg_matches* m, uint64_t* steps);
  * to_host != 0: destination pointers are host memory, else device memory. */
 int fmg_matches_copy(const fmg_matches* m, uint64_t* row_offsets, uint32_t* k, uint32_t* l,
                      uint8_t* diffs, int to_host);
+/* Releases the result buffers, stream-ordered on the stream the search ran on
+ * (that stream must still exist). */
 void fmg_matches_free(fmg_matches* m);
 
 /* ---------------------------------------------------------------------------

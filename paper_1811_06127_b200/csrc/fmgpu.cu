@@ -1051,7 +1051,6 @@ bool run_z1b(const fmg_index* ix, const BiIndex& bi, const CodePatterns& cp, uin
   res->total = info->total;
   res->steps = info->steps;
   res->lines = info->lines;
-  res->stream = s;
   if (trace) {
     float a = 0, b = 0;
     cudaEventElapsedTime(&a, ev[0], ev[1]);
@@ -1098,6 +1097,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
   if (count >= (1u << 16)) pool_reserve(ix->device, std::min<size_t>(available_bytes(ix->device) / 4, size_t(32) << 30), s);
   auto* res = new fmg_matches();
   res->device = ix->device;
+  res->stream = s;  // the result buffers are pool allocations of this stream: freed on it too
   res->patterns = count;
   try {
     FMG_CK(amalloc(reinterpret_cast<void**>(&res->row_off), (count + 1) * sizeof(uint64_t), s));
@@ -2166,11 +2166,14 @@ void fmg_matches_free(fmg_matches* m) {
   cudaGetDevice(&prev);
   cudaSetDevice(m->device);
   // pool allocations (run_inexact synchronised its stream before returning)
-  afree(m->row_off, 0);
-  afree(m->k, 0);
-  afree(m->l, 0);
-  afree(m->kl, 0);
-  afree(m->diffs, 0);
+  // stream-ordered frees on the stream the search allocated on: the pool
+  // reuses the blocks for that stream's next call without any cross-stream
+  // dependency (freeing on the legacy stream made the next call map memory)
+  afree(m->row_off, m->stream);
+  afree(m->k, m->stream);
+  afree(m->l, m->stream);
+  afree(m->kl, m->stream);
+  afree(m->diffs, m->stream);
   if (prev >= 0) cudaSetDevice(prev);
   delete m;
 }
