@@ -474,9 +474,16 @@ def config_of(config: str, world: int, units: int) -> dict:
         "config3": "BASELINE configs[3]: 3.1 Gbp family genome (seed 11), 10M x 150 bp reads, 14 x 19 bp seeds "
                    "per read, exact + z=1 on every seed",
     }[config]
-    return {"workload": desc, "units_per_step_per_rank": units, "parallelism": f"query-sharded x{world}",
-            "l2": "inputs larger than L2 (no flush)" if config != "config0" else
-                  "inputs smaller than L2; index L2-resident"}
+    l2 = {
+        "config1": "no flush: the 640 MiB of pairs in + counts out per step exceed L2; the 8.4 MB index is "
+                   "L2-resident by design (the roofline is the L2 random-read ceiling)",
+        "config1h": "no flush: pairs + counts (640 MiB) and the 308 MB chunk layout of the index exceed L2",
+        "config0": "inputs smaller than L2; the 1 Mbp index is L2-resident",
+        "config2": "no flush: the 32 MB index lines are L2-resident, patterns + results stream",
+        "config3": "no flush: the 3.1 Gbp index (1.55 GB of lines) and 140M seeds exceed L2",
+        "config4": "no flush: the 1 Gbp index (500 MB of lines) and 2^28 seeds exceed L2",
+    }[config]
+    return {"workload": desc, "units_per_step_per_rank": units, "parallelism": f"query-sharded x{world}", "l2": l2}
 
 
 # ---------------------------------------------------------------------------

@@ -1133,13 +1133,32 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       k_pack_patterns<<<unsigned((count + 255) / 256), 256, 0, s>>>(codes, offsets, count, packed.ptr);
       FMG_CK(cudaGetLastError());
     }
+    // shallow DFS nodes step through the prefix table (FMG_INEXACT_LUT=0: off, A/B)
+    const bool lut_off = [] {
+      const char* e = std::getenv("FMG_INEXACT_LUT");
+      return e != nullptr && std::atoi(e) == 0;
+    }();
+    const PrefixTable pt = lut_off ? PrefixTable{} : prefix_table(ix, count, s);
     DevBuf<uint64_t> dbits(short_pat ? count : 0, s);
     if (short_pat) {
       CodePatterns cpd{codes, offsets, packed.ptr, packed1, uint32_t(max_len)};
+      // the lower-bound pass resolves each present run's first Kt characters
+      // with one table gather (absent runs: a binary search over the levels)
+      // instead of Kt dependent Occ steps; the level-(K + 1) table joins in
+      // when it is the exact search's table
+      const uint2* tx = nullptr;
+      uint32_t kx = 0;
+      {
+        std::lock_guard<std::mutex> lock(const_cast<fmg_index*>(ix)->lut_mu);
+        if (pt.base && ix->lut_x && ix->lut_x_k == pt.k + 1) {
+          tx = ix->lut_x;
+          kx = ix->lut_x_k;
+        }
+      }
       with_words(ix, [&](auto wt) {
         constexpr int W = decltype(wt)::value;
         k_dbound<W><<<unsigned((count + 255) / 256), 256, 0, s>>>(ix->view(), cpd, count, dbits.ptr,
-                                                                    counters.ptr + 2);
+                                                                    counters.ptr + 2, pt, tx, kx);
       });
       FMG_CK(cudaGetLastError());
     }
@@ -1163,12 +1182,6 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       if (run_z1(ix, cpz, count, max_len, s, counters.ptr + 2, res)) return res;
       // queues overflowed: fall through to the DFS engine (same results)
     }
-    // shallow DFS nodes step through the prefix table (FMG_INEXACT_LUT=0: off, A/B)
-    const bool lut_off = [] {
-      const char* e = std::getenv("FMG_INEXACT_LUT");
-      return e != nullptr && std::atoi(e) == 0;
-    }();
-    const PrefixTable pt = lut_off ? PrefixTable{} : prefix_table(ix, count, s);
     // z = 1 with a reverse index attached: the bidirectional engine for the
     // first pass (FMG_INEXACT_BIDIR=0: off, A/B); retries use the DFS engine.
     const bool bidir_off = [] {

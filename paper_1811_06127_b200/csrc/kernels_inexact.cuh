@@ -19,7 +19,8 @@ namespace fmg {
 // one phase.
 template <int W>
 __global__ void __launch_bounds__(256) k_dbound(IndexView ix, CodePatterns cp, uint64_t count,
-                                                uint64_t* __restrict__ dbits_out, unsigned long long* steps) {
+                                                uint64_t* __restrict__ dbits_out, unsigned long long* steps,
+                                                PrefixTable pt, const uint2* __restrict__ tx, uint32_t kx) {
   const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (q >= count) return;
   uint64_t pw0, pw1;
@@ -35,44 +36,87 @@ __global__ void __launch_bounds__(256) k_dbound(IndexView ix, CodePatterns cp, u
     m = int(cp.offsets[q + 1] - cp.offsets[q]);
   }
   constexpr uint32_t kC = LineTraits<W>::kChars;
+  // Table depth: prefix levels 1..pt.k, plus level kx = pt.k + 1 when given.
+  const int Kt = pt.base ? int(tx ? kx : pt.k) : 0;
+  auto gather = [&](int len, int a) -> uint2 {  // interval of W[a .. a+len-1] (first empty one if absent)
+    uint64_t x = pw0, y = pw1;
+    const uint32_t sh = uint32_t(2 * a);
+    uint64_t lo, mid, hi;  // 128-bit funnel shift (counts >= 64 give 0, see pat_key)
+    asm("shr.b64 %0, %1, %2;" : "=l"(lo) : "l"(x), "r"(sh));
+    asm("shl.b64 %0, %1, %2;" : "=l"(mid) : "l"(y), "r"(64u - sh));
+    asm("shr.b64 %0, %1, %2;" : "=l"(hi) : "l"(y), "r"(sh - 64u));
+    const uint32_t key = uint32_t((lo | mid | hi) & ((uint64_t(1) << (2 * len)) - 1u));
+    return len > int(pt.k) ? __ldg(tx + key) : __ldg(pt.base + PrefixTable::off(uint32_t(len)) + key);
+  };
   uint64_t bits = 0;
-  uint32_t k = 0, l = ix.n;
-  int seg_end = m - 1;
   uint64_t work = 0;
-  for (int pos = m - 1; pos >= 0; --pos) {
-    const uint32_t b = uint32_t((pos < 32 ? pw0 : pw1) >> ((pos & 31) << 1)) & 3u;
-    const uint32_t cb = c_of(ix, b);
-    uint32_t k2, l2;
-    if (k == 0u && l == ix.n) {  // root: init_interval, no memory
-      k2 = cb + 1u;
-      l2 = c_of(ix, b + 1u);
-    } else {
-      const uint32_t low = k - 1u;
-      const uint32_t jh = line_of<W>(l), jl = line_of<W>(low);
-      const uint32_t rh = l - jh * kC, rl = low - jl * kC;
-      uint32_t bh[4], bl[4];
-      uint64_t wh[W], wl[W];
-      load_line<W, false>(ix, jh, rh, bh, wh);
-      uint32_t ol;
-      if (jl != jh) {
-        load_line<W, false>(ix, jl, rl, bl, wl);
-        ol = occ1_from_line<W>(ix, bl, wl, low, rl, b);
+  int seg_end = m - 1;
+  while (seg_end >= 0) {
+    // the run W[pos+1 .. seg_end] is present with interval (k, l); (0, n) = empty run
+    uint32_t k = 0, l = ix.n;
+    int pos = seg_end;
+    if (Kt > 0) {
+      // the longest run the tables cover in ONE gather; absent: binary search
+      // for the shortest absent suffix (presence is monotone in the length)
+      const int L = min(Kt, seg_end + 1);
+      const uint2 e = gather(L, seg_end - L + 1);
+      work += work_unit(1u);
+      if (e.x <= e.y) {
+        k = e.x;
+        l = e.y;
+        pos = seg_end - L;
       } else {
-        ol = occ1_from_line<W>(ix, bh, wh, low, rl, b);
+        int lo = 0, hi = L;  // suffix of length lo present, hi absent
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          const uint2 f = gather(mid, seg_end - mid + 1);
+          work += work_unit(1u);
+          if (f.x <= f.y)
+            lo = mid;
+          else
+            hi = mid;
+        }
+        bits |= 1ull << seg_end;  // W[seg_end-hi+1 .. seg_end] is absent
+        seg_end -= hi;
+        continue;
       }
-      k2 = cb + ol + 1u;
-      l2 = cb + occ1_from_line<W>(ix, bh, wh, l, rh, b);
-      work += work_unit(jl != jh ? 2u : 1u);
     }
-    if (k2 > l2) {  // W[pos..seg_end] is absent from the text
-      bits |= 1ull << seg_end;
-      k = 0;
-      l = ix.n;
-      seg_end = pos - 1;
-    } else {
+    bool reset = false;
+    for (; pos >= 0; --pos) {
+      const uint32_t b = uint32_t((pos < 32 ? pw0 : pw1) >> ((pos & 31) << 1)) & 3u;
+      const uint32_t cb = c_of(ix, b);
+      uint32_t k2, l2;
+      if (k == 0u && l == ix.n) {  // root: init_interval, no memory
+        k2 = cb + 1u;
+        l2 = c_of(ix, b + 1u);
+      } else {
+        const uint32_t low = k - 1u;
+        const uint32_t jh = line_of<W>(l), jl = line_of<W>(low);
+        const uint32_t rh = l - jh * kC, rl = low - jl * kC;
+        uint32_t bh[4], bl[4];
+        uint64_t wh[W], wl[W];
+        load_line<W, false>(ix, jh, rh, bh, wh);
+        uint32_t ol;
+        if (jl != jh) {
+          load_line<W, false>(ix, jl, rl, bl, wl);
+          ol = occ1_from_line<W>(ix, bl, wl, low, rl, b);
+        } else {
+          ol = occ1_from_line<W>(ix, bh, wh, low, rl, b);
+        }
+        k2 = cb + ol + 1u;
+        l2 = cb + occ1_from_line<W>(ix, bh, wh, l, rh, b);
+        work += work_unit(jl != jh ? 2u : 1u);
+      }
+      if (k2 > l2) {  // W[pos..seg_end] is absent from the text
+        bits |= 1ull << seg_end;
+        seg_end = pos - 1;
+        reset = true;
+        break;
+      }
       k = k2;
       l = l2;
     }
+    if (!reset) break;  // the run reached the pattern's left end
   }
   dbits_out[q] = bits;
   flush_work(steps, work);
