@@ -19,7 +19,7 @@ LIB_PATH = PKG_DIR / "libfmgpu.so"
 
 SOURCES = ["fmgpu.cu", "build_gpu.cu", "builder.cpp"]
 HEADERS = ["fmgpu_internal.h", "occ_device.cuh", "kernels_occ.cuh", "kernels_search.cuh", "kernels_inexact.cuh",
-           "kernels_bidir.cuh", "kernels_bucket.cuh", "kernels_chunk.cuh"]
+           "kernels_bidir.cuh", "kernels_flat.cuh", "kernels_bucket.cuh", "kernels_chunk.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

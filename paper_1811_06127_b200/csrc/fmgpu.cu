@@ -6,6 +6,8 @@
 //   kernels_search.cuh   k_exact, k_psi, k_locate              (search.py:74-94, 172-208)
 //   kernels_inexact.cuh  k_dbound, k_inexact (DFS), k_spine / k_chain (z = 1),
 //                        sort / dedup / gather                 (search.py:97-159)
+//   kernels_bidir.cuh    bidirectional z = 1 engines (split DFS, level-synchronous)
+//   kernels_flat.cuh     k_z1_flat: one warp per pattern over its one-edit neighbourhood
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -249,6 +251,7 @@ struct DevBuf {
 #include "kernels_search.cuh"
 #include "kernels_inexact.cuh"
 #include "kernels_bidir.cuh"
+#include "kernels_flat.cuh"
 #include "kernels_bucket.cuh"
 #include "kernels_chunk.cuh"
 
@@ -1087,6 +1090,11 @@ void pool_reserve(int device, size_t bytes, cudaStream_t s) {
   FMG_CK(cudaStreamSynchronize(s));
 }
 
+// The flat z = 1 engine is the default while the pattern is at most this many
+// characters longer than the deepest table level (each extra character is
+// one more dependent step for the candidates still alive).
+constexpr uint64_t kFlatTail = 6;
+
 fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64_t* offsets, uint64_t count,
                          uint64_t max_len, int max_diff, cudaStream_t s, const uint64_t* packed1 = nullptr) {
   FMG_REQUIRE(max_diff >= 0, "difference budget is negative");
@@ -1170,13 +1178,39 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     // split engine below beats both (config 2: 9.4 -> 6.4 ms per 1M seeds).
     const bool force_dfs = std::getenv("FMG_INEXACT_DFS") != nullptr;  // read per call (tests flip it)
     const bool has_rev = ix->rev_lines.load(std::memory_order_acquire) != nullptr;
+    const std::string engine_env = [] {  // read per call (tests flip it)
+      const char* e = std::getenv("FMG_BIDIR_ENGINE");
+      return std::string(e ? e : "");
+    }();
     const bool bidir_off_env = [] {
       const char* e = std::getenv("FMG_INEXACT_BIDIR");
       return e != nullptr && std::atoi(e) == 0;
     }();
     uint64_t line_bytes = 0;
     with_words(ix, [&](auto wt) { line_bytes = ix->n_lines * fmg::LineTraits<decltype(wt)::value>::kBytes; });
-    if (z == 1 && short_pat && !force_dfs && line_bytes <= (uint64_t(64) << 20) &&
+    // z = 1, patterns a few characters longer than the deepest table level,
+    // HBM-resident index: the flat engine (kernels_flat.cuh) — every string
+    // of the one-edit neighbourhood is one table gather plus at most
+    // m + 1 - kmax backward steps, a warp per pattern, no reverse index.
+    // Config 3 (m = 19, level 16): 113 -> see profiles/r02_flat.md.
+    // FMG_BIDIR_ENGINE=flat forces it (any size, m <= 31), any other value
+    // keeps it off.
+    const uint2* flat_tx = nullptr;
+    uint32_t flat_kx = 0;
+    bool use_flat = false;
+    if (z == 1 && short_pat && max_len <= 31 && pt.base && !force_dfs &&
+        (engine_env == "flat" || (engine_env.empty() && line_bytes > (uint64_t(64) << 20)))) {
+      if (exact_table_level(ix, pt) == pt.k + 1) {
+        const KmerTable kt = kmer_table(ix, count, s);
+        if (kt.lut && kt.k == pt.k + 1) {
+          flat_tx = kt.lut;
+          flat_kx = kt.k;
+        }
+      }
+      const uint32_t kmax = flat_tx ? flat_kx : pt.k;
+      use_flat = engine_env == "flat" || max_len <= uint64_t(kmax) + kFlatTail;
+    }
+    if (z == 1 && short_pat && !force_dfs && !use_flat && line_bytes <= (uint64_t(64) << 20) &&
         (!has_rev || bidir_off_env)) {
       CodePatterns cpz{codes, offsets, packed.ptr, packed1, uint32_t(max_len), dbits.ptr};
       if (run_z1(ix, cpz, count, max_len, s, counters.ptr + 2, res)) return res;
@@ -1190,7 +1224,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     }();
     BiIndex bi{};
     bool bidir = false;
-    if (z == 1 && short_pat && has_rev && pt.base && !bidir_off) {
+    if (z == 1 && short_pat && has_rev && pt.base && !bidir_off && !use_flat) {
       bi.rev = ix->view_rev();
       bi.tf = pt;
       bi.tr = prefix_table_rev(ix, count, s);
@@ -1216,10 +1250,8 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     // is L2-resident: config 2 5.9 -> 3.6 ms per 1M seeds, while on config 3
     // its queued continuations re-fetch from DRAM), "dfs" (both cases per
     // thread); FMG_BIDIR_ENGINE selects.
-    const std::string bidir_engine = [&] {
-      const char* e = std::getenv("FMG_BIDIR_ENGINE");
-      return std::string(e ? e : line_bytes <= (uint64_t(64) << 20) ? "sync" : "split");
-    }();
+    const std::string bidir_engine =
+        !engine_env.empty() ? engine_env : line_bytes <= (uint64_t(64) << 20) ? "sync" : "split";
     const bool bidir_dfs = bidir_engine == "dfs";
     bool bidir_split = bidir && bidir_engine == "split";
     if (bidir && bidir_engine == "sync") {
@@ -1263,6 +1295,84 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     if (const char* e = std::getenv("FMG_STACK_S")) S = std::max<uint32_t>(2, uint32_t(std::atoi(e)));  // A/B
     int first_pass = 0;
     DevBuf<uint32_t> retry_list;
+    if (use_flat) {
+      // ---- pass 0 = the flat engine; patterns that do not fit this pass's
+      // result buffer are retried by the DFS engine below ----
+      const int nt = 128;
+      const int nr = max_len <= 11 ? 3 : max_len <= 19 ? 5 : 8;  // 32 nr >= 8 m + 1
+      const void* kf = nullptr;
+      size_t smem = 0;
+      auto pick = [&](auto wt, auto nrt) {
+        constexpr int W = decltype(wt)::value;
+        constexpr int NR = decltype(nrt)::value;
+        kf = (const void*)k_z1_flat<W, NR>;
+        smem = size_t(nt / 32) * FlatSmem<NR>::words_per_warp * 4;
+      };
+      with_words(ix, [&](auto wt) {
+        if (nr == 3) pick(wt, std::integral_constant<int, 3>{});
+        else if (nr == 5) pick(wt, std::integral_constant<int, 5>{});
+        else pick(wt, std::integral_constant<int, 8>{});
+      });
+      FMG_CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      int per_sm = 0;
+      FMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, nt, smem));
+      per_sm = std::max(per_sm, 1);
+      const uint64_t warps_wanted = count;  // one pattern per warp at a time
+      const unsigned blocks = unsigned(std::max<uint64_t>(
+          1, std::min<uint64_t>(uint64_t(per_sm) * ix->sms, (warps_wanted + nt / 32 - 1) / (nt / 32))));
+      pass_kl.emplace_back(cap, s);
+      pass_d.emplace_back(cap, s);
+      FMG_CK(cudaMemsetAsync(counters.ptr, 0, 2 * sizeof(unsigned long long), s));
+      FMG_CK(cudaMemsetAsync(counters.ptr + 4, 0, sizeof(unsigned long long), s));
+      InexactOut o{};
+      o.kl = pass_kl.back().ptr;
+      o.diffs = pass_d.back().ptr;
+      o.total = counters.ptr;
+      o.cap = cap;
+      o.res_off = res_off.ptr;
+      o.res_cnt = res_cnt.ptr;
+      o.res_pass = res_pass.ptr;
+      o.pass = 0;
+      o.fail_list = lists[0].ptr;
+      o.fail_count = counters.ptr + 1;
+      o.steps = counters.ptr + 2;
+      o.next = counters.ptr + 4;
+      o.unsorted = counters.ptr + 5;
+      o.unsorted_list = unsorted_list.ptr;
+      CodePatterns cp{codes, offsets, packed.ptr, packed1, uint32_t(max_len), dbits.ptr};
+      static const bool trace_flat = std::getenv("FMG_TRACE") != nullptr;
+      cudaEvent_t fe[2] = {};
+      if (trace_flat) {
+        for (auto& e : fe) cudaEventCreate(&e);
+        cudaEventRecord(fe[0], s);
+      }
+      with_words(ix, [&](auto wt) {
+        constexpr int W = decltype(wt)::value;
+        if (nr == 3)
+          k_z1_flat<W, 3><<<blocks, nt, smem, s>>>(ix->view(), pt, flat_tx, flat_kx, cp, nullptr, count, o);
+        else if (nr == 5)
+          k_z1_flat<W, 5><<<blocks, nt, smem, s>>>(ix->view(), pt, flat_tx, flat_kx, cp, nullptr, count, o);
+        else
+          k_z1_flat<W, 8><<<blocks, nt, smem, s>>>(ix->view(), pt, flat_tx, flat_kx, cp, nullptr, count, o);
+      });
+      FMG_CK(cudaGetLastError());
+      unsigned long long host_ctr[2];
+      FMG_CK(cudaMemcpyAsync(host_ctr, counters.ptr, sizeof(host_ctr), cudaMemcpyDeviceToHost, s));
+      if (trace_flat) cudaEventRecord(fe[1], s);
+      FMG_CK(cudaStreamSynchronize(s));
+      if (trace_flat) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, fe[0], fe[1]);
+        fprintf(stderr, "[fmg] flat z=1 engine: %llu patterns, NR=%d, %u blocks (%d per SM, %zu B smem): %.3f ms, "
+                "%llu results, %llu retried\n", (unsigned long long)count, nr, blocks, per_sm, smem, ms, host_ctr[0],
+                host_ctr[1]);
+        for (auto& e : fe) cudaEventDestroy(e);
+      }
+      list = lists[0].ptr;
+      pending = host_ctr[1];
+      first_pass = 1;
+      if (pending > 0) cap = std::max<uint64_t>(cap, std::min<uint64_t>(pending * 256, 1ull << 31));
+    }
     if (bidir_split) {
       // ---- pass 0 = case-A launch + case-B launch + merge (kernels_bidir.cuh) ----
       const uint32_t Sp = 9;  // z = 1: one budget-1 node's children at a time

@@ -1,0 +1,363 @@
+// Flat z = 1 engine for the bounded-difference search (search.py:97-159):
+// the one-edit neighbourhood of each pattern enumerated candidate by
+// candidate, one WARP per pattern.  Part of libfmgpu.so (sm_100a); included
+// once by fmgpu.cu after kernels_inexact.cuh.
+//
+// For z = 1 the reference's DFS reports (interval(S), diffs) for every string
+// S within one edit of W that occurs in the text — W itself (diffs 0), a
+// substitution or deletion at i in [0, m-1], an insertion after W[i], i in
+// [0, m-1] (never before W[0]) — equal intervals keeping the smallest diffs;
+// the visiting order is free (kernels_bidir.cuh).  When the
+// pattern is only a few characters longer than the deepest k-mer table level
+// (config 3: m = 19 against level 16), walking a tree shares almost nothing:
+// every candidate string is ONE gather of its last min(L, kmax) characters
+// away from a nearly final answer, and the gathers of different candidates
+// are independent.  So instead of a per-thread DFS (8 of 32 lanes active,
+// ~1 request in flight per thread) a warp takes a pattern, its lanes take the
+// 8m + 1 candidates (8 per position: 4 insertions, 3 substitutions, 1
+// deletion; plus W), each lane issues all its gathers back to back, and the
+// candidates still alive (about half at level 16 of a 3.1 Gbp text) are
+// compacted through shared memory and extended level by level — every lane
+// active at every level — with one-symbol Occ steps on the index lines.
+// Results are collected, sorted by (k, l) and deduplicated in shared memory;
+// one atomic per pattern reserves the output rows.  No reverse index, no
+// per-thread hash table, no merge pass.
+//
+// Pruning (result-preserving, same bound as the DFS engines): dbits marks the
+// right ends of disjoint absent segments of W (k_dbound).  Two segments: no
+// string within one edit occurs.  A substitution / deletion at i keeps
+// W[0..i-1] verbatim, an insertion after W[i] keeps W[0..i]: a marked segment
+// inside that prefix rules the candidate out.  Duplicate spellings are
+// enumerated once: inserting W[i] after W[i] (i >= 1) equals inserting it
+// after W[i-1]; deleting W[i] equals deleting W[i-1] when they are equal.
+#pragma once
+
+#include <cstdint>
+
+#include "kernels_inexact.cuh"
+#include "occ_device.cuh"
+
+namespace fmg {
+
+__device__ __forceinline__ uint64_t shl64(uint64_t x, uint32_t n) {  // PTX clamps n >= 64 to 0
+  uint64_t r;
+  asm("shl.b64 %0, %1, %2;" : "=l"(r) : "l"(x), "r"(n));
+  return r;
+}
+__device__ __forceinline__ uint64_t shr64(uint64_t x, uint32_t n) {
+  uint64_t r;
+  asm("shr.b64 %0, %1, %2;" : "=l"(r) : "l"(x), "r"(n));
+  return r;
+}
+
+// one table entry, no reuse expected: 64-byte DRAM fetch, no L1 allocation
+__device__ __forceinline__ uint2 ld_table_entry(const uint2* p) {
+  uint2 v;
+  asm("ld.global.nc.L1::no_allocate.L2::64B.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+
+// Candidate c of pattern pw (m characters, character t in bits 2t..2t+1):
+// c = 8i + s, s = 0..3 insertion of s after W[i], s = 4..6 substitution of
+// W[i] by (W[i] + s - 3) & 3, s = 7 deletion of W[i]; c = 8m is W itself.
+// Returns the string S (L characters, same packing) and whether it has to be
+// searched at all.
+__device__ __forceinline__ bool flat_candidate(uint64_t pw, int m, uint64_t db, uint32_t c, uint64_t& S, int& L) {
+  if (c >= uint32_t(8 * m)) {
+    S = pw;
+    L = m;
+    return c == uint32_t(8 * m) && db == 0ull;
+  }
+  const uint32_t i = c >> 3, s = c & 7u;
+  const uint32_t wi = uint32_t(pw >> (2u * i)) & 3u;
+  const uint64_t hi = shr64(pw, 2u * i + 2u);                    // W[i+1..]
+  const bool prev_ok = (db & ((1ull << i) - 1ull)) == 0ull;     // no absent segment inside W[0..i-1]
+  const bool cur_ok = (db & ((2ull << i) - 1ull)) == 0ull;      // ... inside W[0..i]
+  if (s < 4u) {  // insertion of s after W[i]
+    S = (pw & ((4ull << (2u * i)) - 1ull)) | (uint64_t(s) << (2u * i + 2u)) | shl64(hi, 2u * i + 4u);
+    L = m + 1;
+    return cur_ok && (s != wi || i == 0u);
+  }
+  if (s < 7u) {  // substitution
+    const uint32_t b = (wi + s - 3u) & 3u;
+    S = pw ^ (uint64_t(wi ^ b) << (2u * i));
+    L = m;
+    return prev_ok;
+  }
+  S = (pw & ((1ull << (2u * i)) - 1ull)) | (hi << (2u * i));  // deletion
+  L = m - 1;
+  return prev_ok && !(i >= 1u && wi == (uint32_t(shr64(pw, 2u * i - 2u)) & 3u));
+}
+
+// Raw line data of one backward step at (k-1, l): the high line always, the
+// low line only when it is a different one (W = 2: predicated, no request).
+template <int W>
+struct StepLines {
+  uint32_t bh[4], bl[4];
+  uint64_t wh[W], wl[W];
+  uint32_t jh, jl;
+};
+
+template <int W>
+__device__ __forceinline__ void step_load(const IndexView& ix, bool go, uint32_t k, uint32_t l, StepLines<W>& sl) {
+  constexpr uint32_t kC = LineTraits<W>::kChars;
+  const uint32_t low = k - 1u;
+  sl.jh = line_of<W>(l);
+  sl.jl = line_of<W>(low);
+  if constexpr (W == 2) {
+    uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0, b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+    ld256_pred(go, ix.lines + size_t(sl.jh) * LineTraits<2>::kBytes, a0, a1, a2, a3);
+    ld256_pred(go && sl.jl != sl.jh, ix.lines + size_t(sl.jl) * LineTraits<2>::kBytes, b0, b1, b2, b3);
+    const bool same = sl.jl == sl.jh;
+    sl.bh[0] = uint32_t(a0), sl.bh[1] = uint32_t(a0 >> 32), sl.bh[2] = uint32_t(a1), sl.bh[3] = uint32_t(a1 >> 32);
+    sl.wh[0] = a2, sl.wh[1] = a3;
+    sl.bl[0] = same ? sl.bh[0] : uint32_t(b0);
+    sl.bl[1] = same ? sl.bh[1] : uint32_t(b0 >> 32);
+    sl.bl[2] = same ? sl.bh[2] : uint32_t(b1);
+    sl.bl[3] = same ? sl.bh[3] : uint32_t(b1 >> 32);
+    sl.wl[0] = same ? a2 : b2;
+    sl.wl[1] = same ? a3 : b3;
+  } else {
+    if (go) {
+      load_line<W, 0>(ix, sl.jh, l - sl.jh * kC, sl.bh, sl.wh);
+      load_line<W, 0>(ix, sl.jl, low - sl.jl * kC, sl.bl, sl.wl);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) sl.bh[t] = sl.bl[t] = 0u;
+#pragma unroll
+      for (int t = 0; t < W; ++t) sl.wh[t] = sl.wl[t] = 0ull;
+    }
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void step_finish(const IndexView& ix, const StepLines<W>& sl, uint32_t sym, uint32_t& k,
+                                            uint32_t& l) {
+  constexpr uint32_t kC = LineTraits<W>::kChars;
+  const uint32_t low = k - 1u;
+  const uint32_t cs = c_of(ix, sym);
+  const uint32_t k2 = cs + occ1_from_line<W>(ix, sl.bl, sl.wl, low, low - sl.jl * kC, sym) + 1u;
+  const uint32_t l2 = cs + occ1_from_line<W>(ix, sl.bh, sl.wh, l, l - sl.jh * kC, sym);
+  k = k2;
+  l = l2;
+}
+
+// NR = rounds of 32 candidates a lane takes (32 NR >= 8m + 1).  Shared
+// memory per warp, cap = 32 NR slots each: the continuation queue (k, l,
+// candidate | next position << 16), the results (k, l) and one flag word per
+// 32 results.  Only W itself carries diffs 0, so the diffs of a result are
+// "is it the exact one" (its index is kept in a register).
+#ifndef FMG_FLAT_MINB
+#define FMG_FLAT_MINB 8  // resident 128-thread blocks per SM the register budget is sized for
+#endif
+
+template <int NR>
+struct FlatSmem {
+  static constexpr uint32_t cap = 32u * NR;
+  static constexpr uint32_t words_per_warp = 5u * cap + NR;
+};
+
+template <int W, int NR>
+__global__ void __launch_bounds__(128, FMG_FLAT_MINB) k_z1_flat(IndexView ix, PrefixTable tf, const uint2* __restrict__ tx,
+                                                 uint32_t kx, CodePatterns cp, const uint32_t* __restrict__ list,
+                                                 uint64_t count, InexactOut out) {
+  extern __shared__ __align__(16) uint32_t flat_smem[];
+  constexpr uint32_t cap = FlatSmem<NR>::cap;
+  const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+  uint32_t* kq = flat_smem + wib * FlatSmem<NR>::words_per_warp;
+  uint32_t* lq = kq + cap;
+  uint32_t* xq = lq + cap;
+  uint32_t* kr = xq + cap;
+  uint32_t* lr = kr + cap;
+  uint32_t* repw = lr + cap;
+  const uint32_t K = tf.k, kmax = tx ? kx : K;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  uint64_t work = 0;
+
+  // the next pattern is claimed and loaded while the current one is searched
+  uint64_t nq_id = 0, npw = 0, ndb = 0;
+  int nm = 0;
+  bool nvalid = false;
+  auto prefetch = [&]() {
+    unsigned long long slot = 0;
+    if (lane == 0u) slot = atomicAdd(out.next, 1ull);
+    slot = __shfl_sync(0xFFFFFFFFu, slot, 0);
+    nvalid = slot < count;
+    if (!nvalid) return;
+    nq_id = list ? list[slot] : slot;
+    if (cp.packed1) {
+      nm = int(cp.fixed_m);
+      npw = cp.packed1[nq_id];
+    } else {
+      nm = int(cp.offsets[nq_id + 1] - cp.offsets[nq_id]);
+      npw = cp.packed[nq_id].x;
+    }
+    ndb = cp.dbits[nq_id];
+  };
+  prefetch();
+
+  while (nvalid) {
+    const uint64_t q = nq_id;
+    const int m = nm;
+    const uint64_t pw = npw & (shl64(1ull, 2u * uint32_t(m)) - 1ull);  // m <= 31
+    const uint64_t db = ndb;
+    prefetch();
+    const uint32_t NC = 8u * uint32_t(m) + 1u;
+    uint32_t nq = 0, nres = 0;
+    uint32_t exact_idx = 0xFFFFFFFFu;  // result index of W itself
+    // a finished candidate joins the results
+    auto add_results = [&](bool done, uint32_t c, uint32_t k, uint32_t l) {
+      const uint32_t bd = __ballot_sync(0xFFFFFFFFu, done);
+      const uint32_t idx = nres + __popc(bd & lt_mask);
+      if (done) {
+        kr[idx] = k;
+        lr[idx] = l;
+      }
+      const uint32_t be = __ballot_sync(0xFFFFFFFFu, done && c == NC - 1u);
+      if (be) exact_idx = __shfl_sync(0xFFFFFFFFu, idx, __ffs(be) - 1);
+      nres += __popc(bd);
+    };
+
+    if (__popcll(db) <= 1) {
+      // ---- every candidate's table gather, all issued before any is used ----
+      uint2 e[NR];
+      uint32_t vmask = 0;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const uint32_t c = uint32_t(r) * 32u + lane;
+        uint64_t S;
+        int L;
+        const bool valid = c < NC && flat_candidate(pw, m, db, c, S, L);
+        e[r] = make_uint2(0u, ix.n);  // the empty string (a deletion from m = 1)
+        if (valid && L > 0) {
+          const uint32_t d = min(uint32_t(L), kmax);
+          const uint32_t key = uint32_t(S >> (2u * (uint32_t(L) - d))) & uint32_t(shl64(1ull, 2u * d) - 1ull);
+          e[r] = ld_table_entry(d > K ? tx + key : tf.base + PrefixTable::off(d) + key);
+          work += work_unit(1u);
+        }
+        vmask |= valid ? (1u << r) : 0u;
+      }
+      // ---- survivors: finished ones to the results, the others to the queue ----
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const uint32_t c = uint32_t(r) * 32u + lane;
+        uint64_t S;
+        int L;
+        flat_candidate(pw, m, db, c < NC ? c : 0u, S, L);
+        const bool alive = ((vmask >> r) & 1u) && e[r].x <= e[r].y;
+        const int pos = L - int(min(uint32_t(L), kmax)) - 1;  // next character to prepend
+        const bool cont = alive && pos >= 0;
+        add_results(alive && pos < 0, c, e[r].x, e[r].y);
+        const uint32_t bc = __ballot_sync(0xFFFFFFFFu, cont);
+        if (cont) {
+          const uint32_t slot = nq + __popc(bc & lt_mask);
+          kq[slot] = e[r].x;
+          lq[slot] = e[r].y;
+          xq[slot] = c | (uint32_t(pos) << 16);
+        }
+        nq += __popc(bc);
+      }
+      __syncwarp();
+      // ---- level by level: one backward step for every queued candidate ----
+      while (nq > 0u) {
+        uint32_t nnew = 0;
+        for (uint32_t base = 0; base < nq; base += 64u) {
+          uint32_t k[2], l[2], x[2];
+          bool go[2];
+          StepLines<W> sl[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const uint32_t j = base + 32u * u + lane;
+            go[u] = j < nq;
+            k[u] = go[u] ? kq[j] : 1u;
+            l[u] = go[u] ? lq[j] : 0u;
+            x[u] = go[u] ? xq[j] : 0u;
+          }
+          __syncwarp();  // the chunk is in registers before its slots are reused (nnew <= base + 64)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) step_load<W>(ix, go[u], k[u], l[u], sl[u]);
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const uint32_t c = x[u] & 0xFFFFu, pos = x[u] >> 16;
+            uint64_t S;
+            int L;
+            flat_candidate(pw, m, db, c, S, L);
+            const uint32_t sym = uint32_t(S >> (2u * pos)) & 3u;
+            if (go[u]) work += work_unit(sl[u].jl != sl[u].jh ? 2u : 1u);
+            step_finish<W>(ix, sl[u], sym, k[u], l[u]);
+            const bool alive = go[u] && k[u] <= l[u];
+            const bool cont = alive && pos != 0u;
+            add_results(alive && pos == 0u, c, k[u], l[u]);
+            const uint32_t bc = __ballot_sync(0xFFFFFFFFu, cont);
+            if (cont) {
+              const uint32_t slot = nnew + __popc(bc & lt_mask);
+              kq[slot] = k[u];
+              lq[slot] = l[u];
+              xq[slot] = c | ((pos - 1u) << 16);
+            }
+            nnew += __popc(bc);
+          }
+        }
+        nq = nnew;
+        __syncwarp();
+      }
+    }
+
+    // ---- results: representatives (first of each interval, W itself before
+    // the others), their rank among the distinct intervals, one reservation,
+    // ordered write ----
+    __syncwarp();
+    uint32_t rep_bits = 0;  // bit t: result 32 t + lane represents its interval
+    uint32_t nuniq = 0;
+    for (uint32_t t = 0; t * 32u < nres; ++t) {
+      const uint32_t r = t * 32u + lane;
+      const bool have = r < nres;
+      const uint32_t mk = kr[have ? r : 0u], ml = lr[have ? r : 0u];
+      const uint32_t md = r == exact_idx ? 0u : 1u;
+      bool rep = have;
+      for (uint32_t j = 0; j < nres; ++j) {
+        const uint32_t dj = j == exact_idx ? 0u : 1u;
+        if (kr[j] == mk && lr[j] == ml && (dj < md || (dj == md && j < r))) rep = false;
+      }
+      const uint32_t br = __ballot_sync(0xFFFFFFFFu, rep);
+      if (lane == 0u) repw[t] = br;
+      rep_bits |= rep ? (1u << t) : 0u;
+      nuniq += __popc(br);
+    }
+    __syncwarp();
+    unsigned long long o = 0;
+    if (lane == 0u && nuniq) o = atomicAdd(out.total, (unsigned long long)nuniq);
+    o = __shfl_sync(0xFFFFFFFFu, o, 0);
+    if (o + nuniq > out.cap) {  // this pass's buffer is full: retried by the next pass
+      if (lane == 0u) {
+        const unsigned long long f = atomicAdd(out.fail_count, 1ull);
+        out.fail_list[f] = uint32_t(q);
+        out.res_cnt[q] = 0u;
+      }
+      __syncwarp();
+      continue;
+    }
+    for (uint32_t t = 0; t * 32u < nres; ++t) {
+      const uint32_t r = t * 32u + lane;
+      if (r < nres && ((rep_bits >> t) & 1u)) {
+        const uint32_t mk = kr[r], ml = lr[r];
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < nres; ++j) {
+          const uint32_t kj = kr[j], lj = lr[j];
+          rank += (((repw[j >> 5] >> (j & 31u)) & 1u) && (kj < mk || (kj == mk && lj < ml))) ? 1u : 0u;
+        }
+        out.kl[o + rank] = make_uint2(mk, ml);
+        out.diffs[o + rank] = r == exact_idx ? uint8_t(0) : uint8_t(1);
+      }
+    }
+    if (lane == 0u) {
+      out.res_off[q] = o;
+      out.res_cnt[q] = nuniq;
+      out.res_pass[q] = out.pass;
+    }
+    __syncwarp();
+  }
+  flush_work(out.steps, work);
+}
+
+}  // namespace fmg

@@ -263,7 +263,8 @@ def test_alternate_line_layouts(small_cases, gpu, words, monkeypatch):
 def test_config3_small_scale_vs_oracle(gpu, monkeypatch):
     """Config-3 generator at 1/150 scale: exact and z=1 on packed 19-bp seeds, through the
     packed host entry point, one-directional (no reverse index) and then bidirectional in its
-    split (the config-3 default at scale: edit range split at 3m/4, case-A jumps into the
+    flat (the config-3 default at scale: one warp per pattern over its one-edit neighbourhood,
+    gathers into the level-(K+1) table), split (edit range split at 3m/4, case-A jumps into the
     level-(K+1) table), level-synchronous and per-thread forms."""
     import ctypes as ct
 
@@ -278,9 +279,10 @@ def test_config3_small_scale_vs_oracle(gpu, monkeypatch):
     orow, ok, ol, od, _ = orc.inexact_batch(ox, seeds, 1)
     lib = _lib.load()
     dix = idx.device_index()
-    for engine in (None, "split", "sync", "dfs"):
+    for engine in (None, "flat", "split", "sync", "dfs"):
         if engine is not None:
-            dix.ensure_reverse()
+            if engine != "flat":
+                dix.ensure_reverse()
             monkeypatch.setenv("FMG_BIDIR_ENGINE", engine)
         h = ct.c_void_p()
         _lib.check(lib.fmg_inexact_packed_host(dix.handle, wl.packed.ctypes.data, 19, wl.packed.size, 1, ct.byref(h)))
@@ -502,6 +504,57 @@ def test_inexact_bidirectional_engine(gpu, monkeypatch, n, lens, engine):
     b = fm.inexact_search_batch(idx, pats, 1)
     assert np.array_equal(b.offsets, ms.offsets) and np.array_equal(b.k, ms.k) and np.array_equal(b.diffs, ms.diffs)
     assert ms.steps < b.steps  # the point of the engine
+
+
+@pytest.mark.parametrize("n,lens", [(200_000, (1, 2, 3, 5, 8, 9, 10, 11, 12, 19, 20, 27, 31)),
+                                    (3_000, (1, 2, 4, 7, 12, 19, 25, 31)), (40, (1, 2, 3, 6, 9, 14)),
+                                    (200_000, (9, 10, 11)), (200_000, (17, 18, 19))])
+def test_inexact_flat_engine(gpu, monkeypatch, n, lens):
+    """z = 1 through the flat engine (kernels_flat.cuh: a warp per pattern, one table gather
+    per string of the one-edit neighbourhood, survivors extended level by level): patterns
+    of mixed lengths 1..31 cut from anywhere (text start / end included), mutated or random,
+    repeats — identical to the oracle; every NR instantiation (m <= 11, <= 19, <= 31)."""
+    monkeypatch.setenv("FMG_BIDIR_ENGINE", "flat")
+    rng = np.random.Generator(np.random.PCG64(99 + n + len(lens)))
+    text = rng.integers(0, 4, n, dtype=np.uint8)
+    if n >= 3000:  # a tandem repeat and a homopolymer run: many candidates occur, many spell the same string
+        text[1000:1400] = np.tile(text[1000:1010], 40)
+        text[2000:2100] = 2
+    idx = fm.build_index(text)
+    pats = []
+    for r in range(3000):
+        m = min(int(rng.choice(lens)), n)
+        kind = r % 6
+        if kind == 0:
+            p = text[n - m:].copy()
+        elif kind == 1:
+            p = text[:m].copy()
+        elif kind == 2:
+            p = rng.integers(0, 4, m, dtype=np.uint8)
+        elif kind == 3 and n >= 3000:
+            s = int(rng.integers(990, 2100 - m))
+            p = text[s:s + m].copy()
+        else:
+            s = int(rng.integers(0, n - m + 1))
+            p = text[s:s + m].copy()
+        if m > 2 and rng.random() < 0.5:  # one random edit
+            j = int(rng.integers(0, m))
+            e = rng.random()
+            if e < 0.4:
+                p[j] = (p[j] + 1 + rng.integers(0, 3)) % 4
+            elif e < 0.7:
+                p = np.delete(p, j)
+            else:
+                p = np.insert(p, j, rng.integers(0, 4))
+        pats.append(codes_to_str(p[:31]))
+    ms = fm.inexact_search_batch(idx, pats, 1)
+    row, k, l, d, _ = orc.inexact_batch(orc.OracleIndex(idx), pats, 1)
+    assert np.array_equal(ms.offsets, row)
+    assert np.array_equal(ms.k.astype(np.int64), k) and np.array_equal(ms.l.astype(np.int64), l)
+    assert np.array_equal(ms.diffs, d)
+    monkeypatch.setenv("FMG_BIDIR_ENGINE", "dfs")
+    b = fm.inexact_search_batch(idx, pats, 1)
+    assert np.array_equal(b.offsets, ms.offsets) and np.array_equal(b.k, ms.k) and np.array_equal(b.diffs, ms.diffs)
 
 
 def test_inexact_repeated_calls_reuse_dedup_table(gpu, monkeypatch):

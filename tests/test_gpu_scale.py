@@ -98,17 +98,18 @@ def test_config3_full_scale_exact_and_hits(gpu, c3):
     assert checked > 1500
 
 
-@pytest.mark.parametrize("engine", ["default", "sync", "dfs", "onedir"])
+@pytest.mark.parametrize("engine", ["default", "split", "sync", "dfs", "onedir"])
 def test_config3_full_scale_z1_every_engine(gpu, c3, monkeypatch, engine):
     wl, idx = c3
     gold = json.loads((GOLDEN / "scale3_cases.json").read_text())
     lib = _lib.load()
     dix = idx.device_index()
-    if engine in ("sync", "dfs"):
+    if engine in ("split", "sync", "dfs"):
+        dix.ensure_reverse()
         monkeypatch.setenv("FMG_BIDIR_ENGINE", engine)
     if engine == "onedir":
         monkeypatch.setenv("FMG_INEXACT_BIDIR", "0")
-    # the split (default) form on every seed; the slower forms on the first 2^15
+    # the default (flat) form on every seed; the other forms on the first 2^15
     count = wl.packed.size if engine == "default" else 1 << 15
     packed = np.ascontiguousarray(wl.packed[:count])
     seeds = workloads.unpack_patterns(packed, 19)
