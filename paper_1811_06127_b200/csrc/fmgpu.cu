@@ -335,6 +335,11 @@ struct fmg_index {
   uint2* lut_x = nullptr;
   uint32_t lut_x_k = 0;
   bool lut_x_tried = false;
+  // presence filter of the flat z = 1 engine (kernels_flat.cuh FlatFilter):
+  // NO bitmaps of 4^B bits, built on first use from the level-lut_x_k table
+  uint32_t* flt_bits = nullptr;
+  uint32_t flt_B = 0, flt_G = 0, flt_NO = 0;
+  bool flt_tried = false;
   // dedup hash table of the inexact engines, kept between calls with a
   // monotone epoch so it is zeroed only when allocated or when the epochs
   // wrap (EpochTable)
@@ -1090,6 +1095,63 @@ void pool_reserve(int device, size_t bytes, cudaStream_t s) {
   FMG_CK(cudaStreamSynchronize(s));
 }
 
+// The flat engine's presence filter (kernels_flat.cuh): B = kx + 2 (config 3:
+// 18, 8.6 GB per copy), as many copies as fit a third of the available memory
+// up to ceil(B / 4) (one group of four window positions per 32-byte sector),
+// groups widened when fewer copies fit.  Built once per index from the
+// level-kx table.  FMG_FLAT_FILTER=0 disables it, FMG_FLAT_FILTER_NO=n and
+// FMG_FLAT_FILTER_D=1..3 (B = kx + D) override the shape (A/B).
+FlatFilter flat_filter(const fmg_index* cix, const uint2* tx, uint32_t kx, uint64_t max_len, cudaStream_t s) {
+  const bool enabled = [] {  // read per call (tests flip it)
+    const char* e = std::getenv("FMG_FLAT_FILTER");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  if (!enabled || !tx) return {};
+  auto* ix = const_cast<fmg_index*>(cix);  // a cache, like the tables
+  std::lock_guard<std::mutex> lock(ix->lut_mu);
+  if (!ix->flt_tried) {
+    int D = 2;
+    if (const char* e = std::getenv("FMG_FLAT_FILTER_D")) D = std::min(3, std::max(1, std::atoi(e)));
+    const uint32_t B = kx + uint32_t(D);
+    if (max_len < B || B > 20) return {};  // nothing (or too little) to filter for these patterns: decide later
+    ix->flt_tried = true;
+    const uint64_t bytes_per = (uint64_t(1) << (2 * B)) / 8;
+    uint32_t NO = (B + 3) / 4;
+    if (const char* e = std::getenv("FMG_FLAT_FILTER_NO")) NO = std::min<uint32_t>(B, std::max(1, std::atoi(e)));
+    const size_t room = available_bytes(ix->device) / 3;
+    while (NO > 1 && bytes_per * NO > room) --NO;
+    if (bytes_per * NO > room) return {};
+    uint32_t* bits = nullptr;
+    if (dmalloc(&bits, bytes_per * NO) != cudaSuccess) {
+      cudaGetLastError();
+      return {};
+    }
+    FlatFilter f{bits, B, (B + NO - 1) / NO, NO};
+    const auto t0 = std::chrono::steady_clock::now();
+    FMG_CK(cudaMemsetAsync(bits, 0, bytes_per * NO, s));
+    const uint64_t cnt = uint64_t(1) << (2 * kx);
+    with_words(ix, [&](auto wt) {
+      constexpr int W = decltype(wt)::value;
+      const unsigned blocks = unsigned((cnt + 255) / 256);
+      if (D == 1) k_flat_filter_build<W, 1><<<blocks, 256, 0, s>>>(ix->view(), tx, cnt, f, bits);
+      else if (D == 2) k_flat_filter_build<W, 2><<<blocks, 256, 0, s>>>(ix->view(), tx, cnt, f, bits);
+      else k_flat_filter_build<W, 3><<<blocks, 256, 0, s>>>(ix->view(), tx, cnt, f, bits);
+    });
+    FMG_CK(cudaGetLastError());
+    FMG_CK(cudaStreamSynchronize(s));
+    if (std::getenv("FMG_TRACE"))
+      fprintf(stderr, "[fmg] flat filter: B=%u G=%u copies=%u, %.2f GB, built in %.1f ms\n", f.B, f.G, f.NO,
+              double(bytes_per * NO) / 1e9,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    ix->flt_bits = bits;
+    ix->flt_B = f.B;
+    ix->flt_G = f.G;
+    ix->flt_NO = f.NO;
+  }
+  if (!ix->flt_bits) return {};
+  return FlatFilter{ix->flt_bits, ix->flt_B, ix->flt_G, ix->flt_NO};
+}
+
 // The flat z = 1 engine is the default while the pattern is at most this many
 // characters longer than the deepest table level (each extra character is
 // one more dependent step for the candidates still alive).
@@ -1340,6 +1402,9 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       o.unsorted = counters.ptr + 5;
       o.unsorted_list = unsorted_list.ptr;
       CodePatterns cp{codes, offsets, packed.ptr, packed1, uint32_t(max_len), dbits.ptr};
+      // the filter's traversal starts from the deepest table level the engine gathers from
+      const FlatFilter flt = flat_tx ? flat_filter(ix, flat_tx, flat_kx, max_len, s)
+                                     : flat_filter(ix, pt.base + PrefixTable::off64(pt.k), pt.k, max_len, s);
       static const bool trace_flat = std::getenv("FMG_TRACE") != nullptr;
       cudaEvent_t fe[2] = {};
       if (trace_flat) {
@@ -1349,11 +1414,11 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       with_words(ix, [&](auto wt) {
         constexpr int W = decltype(wt)::value;
         if (nr == 3)
-          k_z1_flat<W, 3><<<blocks, nt, smem, s>>>(ix->view(), pt, flat_tx, flat_kx, cp, nullptr, count, o);
+          k_z1_flat<W, 3><<<blocks, nt, smem, s>>>(ix->view(), pt, flat_tx, flat_kx, cp, nullptr, count, o, flt);
         else if (nr == 5)
-          k_z1_flat<W, 5><<<blocks, nt, smem, s>>>(ix->view(), pt, flat_tx, flat_kx, cp, nullptr, count, o);
+          k_z1_flat<W, 5><<<blocks, nt, smem, s>>>(ix->view(), pt, flat_tx, flat_kx, cp, nullptr, count, o, flt);
         else
-          k_z1_flat<W, 8><<<blocks, nt, smem, s>>>(ix->view(), pt, flat_tx, flat_kx, cp, nullptr, count, o);
+          k_z1_flat<W, 8><<<blocks, nt, smem, s>>>(ix->view(), pt, flat_tx, flat_kx, cp, nullptr, count, o, flt);
       });
       FMG_CK(cudaGetLastError());
       unsigned long long host_ctr[2];
@@ -1939,6 +2004,7 @@ void fmg_index_destroy(fmg_index* ix) {
   dfree(ix->lut);
   dfree(ix->lut_r);
   dfree(ix->lut_x);
+  dfree(ix->flt_bits);
   dfree(ix->ep_table);
   dfree(ix->rev_lines.load());
   dfree(ix->samples.load());
@@ -2029,6 +2095,21 @@ int fmgx_kmer_table(const fmg_index* ix, uint32_t* k_out, uint64_t* ext_bytes_ou
     const KmerTable kt = kmer_table(ix, 1u << 20, nullptr);
     if (k_out) *k_out = kt.k;
     if (ext_bytes_out) *ext_bytes_out = ix->lut_x ? (uint64_t(1) << (2 * ix->lut_x_k)) * sizeof(uint2) : 0;
+  });
+}
+
+// Reporting hook: the flat engine's presence filter as built so far (all zero
+// when none): window length B, group width G, copies, bytes.
+int fmgx_flat_filter_info(const fmg_index* ix, uint32_t* b_out, uint32_t* g_out, uint32_t* copies_out,
+                          uint64_t* bytes_out) {
+  return fmg::guard([&] {
+    check_index(ix);
+    std::lock_guard<std::mutex> lock(const_cast<fmg_index*>(ix)->lut_mu);
+    const bool have = ix->flt_bits != nullptr;
+    if (b_out) *b_out = have ? ix->flt_B : 0;
+    if (g_out) *g_out = have ? ix->flt_G : 0;
+    if (copies_out) *copies_out = have ? ix->flt_NO : 0;
+    if (bytes_out) *bytes_out = have ? (uint64_t(1) << (2 * ix->flt_B)) / 8 * ix->flt_NO : 0;
   });
 }
 

@@ -509,12 +509,22 @@ def test_inexact_bidirectional_engine(gpu, monkeypatch, n, lens, engine):
 @pytest.mark.parametrize("n,lens", [(200_000, (1, 2, 3, 5, 8, 9, 10, 11, 12, 19, 20, 27, 31)),
                                     (3_000, (1, 2, 4, 7, 12, 19, 25, 31)), (40, (1, 2, 3, 6, 9, 14)),
                                     (200_000, (9, 10, 11)), (200_000, (17, 18, 19))])
-def test_inexact_flat_engine(gpu, monkeypatch, n, lens):
+@pytest.mark.parametrize("filt", ["default", "off", "copies1_d1", "copies2_d3"])
+def test_inexact_flat_engine(gpu, monkeypatch, n, lens, filt):
     """z = 1 through the flat engine (kernels_flat.cuh: a warp per pattern, one table gather
     per string of the one-edit neighbourhood, survivors extended level by level): patterns
     of mixed lengths 1..31 cut from anywhere (text start / end included), mutated or random,
-    repeats — identical to the oracle; every NR instantiation (m <= 11, <= 19, <= 31)."""
+    repeats — identical to the oracle; every NR instantiation (m <= 11, <= 19, <= 31); with
+    the presence filter in its default shape (B = table level + 2, one copy per four window
+    positions), off, and in two other shapes (one ungrouped copy of level + 1; two copies of
+    level + 3)."""
     monkeypatch.setenv("FMG_BIDIR_ENGINE", "flat")
+    if filt == "off":
+        monkeypatch.setenv("FMG_FLAT_FILTER", "0")
+    elif filt != "default":
+        copies, d = filt.split("_")
+        monkeypatch.setenv("FMG_FLAT_FILTER_NO", copies[-1])
+        monkeypatch.setenv("FMG_FLAT_FILTER_D", d[-1])
     rng = np.random.Generator(np.random.PCG64(99 + n + len(lens)))
     text = rng.integers(0, 4, n, dtype=np.uint8)
     if n >= 3000:  # a tandem repeat and a homopolymer run: many candidates occur, many spell the same string
@@ -552,6 +562,22 @@ def test_inexact_flat_engine(gpu, monkeypatch, n, lens):
     assert np.array_equal(ms.offsets, row)
     assert np.array_equal(ms.k.astype(np.int64), k) and np.array_equal(ms.l.astype(np.int64), l)
     assert np.array_equal(ms.diffs, d)
+    # the filter really was in play (or really was not)
+    import ctypes as ct
+
+    from paper_1811_06127_b200 import _lib
+
+    fb, fg, fc = ct.c_uint32(), ct.c_uint32(), ct.c_uint32()
+    _lib.check(_lib.load().fmgx_flat_filter_info(idx.device_index().handle, ct.byref(fb), ct.byref(fg),
+                                                 ct.byref(fc), None))
+    kk, nb = ct.c_uint32(), ct.c_uint64()
+    _lib.check(_lib.load().fmgx_prefix_table(idx.device_index().handle, ct.byref(kk), ct.byref(nb)))
+    depth = 2 if filt == "default" else int(filt[-1]) if filt != "off" else 0
+    if filt == "off":
+        assert fc.value == 0
+    elif max(lens) >= kk.value + depth:  # some candidate is long enough for a window
+        assert fb.value == kk.value + depth and fg.value * fc.value >= fb.value
+        assert fc.value == ((fb.value + 3) // 4 if filt == "default" else int(filt[6]))
     monkeypatch.setenv("FMG_BIDIR_ENGINE", "dfs")
     b = fm.inexact_search_batch(idx, pats, 1)
     assert np.array_equal(b.offsets, ms.offsets) and np.array_equal(b.k, ms.k) and np.array_equal(b.diffs, ms.diffs)
