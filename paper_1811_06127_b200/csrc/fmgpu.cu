@@ -1117,7 +1117,7 @@ FlatFilter flat_filter(const fmg_index* cix, const uint2* tx, uint32_t kx, uint6
     ix->flt_tried = true;
     const uint64_t bytes_per = (uint64_t(1) << (2 * B)) / 8;
     uint32_t NO = (B + 3) / 4;
-    if (const char* e = std::getenv("FMG_FLAT_FILTER_NO")) NO = std::min<uint32_t>(B, std::max(1, std::atoi(e)));
+    if (const char* e = std::getenv("FMG_FLAT_FILTER_NO")) NO = std::min<uint32_t>((B + 1) / 2, std::max(1, std::atoi(e)));
     const size_t room = available_bytes(ix->device) / 3;
     while (NO > 1 && bytes_per * NO > room) --NO;
     if (bytes_per * NO > room) return {};
@@ -1126,7 +1126,8 @@ FlatFilter flat_filter(const fmg_index* cix, const uint2* tx, uint32_t kx, uint6
       cudaGetLastError();
       return {};
     }
-    FlatFilter f{bits, B, (B + NO - 1) / NO, NO};
+    FlatFilter f{bits, B, (B + NO - 1) / NO, NO, 0};
+    f.rcpG = uint32_t(((uint64_t(1) << 32) + f.G - 1) / f.G);  // G >= 2
     const auto t0 = std::chrono::steady_clock::now();
     FMG_CK(cudaMemsetAsync(bits, 0, bytes_per * NO, s));
     const uint64_t cnt = uint64_t(1) << (2 * kx);
@@ -1149,7 +1150,8 @@ FlatFilter flat_filter(const fmg_index* cix, const uint2* tx, uint32_t kx, uint6
     ix->flt_NO = f.NO;
   }
   if (!ix->flt_bits) return {};
-  return FlatFilter{ix->flt_bits, ix->flt_B, ix->flt_G, ix->flt_NO};
+  return FlatFilter{ix->flt_bits, ix->flt_B, ix->flt_G, ix->flt_NO,
+                    uint32_t(((uint64_t(1) << 32) + ix->flt_G - 1) / ix->flt_G)};
 }
 
 // The flat z = 1 engine is the default while the pattern is at most this many

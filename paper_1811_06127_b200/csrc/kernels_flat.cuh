@@ -75,6 +75,7 @@ __device__ __forceinline__ uint2 ld_table_entry(const uint2* p) {
 struct FlatFilter {
   const uint32_t* bits = nullptr;  // NO bitmaps of 4^B bits
   uint32_t B = 0, G = 0, NO = 0;
+  uint32_t rcpG = 0;  // ceil(2^32 / G), G >= 2: x / G = umulhi(x, rcpG) for the small x used here
 };
 
 // Bit index of window w (B characters, character t in bits 2t..2t+1) in copy
@@ -97,14 +98,11 @@ __device__ __forceinline__ uint64_t filter_word(const FlatFilter& f, uint64_t ke
 // when it holds e, else the last.
 __device__ __forceinline__ uint64_t filter_probe_addr(const FlatFilter& f, uint32_t c, int m, uint64_t S, int L,
                                                       uint32_t& bit) {
-  uint32_t e = 0;
-  if (c < uint32_t(8 * m)) {
-    const uint32_t i = c >> 3, s = c & 7u;
-    e = s < 4u ? i + 1u : s < 7u ? i : min(i, uint32_t(L) - 1u);
-  }
+  const uint32_t i = c >> 3, s = c & 7u;
+  const uint32_t e = c >= uint32_t(8 * m) ? 0u : s < 4u ? i + 1u : s < 7u ? i : min(i, uint32_t(L) - 1u);
   const uint32_t ws = e < f.B ? 0u : uint32_t(L) - f.B;
   const uint64_t w = shr64(S, 2u * ws) & (shl64(1ull, 2u * f.B) - 1ull);
-  const uint32_t o = min((e - ws) / f.G, f.NO - 1u);
+  const uint32_t o = min(__umulhi(e - ws, f.rcpG), f.NO - 1u);
   const uint64_t key = filter_key(f, w, o);
   bit = uint32_t(key) & 31u;
   return filter_word(f, key, o);
@@ -121,31 +119,33 @@ __device__ __forceinline__ uint32_t ld_filter_word(const uint32_t* p) {
 // W[i] by (W[i] + s - 3) & 3, s = 7 deletion of W[i]; c = 8m is W itself.
 // Returns the string S (L characters, same packing) and whether it has to be
 // searched at all.
+//
+// Branch-free on purpose: the lanes of a warp hold all three kinds of edit,
+// and a branch per kind made the warp run the probe code after it three times
+// over (ncu: 1,200 of 2,500 warp instructions per pattern).  Every candidate
+// is one splice: the first a characters of W, `put` inserted characters (b),
+// then W from position i + 1 on.
 __device__ __forceinline__ bool flat_candidate(uint64_t pw, int m, uint64_t db, uint32_t c, uint64_t& S, int& L) {
-  if (c >= uint32_t(8 * m)) {
-    S = pw;
-    L = m;
-    return c == uint32_t(8 * m) && db == 0ull;
-  }
-  const uint32_t i = c >> 3, s = c & 7u;
-  const uint32_t wi = uint32_t(pw >> (2u * i)) & 3u;
-  const uint64_t hi = shr64(pw, 2u * i + 2u);                    // W[i+1..]
-  const bool prev_ok = (db & ((1ull << i) - 1ull)) == 0ull;     // no absent segment inside W[0..i-1]
-  const bool cur_ok = (db & ((2ull << i) - 1ull)) == 0ull;      // ... inside W[0..i]
-  if (s < 4u) {  // insertion of s after W[i]
-    S = (pw & ((4ull << (2u * i)) - 1ull)) | (uint64_t(s) << (2u * i + 2u)) | shl64(hi, 2u * i + 4u);
-    L = m + 1;
-    return cur_ok && (s != wi || i == 0u);
-  }
-  if (s < 7u) {  // substitution
-    const uint32_t b = (wi + s - 3u) & 3u;
-    S = pw ^ (uint64_t(wi ^ b) << (2u * i));
-    L = m;
-    return prev_ok;
-  }
-  S = (pw & ((1ull << (2u * i)) - 1ull)) | (hi << (2u * i));  // deletion
-  L = m - 1;
-  return prev_ok && !(i >= 1u && wi == (uint32_t(shr64(pw, 2u * i - 2u)) & 3u));
+  const uint32_t m8 = 8u * uint32_t(m);
+  const bool is_w = c >= m8;  // W itself (c == 8m), or padding past it
+  const uint32_t i = is_w ? 0u : c >> 3, s = c & 7u;
+  const bool ins = s < 4u, del = s == 7u;
+  const uint32_t wi = uint32_t(shr64(pw, 2u * i)) & 3u;
+  const uint32_t wprev = uint32_t(shr64(pw, 2u * i - 2u)) & 3u;  // W[i-1] (i >= 1; unused otherwise)
+  const uint32_t b = ins ? s : (wi + s - 3u) & 3u;               // inserted / substituted character
+  const uint32_t a = i + (ins ? 1u : 0u);                         // characters of W kept below the edit
+  const uint32_t put = del ? 0u : 1u;
+  const uint64_t low = pw & (shl64(1ull, 2u * a) - 1ull);
+  const uint64_t mid = shl64(uint64_t(del ? 0u : b), 2u * a);
+  const uint64_t high = shl64(shr64(pw, 2u * i + 2u), 2u * (a + put));  // W[i+1..]
+  const bool prev_ok = (db & (shl64(1ull, i) - 1ull)) == 0ull;   // no absent segment inside W[0..i-1]
+  const bool cur_ok = (db & (shl64(2ull, i) - 1ull)) == 0ull;    // ... inside W[0..i]
+  const bool ok_ins = cur_ok && (s != wi || i == 0u);
+  const bool ok_del = prev_ok && !(i >= 1u && wi == wprev);
+  const bool ok = ins ? ok_ins : del ? ok_del : prev_ok;
+  S = is_w ? pw : (low | mid | high);
+  L = m + (is_w ? 0 : (ins ? 1 : 0) - (del ? 1 : 0));
+  return is_w ? (c == m8 && db == 0ull) : ok;
 }
 
 // Raw line data of one backward step at (k-1, l): the high line always, the
