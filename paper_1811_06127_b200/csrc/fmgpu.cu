@@ -1362,28 +1362,6 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     if (use_flat) {
       // ---- pass 0 = the flat engine; patterns that do not fit this pass's
       // result buffer are retried by the DFS engine below ----
-      const int nt = 128;
-      const int nr = max_len <= 11 ? 3 : max_len <= 19 ? 5 : 8;  // 32 nr >= 8 m + 1
-      const void* kf = nullptr;
-      size_t smem = 0;
-      auto pick = [&](auto wt, auto nrt) {
-        constexpr int W = decltype(wt)::value;
-        constexpr int NR = decltype(nrt)::value;
-        kf = (const void*)k_z1_flat<W, NR>;
-        smem = size_t(nt / 32) * FlatSmem<NR>::words_per_warp * 4;
-      };
-      with_words(ix, [&](auto wt) {
-        if (nr == 3) pick(wt, std::integral_constant<int, 3>{});
-        else if (nr == 5) pick(wt, std::integral_constant<int, 5>{});
-        else pick(wt, std::integral_constant<int, 8>{});
-      });
-      FMG_CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      int per_sm = 0;
-      FMG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, nt, smem));
-      per_sm = std::max(per_sm, 1);
-      const uint64_t warps_wanted = count;  // one pattern per warp at a time
-      const unsigned blocks = unsigned(std::max<uint64_t>(
-          1, std::min<uint64_t>(uint64_t(per_sm) * ix->sms, (warps_wanted + nt / 32 - 1) / (nt / 32))));
       pass_kl.emplace_back(cap, s);
       pass_d.emplace_back(cap, s);
       FMG_CK(cudaMemsetAsync(counters.ptr, 0, 2 * sizeof(unsigned long long), s));
@@ -1407,22 +1385,61 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       // the filter's traversal starts from the deepest table level the engine gathers from
       const FlatFilter flt = flat_tx ? flat_filter(ix, flat_tx, flat_kx, max_len, s)
                                      : flat_filter(ix, pt.base + PrefixTable::off64(pt.k), pt.k, max_len, s);
+      // survivor queue sized for EVERY candidate of a chunk of patterns (no
+      // overflow path to get wrong): 24 bytes per entry, an eighth of the
+      // available memory, patterns in chunks of cap / (8 m + 1)
+      const uint64_t max_cand = 8 * max_len + 1;
+      // Survivor queue: with the filter a pattern keeps ~11 of its 8m + 1
+      // candidates (config 3), so a chunk is sized for 48 per pattern on
+      // average, and always for one pattern's worth; a chunk whose patterns
+      // keep more than that overflows into the retry list (DFS engine).
+      // Without a filter every candidate survives the probe.  At most 2^26
+      // entries (1.5 GB): large buffers cost more to allocate than the extra
+      // chunk launches (12 GB queues: 40-100 ms per call against 44 ms of work).
+      uint64_t per_pat = flt.bits ? std::min<uint64_t>(max_cand, 48) : max_cand;
+      if (const char* e = std::getenv("FMG_FLAT_PER_PAT")) per_pat = std::max(1, std::atoi(e));  // tests: force overflow
+      const uint64_t q_cap = std::max<uint64_t>(
+          std::getenv("FMG_FLAT_PER_PAT") ? per_pat : max_cand * 64, std::min<uint64_t>(count * per_pat, std::min<uint64_t>(uint64_t(1) << 26, free_b / 8 / 24)));
+      const uint64_t chunk = std::max<uint64_t>(1, q_cap / per_pat);
+      DevBuf<FlatSurvivor> surv(q_cap, s);
+      DevBuf<uint2> raw(q_cap, s);
+      DevBuf<uint64_t> seg_base(count, s);
+      DevBuf<uint32_t> seg_cnt(count, s);
+      DevBuf<unsigned long long> n_surv(1, s);
+      FlatQueues fq{surv.ptr, raw.ptr, n_surv.ptr, q_cap, seg_base.ptr, seg_cnt.ptr};
+      const int nrs = int((3 * max_len + 1 + 31) / 32);  // rounds of 32 slots, 1..3 (m <= 31)
       static const bool trace_flat = std::getenv("FMG_TRACE") != nullptr;
       cudaEvent_t fe[2] = {};
       if (trace_flat) {
+        FMG_CK(cudaStreamSynchronize(s));
+        fprintf(stderr, "[fmg] flat pre-engine host time %.3f ms\n",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_entry).count());
         for (auto& e : fe) cudaEventCreate(&e);
         cudaEventRecord(fe[0], s);
       }
+      const void* kp = nrs == 1 ? (const void*)k_flat_probe<1> : nrs == 2 ? (const void*)k_flat_probe<2>
+                                                                           : (const void*)k_flat_probe<3>;
+      const int bp = std::max(1, blocks_per_sm(kp, 256, 0)) * ix->sms;
+      const int bc = std::max(1, blocks_per_sm((const void*)k_flat_collect, 128, 0)) * ix->sms;
+      int be = 1;
       with_words(ix, [&](auto wt) {
-        constexpr int W = decltype(wt)::value;
-        if (nr == 3)
-          k_z1_flat<W, 3><<<blocks, nt, smem, s>>>(ix->view(), pt, flat_tx, flat_kx, cp, nullptr, count, o, flt);
-        else if (nr == 5)
-          k_z1_flat<W, 5><<<blocks, nt, smem, s>>>(ix->view(), pt, flat_tx, flat_kx, cp, nullptr, count, o, flt);
-        else
-          k_z1_flat<W, 8><<<blocks, nt, smem, s>>>(ix->view(), pt, flat_tx, flat_kx, cp, nullptr, count, o, flt);
+        be = std::max(1, blocks_per_sm((const void*)k_flat_extend<decltype(wt)::value>, 256, 0)) * ix->sms;
       });
-      FMG_CK(cudaGetLastError());
+      for (uint64_t c0 = 0; c0 < count; c0 += chunk) {
+        const uint64_t cn = std::min<uint64_t>(chunk, count - c0);
+        FMG_CK(cudaMemsetAsync(n_surv.ptr, 0, sizeof(unsigned long long), s));
+        const unsigned gp = unsigned(std::min<uint64_t>(uint64_t(bp), (cn + 7) / 8));  // 8 warps per block
+        if (nrs == 1) k_flat_probe<1><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
+        else if (nrs == 2) k_flat_probe<2><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
+        else k_flat_probe<3><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
+        with_words(ix, [&](auto wt) {
+          constexpr int W = decltype(wt)::value;
+          k_flat_extend<W><<<unsigned(be), 256, 0, s>>>(ix->view(), pt, flat_tx, flat_kx, fq, counters.ptr + 2);
+        });
+        const unsigned gc = unsigned(std::min<uint64_t>(uint64_t(bc), (cn + 3) / 4));  // 4 warps per block
+        k_flat_collect<<<gc, 128, 0, s>>>(nullptr, c0, cn, fq, o);
+        FMG_CK(cudaGetLastError());
+      }
       unsigned long long host_ctr[2];
       FMG_CK(cudaMemcpyAsync(host_ctr, counters.ptr, sizeof(host_ctr), cudaMemcpyDeviceToHost, s));
       if (trace_flat) cudaEventRecord(fe[1], s);
@@ -1430,8 +1447,9 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       if (trace_flat) {
         float ms = 0;
         cudaEventElapsedTime(&ms, fe[0], fe[1]);
-        fprintf(stderr, "[fmg] flat z=1 engine: %llu patterns, NR=%d, %u blocks (%d per SM, %zu B smem): %.3f ms, "
-                "%llu results, %llu retried\n", (unsigned long long)count, nr, blocks, per_sm, smem, ms, host_ctr[0],
+        fprintf(stderr, "[fmg] flat z=1 engine: %llu patterns in chunks of %llu (probe %d rounds x %d blocks, extend %d "
+                "blocks, collect %d blocks; filter B=%u x %u copies): %.3f ms, %llu results, %llu retried\n",
+                (unsigned long long)count, (unsigned long long)chunk, nrs, bp, be, bc, flt.B, flt.NO, ms, host_ctr[0],
                 host_ctr[1]);
         for (auto& e : fe) cudaEventDestroy(e);
       }

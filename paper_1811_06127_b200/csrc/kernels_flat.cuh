@@ -1,7 +1,7 @@
 // Flat z = 1 engine for the bounded-difference search (search.py:97-159):
-// the one-edit neighbourhood of each pattern enumerated candidate by
-// candidate, one WARP per pattern.  Part of libfmgpu.so (sm_100a); included
-// once by fmgpu.cu after kernels_inexact.cuh.
+// the one-edit neighbourhood of each pattern enumerated string by string.
+// Part of libfmgpu.so (sm_100a); included once by fmgpu.cu after
+// kernels_inexact.cuh.
 //
 // For z = 1 the reference's DFS reports (interval(S), diffs) for every string
 // S within one edit of W that occurs in the text — W itself (diffs 0), a
@@ -11,17 +11,27 @@
 // pattern is only a few characters longer than the deepest k-mer table level
 // (config 3: m = 19 against level 16), walking a tree shares almost nothing:
 // every candidate string is ONE gather of its last min(L, kmax) characters
-// away from a nearly final answer, and the gathers of different candidates
-// are independent.  So instead of a per-thread DFS (8 of 32 lanes active,
-// ~1 request in flight per thread) a warp takes a pattern, its lanes take the
-// 8m + 1 candidates (8 per position: 4 insertions, 3 substitutions, 1
-// deletion; plus W), each lane issues all its gathers back to back, and the
-// candidates still alive (about half at level 16 of a 3.1 Gbp text) are
-// compacted through shared memory and extended level by level — every lane
-// active at every level — with one-symbol Occ steps on the index lines.
-// Results are collected, sorted by (k, l) and deduplicated in shared memory;
-// one atomic per pattern reserves the output rows.  No reverse index, no
-// per-thread hash table, no merge pass.
+// away from a nearly final answer, and the candidates are independent.
+//
+// Three kernels, each with the thread mapping its work wants (the first form
+// was one warp-per-pattern kernel: 3,800 warp instructions per pattern with
+// a third of the lanes idle after the first phase, issue-bound):
+//   k_flat_probe    a warp per pattern, a lane per (kind of edit, position):
+//                   the lane builds its up to four candidate strings as one
+//                   splice of W, asks the presence filter about each (below)
+//                   and the warp appends the survivors — the candidates the
+//                   text may hold — to a queue, one contiguous segment per
+//                   pattern, W itself first;
+//   k_flat_extend   a thread per survivor: one table gather, then one-symbol
+//                   backward steps on the index lines until the string is
+//                   complete or its interval empties; the interval (or
+//                   "absent") goes to the survivor's own slot, so results stay
+//                   grouped by pattern without a sort;
+//   k_flat_collect  a warp per pattern: its segment's intervals, sorted by
+//                   (k, l) and deduplicated (one match instruction when there
+//                   are at most 32), written to the pass's output buffer with
+//                   one reservation.
+// No reverse index, no per-thread hash table, no merge pass.
 //
 // Pruning (result-preserving, same bound as the DFS engines): dbits marks the
 // right ends of disjoint absent segments of W (k_dbound).  Two segments: no
@@ -92,60 +102,10 @@ __device__ __forceinline__ uint64_t filter_word(const FlatFilter& f, uint64_t ke
   return (uint64_t(o) << (2u * f.B - 5u)) + (key >> 5);
 }
 
-// Window and copy a candidate is probed through: e = position of the edited
-// character in S (substitution: i; insertion after W[i]: i + 1; deletion of
-// W[i]: the character that followed it, or the last one), the first window
-// when it holds e, else the last.
-__device__ __forceinline__ uint64_t filter_probe_addr(const FlatFilter& f, uint32_t c, int m, uint64_t S, int L,
-                                                      uint32_t& bit) {
-  const uint32_t i = c >> 3, s = c & 7u;
-  const uint32_t e = c >= uint32_t(8 * m) ? 0u : s < 4u ? i + 1u : s < 7u ? i : min(i, uint32_t(L) - 1u);
-  const uint32_t ws = e < f.B ? 0u : uint32_t(L) - f.B;
-  const uint64_t w = shr64(S, 2u * ws) & (shl64(1ull, 2u * f.B) - 1ull);
-  const uint32_t o = min(__umulhi(e - ws, f.rcpG), f.NO - 1u);
-  const uint64_t key = filter_key(f, w, o);
-  bit = uint32_t(key) & 31u;
-  return filter_word(f, key, o);
-}
-
 __device__ __forceinline__ uint32_t ld_filter_word(const uint32_t* p) {
   uint32_t v;
   asm("ld.global.nc.L2::64B.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
-}
-
-// Candidate c of pattern pw (m characters, character t in bits 2t..2t+1):
-// c = 8i + s, s = 0..3 insertion of s after W[i], s = 4..6 substitution of
-// W[i] by (W[i] + s - 3) & 3, s = 7 deletion of W[i]; c = 8m is W itself.
-// Returns the string S (L characters, same packing) and whether it has to be
-// searched at all.
-//
-// Branch-free on purpose: the lanes of a warp hold all three kinds of edit,
-// and a branch per kind made the warp run the probe code after it three times
-// over (ncu: 1,200 of 2,500 warp instructions per pattern).  Every candidate
-// is one splice: the first a characters of W, `put` inserted characters (b),
-// then W from position i + 1 on.
-__device__ __forceinline__ bool flat_candidate(uint64_t pw, int m, uint64_t db, uint32_t c, uint64_t& S, int& L) {
-  const uint32_t m8 = 8u * uint32_t(m);
-  const bool is_w = c >= m8;  // W itself (c == 8m), or padding past it
-  const uint32_t i = is_w ? 0u : c >> 3, s = c & 7u;
-  const bool ins = s < 4u, del = s == 7u;
-  const uint32_t wi = uint32_t(shr64(pw, 2u * i)) & 3u;
-  const uint32_t wprev = uint32_t(shr64(pw, 2u * i - 2u)) & 3u;  // W[i-1] (i >= 1; unused otherwise)
-  const uint32_t b = ins ? s : (wi + s - 3u) & 3u;               // inserted / substituted character
-  const uint32_t a = i + (ins ? 1u : 0u);                         // characters of W kept below the edit
-  const uint32_t put = del ? 0u : 1u;
-  const uint64_t low = pw & (shl64(1ull, 2u * a) - 1ull);
-  const uint64_t mid = shl64(uint64_t(del ? 0u : b), 2u * a);
-  const uint64_t high = shl64(shr64(pw, 2u * i + 2u), 2u * (a + put));  // W[i+1..]
-  const bool prev_ok = (db & (shl64(1ull, i) - 1ull)) == 0ull;   // no absent segment inside W[0..i-1]
-  const bool cur_ok = (db & (shl64(2ull, i) - 1ull)) == 0ull;    // ... inside W[0..i]
-  const bool ok_ins = cur_ok && (s != wi || i == 0u);
-  const bool ok_del = prev_ok && !(i >= 1u && wi == wprev);
-  const bool ok = ins ? ok_ins : del ? ok_del : prev_ok;
-  S = is_w ? pw : (low | mid | high);
-  L = m + (is_w ? 0 : (ins ? 1 : 0) - (del ? 1 : 0));
-  return is_w ? (c == m8 && db == 0ull) : ok;
 }
 
 // Raw line data of one backward step at (k-1, l): the high line always, the
@@ -201,233 +161,249 @@ __device__ __forceinline__ void step_finish(const IndexView& ix, const StepLines
   l = l2;
 }
 
-// NR = rounds of 32 candidates a lane takes (32 NR >= 8m + 1).  Shared
-// memory per warp, cap = 32 NR slots each: the candidates that passed the
-// filter (cq), the continuation queue (k, l, candidate | next position << 16,
-// and the candidate's first 16 characters: the ones still to prepend), the
-// results (k, l) and one flag word per 32 results.  Only W itself carries
-// diffs 0, so the diffs of a result are "is it the exact one" (its index is
-// kept in a register).
-//
-// Instruction budget (ncu, config 3): the first form of this kernel spent
-// 3,800 warp instructions per pattern, a quarter of them rebuilding the
-// candidate string three times per candidate, and was issue-bound once the
-// filter had removed most memory requests.  Now a candidate string is built
-// once for its probe, and again only if it survives (7 %); the continuation
-// queue carries the characters still needed; results are deduplicated with
-// one match instruction when there are at most 32.
-#ifndef FMG_FLAT_MINB
-#define FMG_FLAT_MINB 8  // resident 128-thread blocks per SM the register budget is sized for
-#endif
-
-template <int NR>
-struct FlatSmem {
-  static constexpr uint32_t cap = 32u * NR;
-  static constexpr uint32_t words_per_warp = 7u * cap + NR;
+// One candidate the text may hold: the string S (L characters, character t
+// in bits 2t..2t+1) of pattern q.
+struct __align__(16) FlatSurvivor {
+  uint64_t S;
+  uint32_t q, L;
 };
 
-template <int W, int NR>
-__global__ void __launch_bounds__(128, FMG_FLAT_MINB) k_z1_flat(IndexView ix, PrefixTable tf, const uint2* __restrict__ tx,
-                                                 uint32_t kx, CodePatterns cp, const uint32_t* __restrict__ list,
-                                                 uint64_t count, InexactOut out, FlatFilter flt) {
-  extern __shared__ __align__(16) uint32_t flat_smem[];
-  constexpr uint32_t cap = FlatSmem<NR>::cap;
-  const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
-  uint32_t* kq = flat_smem + wib * FlatSmem<NR>::words_per_warp;
-  uint32_t* lq = kq + cap;
-  uint32_t* xq = lq + cap;
-  uint32_t* sq = xq + cap;
-  uint32_t* cq = sq + cap;
-  uint32_t* kr = cq + cap;
-  uint32_t* lr = kr + cap;
-  uint32_t* repw = lr + cap;
-  const uint32_t K = tf.k, kmax = tx ? kx : K;
+// Queues of one pass: survivors, their intervals (same index; k > l =
+// absent), and per pattern the segment both share.  seg_cnt bit 31: the
+// segment's first entry is W itself (diffs 0).
+struct FlatQueues {
+  FlatSurvivor* surv;
+  uint2* raw;
+  unsigned long long* n_surv;
+  uint64_t cap;
+  uint64_t* seg_base;
+  uint32_t* seg_cnt;
+};
+
+constexpr uint32_t kFlatExactBit = 0x80000000u;
+constexpr uint32_t kFlatMaxCand = 8u * 31u + 1u;  // candidates of the longest pattern (m <= 31)
+
+// ---- k_flat_probe ----------------------------------------------------------
+// Slot t of a pattern: t = 0 is W itself, then m substitution slots (the
+// three other characters at i), m insertion slots (the four characters after
+// W[i]; never W[i] itself unless i = 0), m deletion slots.  Every slot is one
+// splice — the first a characters of W, a gap of `put` characters, then W
+// from position i + 1 on — whose variants differ only in the gap, so a slot
+// computes one filter address and its variants read bits next to each other.
+// Branch-free: a warp holds every kind of slot.
+// NRS = rounds of 32 slots a lane takes (32 NRS >= 3m + 1).
+template <int NRS>
+__global__ void __launch_bounds__(256) k_flat_probe(CodePatterns cp, const uint32_t* __restrict__ list, uint64_t q0,
+                                                    uint64_t count, FlatFilter flt, FlatQueues fq, InexactOut out) {
+  const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt_mask = (1u << lane) - 1u;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   uint64_t work = 0;
-
-  // the next pattern is claimed and loaded while the current one is searched
-  uint64_t nq_id = 0, npw = 0, ndb = 0;
-  int nm = 0;
-  bool nvalid = false;
-  auto prefetch = [&]() {
-    unsigned long long slot = 0;
-    if (lane == 0u) slot = atomicAdd(out.next, 1ull);
-    slot = __shfl_sync(0xFFFFFFFFu, slot, 0);
-    nvalid = slot < count;
-    if (!nvalid) return;
-    nq_id = list ? list[slot] : slot;
+  for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < count; w += nwarps) {
+    const uint64_t q = list ? list[q0 + w] : q0 + w;
+    int m;
+    uint64_t pw;
     if (cp.packed1) {
-      nm = int(cp.fixed_m);
-      npw = cp.packed1[nq_id];
+      m = int(cp.fixed_m);
+      pw = cp.packed1[q];
     } else {
-      nm = int(cp.offsets[nq_id + 1] - cp.offsets[nq_id]);
-      npw = cp.packed[nq_id].x;
+      m = int(cp.offsets[q + 1] - cp.offsets[q]);
+      pw = cp.packed[q].x;
     }
-    ndb = cp.dbits[nq_id];
-  };
-  prefetch();
-
-  while (nvalid) {
-    const uint64_t q = nq_id;
-    const int m = nm;
-    const uint64_t pw = npw & (shl64(1ull, 2u * uint32_t(m)) - 1ull);  // m <= 31
-    const uint64_t db = ndb;
-    prefetch();
-    const uint32_t NC = 8u * uint32_t(m) + 1u;
-    uint32_t nres = 0;
-    uint32_t exact_idx = 0xFFFFFFFFu;  // result index of W itself
-    // a finished candidate joins the results
-    auto add_results = [&](bool done, uint32_t c, uint32_t k, uint32_t l) {
-      const uint32_t bd = __ballot_sync(0xFFFFFFFFu, done);
-      if (bd == 0u) return;
-      const uint32_t idx = nres + __popc(bd & lt_mask);
-      if (done) {
-        kr[idx] = k;
-        lr[idx] = l;
+    pw &= shl64(1ull, 2u * uint32_t(m)) - 1ull;  // m <= 31
+    const uint64_t db = cp.dbits[q];
+    if (__popcll(db) > 1) {  // two absent segments: nothing within one edit occurs
+      if (lane == 0u) {
+        fq.seg_base[q] = 0;
+        fq.seg_cnt[q] = 0u;
       }
-      const uint32_t be = __ballot_sync(0xFFFFFFFFu, done && c == NC - 1u);
-      if (be) exact_idx = __shfl_sync(0xFFFFFFFFu, idx, __ffs(be) - 1);
-      nres += __popc(bd);
-    };
-
-    if (__popcll(db) <= 1) {
-      // ---- the candidates worth searching: every probe issued, then read ----
-      uint32_t fw[NR];
-      uint32_t vmask = 0;
+      continue;
+    }
+    const uint32_t first_db = db ? uint32_t(__ffsll((long long)db) - 1) : 64u;
+    const uint32_t um = uint32_t(m);
+    uint64_t S0[NRS];
+    uint32_t meta[NRS];  // survivor variants (4 bits) | a << 8 | L << 16
+    uint32_t total = 0, pre[NRS];
 #pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const uint32_t c = uint32_t(r) * 32u + lane;
-        uint64_t S;
-        int L;
-        fw[r] = 1u;
-        if (c < NC && flat_candidate(pw, m, db, c, S, L)) {
-          vmask |= 1u << r;
-          if (flt.bits && uint32_t(L) >= flt.B) {
-            uint32_t bit;
-            const uint64_t a = filter_probe_addr(flt, c, m, S, L, bit);
-            fw[r] = ld_filter_word(flt.bits + a) >> bit;
+    for (int r = 0; r < NRS; ++r) {
+      const uint32_t t = uint32_t(r) * 32u + lane;
+      const bool is_w = t == 0u, slot_ok = t <= 3u * um;
+      const uint32_t u = t - 1u;
+      const uint32_t ty = is_w ? 0u : (u >= um ? 1u : 0u) + (u >= 2u * um ? 1u : 0u);  // 0 sub, 1 ins, 2 del
+      const uint32_t i = is_w ? 0u : u - ty * um;
+      const uint32_t wi = uint32_t(shr64(pw, 2u * i)) & 3u;
+      const uint32_t wprev = uint32_t(shr64(pw, 2u * i - 2u)) & 3u;  // W[i-1] (i >= 1; unused otherwise)
+      const bool prev_ok = first_db >= i, cur_ok = first_db > i;
+      const uint32_t others = 0xFu & ~(1u << wi);
+      uint32_t vm = ty == 0u ? (prev_ok ? others : 0u)
+                  : ty == 1u ? (cur_ok ? (i == 0u ? 0xFu : others) : 0u)
+                             : ((prev_ok && !(i >= 1u && wi == wprev)) ? 1u : 0u);
+      if (is_w) vm = db == 0ull ? 1u : 0u;
+      if (!slot_ok) vm = 0u;
+      const uint32_t a = is_w ? 0u : i + (ty == 1u ? 1u : 0u);
+      const uint32_t put = ty == 2u ? 0u : 1u;
+      const uint64_t low = pw & (shl64(1ull, 2u * a) - 1ull);
+      const uint64_t high = shl64(shr64(pw, 2u * i + 2u), 2u * (a + put));
+      const uint64_t s0 = is_w ? pw : (low | high);
+      const uint32_t L = um + (is_w ? 0u : (ty == 1u ? 1u : 0u)) - ((!is_w && ty == 2u) ? 1u : 0u);
+      uint32_t sm = vm;
+      if (flt.bits && L >= flt.B && vm) {
+        // the window that holds the edit: the first one when it does, else the last
+        const uint32_t e = is_w ? 0u : ty == 2u ? min(a, L - 1u) : a;
+        const uint32_t ws = e < flt.B ? 0u : L - flt.B;
+        const uint32_t p = e - ws;
+        const uint32_t o = min(__umulhi(p, flt.rcpG), flt.NO - 1u);
+        const uint32_t gs = min(o * flt.G, flt.B - flt.G);
+        const uint64_t key0 = filter_key(flt, shr64(s0, 2u * ws) & (shl64(1ull, 2u * flt.B) - 1ull), o);
+        uint32_t got = 0;
+#pragma unroll
+        for (uint32_t b = 0; b < 4u; ++b) {
+          const uint64_t key = key0 | (uint64_t(b) << (2u * (p - gs)));  // the gap is inside the copy's group
+          if ((vm >> b) & 1u) {
+            got |= ((ld_filter_word(flt.bits + filter_word(flt, key, o)) >> (uint32_t(key) & 31u)) & 1u) << b;
             work += 1ull;  // one sector, no Occ step
           }
         }
+        sm = got;
       }
-      uint32_t nc = 0;
+      S0[r] = s0;
+      meta[r] = sm | (a << 8) | (L << 16);
+      // this round's survivors: offsets within the pattern's segment
+      const uint32_t cnt = uint32_t(__popc(sm));
+      uint32_t prefix = 0, rt = 0;
 #pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const bool pass = ((vmask >> r) & 1u) && (fw[r] & 1u);
-        const uint32_t bp = __ballot_sync(0xFFFFFFFFu, pass);
-        if (pass) cq[nc + __popc(bp & lt_mask)] = uint32_t(r) * 32u + lane;
-        nc += __popc(bp);
+      for (int bit = 0; bit < 3; ++bit) {
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, (cnt >> bit) & 1u);
+        prefix += uint32_t(__popc(bal & lt_mask)) << bit;
+        rt += uint32_t(__popc(bal)) << bit;
       }
-      __syncwarp();
-      // ---- their table gathers (two chunks of 32 in flight), finished ones
-      // to the results, the others to the continuation queue ----
-      uint32_t nq = 0;
-      for (uint32_t base = 0; base < nc; base += 64u) {
-        uint2 e[2];
-        uint32_t cc[2], s32[2];
-        int pos[2];
-        bool go[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const uint32_t j = base + 32u * u + lane;
-          go[u] = j < nc;
-          cc[u] = 0u, s32[u] = 0u, pos[u] = -1;
-          e[u] = make_uint2(1u, 0u);
-          if (u == 1 && base + 32u >= nc) continue;  // warp-uniform
-          if (go[u]) {
-            cc[u] = cq[j];
-            uint64_t S;
-            int L;
-            flat_candidate(pw, m, db, cc[u], S, L);
-            s32[u] = uint32_t(S);
-            e[u] = make_uint2(0u, ix.n);  // the empty string (a deletion from m = 1)
-            const uint32_t d = min(uint32_t(L), kmax);
-            pos[u] = L - int(d) - 1;  // next character to prepend
-            if (L > 0) {
-              const uint32_t key = uint32_t(S >> (2u * (uint32_t(L) - d))) & uint32_t(shl64(1ull, 2u * d) - 1ull);
-              e[u] = ld_table_entry(d > K ? tx + key : tf.base + PrefixTable::off(d) + key);
-              work += work_unit(1u);
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          if (u == 1 && base + 32u >= nc) continue;
-          const bool alive = go[u] && e[u].x <= e[u].y;
-          const bool cont = alive && pos[u] >= 0;
-          add_results(alive && pos[u] < 0, cc[u], e[u].x, e[u].y);
-          const uint32_t bc = __ballot_sync(0xFFFFFFFFu, cont);
-          if (cont) {
-            const uint32_t slot = nq + __popc(bc & lt_mask);
-            kq[slot] = e[u].x;
-            lq[slot] = e[u].y;
-            xq[slot] = cc[u] | (uint32_t(pos[u]) << 16);
-            sq[slot] = s32[u];
-          }
-          nq += __popc(bc);
-        }
+      pre[r] = total + prefix;
+      total += rt;
+    }
+    const uint32_t has_exact = __shfl_sync(0xFFFFFFFFu, meta[0] & 1u, 0);  // slot 0 = W itself, first in the segment
+    unsigned long long base = 0;
+    if (lane == 0u && total) base = atomicAdd(fq.n_surv, (unsigned long long)total);
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    if (base + total > fq.cap) {  // the chunk's patterns kept more candidates than it was sized for: retried
+      if (lane == 0u) {
+        const unsigned long long f = atomicAdd(out.fail_count, 1ull);
+        out.fail_list[f] = uint32_t(q);
+        out.res_cnt[q] = 0u;
+        fq.seg_base[q] = 0;
+        fq.seg_cnt[q] = 0xFFFFFFFFu;  // k_flat_collect skips it
       }
-      __syncwarp();
-      // ---- level by level: one backward step for every queued candidate ----
-      while (nq > 0u) {
-        uint32_t nnew = 0;
-        for (uint32_t base = 0; base < nq; base += 64u) {
-          const bool two = base + 32u < nq;  // warp-uniform
-          uint32_t k[2], l[2], x[2], sv[2];
-          bool go[2];
-          StepLines<W> sl[2];
+      continue;
+    }
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const uint32_t j = base + 32u * u + lane;
-            go[u] = j < nq;
-            k[u] = go[u] ? kq[j] : 1u;
-            l[u] = go[u] ? lq[j] : 0u;
-            x[u] = go[u] ? xq[j] : 0u;
-            sv[u] = go[u] ? sq[j] : 0u;
-          }
-          __syncwarp();  // the chunk is in registers before its slots are reused (nnew <= base + 64)
-          step_load<W>(ix, go[0], k[0], l[0], sl[0]);
-          if (two) step_load<W>(ix, go[1], k[1], l[1], sl[1]);
+    for (int r = 0; r < NRS; ++r) {
+      const uint32_t a = (meta[r] >> 8) & 0xFFu, L = meta[r] >> 16;
+      uint64_t slot = base + pre[r];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            if (u == 1 && !two) continue;
-            const uint32_t c = x[u] & 0xFFFFu, pos = x[u] >> 16;
-            uint32_t sym = (sv[u] >> (2u * (pos & 15u))) & 3u;
-            if (pos >= 16u) {  // beyond the 16 characters the queue carries (never in production shapes)
-              uint64_t S;
-              int L;
-              flat_candidate(pw, m, db, c, S, L);
-              sym = uint32_t(S >> (2u * pos)) & 3u;
-            }
-            if (go[u]) work += work_unit(sl[u].jl != sl[u].jh ? 2u : 1u);
-            step_finish<W>(ix, sl[u], sym, k[u], l[u]);
-            const bool alive = go[u] && k[u] <= l[u];
-            const bool cont = alive && pos != 0u;
-            add_results(alive && pos == 0u, c, k[u], l[u]);
-            const uint32_t bc = __ballot_sync(0xFFFFFFFFu, cont);
-            if (cont) {
-              const uint32_t slot = nnew + __popc(bc & lt_mask);
-              kq[slot] = k[u];
-              lq[slot] = l[u];
-              xq[slot] = c | ((pos - 1u) << 16);
-              sq[slot] = sv[u];
-            }
-            nnew += __popc(bc);
-          }
+      for (uint32_t b = 0; b < 4u; ++b) {
+        if ((meta[r] >> b) & 1u) {
+          FlatSurvivor sv;
+          sv.S = S0[r] | shl64(uint64_t(b), 2u * a);
+          sv.q = uint32_t(q);
+          sv.L = L;
+          fq.surv[slot++] = sv;
         }
-        nq = nnew;
-        __syncwarp();
       }
     }
+    if (lane == 0u) {
+      fq.seg_base[q] = base;
+      fq.seg_cnt[q] = total | (has_exact ? kFlatExactBit : 0u);
+    }
+  }
+  flush_work(out.steps, work);
+}
 
-    // ---- results: representatives (first of each interval, W itself before
-    // the others), their rank among the distinct intervals, one reservation,
-    // ordered write ----
-    __syncwarp();
+// ---- k_flat_extend ---------------------------------------------------------
+template <int W>
+__global__ void __launch_bounds__(256) k_flat_extend(IndexView ix, PrefixTable tf, const uint2* __restrict__ tx,
+                                                     uint32_t kx, FlatQueues fq, unsigned long long* steps) {
+  const uint64_t n = min(uint64_t(*fq.n_surv), fq.cap);
+  const uint32_t K = tf.k, kmax = tx ? kx : K;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t work = 0;
+  for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n; t += stride) {
+    const FlatSurvivor sv = fq.surv[t];
+    const uint32_t L = sv.L;
+    const uint32_t d = min(L, kmax);
+    uint2 e = make_uint2(0u, ix.n);  // the empty string (a deletion from m = 1)
+    if (L > 0u) {
+      const uint32_t key = uint32_t(shr64(sv.S, 2u * (L - d))) & uint32_t(shl64(1ull, 2u * d) - 1ull);
+      e = ld_table_entry(d > K ? tx + key : tf.base + PrefixTable::off(d) + key);
+      work += work_unit(1u);
+    }
+    uint32_t k = e.x, l = e.y;
+    int pos = int(L) - int(d) - 1;  // next character to prepend
+    while (k <= l && pos >= 0) {
+      StepLines<W> sl;
+      step_load<W>(ix, true, k, l, sl);
+      work += work_unit(sl.jl != sl.jh ? 2u : 1u);
+      step_finish<W>(ix, sl, uint32_t(shr64(sv.S, 2u * uint32_t(pos))) & 3u, k, l);
+      --pos;
+    }
+    fq.raw[t] = k <= l ? make_uint2(k, l) : make_uint2(1u, 0u);
+  }
+  flush_work(steps, work);
+}
+
+// ---- k_flat_collect --------------------------------------------------------
+// Results of a pattern: representatives (first of each interval, W itself
+// before the others), their rank among the distinct intervals, one
+// reservation, ordered write.  128 threads = 4 patterns per block at a time.
+__global__ void __launch_bounds__(128) k_flat_collect(const uint32_t* __restrict__ list, uint64_t q0, uint64_t count,
+                                                      FlatQueues fq, InexactOut out) {
+  constexpr uint32_t cap = 256u;  // >= kFlatMaxCand
+  __shared__ uint32_t sm[4][2u * cap + 8u];
+  const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  uint32_t* kr = sm[wib];
+  uint32_t* lr = kr + cap;
+  uint32_t* repw = lr + cap;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < count; w += nwarps) {
+    const uint64_t q = list ? list[q0 + w] : q0 + w;
+    const uint32_t sc = fq.seg_cnt[q];
+    if (sc == 0xFFFFFFFFu) continue;  // did not fit this pass (already on the retry list)
+    const uint32_t cnt = sc & ~kFlatExactBit;
+    const uint64_t base = fq.seg_base[q];
+    uint32_t nres = 0;
+    uint32_t exact_idx = 0xFFFFFFFFu;  // result index of W itself
+    uint32_t mk = 0xFFFFFFFFu, ml = lane;  // this lane's result when nres <= 32
+    if (cnt <= 32u) {
+      uint2 e = make_uint2(1u, 0u);
+      if (lane < cnt) e = fq.raw[base + lane];
+      const bool alive = e.x <= e.y;
+      const uint32_t ba = __ballot_sync(0xFFFFFFFFu, alive);
+      nres = uint32_t(__popc(ba));
+      if ((sc & kFlatExactBit) && (ba & 1u)) exact_idx = 0u;
+      // compact to lanes 0..nres-1 (source lane of result j = the j-th set bit of ba)
+      const uint32_t src = __fns(ba, 0, int(lane) + 1);
+      const uint32_t sk = __shfl_sync(0xFFFFFFFFu, e.x, src & 31u), sl = __shfl_sync(0xFFFFFFFFu, e.y, src & 31u);
+      if (lane < nres) mk = sk, ml = sl;
+    } else {
+      __syncwarp();
+      for (uint32_t j0 = 0; j0 < cnt; j0 += 32u) {
+        uint2 e = make_uint2(1u, 0u);
+        if (j0 + lane < cnt) e = fq.raw[base + j0 + lane];
+        const bool alive = e.x <= e.y;
+        const uint32_t ba = __ballot_sync(0xFFFFFFFFu, alive);
+        if (alive) {
+          const uint32_t idx = nres + uint32_t(__popc(ba & lt_mask));
+          kr[idx] = e.x;
+          lr[idx] = e.y;
+        }
+        if (j0 == 0u && (sc & kFlatExactBit) && (ba & 1u)) exact_idx = 0u;
+        nres += uint32_t(__popc(ba));
+      }
+      __syncwarp();
+      if (nres <= 32u && lane < nres) mk = kr[lane], ml = lr[lane];
+    }
     if (nres <= 32u) {
       // one result per lane: equal intervals found by one match instruction
       const bool have = lane < nres;
-      const uint32_t mk = have ? kr[lane] : 0xFFFFFFFFu, ml = have ? lr[lane] : lane;
       const unsigned long long key = (uint64_t(mk) << 32) | ml;
       const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
       const uint32_t be = exact_idx < 32u ? (1u << exact_idx) : 0u;
@@ -444,7 +420,6 @@ __global__ void __launch_bounds__(128, FMG_FLAT_MINB) k_z1_flat(IndexView ix, Pr
           out.fail_list[f] = uint32_t(q);
           out.res_cnt[q] = 0u;
         }
-        __syncwarp();
         continue;
       }
       uint32_t rank = 0;
@@ -461,7 +436,6 @@ __global__ void __launch_bounds__(128, FMG_FLAT_MINB) k_z1_flat(IndexView ix, Pr
         out.res_cnt[q] = nuniq;
         out.res_pass[q] = out.pass;
       }
-      __syncwarp();
       continue;
     }
     uint32_t rep_bits = 0;  // bit t: result 32 t + lane represents its interval
@@ -469,12 +443,12 @@ __global__ void __launch_bounds__(128, FMG_FLAT_MINB) k_z1_flat(IndexView ix, Pr
     for (uint32_t t = 0; t * 32u < nres; ++t) {
       const uint32_t r = t * 32u + lane;
       const bool have = r < nres;
-      const uint32_t mk = kr[have ? r : 0u], ml = lr[have ? r : 0u];
+      const uint32_t rk = kr[have ? r : 0u], rl = lr[have ? r : 0u];
       const uint32_t md = r == exact_idx ? 0u : 1u;
       bool rep = have;
       for (uint32_t j = 0; j < nres; ++j) {
         const uint32_t dj = j == exact_idx ? 0u : 1u;
-        if (kr[j] == mk && lr[j] == ml && (dj < md || (dj == md && j < r))) rep = false;
+        if (kr[j] == rk && lr[j] == rl && (dj < md || (dj == md && j < r))) rep = false;
       }
       const uint32_t br = __ballot_sync(0xFFFFFFFFu, rep);
       if (lane == 0u) repw[t] = br;
@@ -497,13 +471,13 @@ __global__ void __launch_bounds__(128, FMG_FLAT_MINB) k_z1_flat(IndexView ix, Pr
     for (uint32_t t = 0; t * 32u < nres; ++t) {
       const uint32_t r = t * 32u + lane;
       if (r < nres && ((rep_bits >> t) & 1u)) {
-        const uint32_t mk = kr[r], ml = lr[r];
+        const uint32_t rk = kr[r], rl = lr[r];
         uint32_t rank = 0;
         for (uint32_t j = 0; j < nres; ++j) {
           const uint32_t kj = kr[j], lj = lr[j];
-          rank += (((repw[j >> 5] >> (j & 31u)) & 1u) && (kj < mk || (kj == mk && lj < ml))) ? 1u : 0u;
+          rank += (((repw[j >> 5] >> (j & 31u)) & 1u) && (kj < rk || (kj == rk && lj < rl))) ? 1u : 0u;
         }
-        out.kl[o + rank] = make_uint2(mk, ml);
+        out.kl[o + rank] = make_uint2(rk, rl);
         out.diffs[o + rank] = r == exact_idx ? uint8_t(0) : uint8_t(1);
       }
     }
@@ -514,7 +488,6 @@ __global__ void __launch_bounds__(128, FMG_FLAT_MINB) k_z1_flat(IndexView ix, Pr
     }
     __syncwarp();
   }
-  flush_work(out.steps, work);
 }
 
 // Filter build: entry x of the level-kx table (a present kx-mer and its

@@ -509,7 +509,7 @@ def test_inexact_bidirectional_engine(gpu, monkeypatch, n, lens, engine):
 @pytest.mark.parametrize("n,lens", [(200_000, (1, 2, 3, 5, 8, 9, 10, 11, 12, 19, 20, 27, 31)),
                                     (3_000, (1, 2, 4, 7, 12, 19, 25, 31)), (40, (1, 2, 3, 6, 9, 14)),
                                     (200_000, (9, 10, 11)), (200_000, (17, 18, 19))])
-@pytest.mark.parametrize("filt", ["default", "off", "copies1_d1", "copies2_d3"])
+@pytest.mark.parametrize("filt", ["default", "off", "copies1_d1", "copies2_d3", "overflow"])
 def test_inexact_flat_engine(gpu, monkeypatch, n, lens, filt):
     """z = 1 through the flat engine (kernels_flat.cuh: a warp per pattern, one table gather
     per string of the one-edit neighbourhood, survivors extended level by level): patterns
@@ -521,6 +521,8 @@ def test_inexact_flat_engine(gpu, monkeypatch, n, lens, filt):
     monkeypatch.setenv("FMG_BIDIR_ENGINE", "flat")
     if filt == "off":
         monkeypatch.setenv("FMG_FLAT_FILTER", "0")
+    elif filt == "overflow":  # a survivor queue of 3 entries per pattern: most patterns go to the retry passes
+        monkeypatch.setenv("FMG_FLAT_PER_PAT", "3")
     elif filt != "default":
         copies, d = filt.split("_")
         monkeypatch.setenv("FMG_FLAT_FILTER_NO", copies[-1])
@@ -572,12 +574,12 @@ def test_inexact_flat_engine(gpu, monkeypatch, n, lens, filt):
                                                  ct.byref(fc), None))
     kk, nb = ct.c_uint32(), ct.c_uint64()
     _lib.check(_lib.load().fmgx_prefix_table(idx.device_index().handle, ct.byref(kk), ct.byref(nb)))
-    depth = 2 if filt == "default" else int(filt[-1]) if filt != "off" else 0
+    depth = 2 if filt in ("default", "overflow") else int(filt[-1]) if filt != "off" else 0
     if filt == "off":
         assert fc.value == 0
     elif max(lens) >= kk.value + depth:  # some candidate is long enough for a window
         assert fb.value == kk.value + depth and fg.value * fc.value >= fb.value
-        assert fc.value == ((fb.value + 3) // 4 if filt == "default" else int(filt[6]))
+        assert fc.value == ((fb.value + 3) // 4 if filt in ("default", "overflow") else int(filt[6]))
     monkeypatch.setenv("FMG_BIDIR_ENGINE", "dfs")
     b = fm.inexact_search_batch(idx, pats, 1)
     assert np.array_equal(b.offsets, ms.offsets) and np.array_equal(b.k, ms.k) and np.array_equal(b.diffs, ms.diffs)
