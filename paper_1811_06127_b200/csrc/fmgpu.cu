@@ -1119,7 +1119,9 @@ FlatFilter flat_filter(const fmg_index* cix, const uint2* tx, uint32_t kx, uint6
     uint32_t NO = (B + 3) / 4;
     if (const char* e = std::getenv("FMG_FLAT_FILTER_NO")) NO = std::min<uint32_t>((B + 1) / 2, std::max(1, std::atoi(e)));
     const size_t room = available_bytes(ix->device) / 3;
-    while (NO > 1 && bytes_per * NO > room) --NO;
+    const uint32_t no_min = (B + 14) / 15;  // G <= 15: a variant's bit offset fits 32 bits (k_flat_probe)
+    NO = std::max(NO, no_min);
+    while (NO > no_min && bytes_per * NO > room) --NO;
     if (bytes_per * NO > room) return {};
     uint32_t* bits = nullptr;
     if (dmalloc(&bits, bytes_per * NO) != cudaSuccess) {
@@ -1420,7 +1422,11 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       const void* kp = nrs == 1 ? (const void*)k_flat_probe<1> : nrs == 2 ? (const void*)k_flat_probe<2>
                                                                            : (const void*)k_flat_probe<3>;
       const int bp = std::max(1, blocks_per_sm(kp, 256, 0)) * ix->sms;
-      const int bc = std::max(1, blocks_per_sm((const void*)k_flat_collect, 128, 0)) * ix->sms;
+      // with the filter a pattern's survivor segment is also its output
+      // reservation (no atomics); without one the rows are reserved exactly
+      const bool seg_rows = flt.bits != nullptr;
+      const int bc = std::max(1, blocks_per_sm(seg_rows ? (const void*)k_flat_collect<true>
+                                                        : (const void*)k_flat_collect<false>, 256, 0)) * ix->sms;
       int be = 1;
       with_words(ix, [&](auto wt) {
         be = std::max(1, blocks_per_sm((const void*)k_flat_extend<decltype(wt)::value>, 256, 0)) * ix->sms;
@@ -1436,8 +1442,13 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
           constexpr int W = decltype(wt)::value;
           k_flat_extend<W><<<unsigned(be), 256, 0, s>>>(ix->view(), pt, flat_tx, flat_kx, fq, counters.ptr + 2);
         });
-        const unsigned gc = unsigned(std::min<uint64_t>(uint64_t(bc), (cn + 3) / 4));  // 4 warps per block
-        k_flat_collect<<<gc, 128, 0, s>>>(nullptr, c0, cn, fq, o);
+        const unsigned gc = unsigned(std::min<uint64_t>(uint64_t(bc), (cn + 7) / 8));  // 8 warps per block
+        if (seg_rows) {
+          k_flat_collect<true><<<gc, 256, 0, s>>>(nullptr, c0, cn, fq, o);
+          k_flat_advance<<<1, 1, 0, s>>>(counters.ptr, n_surv.ptr, q_cap);
+        } else {
+          k_flat_collect<false><<<gc, 256, 0, s>>>(nullptr, c0, cn, fq, o);
+        }
         FMG_CK(cudaGetLastError());
       }
       unsigned long long host_ctr[2];

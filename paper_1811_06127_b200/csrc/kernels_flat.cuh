@@ -195,14 +195,19 @@ constexpr uint32_t kFlatMaxCand = 8u * 31u + 1u;  // candidates of the longest p
 template <int NRS>
 __global__ void __launch_bounds__(256) k_flat_probe(CodePatterns cp, const uint32_t* __restrict__ list, uint64_t q0,
                                                     uint64_t count, FlatFilter flt, FlatQueues fq, InexactOut out) {
-  const uint32_t lane = threadIdx.x & 31u;
+  // one queue reservation per block and round of patterns (a same-address
+  // atomic per pattern capped the kernel at ~0.6 G patterns/s)
+  __shared__ uint32_t s_tot[8];
+  __shared__ unsigned long long s_base;
+  const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t per_round = uint64_t(gridDim.x) * 8u;
   uint64_t work = 0;
-  for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < count; w += nwarps) {
-    const uint64_t q = list ? list[q0 + w] : q0 + w;
-    int m;
-    uint64_t pw;
+  // pattern words of the next round are loaded while this one is probed
+  auto load_pattern = [&](uint64_t w, uint64_t& q, int& m, uint64_t& pw, uint64_t& db) {
+    q = 0, m = 0, pw = 0, db = 0;
+    if (w >= count) return;
+    q = list ? list[q0 + w] : q0 + w;
     if (cp.packed1) {
       m = int(cp.fixed_m);
       pw = cp.packed1[q];
@@ -210,15 +215,19 @@ __global__ void __launch_bounds__(256) k_flat_probe(CodePatterns cp, const uint3
       m = int(cp.offsets[q + 1] - cp.offsets[q]);
       pw = cp.packed[q].x;
     }
-    pw &= shl64(1ull, 2u * uint32_t(m)) - 1ull;  // m <= 31
-    const uint64_t db = cp.dbits[q];
-    if (__popcll(db) > 1) {  // two absent segments: nothing within one edit occurs
-      if (lane == 0u) {
-        fq.seg_base[q] = 0;
-        fq.seg_cnt[q] = 0u;
-      }
-      continue;
-    }
+    db = cp.dbits[q];
+  };
+  uint64_t nq, npw, ndb;
+  int nm;
+  load_pattern(uint64_t(blockIdx.x) * 8u + wib, nq, nm, npw, ndb);
+  for (uint64_t wb = uint64_t(blockIdx.x) * 8u; wb < count; wb += per_round) {
+    const bool active = wb + wib < count;
+    const uint64_t q = nq, db = ndb;
+    const int m = nm;
+    const uint64_t pw = npw & (shl64(1ull, 2u * uint32_t(m)) - 1ull);  // m <= 31
+    load_pattern(wb + per_round + wib, nq, nm, npw, ndb);
+    // two absent segments: nothing within one edit occurs
+    const bool search = active && __popcll(db) <= 1;
     const uint32_t first_db = db ? uint32_t(__ffsll((long long)db) - 1) : 64u;
     const uint32_t um = uint32_t(m);
     uint64_t S0[NRS];
@@ -227,7 +236,7 @@ __global__ void __launch_bounds__(256) k_flat_probe(CodePatterns cp, const uint3
 #pragma unroll
     for (int r = 0; r < NRS; ++r) {
       const uint32_t t = uint32_t(r) * 32u + lane;
-      const bool is_w = t == 0u, slot_ok = t <= 3u * um;
+      const bool is_w = t == 0u, slot_ok = search && t <= 3u * um;
       const uint32_t u = t - 1u;
       const uint32_t ty = is_w ? 0u : (u >= um ? 1u : 0u) + (u >= 2u * um ? 1u : 0u);  // 0 sub, 1 ins, 2 del
       const uint32_t i = is_w ? 0u : u - ty * um;
@@ -255,15 +264,17 @@ __global__ void __launch_bounds__(256) k_flat_probe(CodePatterns cp, const uint3
         const uint32_t o = min(__umulhi(p, flt.rcpG), flt.NO - 1u);
         const uint32_t gs = min(o * flt.G, flt.B - flt.G);
         const uint64_t key0 = filter_key(flt, shr64(s0, 2u * ws) & (shl64(1ull, 2u * flt.B) - 1ull), o);
+        // variant b sets the gap digit (zero in key0, inside the copy's group,
+        // below bit 2G): the word and bit of each variant by 32-bit offsets
+        const uint32_t* w0 = flt.bits + filter_word(flt, key0, o);
+        const uint32_t bit0 = uint32_t(key0) & 31u, sh = 2u * (p - gs);
         uint32_t got = 0;
 #pragma unroll
         for (uint32_t b = 0; b < 4u; ++b) {
-          const uint64_t key = key0 | (uint64_t(b) << (2u * (p - gs)));  // the gap is inside the copy's group
-          if ((vm >> b) & 1u) {
-            got |= ((ld_filter_word(flt.bits + filter_word(flt, key, o)) >> (uint32_t(key) & 31u)) & 1u) << b;
-            work += 1ull;  // one sector, no Occ step
-          }
+          const uint32_t delta = (b << sh) + bit0;  // no carry into a set bit: key0's gap digit is zero
+          if ((vm >> b) & 1u) got |= ((ld_filter_word(w0 + (delta >> 5)) >> (delta & 31u)) & 1u) << b;
         }
+        work += uint64_t(__popc(vm));  // one sector each, no Occ step
         sm = got;
       }
       S0[r] = s0;
@@ -281,9 +292,22 @@ __global__ void __launch_bounds__(256) k_flat_probe(CodePatterns cp, const uint3
       total += rt;
     }
     const uint32_t has_exact = __shfl_sync(0xFFFFFFFFu, meta[0] & 1u, 0);  // slot 0 = W itself, first in the segment
-    unsigned long long base = 0;
-    if (lane == 0u && total) base = atomicAdd(fq.n_surv, (unsigned long long)total);
-    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    if (lane == 0u) s_tot[wib] = total;
+    __syncthreads();
+    if (threadIdx.x == 0u) {
+      uint32_t sum = 0;
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const uint32_t c = s_tot[v];
+        s_tot[v] = sum;  // exclusive prefix: each warp's offset in the block's reservation
+        sum += c;
+      }
+      s_base = sum ? atomicAdd(fq.n_surv, (unsigned long long)sum) : 0ull;
+    }
+    __syncthreads();
+    const unsigned long long base = s_base + s_tot[wib];
+    __syncthreads();  // s_tot / s_base are rewritten by the next round
+    if (!active) continue;
     if (base + total > fq.cap) {  // the chunk's patterns kept more candidates than it was sized for: retried
       if (lane == 0u) {
         const unsigned long long f = atomicAdd(out.fail_count, 1ull);
@@ -298,15 +322,13 @@ __global__ void __launch_bounds__(256) k_flat_probe(CodePatterns cp, const uint3
     for (int r = 0; r < NRS; ++r) {
       const uint32_t a = (meta[r] >> 8) & 0xFFu, L = meta[r] >> 16;
       uint64_t slot = base + pre[r];
-#pragma unroll
-      for (uint32_t b = 0; b < 4u; ++b) {
-        if ((meta[r] >> b) & 1u) {
-          FlatSurvivor sv;
-          sv.S = S0[r] | shl64(uint64_t(b), 2u * a);
-          sv.q = uint32_t(q);
-          sv.L = L;
-          fq.surv[slot++] = sv;
-        }
+      for (uint32_t rest = meta[r] & 0xFu; rest; rest &= rest - 1u) {  // few lanes keep anything: a short loop
+        const uint32_t b = uint32_t(__ffs(rest)) - 1u;
+        FlatSurvivor sv;
+        sv.S = S0[r] | shl64(uint64_t(b), 2u * a);
+        sv.q = uint32_t(q);
+        sv.L = L;
+        fq.surv[slot++] = sv;
       }
     }
     if (lane == 0u) {
@@ -351,76 +373,63 @@ __global__ void __launch_bounds__(256) k_flat_extend(IndexView ix, PrefixTable t
 
 // ---- k_flat_collect --------------------------------------------------------
 // Results of a pattern: representatives (first of each interval, W itself
-// before the others), their rank among the distinct intervals, one
-// reservation, ordered write.  128 threads = 4 patterns per block at a time.
-__global__ void __launch_bounds__(128) k_flat_collect(const uint32_t* __restrict__ list, uint64_t q0, uint64_t count,
+// before the others), their rank among the distinct intervals, ordered write.
+// A warp per pattern; at most 32 candidates of the pattern survived the
+// filter in the common case, so each lane holds one and a match instruction
+// finds the equal intervals.  Output rows: with the filter the pattern's
+// survivor segment doubles as its reservation (rows *out.total + seg_base ..;
+// no atomics — k_flat_advance moves *out.total past the chunk afterwards);
+// without one (every candidate is a survivor, few are results) one atomic
+// per pattern reserves exactly the rows used.
+template <bool kSegmentRows>
+__global__ void __launch_bounds__(256) k_flat_collect(const uint32_t* __restrict__ list, uint64_t q0, uint64_t count,
                                                       FlatQueues fq, InexactOut out) {
   constexpr uint32_t cap = 256u;  // >= kFlatMaxCand
-  __shared__ uint32_t sm[4][2u * cap + 8u];
+  __shared__ uint32_t sm[8][2u * cap + 8u];
   const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
   uint32_t* kr = sm[wib];
   uint32_t* lr = kr + cap;
   uint32_t* repw = lr + cap;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const unsigned long long chunk_rows = kSegmentRows ? *out.total : 0ull;
   for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < count; w += nwarps) {
     const uint64_t q = list ? list[q0 + w] : q0 + w;
     const uint32_t sc = fq.seg_cnt[q];
     if (sc == 0xFFFFFFFFu) continue;  // did not fit this pass (already on the retry list)
     const uint32_t cnt = sc & ~kFlatExactBit;
     const uint64_t base = fq.seg_base[q];
-    uint32_t nres = 0;
-    uint32_t exact_idx = 0xFFFFFFFFu;  // result index of W itself
-    uint32_t mk = 0xFFFFFFFFu, ml = lane;  // this lane's result when nres <= 32
+    // reserve (or fail) first when the segment is the reservation
+    unsigned long long o = chunk_rows + base;
+    auto fail = [&]() {  // this pass's buffer is full: retried by the next pass
+      if (lane == 0u) {
+        const unsigned long long f = atomicAdd(out.fail_count, 1ull);
+        out.fail_list[f] = uint32_t(q);
+        out.res_cnt[q] = 0u;
+      }
+    };
+    if (kSegmentRows && o + cnt > out.cap) {
+      fail();
+      continue;
+    }
     if (cnt <= 32u) {
+      // one candidate per lane: equal intervals found by one match instruction
       uint2 e = make_uint2(1u, 0u);
       if (lane < cnt) e = fq.raw[base + lane];
       const bool alive = e.x <= e.y;
-      const uint32_t ba = __ballot_sync(0xFFFFFFFFu, alive);
-      nres = uint32_t(__popc(ba));
-      if ((sc & kFlatExactBit) && (ba & 1u)) exact_idx = 0u;
-      // compact to lanes 0..nres-1 (source lane of result j = the j-th set bit of ba)
-      const uint32_t src = __fns(ba, 0, int(lane) + 1);
-      const uint32_t sk = __shfl_sync(0xFFFFFFFFu, e.x, src & 31u), sl = __shfl_sync(0xFFFFFFFFu, e.y, src & 31u);
-      if (lane < nres) mk = sk, ml = sl;
-    } else {
-      __syncwarp();
-      for (uint32_t j0 = 0; j0 < cnt; j0 += 32u) {
-        uint2 e = make_uint2(1u, 0u);
-        if (j0 + lane < cnt) e = fq.raw[base + j0 + lane];
-        const bool alive = e.x <= e.y;
-        const uint32_t ba = __ballot_sync(0xFFFFFFFFu, alive);
-        if (alive) {
-          const uint32_t idx = nres + uint32_t(__popc(ba & lt_mask));
-          kr[idx] = e.x;
-          lr[idx] = e.y;
-        }
-        if (j0 == 0u && (sc & kFlatExactBit) && (ba & 1u)) exact_idx = 0u;
-        nres += uint32_t(__popc(ba));
-      }
-      __syncwarp();
-      if (nres <= 32u && lane < nres) mk = kr[lane], ml = lr[lane];
-    }
-    if (nres <= 32u) {
-      // one result per lane: equal intervals found by one match instruction
-      const bool have = lane < nres;
-      const unsigned long long key = (uint64_t(mk) << 32) | ml;
+      const unsigned long long key = alive ? ((uint64_t(e.x) << 32) | e.y) : (0xFFFFFFFF00000000ull | lane);
       const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
-      const uint32_t be = exact_idx < 32u ? (1u << exact_idx) : 0u;
-      const bool with_exact = (peers & be) != 0u;
-      const bool rep = have && (with_exact ? lane == exact_idx : lane == uint32_t(__ffs(peers) - 1));
+      const bool with_exact = (sc & kFlatExactBit) && (peers & 1u);  // lane 0 = W itself
+      const bool rep = alive && (with_exact ? lane == 0u : lane == uint32_t(__ffs(peers) - 1));
       const uint32_t repmask = __ballot_sync(0xFFFFFFFFu, rep);
-      const uint32_t nuniq = __popc(repmask);
-      unsigned long long o = 0;
-      if (lane == 0u && nuniq) o = atomicAdd(out.total, (unsigned long long)nuniq);
-      o = __shfl_sync(0xFFFFFFFFu, o, 0);
-      if (o + nuniq > out.cap) {  // this pass's buffer is full: retried by the next pass
-        if (lane == 0u) {
-          const unsigned long long f = atomicAdd(out.fail_count, 1ull);
-          out.fail_list[f] = uint32_t(q);
-          out.res_cnt[q] = 0u;
+      const uint32_t nuniq = uint32_t(__popc(repmask));
+      if (!kSegmentRows) {
+        if (lane == 0u && nuniq) o = atomicAdd(out.total, (unsigned long long)nuniq);
+        o = __shfl_sync(0xFFFFFFFFu, o, 0);
+        if (o + nuniq > out.cap) {
+          fail();
+          continue;
         }
-        continue;
       }
       uint32_t rank = 0;
       for (uint32_t rest = repmask; rest; rest &= rest - 1u) {
@@ -428,7 +437,7 @@ __global__ void __launch_bounds__(128) k_flat_collect(const uint32_t* __restrict
         rank += kj < key ? 1u : 0u;
       }
       if (rep) {
-        out.kl[o + rank] = make_uint2(mk, ml);
+        out.kl[o + rank] = e;
         out.diffs[o + rank] = with_exact ? uint8_t(0) : uint8_t(1);
       }
       if (lane == 0u) {
@@ -438,6 +447,24 @@ __global__ void __launch_bounds__(128) k_flat_collect(const uint32_t* __restrict
       }
       continue;
     }
+    // ---- more than 32 candidates survived: through shared memory ----
+    uint32_t nres = 0;
+    uint32_t exact_idx = 0xFFFFFFFFu;  // result index of W itself
+    __syncwarp();
+    for (uint32_t j0 = 0; j0 < cnt; j0 += 32u) {
+      uint2 e = make_uint2(1u, 0u);
+      if (j0 + lane < cnt) e = fq.raw[base + j0 + lane];
+      const bool alive = e.x <= e.y;
+      const uint32_t ba = __ballot_sync(0xFFFFFFFFu, alive);
+      if (alive) {
+        const uint32_t idx = nres + uint32_t(__popc(ba & lt_mask));
+        kr[idx] = e.x;
+        lr[idx] = e.y;
+      }
+      if (j0 == 0u && (sc & kFlatExactBit) && (ba & 1u)) exact_idx = 0u;
+      nres += uint32_t(__popc(ba));
+    }
+    __syncwarp();
     uint32_t rep_bits = 0;  // bit t: result 32 t + lane represents its interval
     uint32_t nuniq = 0;
     for (uint32_t t = 0; t * 32u < nres; ++t) {
@@ -445,28 +472,25 @@ __global__ void __launch_bounds__(128) k_flat_collect(const uint32_t* __restrict
       const bool have = r < nres;
       const uint32_t rk = kr[have ? r : 0u], rl = lr[have ? r : 0u];
       const uint32_t md = r == exact_idx ? 0u : 1u;
-      bool rep = have;
+      bool rp = have;
       for (uint32_t j = 0; j < nres; ++j) {
         const uint32_t dj = j == exact_idx ? 0u : 1u;
-        if (kr[j] == rk && lr[j] == rl && (dj < md || (dj == md && j < r))) rep = false;
+        if (kr[j] == rk && lr[j] == rl && (dj < md || (dj == md && j < r))) rp = false;
       }
-      const uint32_t br = __ballot_sync(0xFFFFFFFFu, rep);
+      const uint32_t br = __ballot_sync(0xFFFFFFFFu, rp);
       if (lane == 0u) repw[t] = br;
-      rep_bits |= rep ? (1u << t) : 0u;
-      nuniq += __popc(br);
+      rep_bits |= rp ? (1u << t) : 0u;
+      nuniq += uint32_t(__popc(br));
     }
     __syncwarp();
-    unsigned long long o = 0;
-    if (lane == 0u && nuniq) o = atomicAdd(out.total, (unsigned long long)nuniq);
-    o = __shfl_sync(0xFFFFFFFFu, o, 0);
-    if (o + nuniq > out.cap) {  // this pass's buffer is full: retried by the next pass
-      if (lane == 0u) {
-        const unsigned long long f = atomicAdd(out.fail_count, 1ull);
-        out.fail_list[f] = uint32_t(q);
-        out.res_cnt[q] = 0u;
+    if (!kSegmentRows) {
+      if (lane == 0u && nuniq) o = atomicAdd(out.total, (unsigned long long)nuniq);
+      o = __shfl_sync(0xFFFFFFFFu, o, 0);
+      if (o + nuniq > out.cap) {
+        fail();
+        __syncwarp();
+        continue;
       }
-      __syncwarp();
-      continue;
     }
     for (uint32_t t = 0; t * 32u < nres; ++t) {
       const uint32_t r = t * 32u + lane;
@@ -488,6 +512,12 @@ __global__ void __launch_bounds__(128) k_flat_collect(const uint32_t* __restrict
     }
     __syncwarp();
   }
+}
+
+// After a chunk collected into its survivor segments: the next chunk's rows
+// start past them.
+__global__ void k_flat_advance(unsigned long long* total, const unsigned long long* n_surv, uint64_t q_cap) {
+  *total += min(uint64_t(*n_surv), q_cap);
 }
 
 // Filter build: entry x of the level-kx table (a present kx-mer and its
