@@ -706,13 +706,18 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
     if wl.max_diff == 1 and wl.pairs is None:
         from paper_1811_06127_b200.search import bidir_min_n
 
-        if idx.n >= bidir_min_n():  # the reversed-text index of the bidirectional z = 1 engine
+        z1_len = wl.meta["m"] if wl.packed is not None else wl.patterns.shape[1]
+        if idx.n >= bidir_min_n() and dix.wants_reverse(units, z1_len, 1):
+            # the reversed-text index of the bidirectional z = 1 engines
             t_rev = time.perf_counter()
             dix.ensure_reverse()
             extra["reverse_index_build_s"] = round(time.perf_counter() - t_rev, 2)
             extra["engine"] = ("bidirectional z=1, level-synchronous (spine + chain kernels; L2-resident lines)"
                                if dix.device_bytes <= (64 << 20) else
                                "bidirectional z=1 (case-A / case-B DFS launches + merge)")
+        elif idx.n >= bidir_min_n():
+            extra["engine"] = ("flat z=1 (k_flat_probe with the neighbourhood presence filter, k_flat_extend, "
+                               "k_flat_collect; no reverse index)")
     if wl.pairs is None:  # search configs: the k-mer / prefix interval table, built before timing
         fn = lib.fmgx_prefix_table
         fn.argtypes = [ct.c_void_p, ct.POINTER(ct.c_uint32), ct.POINTER(ct.c_uint64)]
@@ -739,7 +744,7 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
         # runs as 2 x 8.75M rather than 16.8M + 0.7M)
         n_chunks = max(1, -(-n_seeds // (1 << 24)))
         chunk = -(-n_seeds // n_chunks)
-        work_seen = [0, 0]  # inexact Occ steps, lines fetched (device counters, per step)
+        work_seen = [0, 0, 0]  # inexact Occ steps, lines fetched, kernels launched (library counters, per step)
 
         def step():
             _lib.check(lib.fmg_exact_packed(dix.handle, d_pat.data_ptr(), m, n_seeds, d_out.data_ptr(), sp))
@@ -747,15 +752,19 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
                 h = ct.c_void_p()
                 _lib.check(lib.fmg_inexact_packed(dix.handle, d_pat.data_ptr() + 8 * c0, m,
                                                   min(chunk, n_seeds - c0), 1, ct.byref(h), sp))
-                st_, ln_ = ct.c_uint64(), ct.c_uint64()
+                st_, ln_, kl_ = ct.c_uint64(), ct.c_uint64(), ct.c_uint64()
                 lib.fmg_matches_steps(h, ct.byref(st_))
                 lib.fmgx_matches_lines(h, ct.byref(ln_))
+                lib.fmgx_matches_launches(h, ct.byref(kl_))
                 work_seen[0] += st_.value
                 work_seen[1] += ln_.value
+                work_seen[2] += kl_.value
                 lib.fmg_matches_free(h)
 
-        # per z = 1 call: k_dbound, case A + its segment sort, case B + its sort, 2 x k_merge_ab,
-        # k_widen_counts, k_gather_matches (CUB scans not counted); + the exact pass
+        # the flat engine counts its own launches (k_dbound, then k_flat_probe / _extend / _collect /
+        # _advance per chunk of its survivor queue, k_widen_counts, k_gather_matches; CUB scans not
+        # counted); the bidirectional split engine: k_dbound, case A + its segment sort, case B + its
+        # sort, 2 x k_merge_ab, k_widen_counts, k_gather_matches; + the exact pass
         launches_per_step = 1 + ((n_seeds + chunk - 1) // chunk) * 9
         kernel_name = "k_inexact"
         h2d_per, d2h_per = n_seeds * 8 * 2, None
@@ -788,9 +797,11 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
         extra["seeds_per_step"] = n_seeds
 
         def count_work():
-            work_seen[0] = work_seen[1] = 0
+            work_seen[0] = work_seen[1] = work_seen[2] = 0
             step()
             torch.cuda.synchronize(dev)
+            if work_seen[2]:
+                extra["gpu_launches_counted"] = 1 + work_seen[2]
             es, el = exact_work(lib, dix, d_pat, m, n_seeds, d_out, sp)
             return {"exact_steps": es, "exact_lines": el, "inexact_steps": work_seen[0],
                     "inexact_lines": work_seen[1]}
@@ -1043,6 +1054,8 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
         # config 2 (level-synchronous bidirectional engine): k_dbound, k_bspine, k_bchain, k_z1_hist_dev,
         # k_widen_counts x2, k_z1_scatter_dev, k_z1_sort_unique, k_z1_write_kl (CUB scans not counted)
         launches_per_step = 9
+    if "gpu_launches_counted" in extra:  # the engine counted its own launches for one step
+        launches_per_step = extra.pop("gpu_launches_counted")
     if rank == 0:
         line = {
             "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,

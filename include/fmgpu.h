@@ -143,6 +143,15 @@ int fmg_inexact(const fmg_index* index, const uint8_t* codes, const uint64_t* of
                 uint64_t count, int max_diff, fmg_matches** out, void* stream);
 int fmg_inexact_host(const fmg_index* index, const uint8_t* codes, const uint64_t* offsets,
                      uint64_t count, int max_diff, fmg_matches** out);
+/* Whether a bounded-difference call of `count` patterns of at most `max_len`
+ * characters would use the reverse index (fmg_index_set_reverse) if one were
+ * attached: 1 for the bidirectional engines, 0 when another engine takes the
+ * batch (small batches, max_diff != 1, or the flat one-edit engine of
+ * HBM-resident indexes, which needs none).  Lets the host skip building and
+ * uploading a reverse index nobody reads (13 GB on the device at 3.1 Gbp).
+ * May build the index's prefix / k-mer tables (the search needs them anyway). */
+int fmg_inexact_wants_reverse(const fmg_index* index, uint64_t count, uint64_t max_len,
+                              int max_diff, int* wants);
 /* Fixed-length patterns (1 <= m <= 32) packed as in fmg_exact_packed. */
 int fmg_inexact_packed(const fmg_index* index, const uint64_t* packed, uint32_t m, uint64_t count,
                        int max_diff, fmg_matches** out, void* stream);

@@ -42,6 +42,7 @@ PROTOTYPES: dict[str, tuple] = {
     "fmg_exact_packed_host": (ct.c_int, [_vp, _vp, ct.c_uint32, ct.c_uint64, _vp]),
     "fmg_inexact": (ct.c_int, [_vp, _vp, _vp, ct.c_uint64, ct.c_int, ct.POINTER(_vp), _vp]),
     "fmg_inexact_host": (ct.c_int, [_vp, _vp, _vp, ct.c_uint64, ct.c_int, ct.POINTER(_vp)]),
+    "fmg_inexact_wants_reverse": (ct.c_int, [_vp, ct.c_uint64, ct.c_uint64, ct.c_int, ct.POINTER(ct.c_int)]),
     "fmg_inexact_packed": (ct.c_int, [_vp, _vp, ct.c_uint32, ct.c_uint64, ct.c_int, ct.POINTER(_vp), _vp]),
     "fmg_inexact_packed_host": (ct.c_int, [_vp, _vp, ct.c_uint32, ct.c_uint64, ct.c_int, ct.POINTER(_vp)]),
     "fmg_matches_size": (ct.c_int, [_vp, _u64p, _u64p]),

@@ -370,6 +370,7 @@ struct fmg_index {
 struct fmg_matches {
   int device = 0;
   uint64_t patterns = 0, total = 0, steps = 0, lines = 0;  // work counters: Occ steps, lines fetched
+  uint64_t launches = 0;  // kernels of this library the search launched (flat engine; 0 = not counted)
   uint64_t* row_off = nullptr;  // device, patterns + 1
   uint32_t* k = nullptr;        // device, total
   uint32_t* l = nullptr;
@@ -1161,6 +1162,38 @@ FlatFilter flat_filter(const fmg_index* cix, const uint2* tx, uint32_t kx, uint6
 // one more dependent step for the candidates still alive).
 constexpr uint64_t kFlatTail = 6;
 
+// Whether a z = 1 batch goes to the flat engine (kernels_flat.cuh), and the
+// level-(K + 1) table it gathers from when that is the exact search's table.
+// One place for run_inexact and fmg_inexact_wants_reverse.
+struct FlatChoice {
+  bool use = false;
+  const uint2* tx = nullptr;
+  uint32_t kx = 0;
+};
+
+FlatChoice flat_choice(const fmg_index* ix, uint64_t count, uint64_t max_len, uint32_t z, const PrefixTable& pt,
+                       cudaStream_t s) {
+  FlatChoice fc;
+  const bool force_dfs = std::getenv("FMG_INEXACT_DFS") != nullptr;  // read per call (tests flip it)
+  const char* ee = std::getenv("FMG_BIDIR_ENGINE");
+  const std::string engine_env(ee ? ee : "");
+  uint64_t line_bytes = 0;
+  with_words(ix, [&](auto wt) { line_bytes = ix->n_lines * fmg::LineTraits<decltype(wt)::value>::kBytes; });
+  if (z == 1 && max_len <= 31 && pt.base && !force_dfs &&
+      (engine_env == "flat" || (engine_env.empty() && line_bytes > (uint64_t(64) << 20)))) {
+    if (exact_table_level(ix, pt) == pt.k + 1) {
+      const KmerTable kt = kmer_table(ix, count, s);
+      if (kt.lut && kt.k == pt.k + 1) {
+        fc.tx = kt.lut;
+        fc.kx = kt.k;
+      }
+    }
+    const uint32_t kmax = fc.tx ? fc.kx : pt.k;
+    fc.use = engine_env == "flat" || max_len <= uint64_t(kmax) + kFlatTail;
+  }
+  return fc;
+}
+
 fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64_t* offsets, uint64_t count,
                          uint64_t max_len, int max_diff, cudaStream_t s, const uint64_t* packed1 = nullptr) {
   FMG_REQUIRE(max_diff >= 0, "difference budget is negative");
@@ -1261,21 +1294,10 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     // Config 3 (m = 19, level 16): 113 -> see profiles/r02_flat.md.
     // FMG_BIDIR_ENGINE=flat forces it (any size, m <= 31), any other value
     // keeps it off.
-    const uint2* flat_tx = nullptr;
-    uint32_t flat_kx = 0;
-    bool use_flat = false;
-    if (z == 1 && short_pat && max_len <= 31 && pt.base && !force_dfs &&
-        (engine_env == "flat" || (engine_env.empty() && line_bytes > (uint64_t(64) << 20)))) {
-      if (exact_table_level(ix, pt) == pt.k + 1) {
-        const KmerTable kt = kmer_table(ix, count, s);
-        if (kt.lut && kt.k == pt.k + 1) {
-          flat_tx = kt.lut;
-          flat_kx = kt.k;
-        }
-      }
-      const uint32_t kmax = flat_tx ? flat_kx : pt.k;
-      use_flat = engine_env == "flat" || max_len <= uint64_t(kmax) + kFlatTail;
-    }
+    const FlatChoice fc = flat_choice(ix, count, max_len, z, pt, s);
+    const uint2* flat_tx = fc.tx;
+    const uint32_t flat_kx = fc.kx;
+    const bool use_flat = fc.use;
     if (z == 1 && short_pat && !force_dfs && !use_flat && line_bytes <= (uint64_t(64) << 20) &&
         (!has_rev || bidir_off_env)) {
       CodePatterns cpz{codes, offsets, packed.ptr, packed1, uint32_t(max_len), dbits.ptr};
@@ -1449,6 +1471,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
         } else {
           k_flat_collect<false><<<gc, 256, 0, s>>>(nullptr, c0, cn, fq, o);
         }
+        res->launches += seg_rows ? 4 : 3;
         FMG_CK(cudaGetLastError());
       }
       unsigned long long host_ctr[2];
@@ -1745,6 +1768,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     }
     // CSR: row_off[q+1] = inclusive sum of counts
     DevBuf<uint64_t> c64(count, s);
+    if (res->launches) res->launches += 3 + (packed1 ? 0 : 1);  // k_dbound, k_widen_counts, k_gather_matches (+ k_pack_patterns)
     k_widen_counts<<<unsigned((count + 255) / 256), 256, 0, s>>>(count, res_cnt.ptr, c64.ptr);
     size_t tmp_bytes = 0;
     FMG_CK(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, c64.ptr, res->row_off + 1, count, s));
@@ -1790,8 +1814,9 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       cudaEventSynchronize(pe1);
       float ms = 0;
       cudaEventElapsedTime(&ms, pe0, pe1);
-      fprintf(stderr, "[fmg] inexact post (CSR, gather, %s): %.3f ms, %llu results\n",
-              unsorted ? "segmented sort" : "no sort", ms, (unsigned long long)total);
+      fprintf(stderr, "[fmg] inexact post (CSR, gather, %s): %.3f ms, %llu results; whole call %.3f ms of host time\n",
+              unsorted ? "segmented sort" : "no sort", ms, (unsigned long long)total,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_entry).count());
       cudaEventDestroy(pe0);
       cudaEventDestroy(pe1);
     }
@@ -2104,6 +2129,15 @@ int fmgx_matches_lines(const fmg_matches* m, uint64_t* lines) {
   });
 }
 
+// Kernels of this library a bounded-difference search launched (counted by
+// the flat engine's path; 0 when the engine does not count).
+int fmgx_matches_launches(const fmg_matches* m, uint64_t* launches) {
+  return fmg::guard([&] {
+    FMG_REQUIRE(m != nullptr && launches != nullptr, "null argument");
+    *launches = m->launches;
+  });
+}
+
 // Builds the prefix / k-mer table now instead of on the first large call
 // (bench.py reports its build time and size apart from the timed region).
 int fmgx_prefix_table(const fmg_index* ix, uint32_t* k_out, uint64_t* bytes_out) {
@@ -2267,6 +2301,22 @@ int fmg_exact_packed_host(const fmg_index* ix, const uint64_t* packed, uint32_t 
                     launch_exact_packed(ix, static_cast<const uint64_t*>(din), m, len, static_cast<uint32_t*>(dout),
                                         s, nullptr);
                   });
+  });
+}
+
+int fmg_inexact_wants_reverse(const fmg_index* ix, uint64_t count, uint64_t max_len, int max_diff, int* wants) {
+  return fmg::guard([&] {
+    check_index(ix);
+    FMG_REQUIRE(wants != nullptr, "null output pointer");
+    *wants = 0;
+    if (max_diff != 1 || count < 1024) return;  // only the bidirectional z = 1 engines read a reverse index
+    fmg::DeviceScope scope(ix->device);
+    const bool lut_off = [] {
+      const char* e = std::getenv("FMG_INEXACT_LUT");
+      return e != nullptr && std::atoi(e) == 0;
+    }();
+    const PrefixTable pt = lut_off ? PrefixTable{} : prefix_table(ix, count, nullptr);
+    *wants = flat_choice(ix, count, max_len, 1u, pt, nullptr).use ? 0 : 1;
   });
 }
 

@@ -385,12 +385,10 @@ template <bool kSegmentRows>
 __global__ void __launch_bounds__(256) k_flat_collect(const uint32_t* __restrict__ list, uint64_t q0, uint64_t count,
                                                       FlatQueues fq, InexactOut out) {
   constexpr uint32_t cap = 256u;  // >= kFlatMaxCand
-  __shared__ uint32_t sm[8][2u * cap + 8u];
+  __shared__ unsigned long long sm[8][cap];
   const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
-  uint32_t* kr = sm[wib];
-  uint32_t* lr = kr + cap;
-  uint32_t* repw = lr + cap;
+  unsigned long long* keys = sm[wib];
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   const unsigned long long chunk_rows = kSegmentRows ? *out.total : 0ull;
   for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < count; w += nwarps) {
@@ -447,43 +445,50 @@ __global__ void __launch_bounds__(256) k_flat_collect(const uint32_t* __restrict
       }
       continue;
     }
-    // ---- more than 32 candidates survived: through shared memory ----
+    // ---- more than 32 candidates survived (patterns inside repeat families):
+    // a bitonic sort of the intervals in shared memory, then one pass keeps
+    // the first of each (the quadratic rank count this replaces was most of
+    // the kernel's instructions on config 3) ----
+    // the intervals that exist, compacted (without a filter most of the segment is absent)
+    unsigned long long exact_key = ~0ull;  // no interval (k = 0xFFFFFFFF never occurs)
     uint32_t nres = 0;
-    uint32_t exact_idx = 0xFFFFFFFFu;  // result index of W itself
     __syncwarp();
     for (uint32_t j0 = 0; j0 < cnt; j0 += 32u) {
       uint2 e = make_uint2(1u, 0u);
       if (j0 + lane < cnt) e = fq.raw[base + j0 + lane];
       const bool alive = e.x <= e.y;
       const uint32_t ba = __ballot_sync(0xFFFFFFFFu, alive);
-      if (alive) {
-        const uint32_t idx = nres + uint32_t(__popc(ba & lt_mask));
-        kr[idx] = e.x;
-        lr[idx] = e.y;
-      }
-      if (j0 == 0u && (sc & kFlatExactBit) && (ba & 1u)) exact_idx = 0u;
+      const unsigned long long x = (uint64_t(e.x) << 32) | e.y;
+      if (alive) keys[nres + uint32_t(__popc(ba & lt_mask))] = x;
+      if (j0 == 0u && (sc & kFlatExactBit) && (ba & 1u)) exact_key = __shfl_sync(0xFFFFFFFFu, x, 0);  // W itself occurs
       nres += uint32_t(__popc(ba));
     }
+    uint32_t P = 32u;
+    while (P < nres) P <<= 1;  // nres <= cnt <= kFlatMaxCand < 256
+    for (uint32_t j = nres + lane; j < P; j += 32u) keys[j] = ~0ull;  // padding sorts to the end
     __syncwarp();
-    uint32_t rep_bits = 0;  // bit t: result 32 t + lane represents its interval
-    uint32_t nuniq = 0;
-    for (uint32_t t = 0; t * 32u < nres; ++t) {
-      const uint32_t r = t * 32u + lane;
-      const bool have = r < nres;
-      const uint32_t rk = kr[have ? r : 0u], rl = lr[have ? r : 0u];
-      const uint32_t md = r == exact_idx ? 0u : 1u;
-      bool rp = have;
-      for (uint32_t j = 0; j < nres; ++j) {
-        const uint32_t dj = j == exact_idx ? 0u : 1u;
-        if (kr[j] == rk && lr[j] == rl && (dj < md || (dj == md && j < r))) rp = false;
+    for (uint32_t kk = 2u; kk <= P; kk <<= 1) {
+      for (uint32_t jj = kk >> 1; jj > 0u; jj >>= 1) {
+        for (uint32_t t = lane; t < (P >> 1); t += 32u) {
+          const uint32_t i = ((t & ~(jj - 1u)) << 1) | (t & (jj - 1u)), p2 = i | jj;
+          const unsigned long long x = keys[i], y = keys[p2];
+          if ((x > y) == ((i & kk) == 0u)) {
+            keys[i] = y;
+            keys[p2] = x;
+          }
+        }
+        __syncwarp();
       }
-      const uint32_t br = __ballot_sync(0xFFFFFFFFu, rp);
-      if (lane == 0u) repw[t] = br;
-      rep_bits |= rp ? (1u << t) : 0u;
-      nuniq += uint32_t(__popc(br));
     }
-    __syncwarp();
+    // first of each interval, in order: its row is its rank
+    uint32_t nuniq = 0;
     if (!kSegmentRows) {
+      for (uint32_t j0 = 0; j0 < P; j0 += 32u) {
+        const uint32_t j = j0 + lane;
+        const unsigned long long x = keys[j];
+        const bool first = x != ~0ull && (j == 0u || keys[j - 1u] != x);
+        nuniq += uint32_t(__popc(__ballot_sync(0xFFFFFFFFu, first)));
+      }
       if (lane == 0u && nuniq) o = atomicAdd(out.total, (unsigned long long)nuniq);
       o = __shfl_sync(0xFFFFFFFFu, o, 0);
       if (o + nuniq > out.cap) {
@@ -491,19 +496,19 @@ __global__ void __launch_bounds__(256) k_flat_collect(const uint32_t* __restrict
         __syncwarp();
         continue;
       }
+      nuniq = 0;
     }
-    for (uint32_t t = 0; t * 32u < nres; ++t) {
-      const uint32_t r = t * 32u + lane;
-      if (r < nres && ((rep_bits >> t) & 1u)) {
-        const uint32_t rk = kr[r], rl = lr[r];
-        uint32_t rank = 0;
-        for (uint32_t j = 0; j < nres; ++j) {
-          const uint32_t kj = kr[j], lj = lr[j];
-          rank += (((repw[j >> 5] >> (j & 31u)) & 1u) && (kj < rk || (kj == rk && lj < rl))) ? 1u : 0u;
-        }
-        out.kl[o + rank] = make_uint2(rk, rl);
-        out.diffs[o + rank] = r == exact_idx ? uint8_t(0) : uint8_t(1);
+    for (uint32_t j0 = 0; j0 < P; j0 += 32u) {
+      const uint32_t j = j0 + lane;
+      const unsigned long long x = keys[j];
+      const bool first = x != ~0ull && (j == 0u || keys[j - 1u] != x);
+      const uint32_t bf = __ballot_sync(0xFFFFFFFFu, first);
+      if (first) {
+        const uint64_t row = o + nuniq + uint32_t(__popc(bf & lt_mask));
+        out.kl[row] = make_uint2(uint32_t(x >> 32), uint32_t(x));
+        out.diffs[row] = x == exact_key ? uint8_t(0) : uint8_t(1);
       }
+      nuniq += uint32_t(__popc(bf));
     }
     if (lane == 0u) {
       out.res_off[q] = o;

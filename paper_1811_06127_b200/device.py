@@ -67,6 +67,15 @@ class DeviceIndex:
                 _lib.check(_lib.load().fmg_index_set_reverse(self.handle, rec.ctypes.data, rec.shape[0], sentinel))
                 self._has_reverse = True
 
+    def wants_reverse(self, count: int, max_len: int, max_diff: int) -> bool:
+        """Whether a bounded-difference batch of this shape would read a reverse index
+        (fmg_inexact_wants_reverse: the bidirectional z = 1 engines do, the flat engine of
+        HBM-resident indexes and every other engine do not)."""
+        wants = ct.c_int()
+        _lib.check(_lib.load().fmg_inexact_wants_reverse(self.handle, int(count), int(max_len), int(max_diff),
+                                                         ct.byref(wants)))
+        return bool(wants.value)
+
     def ensure_samples(self) -> None:
         if self._has_samples:
             return

@@ -222,20 +222,25 @@ def _build_arrays(codes: np.ndarray, builder: str, device: int | None, threads: 
     c = np.zeros(5, dtype=np.uint64)
     sentinel = np.zeros(1, dtype=np.uint64)
     lib = _lib.load()
-    if builder == "auto":
+    auto = builder == "auto"
+    if auto:
         builder = "gpu" if n >= GPU_BUILD_MIN and _lib.device_count() > 0 else "host"
     if builder == "gpu":
         from .device import current_device, require_gpu
 
         require_gpu()
         dev = current_device() if device is None else int(device)
-        _lib.check(
-            lib.fmb_build_gpu(
-                dev, codes.ctypes.data, n, rec.ctypes.data, samples.ctypes.data, c.ctypes.data,
-                sentinel.ctypes.data, None,
-            )
+        status = lib.fmb_build_gpu(
+            dev, codes.ctypes.data, n, rec.ctypes.data, samples.ctypes.data, c.ctypes.data,
+            sentinel.ctypes.data, None,
         )
-    else:
+        if auto and status != _lib.FMG_OK and "out of memory" in _lib.last_error():
+            # the GPU builder wants ~36 bytes per character of device memory; when search
+            # tables already hold it (a reverse index built late), the host builder does the job
+            builder = "host"
+        else:
+            _lib.check(status)
+    if builder != "gpu":
         _lib.check(
             lib.fmb_build(
                 codes.ctypes.data, n, rec.ctypes.data, samples.ctypes.data, c.ctypes.data,

@@ -182,7 +182,9 @@ def inexact_search_batch(index: FmIndex, patterns, max_diff: int,
     require_gpu()
     dev = index.device_index(device)
     if max_diff == 1 and index.n >= bidir_min_n() and n >= 1024:
-        dev.ensure_reverse()  # the bidirectional engine (kernels_bidir.cuh)
+        max_len = int(np.diff(offsets).max())
+        if dev.wants_reverse(n, max_len, max_diff):  # not for the flat engine (kernels_flat.cuh)
+            dev.ensure_reverse()  # the bidirectional engines (kernels_bidir.cuh)
     handle = ct.c_void_p()
     _lib.check(lib.fmg_inexact_host(dev.handle, codes.ctypes.data, offsets.ctypes.data, n,
                                     int(max_diff), ct.byref(handle)))

@@ -98,7 +98,9 @@ def test_config3_full_scale_exact_and_hits(gpu, c3):
     assert checked > 1500
 
 
-@pytest.mark.parametrize("engine", ["default", "split", "sync", "dfs", "onedir"])
+# engines that read the reverse index first: its GPU build wants ~36 bytes per character (112 GB
+# here), which no longer fits once the flat engine's presence filter (43 GB) is resident
+@pytest.mark.parametrize("engine", ["split", "sync", "dfs", "default", "onedir"])
 def test_config3_full_scale_z1_every_engine(gpu, c3, monkeypatch, engine):
     wl, idx = c3
     gold = json.loads((GOLDEN / "scale3_cases.json").read_text())

@@ -22,7 +22,7 @@ idx = fm.build_index(wl.text, builder="gpu")
 print(f"gen+build {time.time() - t0:.1f}s, seeds {wl.packed.size}", flush=True)
 lib = _lib.load()
 dix = idx.device_index(0)
-if int(__import__("os").environ.get("FMG_BIDIR", "1")):
+if int(__import__("os").environ.get("FMG_BIDIR", "1")) and dix.wants_reverse(wl.packed.size, 19, 1):
     t3 = time.time()
     dix.ensure_reverse()
     print(f"reverse index {time.time() - t3:.1f}s", flush=True)
