@@ -135,16 +135,20 @@ __device__ __forceinline__ void chunk_count3(const uint64_t v[4], uint32_t s, ui
 
 // Sector s of chunk j, predicated (no request when !go).  Two-sector chunks
 // carry the L2::64B hint: the miss fetches the 64-byte chunk, not 128 bytes.
+// `wide` (two-sector chunks only): the step's two chunks are the halves of one
+// 128-byte line, so the loads go without the hint and ONE 128-byte fetch
+// serves both ends instead of two 64-byte ones.
 template <int NS>
 __device__ __forceinline__ void ld_sector_pred(bool go, const uint32_t* chunks, uint64_t j, uint32_t s,
-                                               uint64_t v[4]) {
+                                               uint64_t v[4], bool wide = false) {
   const uint32_t* p = chunks + j * ChunkTraits<NS>::kWords + 8 * s;
   if constexpr (NS == 2) {
     asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
-        "@q ld.global.nc.L1::no_allocate.L2::64B.v4.u64 {%0,%1,%2,%3}, [%5];\n\t}"
+        "{\n\t.reg .pred q, w;\n\tsetp.ne.u32 q, %4, 0;\n\tsetp.ne.u32 w, %6, 0;\n\t"
+        "@q ld.global.nc.L1::no_allocate.L2::64B.v4.u64 {%0,%1,%2,%3}, [%5];\n\t"
+        "@w ld.global.nc.L1::no_allocate.L2::128B.v4.u64 {%0,%1,%2,%3}, [%5];\n\t}"
         : "+l"(v[0]), "+l"(v[1]), "+l"(v[2]), "+l"(v[3])
-        : "r"(uint32_t(go)), "l"(p));
+        : "r"(uint32_t(go && !wide)), "l"(p), "r"(uint32_t(go && wide)));
   } else {
     asm volatile(
         "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
@@ -200,11 +204,19 @@ __global__ void __launch_bounds__(256) k_occ_pair_chunk(IndexView ix, const uint
   const uint32_t jh = hp / kC, jl = lp / kC;
   const uint32_t sh = chunk_sector_of(hp - jh * kC), sl = chunk_sector_of(lp - jl * kC);
   uint64_t h_hi[4] = {0, 0, 0, 0}, d_hi[4] = {0, 0, 0, 0}, h_lo[4] = {0, 0, 0, 0}, d_lo[4] = {0, 0, 0, 0};
-  ld_sector_pred<NS>(true, chunks, jh, 0, h_hi);
-  ld_sector_pred<NS>(sh != 0u, chunks, jh, sh, d_hi);
   const bool other = jl != jh;
-  ld_sector_pred<NS>(other, chunks, jl, 0, h_lo);
-  ld_sector_pred<NS>(sl != 0u && (other || sl != sh), chunks, jl, sl, d_lo);
+#ifndef FMG_CHUNK2_WIDE
+// 1: when the step's two 64-byte chunks are the halves of one 128-byte line,
+// load them without the 64-byte hint (one 128-byte fetch instead of two
+// 64-byte ones).  Measured on config 1-H: 31.9 G steps/s against 38.25 G with
+// every load hinted (profiles/r02_ab_1h_chunk2_wide.log) — off.
+#define FMG_CHUNK2_WIDE 0
+#endif
+  const bool wide = NS == 2 && FMG_CHUNK2_WIDE && other && (jl >> 1) == (jh >> 1);
+  ld_sector_pred<NS>(true, chunks, jh, 0, h_hi, wide);
+  ld_sector_pred<NS>(sh != 0u, chunks, jh, sh, d_hi, wide);
+  ld_sector_pred<NS>(other, chunks, jl, 0, h_lo, wide);
+  ld_sector_pred<NS>(sl != 0u && (other || sl != sh), chunks, jl, sl, d_lo, wide);
   // resolve aliases: the low end shares whatever the high end loaded
 #pragma unroll
   for (int z = 0; z < 4; ++z) {
