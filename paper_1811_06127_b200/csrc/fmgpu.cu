@@ -2425,9 +2425,12 @@ int fmg_matches_copy(const fmg_matches* m, uint64_t* row_offsets, uint32_t* k, u
     FMG_REQUIRE(m != nullptr, "null matches handle");
     fmg::DeviceScope scope(m->device);
     const cudaMemcpyKind kind = to_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-    if (row_offsets) FMG_CK(cudaMemcpy(row_offsets, m->row_off, (m->patterns + 1) * 8, kind));
+    // the calling thread's own copy stream, never the legacy stream: a result
+    // set copied out by one thread while another searches must not queue
+    // behind, or in front of, that search
+    cudaStream_t s = host_stream(m->device, 1);
+    if (row_offsets) FMG_CK(cudaMemcpyAsync(row_offsets, m->row_off, (m->patterns + 1) * 8, kind, s));
     if (m->total && m->kl && (k || l)) {  // packed k | l: split on the device, then copy
-      cudaStream_t s = host_stream(m->device, 1);
       DevBuf<uint32_t> dk(to_host && k ? m->total : 0, s), dl(to_host && l ? m->total : 0, s);
       uint32_t* ok = to_host ? dk.ptr : k;
       uint32_t* ol = to_host ? dl.ptr : l;
@@ -2436,12 +2439,15 @@ int fmg_matches_copy(const fmg_matches* m, uint64_t* row_offsets, uint32_t* k, u
       FMG_CK(cudaGetLastError());
       if (to_host && k) FMG_CK(cudaMemcpyAsync(k, dk.ptr, m->total * 4, cudaMemcpyDeviceToHost, s));
       if (to_host && l) FMG_CK(cudaMemcpyAsync(l, dl.ptr, m->total * 4, cudaMemcpyDeviceToHost, s));
-      FMG_CK(cudaStreamSynchronize(s));
+      if (m->total && diffs) FMG_CK(cudaMemcpyAsync(diffs, m->diffs, m->total, kind, s));
+      FMG_CK(cudaStreamSynchronize(s));  // before dk / dl go out of scope
+      return;
     } else if (m->total) {
-      if (k) FMG_CK(cudaMemcpy(k, m->k, m->total * 4, kind));
-      if (l) FMG_CK(cudaMemcpy(l, m->l, m->total * 4, kind));
+      if (k) FMG_CK(cudaMemcpyAsync(k, m->k, m->total * 4, kind, s));
+      if (l) FMG_CK(cudaMemcpyAsync(l, m->l, m->total * 4, kind, s));
     }
-    if (m->total && diffs) FMG_CK(cudaMemcpy(diffs, m->diffs, m->total, kind));
+    if (m->total && diffs) FMG_CK(cudaMemcpyAsync(diffs, m->diffs, m->total, kind, s));
+    FMG_CK(cudaStreamSynchronize(s));
   });
 }
 
