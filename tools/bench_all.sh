@@ -4,6 +4,7 @@ mkdir -p gpurun_out
 out=gpurun_out/bench_all.jsonl
 : > $out
 for c in config1 config0 config1h config2 config4 config3; do
+  sleep 10  # the previous process has released its device memory before this one sizes its scratch
   # enough steps for a timed region of tens of ms (config 0 steps are ~12 us each)
   steps=10; [ $c = config3 ] && steps=2; [ $c = config0 ] && steps=2000; [ $c = config2 ] && steps=50
   timeout 1500 python bench.py --config $c --steps $steps --warmup 3 --no-hbm-extra 2>gpurun_out/bench_$c.err | tail -1 >> $out

@@ -8,3 +8,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_occ_pair -s 3 -c 1 -o gpurun_out/r02_occ_config1 -f python tools/prof_occ.py config1 > gpurun_out/ncu_c1.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_exact -s 1 -c 1 -o gpurun_out/r02_c4_exact -f python tools/prof_exact.py 24 1 > gpurun_out/ncu_c4.log 2>&1
 ls -la gpurun_out/*.ncu-rep
+bash tools/flat_check.sh > gpurun_out/flat_check.log 2>&1; tail -4 gpurun_out/flat_check.log | cut -c1-200
+bash tools/flat_prof.sh
