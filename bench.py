@@ -766,7 +766,8 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
         # counted); the bidirectional split engine: k_dbound, case A + its segment sort, case B + its
         # sort, 2 x k_merge_ab, k_widen_counts, k_gather_matches; + the exact pass
         launches_per_step = 1 + ((n_seeds + chunk - 1) // chunk) * 9
-        kernel_name = "k_inexact"
+        # the flat engine's three kernels when no reverse index is wanted (HBM-resident index, 19-bp seeds)
+        kernel_name = "k_inexact" if "reverse_index_build_s" in extra else "k_flat_probe + k_flat_extend + k_flat_collect"
         h2d_per, d2h_per = n_seeds * 8 * 2, None
         pin_in = torch.from_numpy(wl.packed.view(np.int64)).pin_memory()
         pin_kl = torch.empty((n_seeds, 2), dtype=torch.int32).pin_memory()

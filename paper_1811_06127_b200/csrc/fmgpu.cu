@@ -1386,6 +1386,13 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     if (use_flat) {
       // ---- pass 0 = the flat engine; patterns that do not fit this pass's
       // result buffer are retried by the DFS engine below ----
+      // the filter's traversal starts from the deepest table level the engine gathers from
+      const FlatFilter flt = flat_tx ? flat_filter(ix, flat_tx, flat_kx, max_len, s)
+                                     : flat_filter(ix, pt.base + PrefixTable::off64(pt.k), pt.k, max_len, s);
+      // with the filter the output rows are the survivor segments (and the
+      // slab tails between them), not the results alone: room for 24 per pattern
+      if (flt.bits)
+        cap = std::min<uint64_t>(std::max<uint64_t>(cap, count * 24), std::max<uint64_t>(1u << 20, free_b / 4 / 9));
       pass_kl.emplace_back(cap, s);
       pass_d.emplace_back(cap, s);
       FMG_CK(cudaMemsetAsync(counters.ptr, 0, 2 * sizeof(unsigned long long), s));
@@ -1406,9 +1413,6 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       o.unsorted = counters.ptr + 5;
       o.unsorted_list = unsorted_list.ptr;
       CodePatterns cp{codes, offsets, packed.ptr, packed1, uint32_t(max_len), dbits.ptr};
-      // the filter's traversal starts from the deepest table level the engine gathers from
-      const FlatFilter flt = flat_tx ? flat_filter(ix, flat_tx, flat_kx, max_len, s)
-                                     : flat_filter(ix, pt.base + PrefixTable::off64(pt.k), pt.k, max_len, s);
       // survivor queue sized for EVERY candidate of a chunk of patterns (no
       // overflow path to get wrong): 24 bytes per entry, an eighth of the
       // available memory, patterns in chunks of cap / (8 m + 1)

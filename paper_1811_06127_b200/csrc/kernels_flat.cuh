@@ -181,6 +181,8 @@ struct FlatQueues {
 };
 
 constexpr uint32_t kFlatExactBit = 0x80000000u;
+constexpr uint32_t kFlatSlab = 512u;        // queue entries a warp reserves at a time (> kFlatMaxCand)
+constexpr uint32_t kFlatDead = 0xFFFFFFFFu;  // FlatSurvivor::L of an unused queue entry
 constexpr uint32_t kFlatMaxCand = 8u * 31u + 1u;  // candidates of the longest pattern (m <= 31)
 
 // ---- k_flat_probe ----------------------------------------------------------
@@ -195,10 +197,11 @@ constexpr uint32_t kFlatMaxCand = 8u * 31u + 1u;  // candidates of the longest p
 template <int NRS>
 __global__ void __launch_bounds__(256) k_flat_probe(CodePatterns cp, const uint32_t* __restrict__ list, uint64_t q0,
                                                     uint64_t count, FlatFilter flt, FlatQueues fq, InexactOut out) {
-  // one queue reservation per block and round of patterns (a same-address
-  // atomic per pattern capped the kernel at ~0.6 G patterns/s)
-  __shared__ uint32_t s_tot[8];
-  __shared__ unsigned long long s_base;
+  // Queue space comes in slabs of kFlatSlab entries, one per warp at a time:
+  // a same-address atomic per pattern capped the kernel at ~0.6 G patterns/s,
+  // and one per block and round of patterns cost 17 % of the warps' time at
+  // its barriers.  What a warp leaves unused of a slab is marked dead.
+  uint64_t slab_pos = 0, slab_end = 0;
   const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
   const uint64_t per_round = uint64_t(gridDim.x) * 8u;
@@ -292,23 +295,17 @@ __global__ void __launch_bounds__(256) k_flat_probe(CodePatterns cp, const uint3
       total += rt;
     }
     const uint32_t has_exact = __shfl_sync(0xFFFFFFFFu, meta[0] & 1u, 0);  // slot 0 = W itself, first in the segment
-    if (lane == 0u) s_tot[wib] = total;
-    __syncthreads();
-    if (threadIdx.x == 0u) {
-      uint32_t sum = 0;
-#pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        const uint32_t c = s_tot[v];
-        s_tot[v] = sum;  // exclusive prefix: each warp's offset in the block's reservation
-        sum += c;
-      }
-      s_base = sum ? atomicAdd(fq.n_surv, (unsigned long long)sum) : 0ull;
-    }
-    __syncthreads();
-    const unsigned long long base = s_base + s_tot[wib];
-    __syncthreads();  // s_tot / s_base are rewritten by the next round
     if (!active) continue;
-    if (base + total > fq.cap) {  // the chunk's patterns kept more candidates than it was sized for: retried
+    if (slab_pos + total > slab_end) {  // a new slab (total <= kFlatMaxCand < kFlatSlab)
+      for (uint64_t t = slab_pos + lane; t < slab_end; t += 32u) fq.surv[t].L = kFlatDead;
+      unsigned long long nb = 0;
+      if (lane == 0u) nb = atomicAdd(fq.n_surv, (unsigned long long)kFlatSlab);
+      slab_pos = __shfl_sync(0xFFFFFFFFu, nb, 0);
+      slab_end = min(slab_pos + kFlatSlab, fq.cap);
+      if (slab_pos > slab_end) slab_pos = slab_end;  // past the queue: every reservation fails from here on
+    }
+    const unsigned long long base = slab_pos;
+    if (base + total > slab_end) {  // the chunk's patterns kept more candidates than it was sized for: retried
       if (lane == 0u) {
         const unsigned long long f = atomicAdd(out.fail_count, 1ull);
         out.fail_list[f] = uint32_t(q);
@@ -331,11 +328,13 @@ __global__ void __launch_bounds__(256) k_flat_probe(CodePatterns cp, const uint3
         fq.surv[slot++] = sv;
       }
     }
+    slab_pos += total;
     if (lane == 0u) {
       fq.seg_base[q] = base;
       fq.seg_cnt[q] = total | (has_exact ? kFlatExactBit : 0u);
     }
   }
+  for (uint64_t t = slab_pos + lane; t < slab_end; t += 32u) fq.surv[t].L = kFlatDead;
   flush_work(out.steps, work);
 }
 
@@ -350,6 +349,7 @@ __global__ void __launch_bounds__(256) k_flat_extend(IndexView ix, PrefixTable t
   for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n; t += stride) {
     const FlatSurvivor sv = fq.surv[t];
     const uint32_t L = sv.L;
+    if (L == kFlatDead) continue;  // the unused tail of a warp's slab
     const uint32_t d = min(L, kmax);
     uint2 e = make_uint2(0u, ix.n);  // the empty string (a deletion from m = 1)
     if (L > 0u) {
