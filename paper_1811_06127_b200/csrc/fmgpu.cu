@@ -1291,7 +1291,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     // HBM-resident index: the flat engine (kernels_flat.cuh) — every string
     // of the one-edit neighbourhood is one table gather plus at most
     // m + 1 - kmax backward steps, a warp per pattern, no reverse index.
-    // Config 3 (m = 19, level 16): 113 -> see profiles/r02_flat.md.
+    // Config 3 (m = 19, level 16): 113 -> 32 ms per 14M seeds, profiles/r02_flat.md.
     // FMG_BIDIR_ENGINE=flat forces it (any size, m <= 31), any other value
     // keeps it off.
     const FlatChoice fc = flat_choice(ix, count, max_len, z, pt, s);
