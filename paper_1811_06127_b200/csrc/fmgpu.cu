@@ -1445,8 +1445,11 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
         for (auto& e : fe) cudaEventCreate(&e);
         cudaEventRecord(fe[0], s);
       }
-      const void* kp = nrs == 1 ? (const void*)k_flat_probe<1> : nrs == 2 ? (const void*)k_flat_probe<2>
-                                                                           : (const void*)k_flat_probe<3>;
+      const bool fixed_m = packed1 != nullptr;
+      const void* kp = fixed_m ? (nrs == 1 ? (const void*)k_flat_probe<1, true> : nrs == 2 ? (const void*)k_flat_probe<2, true>
+                                                                                           : (const void*)k_flat_probe<3, true>)
+                               : (nrs == 1 ? (const void*)k_flat_probe<1, false> : nrs == 2 ? (const void*)k_flat_probe<2, false>
+                                                                                            : (const void*)k_flat_probe<3, false>);
       const int bp = std::max(1, blocks_per_sm(kp, 256, 0)) * ix->sms;
       // with the filter a pattern's survivor segment is also its output
       // reservation (no atomics); without one the rows are reserved exactly
@@ -1461,9 +1464,15 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
         const uint64_t cn = std::min<uint64_t>(chunk, count - c0);
         FMG_CK(cudaMemsetAsync(n_surv.ptr, 0, sizeof(unsigned long long), s));
         const unsigned gp = unsigned(std::min<uint64_t>(uint64_t(bp), (cn + 7) / 8));  // 8 warps per block
-        if (nrs == 1) k_flat_probe<1><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
-        else if (nrs == 2) k_flat_probe<2><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
-        else k_flat_probe<3><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
+        if (fixed_m) {
+          if (nrs == 1) k_flat_probe<1, true><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
+          else if (nrs == 2) k_flat_probe<2, true><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
+          else k_flat_probe<3, true><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
+        } else {
+          if (nrs == 1) k_flat_probe<1, false><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
+          else if (nrs == 2) k_flat_probe<2, false><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
+          else k_flat_probe<3, false><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
+        }
         with_words(ix, [&](auto wt) {
           constexpr int W = decltype(wt)::value;
           k_flat_extend<W><<<unsigned(be), 256, 0, s>>>(ix->view(), pt, flat_tx, flat_kx, fq, counters.ptr + 2);

@@ -194,7 +194,10 @@ constexpr uint32_t kFlatMaxCand = 8u * 31u + 1u;  // candidates of the longest p
 // computes one filter address and its variants read bits next to each other.
 // Branch-free: a warp holds every kind of slot.
 // NRS = rounds of 32 slots a lane takes (32 NRS >= 3m + 1).
-template <int NRS>
+// kFixed: every pattern has cp.fixed_m characters (the packed entry points),
+// so the slots' geometry — kind, position, window, copy, shifts — is the same
+// for every pattern and is computed once per thread, outside the pattern loop.
+template <int NRS, bool kFixed>
 __global__ void __launch_bounds__(256) k_flat_probe(CodePatterns cp, const uint32_t* __restrict__ list, uint64_t q0,
                                                     uint64_t count, FlatFilter flt, FlatQueues fq, InexactOut out) {
   // Queue space comes in slabs of kFlatSlab entries, one per warp at a time:
@@ -211,7 +214,10 @@ __global__ void __launch_bounds__(256) k_flat_probe(CodePatterns cp, const uint3
     q = 0, m = 0, pw = 0, db = 0;
     if (w >= count) return;
     q = list ? list[q0 + w] : q0 + w;
-    if (cp.packed1) {
+    if (kFixed) {
+      m = int(cp.fixed_m);
+      pw = cp.packed1[q];
+    } else if (cp.packed1) {
       m = int(cp.fixed_m);
       pw = cp.packed1[q];
     } else {
@@ -226,7 +232,7 @@ __global__ void __launch_bounds__(256) k_flat_probe(CodePatterns cp, const uint3
   for (uint64_t wb = uint64_t(blockIdx.x) * 8u; wb < count; wb += per_round) {
     const bool active = wb + wib < count;
     const uint64_t q = nq, db = ndb;
-    const int m = nm;
+    const int m = kFixed ? int(cp.fixed_m) : nm;
     const uint64_t pw = npw & (shl64(1ull, 2u * uint32_t(m)) - 1ull);  // m <= 31
     load_pattern(wb + per_round + wib, nq, nm, npw, ndb);
     // two absent segments: nothing within one edit occurs
