@@ -1162,6 +1162,19 @@ FlatFilter flat_filter(const fmg_index* cix, const uint2* tx, uint32_t kx, uint6
 // one more dependent step for the candidates still alive).
 constexpr uint64_t kFlatTail = 6;
 
+// The calling thread's auxiliary streams on `device` for the flat engine's
+// chunk pipeline (created once per thread and device, non-blocking).
+cudaStream_t flat_stream(int device, int slot) {
+  thread_local std::unordered_map<int, std::array<cudaStream_t, 4>> cache;
+  auto it = cache.find(device);
+  if (it == cache.end()) {
+    std::array<cudaStream_t, 4> st{};
+    for (auto& x : st) FMG_CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    it = cache.emplace(device, st).first;
+  }
+  return it->second[size_t(slot)];
+}
+
 // Whether a z = 1 batch goes to the flat engine (kernels_flat.cuh), and the
 // level-(K + 1) table it gathers from when that is the exact search's table.
 // One place for run_inexact and fmg_inexact_wants_reverse.
@@ -1421,20 +1434,40 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       // candidates (config 3), so a chunk is sized for 48 per pattern on
       // average, and always for one pattern's worth; a chunk whose patterns
       // keep more than that overflows into the retry list (DFS engine).
-      // Without a filter every candidate survives the probe.  At most 2^26
-      // entries (1.5 GB): large buffers cost more to allocate than the extra
-      // chunk launches (12 GB queues: 40-100 ms per call against 44 ms of work).
+      // Without a filter every candidate survives the probe.  At most 2^25
+      // entries (0.75 GB) per stream: large buffers cost more to allocate than
+      // the extra chunk launches (12 GB queues: 40-100 ms per call against 44 ms
+      // of work), and smaller chunks pipeline better across the streams.
       uint64_t per_pat = flt.bits ? std::min<uint64_t>(max_cand, 48) : max_cand;
       if (const char* e = std::getenv("FMG_FLAT_PER_PAT")) per_pat = std::max(1, std::atoi(e));  // tests: force overflow
+      uint64_t q_cap_max = uint64_t(1) << 25;
+      if (const char* e = std::getenv("FMG_FLAT_QCAP_LOG2")) q_cap_max = uint64_t(1) << std::min(30, std::max(16, std::atoi(e)));  // A/B
       const uint64_t q_cap = std::max<uint64_t>(
-          std::getenv("FMG_FLAT_PER_PAT") ? per_pat : max_cand * 64, std::min<uint64_t>(count * per_pat, std::min<uint64_t>(uint64_t(1) << 26, free_b / 8 / 24)));
+          std::getenv("FMG_FLAT_PER_PAT") ? per_pat : max_cand * 64,
+          std::min<uint64_t>(count * per_pat, std::min<uint64_t>(q_cap_max, free_b / 8 / 24)));
       const uint64_t chunk = std::max<uint64_t>(1, q_cap / per_pat);
-      DevBuf<FlatSurvivor> surv(q_cap, s);
-      DevBuf<uint2> raw(q_cap, s);
+      // Chunks are pipelined over up to four streams, each with its own
+      // queue: the probe is SM-issue-bound, the extend kernel DRAM-request-
+      // bound and the collect kernel shared-memory-bound, so chunk i + 1's
+      // probe runs under chunk i's extend instead of after it.  Grids are
+      // sized so blocks of different kernels fit an SM together.
+      // FMG_FLAT_STREAMS=1..4 (1: everything on the caller's stream) and
+      // FMG_FLAT_BPS=p,e,c (resident blocks per SM of each kernel) are A/B hooks.
+      const uint64_t n_chunks = (count + chunk - 1) / chunk;
+      int nstr = 4;
+      if (const char* e = std::getenv("FMG_FLAT_STREAMS")) nstr = std::min(4, std::max(1, std::atoi(e)));
+      nstr = int(std::min<uint64_t>(uint64_t(nstr), n_chunks));
+      std::vector<DevBuf<FlatSurvivor>> surv;
+      std::vector<DevBuf<uint2>> raw;
+      for (int j = 0; j < nstr; ++j) {
+        surv.emplace_back(q_cap, s);
+        raw.emplace_back(q_cap, s);
+      }
       DevBuf<uint64_t> seg_base(count, s);
       DevBuf<uint32_t> seg_cnt(count, s);
-      DevBuf<unsigned long long> n_surv(1, s);
-      FlatQueues fq{surv.ptr, raw.ptr, n_surv.ptr, q_cap, seg_base.ptr, seg_cnt.ptr};
+      DevBuf<unsigned long long> n_surv(size_t(nstr), s);
+      DevBuf<unsigned long long> rows_base(n_chunks + 1, s);
+      FMG_CK(cudaMemsetAsync(rows_base.ptr, 0, sizeof(unsigned long long), s));
       const int nrs = int((3 * max_len + 1 + 31) / 32);  // rounds of 32 slots, 1..3 (m <= 31)
       static const bool trace_flat = std::getenv("FMG_TRACE") != nullptr;
       cudaEvent_t fe[2] = {};
@@ -1450,42 +1483,78 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
                                                                                            : (const void*)k_flat_probe<3, true>)
                                : (nrs == 1 ? (const void*)k_flat_probe<1, false> : nrs == 2 ? (const void*)k_flat_probe<2, false>
                                                                                             : (const void*)k_flat_probe<3, false>);
-      const int bp = std::max(1, blocks_per_sm(kp, 256, 0)) * ix->sms;
       // with the filter a pattern's survivor segment is also its output
       // reservation (no atomics); without one the rows are reserved exactly
       const bool seg_rows = flt.bits != nullptr;
-      const int bc = std::max(1, blocks_per_sm(seg_rows ? (const void*)k_flat_collect<true>
-                                                        : (const void*)k_flat_collect<false>, 256, 0)) * ix->sms;
-      int be = 1;
+      int occ_p = std::max(1, blocks_per_sm(kp, 256, 0));
+      int occ_c = std::max(1, blocks_per_sm(seg_rows ? (const void*)k_flat_collect<true>
+                                                     : (const void*)k_flat_collect<false>, 256, 0));
+      int occ_e = 1;
       with_words(ix, [&](auto wt) {
-        be = std::max(1, blocks_per_sm((const void*)k_flat_extend<decltype(wt)::value>, 256, 0)) * ix->sms;
+        occ_e = std::max(1, blocks_per_sm((const void*)k_flat_extend<decltype(wt)::value>, 256, 0));
       });
-      for (uint64_t c0 = 0; c0 < count; c0 += chunk) {
+      // (grids capped at 2-3 blocks per SM so that kernels of different chunks
+      // share every SM measured slower than full grids taking turns: 25.3 vs
+      // 22.5 ms per 14M config-3 seeds, profiles/r02_ab_flat_streams.log)
+      if (const char* e = std::getenv("FMG_FLAT_BPS")) {
+        int lp = 99, le = 99, lc = 99;
+        std::sscanf(e, "%d,%d,%d", &lp, &le, &lc);
+        occ_p = std::min(occ_p, std::max(1, lp));
+        occ_e = std::min(occ_e, std::max(1, le));
+        occ_c = std::min(occ_c, std::max(1, lc));
+      }
+      const int bp = occ_p * ix->sms, be = occ_e * ix->sms, bc = occ_c * ix->sms;
+      // streams and events of this call (nstr == 1: the caller's stream, no events)
+      std::vector<cudaStream_t> st(size_t(nstr), s);
+      std::vector<cudaEvent_t> ev_adv(nstr > 1 ? n_chunks : 0), ev_join(nstr > 1 ? size_t(nstr) : 0);
+      cudaEvent_t ev_fork = nullptr;
+      if (nstr > 1) {
+        for (int j = 0; j < nstr; ++j) st[size_t(j)] = flat_stream(ix->device, j);
+        FMG_CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+        for (auto& e : ev_adv) FMG_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : ev_join) FMG_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        FMG_CK(cudaEventRecord(ev_fork, s));
+        for (int j = 0; j < nstr; ++j) FMG_CK(cudaStreamWaitEvent(st[size_t(j)], ev_fork, 0));
+      }
+      uint64_t ci = 0;
+      for (uint64_t c0 = 0; c0 < count; c0 += chunk, ++ci) {
         const uint64_t cn = std::min<uint64_t>(chunk, count - c0);
-        FMG_CK(cudaMemsetAsync(n_surv.ptr, 0, sizeof(unsigned long long), s));
+        const size_t j = size_t(ci % uint64_t(nstr));
+        cudaStream_t sj = st[j];
+        FlatQueues fq{surv[j].ptr, raw[j].ptr, n_surv.ptr + j, q_cap, seg_base.ptr, seg_cnt.ptr};
+        FMG_CK(cudaMemsetAsync(fq.n_surv, 0, sizeof(unsigned long long), sj));
         const unsigned gp = unsigned(std::min<uint64_t>(uint64_t(bp), (cn + 7) / 8));  // 8 warps per block
         if (fixed_m) {
-          if (nrs == 1) k_flat_probe<1, true><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
-          else if (nrs == 2) k_flat_probe<2, true><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
-          else k_flat_probe<3, true><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
+          if (nrs == 1) k_flat_probe<1, true><<<gp, 256, 0, sj>>>(cp, nullptr, c0, cn, flt, fq, o);
+          else if (nrs == 2) k_flat_probe<2, true><<<gp, 256, 0, sj>>>(cp, nullptr, c0, cn, flt, fq, o);
+          else k_flat_probe<3, true><<<gp, 256, 0, sj>>>(cp, nullptr, c0, cn, flt, fq, o);
         } else {
-          if (nrs == 1) k_flat_probe<1, false><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
-          else if (nrs == 2) k_flat_probe<2, false><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
-          else k_flat_probe<3, false><<<gp, 256, 0, s>>>(cp, nullptr, c0, cn, flt, fq, o);
+          if (nrs == 1) k_flat_probe<1, false><<<gp, 256, 0, sj>>>(cp, nullptr, c0, cn, flt, fq, o);
+          else if (nrs == 2) k_flat_probe<2, false><<<gp, 256, 0, sj>>>(cp, nullptr, c0, cn, flt, fq, o);
+          else k_flat_probe<3, false><<<gp, 256, 0, sj>>>(cp, nullptr, c0, cn, flt, fq, o);
         }
         with_words(ix, [&](auto wt) {
           constexpr int W = decltype(wt)::value;
-          k_flat_extend<W><<<unsigned(be), 256, 0, s>>>(ix->view(), pt, flat_tx, flat_kx, fq, counters.ptr + 2);
+          k_flat_extend<W><<<unsigned(be), 256, 0, sj>>>(ix->view(), pt, flat_tx, flat_kx, fq, counters.ptr + 2);
         });
         const unsigned gc = unsigned(std::min<uint64_t>(uint64_t(bc), (cn + 7) / 8));  // 8 warps per block
         if (seg_rows) {
-          k_flat_collect<true><<<gc, 256, 0, s>>>(nullptr, c0, cn, fq, o);
-          k_flat_advance<<<1, 1, 0, s>>>(counters.ptr, n_surv.ptr, q_cap);
+          // rows of this chunk start where the previous chunk's end (another stream's advance)
+          if (nstr > 1 && ci > 0) FMG_CK(cudaStreamWaitEvent(sj, ev_adv[ci - 1], 0));
+          k_flat_advance<<<1, 1, 0, sj>>>(rows_base.ptr + ci, fq.n_surv, q_cap, counters.ptr);
+          if (nstr > 1) FMG_CK(cudaEventRecord(ev_adv[ci], sj));
+          k_flat_collect<true><<<gc, 256, 0, sj>>>(nullptr, c0, cn, fq, o, rows_base.ptr + ci);
         } else {
-          k_flat_collect<false><<<gc, 256, 0, s>>>(nullptr, c0, cn, fq, o);
+          k_flat_collect<false><<<gc, 256, 0, sj>>>(nullptr, c0, cn, fq, o, nullptr);
         }
         res->launches += seg_rows ? 4 : 3;
         FMG_CK(cudaGetLastError());
+      }
+      if (nstr > 1) {
+        for (int j = 0; j < nstr; ++j) {
+          FMG_CK(cudaEventRecord(ev_join[size_t(j)], st[size_t(j)]));
+          FMG_CK(cudaStreamWaitEvent(s, ev_join[size_t(j)], 0));
+        }
       }
       unsigned long long host_ctr[2];
       FMG_CK(cudaMemcpyAsync(host_ctr, counters.ptr, sizeof(host_ctr), cudaMemcpyDeviceToHost, s));
@@ -1494,12 +1563,15 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       if (trace_flat) {
         float ms = 0;
         cudaEventElapsedTime(&ms, fe[0], fe[1]);
-        fprintf(stderr, "[fmg] flat z=1 engine: %llu patterns in chunks of %llu (probe %d rounds x %d blocks, extend %d "
-                "blocks, collect %d blocks; filter B=%u x %u copies): %.3f ms, %llu results, %llu retried\n",
-                (unsigned long long)count, (unsigned long long)chunk, nrs, bp, be, bc, flt.B, flt.NO, ms, host_ctr[0],
-                host_ctr[1]);
+        fprintf(stderr, "[fmg] flat z=1 engine: %llu patterns in chunks of %llu on %d stream(s) (probe %d rounds x %d "
+                "blocks, extend %d blocks, collect %d blocks; filter B=%u x %u copies): %.3f ms, %llu rows, %llu retried\n",
+                (unsigned long long)count, (unsigned long long)chunk, nstr, nrs, bp, be, bc, flt.B, flt.NO, ms,
+                host_ctr[0], host_ctr[1]);
         for (auto& e : fe) cudaEventDestroy(e);
       }
+      if (ev_fork) cudaEventDestroy(ev_fork);
+      for (auto& e : ev_adv) cudaEventDestroy(e);
+      for (auto& e : ev_join) cudaEventDestroy(e);
       list = lists[0].ptr;
       pending = host_ctr[1];
       first_pass = 1;

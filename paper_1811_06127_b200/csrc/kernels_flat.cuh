@@ -383,20 +383,21 @@ __global__ void __launch_bounds__(256) k_flat_extend(IndexView ix, PrefixTable t
 // A warp per pattern; at most 32 candidates of the pattern survived the
 // filter in the common case, so each lane holds one and a match instruction
 // finds the equal intervals.  Output rows: with the filter the pattern's
-// survivor segment doubles as its reservation (rows *out.total + seg_base ..;
-// no atomics — k_flat_advance moves *out.total past the chunk afterwards);
+// survivor segment doubles as its reservation (rows *row_base + seg_base ..;
+// no atomics — k_flat_advance chains the chunks' row bases);
 // without one (every candidate is a survivor, few are results) one atomic
 // per pattern reserves exactly the rows used.
 template <bool kSegmentRows>
 __global__ void __launch_bounds__(256) k_flat_collect(const uint32_t* __restrict__ list, uint64_t q0, uint64_t count,
-                                                      FlatQueues fq, InexactOut out) {
+                                                      FlatQueues fq, InexactOut out,
+                                                      const unsigned long long* __restrict__ row_base) {
   constexpr uint32_t cap = 256u;  // >= kFlatMaxCand
   __shared__ unsigned long long sm[8][cap];
   const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
   unsigned long long* keys = sm[wib];
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  const unsigned long long chunk_rows = kSegmentRows ? *out.total : 0ull;
+  const unsigned long long chunk_rows = kSegmentRows ? *row_base : 0ull;
   for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < count; w += nwarps) {
     const uint64_t q = list ? list[q0 + w] : q0 + w;
     const uint32_t sc = fq.seg_cnt[q];
@@ -525,10 +526,13 @@ __global__ void __launch_bounds__(256) k_flat_collect(const uint32_t* __restrict
   }
 }
 
-// After a chunk collected into its survivor segments: the next chunk's rows
-// start past them.
-__global__ void k_flat_advance(unsigned long long* total, const unsigned long long* n_surv, uint64_t q_cap) {
-  *total += min(uint64_t(*n_surv), q_cap);
+// Output rows of chunk i start at rows[i]: rows[i + 1] = rows[i] + the queue
+// entries chunk i used (its survivor segments double as its rows).  Chunks
+// run on several streams; this chain (and the events around it) orders them.
+__global__ void k_flat_advance(unsigned long long* rows, const unsigned long long* n_surv, uint64_t q_cap,
+                               unsigned long long* total) {
+  rows[1] = rows[0] + min(uint64_t(*n_surv), q_cap);
+  *total = rows[1];
 }
 
 // Filter build: entry x of the level-kx table (a present kx-mer and its
