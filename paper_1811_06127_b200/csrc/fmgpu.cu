@@ -1260,28 +1260,32 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     }();
     const PrefixTable pt = lut_off ? PrefixTable{} : prefix_table(ix, count, s);
     DevBuf<uint64_t> dbits(short_pat ? count : 0, s);
+    // the flat engine (decided here) runs the lower-bound pass chunk by chunk on its own streams
+    const FlatChoice fc = flat_choice(ix, count, max_len, z, pt, s);
+    // the lower-bound pass resolves each present run's first Kt characters
+    // with one table gather (absent runs: a binary search over the levels)
+    // instead of Kt dependent Occ steps; the level-(K + 1) table joins in
+    // when it is the exact search's table
+    const uint2* db_tx = nullptr;
+    uint32_t db_kx = 0;
     if (short_pat) {
-      CodePatterns cpd{codes, offsets, packed.ptr, packed1, uint32_t(max_len)};
-      // the lower-bound pass resolves each present run's first Kt characters
-      // with one table gather (absent runs: a binary search over the levels)
-      // instead of Kt dependent Occ steps; the level-(K + 1) table joins in
-      // when it is the exact search's table
-      const uint2* tx = nullptr;
-      uint32_t kx = 0;
-      {
-        std::lock_guard<std::mutex> lock(const_cast<fmg_index*>(ix)->lut_mu);
-        if (pt.base && ix->lut_x && ix->lut_x_k == pt.k + 1) {
-          tx = ix->lut_x;
-          kx = ix->lut_x_k;
-        }
+      std::lock_guard<std::mutex> lock(const_cast<fmg_index*>(ix)->lut_mu);
+      if (pt.base && ix->lut_x && ix->lut_x_k == pt.k + 1) {
+        db_tx = ix->lut_x;
+        db_kx = ix->lut_x_k;
       }
+    }
+    auto launch_dbound = [&](uint64_t c0, uint64_t cn, cudaStream_t sd) {  // patterns c0 .. c0 + cn - 1
+      CodePatterns cpd{codes, offsets ? offsets + c0 : nullptr, packed.ptr ? packed.ptr + c0 : nullptr,
+                       packed1 ? packed1 + c0 : nullptr, uint32_t(max_len)};
       with_words(ix, [&](auto wt) {
         constexpr int W = decltype(wt)::value;
-        k_dbound<W><<<unsigned((count + 255) / 256), 256, 0, s>>>(ix->view(), cpd, count, dbits.ptr,
-                                                                    counters.ptr + 2, pt, tx, kx);
+        k_dbound<W><<<unsigned((cn + 255) / 256), 256, 0, sd>>>(ix->view(), cpd, cn, dbits.ptr + c0,
+                                                                 counters.ptr + 2, pt, db_tx, db_kx);
       });
       FMG_CK(cudaGetLastError());
-    }
+    };
+    if (short_pat && !fc.use) launch_dbound(0, count, s);
     // z = 1 on an L2-resident index without a reverse index: the
     // level-synchronous engine (uniform warps).  On HBM-resident indexes the
     // DFS engine wins: its chains start from intervals already in L1/L2, while
@@ -1307,7 +1311,6 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     // Config 3 (m = 19, level 16): 113 -> 32 ms per 14M seeds, profiles/r02_flat.md.
     // FMG_BIDIR_ENGINE=flat forces it (any size, m <= 31), any other value
     // keeps it off.
-    const FlatChoice fc = flat_choice(ix, count, max_len, z, pt, s);
     const uint2* flat_tx = fc.tx;
     const uint32_t flat_kx = fc.kx;
     const bool use_flat = fc.use;
@@ -1523,6 +1526,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
         cudaStream_t sj = st[j];
         FlatQueues fq{surv[j].ptr, raw[j].ptr, n_surv.ptr + j, q_cap, seg_base.ptr, seg_cnt.ptr};
         FMG_CK(cudaMemsetAsync(fq.n_surv, 0, sizeof(unsigned long long), sj));
+        launch_dbound(c0, cn, sj);
         const unsigned gp = unsigned(std::min<uint64_t>(uint64_t(bp), (cn + 7) / 8));  // 8 warps per block
         if (fixed_m) {
           if (nrs == 1) k_flat_probe<1, true><<<gp, 256, 0, sj>>>(cp, nullptr, c0, cn, flt, fq, o);
@@ -1547,7 +1551,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
         } else {
           k_flat_collect<false><<<gc, 256, 0, sj>>>(nullptr, c0, cn, fq, o, nullptr);
         }
-        res->launches += seg_rows ? 4 : 3;
+        res->launches += seg_rows ? 5 : 4;
         FMG_CK(cudaGetLastError());
       }
       if (nstr > 1) {
@@ -1853,7 +1857,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
     }
     // CSR: row_off[q+1] = inclusive sum of counts
     DevBuf<uint64_t> c64(count, s);
-    if (res->launches) res->launches += 3 + (packed1 ? 0 : 1);  // k_dbound, k_widen_counts, k_gather_matches (+ k_pack_patterns)
+    if (res->launches) res->launches += 2 + (packed1 ? 0 : 1);  // k_widen_counts, k_gather_matches (+ k_pack_patterns)
     k_widen_counts<<<unsigned((count + 255) / 256), 256, 0, s>>>(count, res_cnt.ptr, c64.ptr);
     size_t tmp_bytes = 0;
     FMG_CK(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, c64.ptr, res->row_off + 1, count, s));
