@@ -585,6 +585,28 @@ def test_inexact_flat_engine(gpu, monkeypatch, n, lens, filt):
     assert np.array_equal(b.offsets, ms.offsets) and np.array_equal(b.k, ms.k) and np.array_equal(b.diffs, ms.diffs)
 
 
+def test_wants_reverse_follows_the_engine_choice(gpu, monkeypatch):
+    """fmg_inexact_wants_reverse: 1 only when a bidirectional z = 1 engine would take the batch;
+    the Python layer then skips the reverse index for the flat engine."""
+    rng = np.random.Generator(np.random.PCG64(5))
+    text = rng.integers(0, 4, 1 << 22, dtype=np.uint8)
+    idx = fm.build_index(text)
+    dix = idx.device_index()
+    assert dix.wants_reverse(4096, 19, 1)          # L2-resident lines: the bidirectional engines
+    assert not dix.wants_reverse(4096, 19, 2)      # z != 1: the DFS engine
+    assert not dix.wants_reverse(100, 19, 1)       # small batch
+    monkeypatch.setenv("FMG_BIDIR_ENGINE", "flat")
+    assert not dix.wants_reverse(4096, 19, 1)      # the flat engine reads none
+    pats = [codes_to_str(text[s:s + 19]) for s in rng.integers(0, text.size - 19, 2048)]
+    ms = fm.inexact_search_batch(idx, pats, 1)
+    assert not dix._has_reverse
+    row, k, l, d, _ = orc.inexact_batch(orc.OracleIndex(idx), pats, 1)
+    assert np.array_equal(ms.offsets, row) and np.array_equal(ms.k.astype(np.int64), k)
+    assert np.array_equal(ms.l.astype(np.int64), l) and np.array_equal(ms.diffs, d)
+    monkeypatch.setenv("FMG_BIDIR_ENGINE", "split")
+    assert dix.wants_reverse(4096, 19, 1)
+
+
 def test_inexact_repeated_calls_reuse_dedup_table(gpu, monkeypatch):
     """The dedup hash table persists in the index between calls (epoch-tagged, zeroed only on
     allocation): back-to-back calls with different batches, budgets and engines on one index
