@@ -26,8 +26,10 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, engine=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if engine:  # e.g. the flat z = 1 engine (the config-3 default at genome scale) forced on this small index
+        os.environ["FMG_BIDIR_ENGINE"] = engine
     sys.path.insert(0, str(REPO))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -38,6 +40,8 @@ def _worker(rank, world, port, out_dir):
         wl = workloads.config2(n=6_000_000, n_reads=30_000)  # repeat genome, both strands, indels; bidirectional z = 1
         idx = fm.build_index(wl.text)
         pats = wl.patterns
+        if engine == "flat":
+            pats = np.ascontiguousarray(pats[:, :24])  # the flat engine takes patterns of at most 31 characters
         lo, hi = shard_range(pats.shape[0], rank, world)
         kl, _ = fm.exact_search_batch(idx, pats[lo:hi])
         ms = fm.inexact_search_batch(idx, pats[lo:hi], 1)
@@ -62,6 +66,13 @@ def _worker(rank, world, port, out_dir):
 
 def test_two_engine_ranks_gather_equals_one_rank(gpu, tmp_path):
     mp.spawn(_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    assert (tmp_path / "ok").read_text() == "1"
+
+
+def test_two_flat_engine_ranks_gather_equals_one_rank(gpu, tmp_path):
+    """The same with the flat z = 1 engine (presence filter, chunk pipeline over the rank's own
+    streams): each rank's engine caches and streams are its own, the gathered results one rank's."""
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), "flat"), nprocs=2, join=True)
     assert (tmp_path / "ok").read_text() == "1"
 
 
