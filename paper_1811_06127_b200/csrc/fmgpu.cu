@@ -2319,7 +2319,9 @@ int fmg_occ_pair_host(const fmg_index* ix, const uint32_t* kl, uint64_t count, u
     check_index(ix);
     fmg::DeviceScope scope(ix->device);
     if (count == 0) return;
-    const uint64_t chunk = std::min<uint64_t>(count, 1ull << 21);
+    uint64_t chunk_log2 = 21;
+    if (const char* e = std::getenv("FMG_OCC_HOST_CHUNK_LOG2")) chunk_log2 = uint64_t(std::min(26, std::max(12, std::atoi(e))));  // A/B
+    const uint64_t chunk = std::min<uint64_t>(count, 1ull << chunk_log2);
     cudaStream_t s0 = host_stream(ix->device, 0);
     CallStatus st(nullptr, s0);
     FMG_CK(cudaStreamSynchronize(s0));  // the word is zeroed before any slot's kernel reads it

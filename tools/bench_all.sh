@@ -4,8 +4,6 @@ mkdir -p gpurun_out
 out=gpurun_out/bench_all.jsonl
 : > $out
 for c in config1 config0 config2 config1h config4 config3; do
-  # config 2 (3 ms steps of ~20 small launches, host-paced) runs before the large configs: right after the
-  # 1 Gbp / 3.1 Gbp reference arms exit, the host is still reclaiming ~100 GB and the launches crawl
   sleep 10  # the previous process has released its device memory before this one sizes its scratch
   # enough steps for a timed region of tens of ms (config 0 steps are ~12 us each)
   steps=10; [ $c = config3 ] && steps=2; [ $c = config0 ] && steps=2000; [ $c = config2 ] && steps=50
