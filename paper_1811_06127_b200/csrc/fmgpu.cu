@@ -7,7 +7,7 @@
 //   kernels_inexact.cuh  k_dbound, k_inexact (DFS), k_spine / k_chain (z = 1),
 //                        sort / dedup / gather                 (search.py:97-159)
 //   kernels_bidir.cuh    bidirectional z = 1 engines (split DFS, level-synchronous)
-//   kernels_flat.cuh     k_z1_flat: one warp per pattern over its one-edit neighbourhood
+//   kernels_flat.cuh     flat z = 1 engine: k_flat_probe / _extend / _collect over the one-edit neighbourhood, presence filter
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -2319,7 +2319,7 @@ int fmg_occ_pair_host(const fmg_index* ix, const uint32_t* kl, uint64_t count, u
     check_index(ix);
     fmg::DeviceScope scope(ix->device);
     if (count == 0) return;
-    uint64_t chunk_log2 = 21;
+    uint64_t chunk_log2 = 20;  // 2^20 pairs per chunk: 1.676 G steps/s e2e on config 1 against 1.662 G at 2^21, 1.619 G at 2^22 (profiles/r02_ab_e2e_chunk.log)
     if (const char* e = std::getenv("FMG_OCC_HOST_CHUNK_LOG2")) chunk_log2 = uint64_t(std::min(26, std::max(12, std::atoi(e))));  // A/B
     const uint64_t chunk = std::min<uint64_t>(count, 1ull << chunk_log2);
     cudaStream_t s0 = host_stream(ix->device, 0);
