@@ -585,6 +585,35 @@ def test_inexact_flat_engine(gpu, monkeypatch, n, lens, filt):
     assert np.array_equal(b.offsets, ms.offsets) and np.array_equal(b.k, ms.k) and np.array_equal(b.diffs, ms.diffs)
 
 
+def test_exact_packed_host_pinned_and_pageable(gpu):
+    """fmg_exact_packed_host with pinned buffers (small batch: the kernel reads and writes the host
+    mappings directly) and with pageable ones (staged pipeline): both equal the oracle."""
+    import ctypes as ct
+
+    import torch
+
+    from paper_1811_06127_b200 import _lib, pack_patterns_u64
+
+    wl = workloads.config0()
+    idx = fm.build_index(wl.text)
+    want = orc.exact_batch(orc.OracleIndex(idx), wl.patterns)
+    packed = pack_patterns_u64(wl.patterns)
+    lib, dix = _lib.load(), idx.device_index()
+    out = np.empty((packed.size, 2), dtype=np.uint32)  # pageable in, pageable out
+    _lib.check(lib.fmg_exact_packed_host(dix.handle, packed.ctypes.data, 32, packed.size, out.ctypes.data))
+    assert np.array_equal(out, want)
+    pin_in = torch.from_numpy(packed.view(np.int64)).pin_memory()
+    pin_out = torch.zeros((packed.size, 2), dtype=torch.int32).pin_memory()
+    for _ in range(3):
+        pin_out.zero_()
+        _lib.check(lib.fmg_exact_packed_host(dix.handle, pin_in.data_ptr(), 32, packed.size, pin_out.data_ptr()))
+        assert np.array_equal(pin_out.numpy().view(np.uint32), want)
+    # pinned in, pageable out: staged
+    out2 = np.empty_like(out)
+    _lib.check(lib.fmg_exact_packed_host(dix.handle, pin_in.data_ptr(), 32, packed.size, out2.ctypes.data))
+    assert np.array_equal(out2, want)
+
+
 def test_wants_reverse_follows_the_engine_choice(gpu, monkeypatch):
     """fmg_inexact_wants_reverse: 1 only when a bidirectional z = 1 engine would take the batch;
     the Python layer then skips the reverse index for the flat engine."""
