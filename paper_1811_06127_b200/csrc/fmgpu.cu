@@ -2330,6 +2330,17 @@ int fmg_occ_pair_host(const fmg_index* ix, const uint32_t* kl, uint64_t count, u
     check_index(ix);
     fmg::DeviceScope scope(ix->device);
     if (count == 0) return;
+    // FMG_OCC_ZEROCOPY=1 (A/B): pinned buffers read and written by the kernel itself, no staging;
+    // slower for a whole config-1 step (1.54 vs 1.68 G steps/s, profiles/r02_ab_zerocopy.log): off
+    if (const char* e = std::getenv("FMG_OCC_ZEROCOPY")) {
+      if (std::atoi(e) != 0 && pinned_host(kl) && pinned_host(out)) {
+        cudaStream_t s0 = host_stream(ix->device, 0);
+        CallStatus st(nullptr, s0);
+        launch_occ_pair(ix, kl, count, out, s0, st.word);
+        st.raise_if_set(s0, "Occ position out of range or pair out of order");
+        return;
+      }
+    }
     uint64_t chunk_log2 = 20;  // 2^20 pairs per chunk: 1.676 G steps/s e2e on config 1 against 1.662 G at 2^21, 1.619 G at 2^22 (profiles/r02_ab_e2e_chunk.log)
     if (const char* e = std::getenv("FMG_OCC_HOST_CHUNK_LOG2")) chunk_log2 = uint64_t(std::min(26, std::max(12, std::atoi(e))));  // A/B
     const uint64_t chunk = std::min<uint64_t>(count, 1ull << chunk_log2);
