@@ -703,6 +703,8 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
     units = unit_count(wl)
     metric, unit = metric_of(args.config)
     extra: dict = {"index_build_s": round(t_build, 2), "index_device_bytes": dix.device_bytes}
+    free_b, total_b = torch.cuda.mem_get_info(dev)  # what else holds device memory when the engine sizes its scratch
+    extra["gpu_mem_free_after_index"] = int(free_b)
     if wl.max_diff == 1 and wl.pairs is None:
         from paper_1811_06127_b200.search import bidir_min_n
 
