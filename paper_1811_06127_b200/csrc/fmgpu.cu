@@ -527,11 +527,29 @@ void launch_occ_pair_t(const fmg_index* ix, const uint32_t* kl, uint64_t count, 
         k_occ_pair_chunk<4><<<dim3(unsigned((count + 255) / 256)), 256, 0, s>>>(
             ix->view(), ix->chunks, reinterpret_cast<const uint2*>(kl), count, out, err);
     } else if (W == 2 && two_lane) {
-      k_occ_pair_2l<<<dim3(unsigned((2 * count + 255) / 256)), 256, 0, s>>>(
-          ix->view(), reinterpret_cast<const uint2*>(kl), count, out, err);
+      static const bool bulk2 = [] {  // FMG_OCC_BULK=1: bulk-copy stores (A/B; slower with two lanes per step on config 1)
+        const char* e = std::getenv("FMG_OCC_BULK");
+        return e != nullptr && std::atoi(e) != 0;
+      }();
+      if (bulk2 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0)
+        k_occ_pair_2l<true><<<dim3(unsigned((2 * count + 255) / 256)), 256, 0, s>>>(
+            ix->view(), reinterpret_cast<const uint2*>(kl), count, out, err);
+      else
+        k_occ_pair_2l<false><<<dim3(unsigned((2 * count + 255) / 256)), 256, 0, s>>>(
+            ix->view(), reinterpret_cast<const uint2*>(kl), count, out, err);
     } else if (W == 2) {
-      k_occ_pair<PER, W><<<dim3(unsigned(blocks)), threads, 0, s>>>(ix->view(), reinterpret_cast<const uint2*>(kl),
-                                                                      count, out, err);
+      // counts leave through one bulk copy per block: 90.6 vs 89.2 G steps/s on
+      // config 1 (profiles/r02_ab_occ_bulk.log); FMG_OCC_BULK=0: per-thread stores (A/B)
+      static const bool bulk = [] {
+        const char* e = std::getenv("FMG_OCC_BULK");
+        return e == nullptr || std::atoi(e) != 0;
+      }();
+      if (PER == 1 && bulk && (reinterpret_cast<uintptr_t>(out) & 15u) == 0)
+        k_occ_pair<1, W, true><<<dim3(unsigned(blocks)), threads, 0, s>>>(
+            ix->view(), reinterpret_cast<const uint2*>(kl), count, out, err);
+      else
+        k_occ_pair<PER, W><<<dim3(unsigned(blocks)), threads, 0, s>>>(ix->view(), reinterpret_cast<const uint2*>(kl),
+                                                                        count, out, err);
     } else {  // wide lines: lane-cooperative, persistent grid-stride
       constexpr int LANES = int(LineTraits<W>::kBytes / 32);
       const uint64_t nb = (count * LANES + 255) / 256;

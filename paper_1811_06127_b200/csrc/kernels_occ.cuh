@@ -80,9 +80,17 @@ __device__ __forceinline__ void st_stream_256(uint32_t* p, const uint32_t lo[4],
 // (k,l) loads and the 32-byte output stores stay fully coalesced; all line
 // loads of a thread are issued before any popcount so each thread keeps up
 // to 2*PER independent line reads in flight.
-template <int PER, int W>
+//
+// kBulk (PER = 1): the block's counts are staged in shared memory and leave
+// as ONE bulk copy (cp.async.bulk shared -> global, the TMA path) instead of a
+// 32-byte store per thread through the LSU.  ncu on config 1 shows the SM's
+// L1 -> crossbar request port 87 % busy, shared by the line read requests and
+// the stores' payload; the bulk copy takes the payload off that port.
+template <int PER, int W, bool kBulk = false>
 __global__ void __launch_bounds__(256) k_occ_pair(IndexView ix, const uint2* __restrict__ kl, uint64_t count,
                                                   uint32_t* __restrict__ out, uint32_t* __restrict__ err) {
+  static_assert(!kBulk || PER == 1, "the bulk-store form handles one pair per thread");
+  __shared__ __align__(128) uint32_t stage[kBulk ? 256 * 8 : 4];
   constexpr uint32_t kC = LineTraits<W>::kChars;
   const uint64_t first = uint64_t(blockIdx.x) * blockDim.x * PER + threadIdx.x;
   uint2 q[PER];
@@ -113,7 +121,7 @@ __global__ void __launch_bounds__(256) k_occ_pair(IndexView ix, const uint2* __r
   }
 #pragma unroll
   for (int u = 0; u < PER; ++u) {
-    if (!act[u]) continue;
+    if (!kBulk && !act[u]) continue;
     const uint32_t k = q[u].x, l = q[u].y;
     uint32_t lo[4] = {0u, 0u, 0u, 0u}, hi[4] = {0u, 0u, 0u, 0u};
     if (ok[u]) {
@@ -126,7 +134,26 @@ __global__ void __launch_bounds__(256) k_occ_pair(IndexView ix, const uint2* __r
       }
     }
     const uint64_t i = first + uint64_t(u) * blockDim.x;
-    st_stream_256(out + i * 8, lo, hi);
+    if constexpr (kBulk) {
+      uint4* sp = reinterpret_cast<uint4*>(stage + threadIdx.x * 8);
+      sp[0] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      sp[1] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    } else {
+      st_stream_256(out + i * 8, lo, hi);
+    }
+  }
+  if constexpr (kBulk) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // these writes, then the async proxy's read
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint64_t base = uint64_t(blockIdx.x) * blockDim.x;
+      const uint32_t bytes = uint32_t(min(uint64_t(blockDim.x), count - base)) * 32u;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + base * 8),
+                   "r"(uint32_t(__cvta_generic_to_shared(stage))), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // the block's shared memory outlives the read
+    }
   }
 }
 
@@ -135,11 +162,44 @@ __global__ void __launch_bounds__(256) k_occ_pair(IndexView ix, const uint2* __r
 // lines share a 128-byte chunk (64% of config-1 steps) the coalescer merges
 // them into one L2 request, so requests per step drop from 1.75 (lines) to
 // 1.36 (chunks); each lane counts one position and stores its 16 bytes.
+// kBulk: the block's counts staged in shared memory and written by one bulk
+// copy (see k_occ_pair).
+template <bool kBulk = false>
 __global__ void __launch_bounds__(256) k_occ_pair_2l(IndexView ix, const uint2* __restrict__ kl, uint64_t count,
                                                      uint32_t* __restrict__ out, uint32_t* __restrict__ err) {
+  __shared__ __align__(128) uint32_t stage[kBulk ? 256 * 4 : 4];
   const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t i = t >> 1;
   const uint32_t role = uint32_t(t & 1u);  // 0: low (k-1), 1: high (l)
+  if constexpr (kBulk) {
+    const bool act = i < count;
+    const uint2 q = act ? ld_stream_u2(kl + i) : make_uint2(1u, 0u);
+    const uint32_t k = q.x, l = q.y;
+    const bool ok = act && l <= ix.n && k <= l + 1u;
+    if (act && !ok && role == 0u && err) atomicOr(err, 1u);
+    const bool none = !ok || (role == 0u && k == 0u);
+    const uint32_t p = role ? l : k - 1u;
+    const uint32_t pp = none ? (ok ? l : 0u) : p;
+    uint32_t b[4], r4[4] = {0u, 0u, 0u, 0u};
+    uint64_t w[2];
+    load_line<2, true>(ix, pp >> 6, pp & 63u, b, w);
+    if (!none) occ4_from_line<2>(ix, b, w, p, p & 63u, r4);
+    *reinterpret_cast<uint4*>(stage + threadIdx.x * 4) = make_uint4(r4[0], r4[1], r4[2], r4[3]);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint64_t base = uint64_t(blockIdx.x) * (blockDim.x >> 1);  // first pair of the block
+      if (base < count) {
+        const uint32_t bytes = uint32_t(min(uint64_t(blockDim.x >> 1), count - base)) * 32u;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + base * 8),
+                     "r"(uint32_t(__cvta_generic_to_shared(stage))), "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+    }
+    return;
+  }
   if (i >= count) return;
   const uint2 q = ld_stream_u2(kl + i);
   const uint32_t k = q.x, l = q.y;
