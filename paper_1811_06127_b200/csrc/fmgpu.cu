@@ -563,7 +563,7 @@ void launch_occ_pair_t(const fmg_index* ix, const uint32_t* kl, uint64_t count, 
 void launch_occ_pair(const fmg_index* ix, const uint32_t* kl, uint64_t count, uint32_t* out, cudaStream_t s,
                      uint32_t* err, int per = kOccPer, int threads = 128) {
   if (count == 0) return;
-  FMG_REQUIRE(threads == 128 || threads == 256, "threads must be 128 or 256");
+  FMG_REQUIRE(threads == 64 || threads == 128 || threads == 256, "threads must be 64, 128 or 256");
   switch (per) {
     case 1: launch_occ_pair_t<1>(ix, kl, count, out, s, err, threads); break;
     case 2: launch_occ_pair_t<2>(ix, kl, count, out, s, err, threads); break;

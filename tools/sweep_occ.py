@@ -45,8 +45,8 @@ def main():
         d_out = torch.empty((kl.shape[0], 8), dtype=torch.int32, device=dev)
         h = idx.device_index(0).handle
         s = torch.cuda.current_stream().cuda_stream
-        for per in (1, 2, 4):
-            for threads in (128, 256):
+        for per in (1, 2):
+            for threads in (64, 128, 256):
                 for _ in range(3):
                     _lib.check(fn(h, d_kl.data_ptr(), kl.shape[0], d_out.data_ptr(), s, per, threads))
                 e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
