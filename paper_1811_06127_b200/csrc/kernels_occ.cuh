@@ -83,9 +83,10 @@ __device__ __forceinline__ void st_stream_256(uint32_t* p, const uint32_t lo[4],
 //
 // kBulk (PER = 1): the block's counts are staged in shared memory and leave
 // as ONE bulk copy (cp.async.bulk shared -> global, the TMA path) instead of a
-// 32-byte store per thread through the LSU.  ncu on config 1 shows the SM's
-// L1 -> crossbar request port 87 % busy, shared by the line read requests and
-// the stores' payload; the bulk copy takes the payload off that port.
+// 32-byte store per thread through the LSU: 89.2 -> 90.6 G steps/s on config
+// 1.  (ncu shows the SM's L1 -> crossbar request port 87 % busy before and 89 %
+// after, so the bulk copy's payload shares that port with the line requests;
+// the gain is the LSU work saved.)
 //
 // kExch (PER = 1, W = 2): neighbouring lanes fetch for each other so that the
 // two lines of ONE step are requested by one instruction — the even lane asks
