@@ -551,9 +551,15 @@ void launch_occ_pair_t(const fmg_index* ix, const uint32_t* kl, uint64_t count, 
       if (PER == 1 && bulk && exch && (reinterpret_cast<uintptr_t>(out) & 15u) == 0)
         k_occ_pair<1, 2, true, true><<<dim3(unsigned(blocks)), threads, 0, s>>>(
             ix->view(), reinterpret_cast<const uint2*>(kl), count, out, err);
-      else if (PER == 1 && bulk && (reinterpret_cast<uintptr_t>(out) & 15u) == 0)
-        k_occ_pair<1, W, true><<<dim3(unsigned(blocks)), threads, 0, s>>>(
+      else if (PER == 1 && bulk && (reinterpret_cast<uintptr_t>(out) & 15u) == 0) {
+        // FMG_OCC_DYNSMEM=bytes: unused dynamic shared memory, to cap the resident blocks per SM (A/B)
+        static const size_t pad = [] {
+          const char* e = std::getenv("FMG_OCC_DYNSMEM");
+          return e ? size_t(std::atoi(e)) : size_t(0);
+        }();
+        k_occ_pair<1, W, true><<<dim3(unsigned(blocks)), threads, pad, s>>>(
             ix->view(), reinterpret_cast<const uint2*>(kl), count, out, err);
+      }
       else
         k_occ_pair<PER, W><<<dim3(unsigned(blocks)), threads, 0, s>>>(ix->view(), reinterpret_cast<const uint2*>(kl),
                                                                         count, out, err);

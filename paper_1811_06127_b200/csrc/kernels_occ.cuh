@@ -95,8 +95,11 @@ __device__ __forceinline__ void st_stream_256(uint32_t* p, const uint32_t lo[4],
 // Lines of one step usually share a 128-byte block, which the coalescer turns
 // into one L1 -> crossbar request (1.36 requests per config-1 step instead of
 // 1.75) without doubling the threads as k_occ_pair_2l does.
+#ifndef FMG_OCC_MINB
+#define FMG_OCC_MINB 1  // resident 256-thread blocks per SM the register budget is sized for (A/B: 8 = 32 registers)
+#endif
 template <int PER, int W, bool kBulk = false, bool kExch = false>
-__global__ void __launch_bounds__(256) k_occ_pair(IndexView ix, const uint2* __restrict__ kl, uint64_t count,
+__global__ void __launch_bounds__(256, FMG_OCC_MINB) k_occ_pair(IndexView ix, const uint2* __restrict__ kl, uint64_t count,
                                                   uint32_t* __restrict__ out, uint32_t* __restrict__ err) {
   static_assert(!kBulk || PER == 1, "the bulk-store form handles one pair per thread");
   static_assert(!kExch || (PER == 1 && W == 2), "the lane-exchange form: one pair per thread, 32-byte lines");
