@@ -1540,13 +1540,25 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
       const int bp = occ_p * ix->sms, be = occ_e * ix->sms, bc = occ_c * ix->sms;
       // streams and events of this call (nstr == 1: the caller's stream, no events)
       std::vector<cudaStream_t> st(size_t(nstr), s);
+      struct Events {  // destroyed on every way out of the call
+        std::vector<cudaEvent_t> v;
+        cudaEvent_t make() {
+          cudaEvent_t e = nullptr;
+          FMG_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          v.push_back(e);
+          return e;
+        }
+        ~Events() {
+          for (cudaEvent_t e : v) cudaEventDestroy(e);
+        }
+      } events;
       std::vector<cudaEvent_t> ev_adv(nstr > 1 ? n_chunks : 0), ev_join(nstr > 1 ? size_t(nstr) : 0);
       cudaEvent_t ev_fork = nullptr;
       if (nstr > 1) {
         for (int j = 0; j < nstr; ++j) st[size_t(j)] = flat_stream(ix->device, j);
-        FMG_CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-        for (auto& e : ev_adv) FMG_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        for (auto& e : ev_join) FMG_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ev_fork = events.make();
+        for (auto& e : ev_adv) e = events.make();
+        for (auto& e : ev_join) e = events.make();
         FMG_CK(cudaEventRecord(ev_fork, s));
         for (int j = 0; j < nstr; ++j) FMG_CK(cudaStreamWaitEvent(st[size_t(j)], ev_fork, 0));
       }
@@ -1604,9 +1616,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
                 host_ctr[0], host_ctr[1]);
         for (auto& e : fe) cudaEventDestroy(e);
       }
-      if (ev_fork) cudaEventDestroy(ev_fork);
-      for (auto& e : ev_adv) cudaEventDestroy(e);
-      for (auto& e : ev_join) cudaEventDestroy(e);
+
       list = lists[0].ptr;
       pending = host_ctr[1];
       first_pass = 1;
