@@ -184,8 +184,13 @@ void guarded_free(void* p) {
   cu.addr_free(r.va, r.reserved);
 }
 
+// Bumped by every synchronous allocation / free of this library: available_bytes()
+// re-reads the device's free memory only after one of them (or after 250 ms).
+std::atomic<uint64_t> g_mem_epoch{1};
+
 // Synchronous allocations of the index structures (lines, chunks, tables).
 cudaError_t dmalloc_v(void** p, size_t bytes) {
+  g_mem_epoch.fetch_add(1, std::memory_order_relaxed);
   if (!guard_mode()) return cudaMalloc(p, bytes);
   try {
     *p = guarded_alloc(bytes);
@@ -200,6 +205,7 @@ cudaError_t dmalloc(T** p, size_t bytes) {
 }
 void dfree(void* p) {
   if (!p) return;
+  g_mem_epoch.fetch_add(1, std::memory_order_relaxed);
   if (!guard_mode()) {
     cudaFree(p);
     return;
@@ -267,6 +273,8 @@ int sm_count(int device) {
   return v;
 }
 
+size_t available_bytes_now(int device);
+
 // Memory a call may size its scratch from: device free memory plus what the
 // stream-ordered pool holds but is not using.  Unlike cudaMemGetInfo alone
 // this does not shrink as the pool keeps freed blocks (release threshold is
@@ -274,6 +282,30 @@ int sm_count(int device) {
 // reuses its blocks instead of mapping fresh memory (measured on B200: the
 // config-2 z = 1 call varied 8 -> 50 ms while sizes followed cudaMemGetInfo).
 size_t available_bytes(int device) {
+  // cudaMemGetInfo is a slow driver call (and run_inexact asks three times per
+  // search): the answer is kept for 250 ms unless this library allocated or
+  // freed device memory synchronously in between
+  struct Cached {
+    size_t value = 0;
+    uint64_t epoch = 0;
+    std::chrono::steady_clock::time_point at{};
+  };
+  static std::mutex cache_mu;
+  static std::unordered_map<int, Cached> cached;
+  const uint64_t epoch = g_mem_epoch.load(std::memory_order_relaxed);
+  const auto now = std::chrono::steady_clock::now();
+  {
+    std::lock_guard<std::mutex> lock(cache_mu);
+    const Cached& c = cached[device];
+    if (c.value && c.epoch == epoch && now - c.at < std::chrono::milliseconds(250)) return c.value;
+  }
+  const size_t fresh = available_bytes_now(device);
+  std::lock_guard<std::mutex> lock(cache_mu);
+  cached[device] = Cached{fresh, epoch, now};
+  return fresh;
+}
+
+size_t available_bytes_now(int device) {
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return size_t(8) << 30;
   cudaMemPool_t pool;
