@@ -297,7 +297,11 @@ size_t available_bytes(int device) {
   {
     std::lock_guard<std::mutex> lock(cache_mu);
     const Cached& c = cached[device];
-    if (c.value && c.epoch == epoch && now - c.at < std::chrono::milliseconds(250)) return c.value;
+    static const int keep_ms = [] {  // FMG_AVAIL_CACHE_MS (A/B; 0: ask the driver every time)
+      const char* e = std::getenv("FMG_AVAIL_CACHE_MS");
+      return e ? std::atoi(e) : 250;
+    }();
+    if (c.value && c.epoch == epoch && now - c.at < std::chrono::milliseconds(keep_ms)) return c.value;
   }
   const size_t fresh = available_bytes_now(device);
   std::lock_guard<std::mutex> lock(cache_mu);
