@@ -745,7 +745,8 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
         d_out = torch.empty((n_seeds, 2), dtype=torch.int32, device=dev)
         # z = 1 calls of at most 2^24 seeds, equal-sized (a rank's shard at 8 GPUs, 17.5M seeds,
         # runs as 2 x 8.75M rather than 16.8M + 0.7M)
-        n_chunks = max(1, -(-n_seeds // (1 << 24)))
+        call_log2 = int(os.environ.get("FMG_C3_CALL_LOG2", 24))  # A/B: seeds per z = 1 call
+        n_chunks = max(1, -(-n_seeds // (1 << call_log2)))
         chunk = -(-n_seeds // n_chunks)
         work_seen = [0, 0, 0]  # inexact Occ steps, lines fetched, kernels launched (library counters, per step)
 
