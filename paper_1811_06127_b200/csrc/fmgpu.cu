@@ -1599,6 +1599,7 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
         for (int j = 0; j < nstr; ++j) FMG_CK(cudaStreamWaitEvent(st[size_t(j)], ev_fork, 0));
       }
       uint64_t ci = 0;
+      try {
       for (uint64_t c0 = 0; c0 < count; c0 += chunk, ++ci) {
         const uint64_t cn = std::min<uint64_t>(chunk, count - c0);
         const size_t j = size_t(ci % uint64_t(nstr));
@@ -1638,6 +1639,10 @@ fmg_matches* run_inexact(const fmg_index* ix, const uint8_t* codes, const uint64
           FMG_CK(cudaEventRecord(ev_join[size_t(j)], st[size_t(j)]));
           FMG_CK(cudaStreamWaitEvent(s, ev_join[size_t(j)], 0));
         }
+      }
+      } catch (...) {  // nothing of this call may still run on the auxiliary streams when its buffers go
+        for (cudaStream_t x : st) cudaStreamSynchronize(x);
+        throw;
       }
       unsigned long long host_ctr[2];
       FMG_CK(cudaMemcpyAsync(host_ctr, counters.ptr, sizeof(host_ctr), cudaMemcpyDeviceToHost, s));
