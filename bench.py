@@ -651,6 +651,9 @@ def run_ours(args, rank: int, local: int, world: int) -> None:
     # a smaller box) share devices round-robin and talk over gloo, since NCCL
     # refuses two ranks on one device — no rank ever waits on another's kernels
     n_dev = torch.cuda.device_count()
+    if n_dev == 0:
+        raise SystemExit("bench.py: no CUDA device visible — the engine runs only on the GPU (no CPU fallback); "
+                         "`--impl reference` times the CPU restatement of the reference")
     oversubscribed = world > n_dev
     local = local % n_dev
     torch.cuda.set_device(local)
